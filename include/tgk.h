@@ -1,0 +1,243 @@
+/* tgk.h — C ABI of the B200-native P1 Galerkin assembly engine (libtgk.so).
+ *
+ * Drop-in boundary for the hot path of the reference library `tg`
+ * (/root/reference/proj): Stage I "Map" (batch.hpp), Stage II "Reduce"
+ * (routing.hpp), the whole-path entry tg::assemble (physics.hpp:55-56) and the
+ * adjoint pieces (adjoint.hpp:27-28 + the per-element chain rule of
+ * tests/acceptance.cpp:357-378 / tools/tg_main.cpp:840-856).  Each entry point
+ * below cites the reference interface it replaces.  INTEGRATION.md shows the
+ * binding a maintainer adds to bindings/module.cpp (pybind11) or a ctypes user.
+ *
+ * Conventions
+ *  - plain C: opaque handles, pointers and sizes; no torch / CUDA types.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - "_d" suffix / d_ arguments: DEVICE pointers.  Functions without it take
+ *    HOST pointers and do the host<->device copies themselves (synchronous,
+ *    like the reference's std::vector API).
+ *  - fp64 throughout; connectivity is int64 on the host side like tg::Mesh
+ *    (mesh.hpp:19) and int32 on the device.
+ *  - Status codes mirror the reference CLI (tools/tg_main.cpp:979-988):
+ *    0 ok, 1 numerical (tg::NumericalError), 2 input (tg::InputError),
+ *    3 CUDA / runtime failure.  tgk_last_error() gives the message; for a
+ *    non-positive Jacobian it is "element <e> has non-positive Jacobian
+ *    determinant" exactly like batch.cpp:124-126 (e = smallest such element).
+ *  - No CPU fallback: every compute entry point fails with status 3 when no
+ *    CUDA device is usable.
+ */
+#ifndef TGK_H
+#define TGK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TGK_OK 0
+#define TGK_ERR_NUMERICAL 1
+#define TGK_ERR_INPUT 2
+#define TGK_ERR_CUDA 3
+
+/* element kinds — same codes as tg::ElementKind (reference.hpp:10) */
+#define TGK_TRI3 0
+#define TGK_QUAD4 1 /* accepted by the host helpers only; P1 kernels are TRI3/TET4 */
+#define TGK_TET4 2
+
+/* problem kinds — tg::ProblemKind (physics.hpp:16) */
+#define TGK_POISSON 0
+#define TGK_ELASTICITY 1
+#define TGK_MASS 2
+
+/* coefficient field types — tg::CoefficientField variants (coefficient.hpp:17-50).
+ * Analytic (a host std::function) has no device form: evaluate it on the host
+ * and pass an element or quadrature table instead. */
+#define TGK_FIELD_CONSTANT 0
+#define TGK_FIELD_ELEMENT 1 /* E values                       */
+#define TGK_FIELD_NODAL 2   /* N_node values, interpolated by the basis (batch.cpp:314-333) */
+
+/* arithmetic modes for the fused path */
+#define TGK_MODE_EXACT 0 /* reference operation order, no FMA: bit-identical CSR values */
+#define TGK_MODE_FAST 1  /* FMA + shared reciprocal: within 1e-13 relative (scaled) */
+
+typedef struct tgk_mesh tgk_mesh;
+typedef struct tgk_routing tgk_routing;
+
+typedef struct {
+    int type;           /* TGK_FIELD_* */
+    double value;       /* TGK_FIELD_CONSTANT */
+    const double* data; /* TGK_FIELD_ELEMENT / TGK_FIELD_NODAL (host or device per entry point) */
+    int64_t n;          /* number of values in data */
+} tgk_field;
+
+/* ProblemSpec (physics.hpp:20-45), assembly-relevant members only. */
+typedef struct {
+    int kind;              /* TGK_POISSON / TGK_ELASTICITY / TGK_MASS */
+    tgk_field diffusion;   /* Poisson / mass coefficient */
+    tgk_field lambda, mu;  /* elasticity Lame fields */
+    int plane_stress;      /* 2D elasticity only */
+    int n_source;          /* 0, 1 (scalar) or d (elasticity body force) */
+    tgk_field source[3];
+    int with_mass;         /* also assemble M (scalar problems only; physics.cpp:68-73) */
+    int mode;              /* TGK_MODE_EXACT (default) or TGK_MODE_FAST */
+} tgk_problem;
+
+/* Routing description (RoutingMatrices, routing.hpp:16-32).  All pointers are
+ * DEVICE pointers owned by the routing handle.  Segment maps are present only
+ * when the routing was built with TGK_ROUTING_SEGMENTS. */
+typedef struct {
+    int64_t N, E, nnz;
+    int k, components;
+    const int64_t* row_ptr;      /* CsrPattern::offsets, N+1 */
+    const int64_t* col_idx;      /* CsrPattern::cols, nnz */
+    const uint32_t* slot_of;     /* element-to-CSR-slot map, E*k*k: slot_of[(e*k+a)*k+b] = t
+                                    (inverse of mat_slots); components==1 only */
+    const uint32_t* vec_offsets; /* N+1 */
+    const uint32_t* vec_slots;   /* E*k   */
+    const uint32_t* mat_offsets; /* nnz+1 */
+    const uint32_t* mat_slots;   /* E*k*k */
+} tgk_routing_view;
+
+#define TGK_ROUTING_SEGMENTS 1 /* also build vec_/mat_ segment maps (reference layout) */
+
+/* ------------------------------------------------------------------ misc */
+const char* tgk_last_error(void);
+int tgk_version(void);
+int tgk_device_count(void);  /* 0 on a host without a usable GPU */
+/* tg::set_thread_count (parallel.hpp:9) — accepted for API parity; the GPU
+ * path's results never depend on it (parallel.hpp:12-14). */
+void tgk_set_thread_count(int n);
+int tgk_thread_count(void);
+
+/* ------------------------------------------------------------------ host helpers (CPU) */
+/* tg::generate_grid (mesh.cpp:96-169) — bit-identical node/element arrays.
+ * Query sizes with nodes == elems == NULL. */
+int tgk_grid_sizes(int kind, const int64_t* divisions, int64_t* n_nodes, int64_t* n_elems);
+int tgk_generate_grid(int kind, const double* extents, const int64_t* divisions, double* nodes,
+                      int64_t* elems);
+/* Mesh::content_hash (mesh.cpp:79-94) */
+uint64_t tgk_content_hash(int kind, const double* nodes, int64_t n_nodes, const int64_t* elems,
+                          int64_t n_elems);
+/* topological_boundary (mesh.cpp:185-209): sorted boundary node ids; returns count,
+ * writes when out != NULL. */
+int64_t tgk_topological_boundary(int kind, const int64_t* elems, int64_t n_elems,
+                                 int64_t n_nodes, int64_t* out);
+/* Mesh::validate (mesh.cpp:56-77) */
+int tgk_validate(int kind, const double* nodes, int64_t n_nodes, const int64_t* elems,
+                 int64_t n_elems);
+/* quadrature tables (reference.cpp:223-247) */
+int tgk_default_degree(int kind, int mass);
+int tgk_tables(int kind, int degree, int* Q, double* points, double* weights, double* B,
+               double* G);
+
+/* ------------------------------------------------------------------ mesh */
+/* Upload a tg::Mesh (host arrays, int64 connectivity) to the device. */
+int tgk_mesh_create(int kind, const double* nodes, int64_t n_nodes, const int64_t* elems,
+                    int64_t n_elems, tgk_mesh** out);
+/* Wrap device arrays (node-major fp64 coordinates, int32 connectivity); not owned. */
+int tgk_mesh_create_d(int kind, const double* d_nodes, int64_t n_nodes, const int32_t* d_elems,
+                      int64_t n_elems, tgk_mesh** out);
+/* Re-upload host arrays into an existing mesh of the same sizes (timed e2e path). */
+int tgk_mesh_upload(tgk_mesh* m, const double* nodes, const int64_t* elems, void* stream);
+void tgk_mesh_destroy(tgk_mesh* m);
+int tgk_mesh_info(const tgk_mesh* m, int* kind, int64_t* n_nodes, int64_t* n_elems,
+                  const double** d_nodes, const int32_t** d_elems);
+
+/* ------------------------------------------------------------------ routing */
+/* build_dofmap (dofmap.cpp:9-25) + build_routing (routing.cpp:12-85) on the GPU.
+ * CSR pattern and slot map are bit-identical to the reference.  components is
+ * 1 or the mesh dimension.  flags: TGK_ROUTING_SEGMENTS. */
+int tgk_routing_build(const tgk_mesh* m, int components, int flags, void* stream,
+                      tgk_routing** out);
+void tgk_routing_destroy(tgk_routing* r);
+int tgk_routing_get_view(const tgk_routing* r, tgk_routing_view* out);
+/* Copy the reference-layout arrays to host (any pointer may be NULL). */
+int tgk_routing_copy(const tgk_routing* r, int64_t* row_ptr, int64_t* col_idx, uint32_t* slot_of,
+                     uint32_t* vec_offsets, uint32_t* vec_slots, uint32_t* mat_offsets,
+                     uint32_t* mat_slots);
+/* Row-owning partitions: restrict the fused assembly to the scalar (node)
+ * rows [row_lo, row_hi) of this routing; elements incident to them are
+ * recomputed as halo.  Other output rows are left untouched.  Resets the plan. */
+int tgk_routing_set_owned_rows(tgk_routing* r, int64_t row_lo, int64_t row_hi);
+/* Fused-plan statistics (builds the plan if needed): CUDA blocks, halo
+ * elements (halo / E = recompute factor), packed records, device bytes. */
+int tgk_routing_plan_stats(tgk_routing* r, int64_t* n_blocks, int64_t* n_halo, int64_t* n_records,
+                           int64_t* bytes);
+/* Routing cache file in the reference layout ("tg-rout2", routing.cpp:178-234). */
+int tgk_routing_save(const tgk_routing* r, uint64_t mesh_hash, const char* path);
+
+/* ------------------------------------------------------------------ Stage I (Map), materialised */
+/* batch_geometry + push_forward (batch.cpp:56-154).  Outputs E x Q x ... like
+ * GeometryBatch/PhysicalGradients; any may be NULL.  Device pointers. */
+int tgk_geometry_d(const tgk_mesh* m, int degree, double* d_jac, double* d_det,
+                   double* d_jac_invT, double* d_qpts, double* d_grads, void* stream);
+/* local_stiffness_diffusion (batch.cpp:156-181): coeff E x Q table, out E x k x k */
+int tgk_local_stiffness_diffusion_d(const tgk_mesh* m, int degree, const double* d_coeff_eq,
+                                    double* d_out, void* stream);
+/* local_stiffness_elasticity (batch.cpp:183-248): out E x (k d) x (k d) */
+int tgk_local_stiffness_elasticity_d(const tgk_mesh* m, int degree, const double* d_lambda_eq,
+                                     const double* d_mu_eq, double* d_out, void* stream);
+/* local_mass (batch.cpp:250-269) */
+int tgk_local_mass_d(const tgk_mesh* m, int degree, const double* d_coeff_eq, double* d_out,
+                     void* stream);
+/* local_load (batch.cpp:271-289) */
+int tgk_local_load_d(const tgk_mesh* m, int degree, const double* d_source_eq, double* d_out,
+                     void* stream);
+/* local_load_vector (batch.cpp:291-312): source E x Q x d */
+int tgk_local_load_vector_d(const tgk_mesh* m, int degree, const double* d_source_eqc,
+                            double* d_out, void* stream);
+/* CoefficientField::evaluate (coefficient.cpp:34-55) for constant / element / nodal
+ * fields (field data on the device): out E x Q */
+int tgk_evaluate_field_d(const tgk_mesh* m, int degree, const tgk_field* f, double* d_out,
+                         void* stream);
+
+/* ------------------------------------------------------------------ Stage II (Reduce), materialised */
+/* reduce_matrix / reduce_vector (routing.cpp:87-125): needs TGK_ROUTING_SEGMENTS.
+ * Bitwise identical to the reference (ascending-slot left fold per output). */
+int tgk_reduce_matrix_d(const tgk_routing* r, const double* d_local, double* d_values,
+                        void* stream);
+int tgk_reduce_vector_d(const tgk_routing* r, const double* d_local, double* d_F, void* stream);
+
+/* ------------------------------------------------------------------ fused assembly */
+/* tg::assemble (physics.cpp:10-75): Map fused with Reduce — local tensors
+ * never touch HBM.  Writes K values (nnz), F (N) and, with with_mass, M values.
+ * Field data pointers in *p are DEVICE pointers.  Output pattern is the
+ * routing's (K, M and dK share one CsrPattern, adjoint.cpp:73). */
+int tgk_assemble_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r,
+                   double* d_K, double* d_F, double* d_M, void* stream);
+/* Asynchronous variant for streams / CUDA-graph capture (scalar problems):
+ * no host synchronisation; the smallest element with det <= 0 (or ~0ull when
+ * none) is written to the 8-byte DEVICE word *d_bad for the caller to check. */
+int tgk_assemble_async_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r,
+                         double* d_K, double* d_F, double* d_M, unsigned long long* d_bad,
+                         void* stream);
+/* Same call on HOST buffers (field data, outputs), with the copies inside. */
+int tgk_assemble(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, double* K,
+                 double* F, double* M);
+
+/* Batched operator-learning assembly: B per-element coefficient fields
+ * (d_rho, B x E, field-major) on one mesh -> B stiffness value arrays
+ * (d_K, B x nnz) and, if d_F != NULL, one load vector for the constant source
+ * `source`.  Same arithmetic as assemble() with diffusion = per_element(rho_b). */
+int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B,
+                           const double* d_rho, double source, double* d_K, double* d_F,
+                           int mode, void* stream);
+
+/* ------------------------------------------------------------------ adjoint */
+/* gradient_products (adjoint.cpp:68-82): dK[t] = lambda_i U_cols[t] on the
+ * pattern, dF = -lambda.  Batched over B fields (lambda, U: B x N). */
+int tgk_gradient_products_d(const tgk_routing* r, int64_t B, const double* d_lambda,
+                            const double* d_U, double* d_dK, double* d_dF, void* stream);
+/* Fused adjoint transpose gather (chain rule of tg_main.cpp:846-850 and
+ * acceptance.cpp:372-377): for each field b and element e,
+ *   out[b,e] = sum_{a,c} (lambda_b[g_a] * K0_e[a,c]) * U_b[g_c]
+ * with K0_e the unit-coefficient local diffusion stiffness at the stiffness
+ * degree, recomputed in registers (dK and K0 are never materialised).
+ * lambda, U: B x N (N = routing.N); out: B x E. */
+int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B,
+                         const double* d_lambda, const double* d_U, double* d_out, int degree,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGK_H */

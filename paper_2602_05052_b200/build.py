@@ -1,0 +1,78 @@
+"""Builds libtgk.so in-tree (paper_2602_05052_b200/lib/) for sm_100a.
+
+nvcc cross-compiles here without a GPU; the .so travels to the GPU box with the
+repo snapshot.  Device code is compiled with -fmad=false: the exact arithmetic
+mode reproduces the reference's FMA-free operation order bit for bit (the fast
+mode uses explicit __fma_rn intrinsics, which -fmad does not affect).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "lib")
+OBJ = os.path.join(OUT, "obj")
+LIB = os.path.join(OUT, "libtgk.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+                  "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                  f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
+CXXFLAGS = ["-O3", "-fPIC", "-std=c++17", "-Wall", "-Wno-unused-function",
+            f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}", f"-I{os.path.join(CUDA, 'include')}"]
+
+CU = ["routing.cu", "stage.cu", "fused.cu", "adjoint.cu"]
+CPP = ["host.cpp", "plan.cpp"]
+HEADERS = ["tgk_internal.hpp", "element.cuh", "cuda_util.cuh"]
+
+
+def _newer(src_list, target):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in src_list)
+
+
+def _compile(src):
+    path = os.path.join(CSRC, src)
+    obj = os.path.join(OBJ, src + ".o")
+    deps = [path] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "tgk.h")]
+    if not _newer(deps, obj):
+        return obj, ""
+    if src.endswith(".cu"):
+        cmd = [NVCC] + NVFLAGS + ["-c", path, "-o", obj]
+    else:
+        cmd = [os.environ.get("CXX", "g++")] + CXXFLAGS + ["-c", path, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return obj, r.stderr
+
+
+def build(verbose=False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        results = list(ex.map(_compile, CU + CPP))
+    objs = [o for o, _ in results]
+    log = "\n".join(f"== {s}\n{msg}" for s, (_, msg) in zip(CU + CPP, results) if msg)
+    if log:
+        with open(os.path.join(OUT, "ptxas.log"), "w") as f:
+            f.write(log)
+    if verbose and log:
+        print(log)
+    if _newer(objs, LIB):
+        cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", LIB] + objs + ["-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

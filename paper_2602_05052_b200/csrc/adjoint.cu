@@ -1,0 +1,231 @@
+// Adjoint pieces (adjoint.cpp:68-82 and the per-element chain rule of
+// acceptance.cpp:357-378 / tg_main.cpp:840-856), batched operator-learning
+// assembly, and the vector (elasticity) assembly path.
+#include <climits>
+
+#include "cuda_util.cuh"
+#include "element.cuh"
+#include "tgk_internal.hpp"
+
+namespace tgk {
+
+int check_bad(unsigned long long* d_bad, cudaStream_t st);
+int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
+                          double* F, double* M, cudaStream_t st, unsigned long long* d_bad);
+
+namespace {
+
+// gradient_products: dK[b,t] = lambda_b[i] * U_b[cols[t]] for t in row i; dF = -lambda
+__global__ void k_gradient_products(const int64_t* row_ptr, const int64_t* cols, int64_t N,
+                                    int64_t nnz, int64_t B, const double* lam, const double* U,
+                                    double* dK, double* dF) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < nnz) {
+        int64_t lo = 0, hi = N;  // row of t: last i with row_ptr[i] <= t
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (row_ptr[mid] <= t) lo = mid; else hi = mid;
+        }
+        const int64_t j = cols[t];
+        for (int64_t b = 0; b < B; ++b) dK[b * nnz + t] = lam[b * N + lo] * U[b * N + j];
+    }
+    if (dF && t < N)
+        for (int64_t b = 0; b < B; ++b) dF[b * N + t] = -lam[b * N + t];
+}
+
+// Fused transpose gather: out[b,e] = sum_{a,c} (lambda_b[g_a] * K0_e[a,c]) * U_b[g_c]
+// (tg_main.cpp:846-850 order), K0_e = local_stiffness_diffusion with unit
+// coefficient at quadrature degree DEG, recomputed in registers.
+template <int KIND, int DEG, int FPB>
+__global__ void __launch_bounds__(128) k_adjoint_gather(const double* nodes, const int32_t* conn,
+                                                        int64_t E, int64_t N, int64_t B,
+                                                        const double* lam, const double* U,
+                                                        double* out, unsigned long long* bad) {
+    constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q;
+    using R = Rule<KIND, DEG>;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int32_t g[k];
+    double X[k][d];
+#pragma unroll
+    for (int a = 0; a < k; ++a) g[a] = __ldg(conn + e * k + a);
+#pragma unroll
+    for (int a = 0; a < k; ++a)
+#pragma unroll
+        for (int c = 0; c < d; ++c) X[a][c] = __ldg(nodes + int64_t(g[a]) * d + c);
+    double det, G[k][d];
+    if (!simplex_geometry<KIND>(X, det, G)) {
+        atomicMin(bad, static_cast<unsigned long long>(e));
+        return;
+    }
+    double K0[k][k];
+#pragma unroll
+    for (int a = 0; a < k; ++a)
+#pragma unroll
+        for (int c = a; c < k; ++c) {
+            const double dot = gdot<KIND>(G, a, c);
+            double v = (R::w(0) * det * 1.0) * dot;
+#pragma unroll
+            for (int q = 1; q < Q; ++q) v += (R::w(q) * det * 1.0) * dot;
+            K0[a][c] = v;
+            K0[c][a] = v;
+        }
+    const int64_t b0 = int64_t(blockIdx.y) * FPB;
+#pragma unroll 1
+    for (int f = 0; f < FPB; ++f) {
+        const int64_t b = b0 + f;
+        if (b >= B) break;
+        const double* lb = lam + b * N;
+        const double* ub = U + b * N;
+        double la[k], uc[k];
+#pragma unroll
+        for (int a = 0; a < k; ++a) {
+            la[a] = __ldg(lb + g[a]);
+            uc[a] = __ldg(ub + g[a]);
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < k; ++a)
+#pragma unroll
+            for (int c = 0; c < k; ++c) s += la[a] * K0[a][c] * uc[c];
+        out[b * E + e] = s;
+    }
+}
+
+// plane-stress lambda (batch.cpp:359-361) in place, and the mu > 0 check
+__global__ void k_plane_stress(double* lam, const double* mu, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) lam[i] = 2.0 * lam[i] * mu[i] / (lam[i] + 2.0 * mu[i]);
+}
+
+__global__ void k_min_value(const double* v, int64_t n, unsigned long long* flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && v[i] <= 0.0) atomicMin(flag, 0ull);
+}
+
+__global__ void k_interleave(const double* comp, int64_t n, int d, int c, double* out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i * d + c] = comp[i];
+}
+
+}  // namespace
+
+// Elasticity (physics.cpp:45-66) through the materialised stage kernels:
+// evaluate -> local_stiffness_elasticity -> reduce_matrix, and the vector
+// load -> reduce_vector.  Bit-identical to the reference.
+int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
+                        double* F, cudaStream_t st) {
+    const int d = m->d;
+    const bool high = pr->diffusion.type != TGK_FIELD_CONSTANT;
+    const int degree = high ? 2 : 1;
+    int Q = 0;
+    TGK_TRY(tgk_tables(m->kind, degree, &Q, nullptr, nullptr, nullptr, nullptr));
+    const int64_t nq = m->E * Q;
+    DevBuf<double> lam, mu, local;
+    TGK_TRY(lam.alloc(nq));
+    TGK_TRY(mu.alloc(nq));
+    TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->lambda, lam.p, st));
+    TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->mu, mu.p, st));
+    if (d == 2 && pr->plane_stress) {
+        k_plane_stress<<<grid_for(nq, 256), 256, 0, st>>>(lam.p, mu.p, nq);
+        KERNEL_CHECK("plane_stress");
+    }
+    {
+        DevBuf<unsigned long long> flag;
+        TGK_TRY(flag.alloc(1));
+        CUDA_TRY(cudaMemsetAsync(flag.p, 0xff, sizeof(unsigned long long), st));
+        k_min_value<<<grid_for(nq, 256), 256, 0, st>>>(mu.p, nq, flag.p);
+        KERNEL_CHECK("mu_check");
+        unsigned long long h = ULLONG_MAX;
+        CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (h != ULLONG_MAX) return set_error(TGK_ERR_INPUT, "elasticity requires mu > 0");
+    }
+    const int kk = m->k * d;
+    TGK_TRY(local.alloc(m->E * kk * kk));
+    TGK_TRY(tgk_local_stiffness_elasticity_d(m, degree, lam.p, mu.p, local.p, st));
+    TGK_TRY(tgk_reduce_matrix_d(r, local.p, K, st));
+    if (F) {
+        if (pr->n_source > 0) {
+            DevBuf<double> src, comp;
+            TGK_TRY(src.alloc(nq * d));
+            TGK_TRY(comp.alloc(nq));
+            for (int c = 0; c < d; ++c) {
+                TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->source[c], comp.p, st));
+                k_interleave<<<grid_for(nq, 256), 256, 0, st>>>(comp.p, nq, d, c, src.p);
+                KERNEL_CHECK("interleave");
+            }
+            TGK_TRY(tgk_local_load_vector_d(m, degree, src.p, local.p, st));
+            TGK_TRY(tgk_reduce_vector_d(r, local.p, F, st));
+        } else {
+            CUDA_TRY(cudaMemsetAsync(F, 0, sizeof(double) * r->N, st));
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return TGK_OK;
+}
+
+}  // namespace tgk
+
+extern "C" {
+
+int tgk_gradient_products_d(const tgk_routing* r, int64_t B, const double* lam, const double* U,
+                            double* dK, double* dF, void* stream) {
+    using namespace tgk;
+    if (!r) return set_error(TGK_ERR_INPUT, "gradient_products: null routing");
+    TGK_TRY(ensure_device());
+    const int64_t n = std::max(r->nnz, r->N);
+    k_gradient_products<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+        r->row_ptr, r->col_idx, r->N, r->nnz, B, lam, U, dK, dF);
+    KERNEL_CHECK("gradient_products");
+    return TGK_OK;
+}
+
+int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, const double* lam,
+                         const double* U, double* out, int degree, void* stream) {
+    using namespace tgk;
+    if (!m || !r) return set_error(TGK_ERR_INPUT, "adjoint_gather: null argument");
+    if (r->components != 1) return set_error(TGK_ERR_INPUT, "adjoint_gather: scalar routing required");
+    TGK_TRY(ensure_device());
+    cudaStream_t st = as_stream(stream);
+    constexpr int FPB = 8;
+    DevBuf<unsigned long long> bad;
+    TGK_TRY(bad.alloc(1));
+    CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    const dim3 grid(grid_for(m->E, 128), static_cast<unsigned>((B + FPB - 1) / FPB));
+    if (m->kind == TGK_TET4) {
+        if (degree == 1) k_adjoint_gather<TGK_TET4, 1, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
+        else k_adjoint_gather<TGK_TET4, 2, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
+    } else if (m->kind == TGK_TRI3) {
+        if (degree == 1) k_adjoint_gather<TGK_TRI3, 1, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
+        else k_adjoint_gather<TGK_TRI3, 2, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
+    } else {
+        return set_error(TGK_ERR_INPUT, "adjoint_gather: TRI3/TET4 only");
+    }
+    KERNEL_CHECK("adjoint_gather");
+    return check_bad(bad.p, st);
+}
+
+// v1: one fused launch per field (shared plan / geometry inputs).
+int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, const double* rho,
+                           double source, double* K, double* F, int mode, void* stream) {
+    using namespace tgk;
+    (void)mode;
+    if (!m || !r) return set_error(TGK_ERR_INPUT, "assemble_batched: null argument");
+    cudaStream_t st = as_stream(stream);
+    DevBuf<unsigned long long> bad;
+    TGK_TRY(bad.alloc(1));
+    for (int64_t b = 0; b < B; ++b) {
+        tgk_problem p{};
+        p.kind = TGK_POISSON;
+        p.diffusion = tgk_field{TGK_FIELD_ELEMENT, 0.0, rho + b * m->E, m->E};
+        p.n_source = (F && b == 0) ? 1 : 0;
+        p.source[0] = tgk_field{TGK_FIELD_CONSTANT, source, nullptr, 0};
+        TGK_TRY(fused_scalar_assemble(&p, m, const_cast<tgk_routing*>(r), K + b * r->nnz,
+                                      b == 0 ? F : nullptr, nullptr, st, bad.p));
+        if (b + 1 == B || (b & 63) == 63) TGK_TRY(check_bad(bad.p, st));
+    }
+    return TGK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,667 @@
+// Host half of libtgk.so: error state, the reference-compatible mesh helpers
+// (grid generation, content hash, boundary, validation, quadrature tables),
+// device mesh handles, the fused-plan upload and the tg::assemble dispatcher.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <type_traits>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <thread>
+#include <unordered_map>
+
+#include "tgk_internal.hpp"
+
+namespace tgk {
+
+namespace {
+thread_local std::string g_err;
+std::atomic<int> g_threads{0};
+}  // namespace
+
+int set_error(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+const std::string& last_error() { return g_err; }
+
+#define HCUDA(call)                                                                    \
+    do {                                                                               \
+        cudaError_t _e = (call);                                                       \
+        if (_e != cudaSuccess)                                                         \
+            return set_error(TGK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+static int host_ensure_device() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        return set_error(TGK_ERR_CUDA, "no usable CUDA device (libtgk has no CPU fallback)");
+    return TGK_OK;
+}
+
+// ---------------------------------------------------------------- reference tables
+// reference.cpp:45-71 (shape functions) and :99-210 (rules), host copy.
+static void shape_values(int kind, const double* p, double* v) {
+    if (kind == TGK_TRI3) {
+        v[0] = 1.0 - p[0] - p[1]; v[1] = p[0]; v[2] = p[1];
+    } else if (kind == TGK_QUAD4) {
+        const double x = p[0], y = p[1];
+        v[0] = (1 - x) * (1 - y); v[1] = x * (1 - y); v[2] = x * y; v[3] = (1 - x) * y;
+    } else {
+        v[0] = 1.0 - p[0] - p[1] - p[2]; v[1] = p[0]; v[2] = p[1]; v[3] = p[2];
+    }
+}
+
+static void shape_gradients(int kind, const double* p, double* g) {
+    if (kind == TGK_TRI3) {
+        const double t[6] = {-1, -1, 1, 0, 0, 1};
+        std::memcpy(g, t, sizeof t);
+    } else if (kind == TGK_QUAD4) {
+        const double x = p[0], y = p[1];
+        const double t[8] = {-(1 - y), -(1 - x), (1 - y), -x, y, x, -y, (1 - x)};
+        std::memcpy(g, t, sizeof t);
+    } else {
+        const double t[12] = {-1, -1, -1, 1, 0, 0, 0, 1, 0, 0, 0, 1};
+        std::memcpy(g, t, sizeof t);
+    }
+}
+
+static int rule(int kind, int degree, int& Q, std::vector<double>& pts, std::vector<double>& w) {
+    if (degree < 1 || degree > 4)
+        return set_error(TGK_ERR_INPUT, "quadrature degree " + std::to_string(degree) +
+                                            " unsupported; supported degrees: 1,2,3,4");
+    if (kind == TGK_TRI3) {
+        switch (degree) {
+            case 1: Q = 1; pts = {1.0 / 3.0, 1.0 / 3.0}; w = {0.5}; break;
+            case 2: Q = 3; pts = {1.0 / 6, 1.0 / 6, 2.0 / 3, 1.0 / 6, 1.0 / 6, 2.0 / 3};
+                    w = {1.0 / 6, 1.0 / 6, 1.0 / 6}; break;
+            case 3: Q = 4; pts = {1.0 / 3, 1.0 / 3, 0.2, 0.2, 0.6, 0.2, 0.2, 0.6};
+                    w = {-27.0 / 96, 25.0 / 96, 25.0 / 96, 25.0 / 96}; break;
+            default: {
+                const double a1 = 0.445948490915965, w1 = 0.223381589678011;
+                const double a2 = 0.091576213509771, w2 = 0.109951743655322;
+                Q = 6;
+                pts = {a1, a1, 1 - 2 * a1, a1, a1, 1 - 2 * a1, a2, a2, 1 - 2 * a2, a2, a2, 1 - 2 * a2};
+                w = {w1 / 2, w1 / 2, w1 / 2, w2 / 2, w2 / 2, w2 / 2};
+            }
+        }
+    } else if (kind == TGK_QUAD4) {
+        std::vector<double> g, gw;
+        if (degree <= 1) { g = {0.5}; gw = {1.0}; }
+        else if (degree <= 3) { const double s = 0.5 / std::sqrt(3.0); g = {0.5 - s, 0.5 + s}; gw = {0.5, 0.5}; }
+        else { const double s = 0.5 * std::sqrt(0.6); g = {0.5 - s, 0.5, 0.5 + s}; gw = {5.0 / 18, 8.0 / 18, 5.0 / 18}; }
+        const int n = static_cast<int>(g.size());
+        Q = n * n;
+        pts.clear(); w.clear();
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) { pts.push_back(g[i]); pts.push_back(g[j]); w.push_back(gw[i] * gw[j]); }
+    } else {
+        switch (degree) {
+            case 1: Q = 1; pts = {0.25, 0.25, 0.25}; w = {1.0 / 6.0}; break;
+            case 2: {
+                const double a = 0.585410196624969, b = 0.138196601125011;
+                Q = 4; pts = {b, b, b, a, b, b, b, a, b, b, b, a}; w.assign(4, 1.0 / 24.0); break;
+            }
+            case 3: {
+                const double s = 1.0 / 6.0;
+                Q = 5; pts = {0.25, 0.25, 0.25, s, s, s, 0.5, s, s, s, 0.5, s, s, s, 0.5};
+                w = {-4.0 / 5.0 / 6.0, 9.0 / 20.0 / 6.0, 9.0 / 20.0 / 6.0, 9.0 / 20.0 / 6.0, 9.0 / 20.0 / 6.0};
+                break;
+            }
+            default: {
+                const double a = 11.0 / 14.0, b = 1.0 / 14.0;
+                const double c = 0.399403576166799, dd = 0.100596423833201;
+                const double w1 = -74.0 / 5625.0, w2 = 343.0 / 45000.0, w3 = 56.0 / 2250.0;
+                Q = 11;
+                pts = {0.25, 0.25, 0.25, b, b, b, a, b, b, b, a, b, b, b, a,
+                       c, dd, dd, dd, c, dd, dd, dd, c, dd, c, c, c, dd, c, c, c, dd};
+                w = {w1, w2, w2, w2, w2, w3, w3, w3, w3, w3, w3};
+            }
+        }
+    }
+    return TGK_OK;
+}
+
+// centroid_det (mesh.cpp:31-52)
+static double centroid_det(int kind, const double* nodes, const int64_t* conn) {
+    const int k = element_nodes(kind), d = element_dim(kind);
+    static const double ref_nodes[3][4][3] = {{{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 0}},
+                                              {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0}},
+                                              {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}}};
+    double centroid[3] = {0, 0, 0};
+    for (int a = 0; a < k; ++a)
+        for (int c = 0; c < d; ++c) centroid[c] += ref_nodes[kind][a][c] / k;
+    double g[12];
+    shape_gradients(kind, centroid, g);
+    double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    for (int a = 0; a < k; ++a) {
+        const double* x = &nodes[conn[a] * d];
+        for (int i = 0; i < d; ++i)
+            for (int j = 0; j < d; ++j) J[i][j] += x[i] * g[a * d + j];
+    }
+    if (d == 2) return J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    return J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+           J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+           J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+}
+
+int ensure_plan(tgk_routing* r);
+int narrow_connectivity(const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
+                        cudaStream_t st);
+int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
+                          double* F, double* M, cudaStream_t st, unsigned long long* d_bad);
+int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
+                        double* F, cudaStream_t st);
+
+}  // namespace tgk
+
+using namespace tgk;
+
+extern "C" {
+
+const char* tgk_last_error(void) { return last_error().c_str(); }
+int tgk_version(void) { return 1; }
+int tgk_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+void tgk_set_thread_count(int n) { g_threads.store(n < 0 ? 0 : n); }
+int tgk_thread_count(void) {
+    int n = g_threads.load();
+    if (n == 0) n = std::max(1u, std::thread::hardware_concurrency());
+    return n;
+}
+
+int tgk_default_degree(int kind, int mass) {
+    if (kind == TGK_QUAD4) return 3;
+    return mass ? 2 : 1;
+}
+
+int tgk_tables(int kind, int degree, int* Q, double* points, double* weights, double* B, double* G) {
+    int q;
+    std::vector<double> pts, w;
+    TGK_TRY(rule(kind, degree, q, pts, w));
+    const int k = element_nodes(kind), d = element_dim(kind);
+    *Q = q;
+    if (points) std::memcpy(points, pts.data(), sizeof(double) * q * d);
+    if (weights) std::memcpy(weights, w.data(), sizeof(double) * q);
+    for (int i = 0; i < q; ++i) {
+        double v[4], g[12];
+        shape_values(kind, &pts[i * d], v);
+        shape_gradients(kind, &pts[i * d], g);
+        for (int a = 0; a < k; ++a) {
+            if (B) B[i * k + a] = v[a];
+            for (int c = 0; c < d; ++c)
+                if (G) G[(i * k + a) * d + c] = g[a * d + c];
+        }
+    }
+    return TGK_OK;
+}
+
+int tgk_grid_sizes(int kind, const int64_t* div, int64_t* n_nodes, int64_t* n_elems) {
+    const int d = element_dim(kind);
+    for (int c = 0; c < d; ++c)
+        if (div[c] < 1) return set_error(TGK_ERR_INPUT, "generate_grid: divisions must be >= 1");
+    if (d == 3) {
+        *n_nodes = (div[0] + 1) * (div[1] + 1) * (div[2] + 1);
+        *n_elems = 6 * div[0] * div[1] * div[2];
+    } else {
+        *n_nodes = (div[0] + 1) * (div[1] + 1);
+        *n_elems = (kind == TGK_TRI3 ? 2 : 1) * div[0] * div[1];
+    }
+    return TGK_OK;
+}
+
+// generate_grid (mesh.cpp:96-169), same node order, Kuhn permutations and
+// orientation fix; threaded over z for large grids.
+int tgk_generate_grid(int kind, const double* ext, const int64_t* div, double* nodes, int64_t* elems) {
+    int64_t nn, ne;
+    TGK_TRY(tgk_grid_sizes(kind, div, &nn, &ne));
+    if (!nodes || !elems) return TGK_OK;
+    if (element_dim(kind) == 2) {
+        const int64_t nx = div[0], ny = div[1];
+        const double hx = ext[0] / nx, hy = ext[1] / ny;
+        int64_t p = 0;
+        for (int64_t j = 0; j <= ny; ++j)
+            for (int64_t i = 0; i <= nx; ++i) {
+                nodes[p++] = i * hx;
+                nodes[p++] = j * hy;
+            }
+        int64_t q = 0;
+        for (int64_t j = 0; j < ny; ++j)
+            for (int64_t i = 0; i < nx; ++i) {
+                const int64_t n00 = i + j * (nx + 1), n10 = (i + 1) + j * (nx + 1);
+                const int64_t n11 = (i + 1) + (j + 1) * (nx + 1), n01 = i + (j + 1) * (nx + 1);
+                if (kind == TGK_QUAD4) {
+                    elems[q++] = n00; elems[q++] = n10; elems[q++] = n11; elems[q++] = n01;
+                } else {
+                    elems[q++] = n00; elems[q++] = n10; elems[q++] = n11;
+                    elems[q++] = n00; elems[q++] = n11; elems[q++] = n01;
+                }
+            }
+        return TGK_OK;
+    }
+    const int64_t nx = div[0], ny = div[1], nz = div[2];
+    const double hx = ext[0] / nx, hy = ext[1] / ny, hz = ext[2] / nz;
+    auto node_work = [&](int64_t z0, int64_t z1) {
+        for (int64_t kz = z0; kz < z1; ++kz)
+            for (int64_t j = 0; j <= ny; ++j)
+                for (int64_t i = 0; i <= nx; ++i) {
+                    const int64_t p = 3 * (i + (nx + 1) * (j + (ny + 1) * kz));
+                    nodes[p] = i * hx;
+                    nodes[p + 1] = j * hy;
+                    nodes[p + 2] = kz * hz;
+                }
+    };
+    static const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    auto elem_work = [&](int64_t z0, int64_t z1) {
+        for (int64_t kz = z0; kz < z1; ++kz)
+            for (int64_t j = 0; j < ny; ++j)
+                for (int64_t i = 0; i < nx; ++i)
+                    for (int s6 = 0; s6 < 6; ++s6) {
+                        const int64_t e = ((kz * ny + j) * nx + i) * 6 + s6;
+                        int64_t* tet = &elems[e * 4];
+                        int64_t c[3] = {0, 0, 0};
+                        tet[0] = i + (nx + 1) * (j + (ny + 1) * kz);
+                        for (int s = 0; s < 3; ++s) {
+                            c[perms[s6][s]] = 1;
+                            tet[s + 1] = (i + c[0]) + (nx + 1) * ((j + c[1]) + (ny + 1) * (kz + c[2]));
+                        }
+                        if (centroid_det(kind, nodes, tet) < 0.0) std::swap(tet[2], tet[3]);
+                    }
+    };
+    const int nt = std::max(1, std::min<int>(tgk_thread_count(), 32));
+    auto par = [&](auto fn, int64_t n) {
+        std::vector<std::thread> pool;
+        const int64_t per = (n + nt - 1) / nt;
+        for (int t = 0; t < nt; ++t) {
+            const int64_t a = t * per, b = std::min(n, a + per);
+            if (a < b) pool.emplace_back(fn, a, b);
+        }
+        for (auto& th : pool) th.join();
+    };
+    par(node_work, nz + 1);
+    par(elem_work, nz);
+    return TGK_OK;
+}
+
+// Mesh::content_hash (mesh.cpp:79-94), FNV-1a
+uint64_t tgk_content_hash(int kind, const double* nodes, int64_t n_nodes, const int64_t* elems,
+                          int64_t n_elems) {
+    uint64_t h = 14695981039346656037ull;
+    auto mix = [&h](const void* data, size_t n) {
+        const auto* p = static_cast<const unsigned char*>(data);
+        for (size_t i = 0; i < n; ++i) {
+            h ^= p[i];
+            h *= 1099511628211ull;
+        }
+    };
+    const int kind_tag = kind, dim = element_dim(kind);
+    mix(&kind_tag, sizeof kind_tag);
+    mix(&dim, sizeof dim);
+    mix(nodes, static_cast<size_t>(n_nodes) * dim * sizeof(double));
+    mix(elems, static_cast<size_t>(n_elems) * element_nodes(kind) * sizeof(int64_t));
+    return h;
+}
+
+// topological_boundary (mesh.cpp:185-209): nodes of facets owned by one element
+int64_t tgk_topological_boundary(int kind, const int64_t* elems, int64_t n_elems, int64_t n_nodes,
+                                 int64_t* out) {
+    const int k = element_nodes(kind);
+    std::vector<std::vector<int>> facets;
+    switch (kind) {
+        case TGK_TRI3: facets = {{0, 1}, {1, 2}, {2, 0}}; break;
+        case TGK_QUAD4: facets = {{0, 1}, {1, 2}, {2, 3}, {3, 0}}; break;
+        default: facets = {{0, 1, 2}, {0, 1, 3}, {0, 2, 3}, {1, 2, 3}}; break;
+    }
+    const int fs = static_cast<int>(facets[0].size());
+    std::vector<std::array<int64_t, 3>> keys;
+    keys.reserve(static_cast<size_t>(n_elems) * facets.size());
+    for (int64_t e = 0; e < n_elems; ++e)
+        for (const auto& f : facets) {
+            std::array<int64_t, 3> key{-1, -1, -1};
+            for (int i = 0; i < fs; ++i) key[i] = elems[e * k + f[i]];
+            std::sort(key.begin(), key.begin() + fs);
+            keys.push_back(key);
+        }
+    std::sort(keys.begin(), keys.end());
+    std::vector<char> on(static_cast<size_t>(n_nodes), 0);
+    for (size_t i = 0; i < keys.size();) {
+        size_t j = i;
+        while (j < keys.size() && keys[j] == keys[i]) ++j;
+        if (j - i == 1)
+            for (int c = 0; c < fs; ++c) on[keys[i][c]] = 1;
+        i = j;
+    }
+    int64_t n = 0;
+    for (int64_t v = 0; v < n_nodes; ++v)
+        if (on[v]) {
+            if (out) out[n] = v;
+            ++n;
+        }
+    return n;
+}
+
+// Mesh::validate (mesh.cpp:56-77)
+int tgk_validate(int kind, const double* nodes, int64_t n_nodes, const int64_t* elems, int64_t n_elems) {
+    const int k = element_nodes(kind);
+    for (int64_t e = 0; e < n_elems; ++e) {
+        const int64_t* conn = &elems[e * k];
+        for (int a = 0; a < k; ++a) {
+            if (conn[a] < 0 || conn[a] >= n_nodes)
+                return set_error(TGK_ERR_INPUT, "element " + std::to_string(e) + " references node " +
+                                                    std::to_string(conn[a]) + " outside [0," +
+                                                    std::to_string(n_nodes) + ")");
+            for (int b = a + 1; b < k; ++b)
+                if (conn[a] == conn[b])
+                    return set_error(TGK_ERR_INPUT, "element " + std::to_string(e) + " repeats node " +
+                                                        std::to_string(conn[a]));
+        }
+        if (centroid_det(kind, nodes, conn) <= 0.0)
+            return set_error(TGK_ERR_INPUT, "element " + std::to_string(e) +
+                                                " has non-positive orientation (det J <= 0)");
+    }
+    return TGK_OK;
+}
+
+// ---------------------------------------------------------------- mesh handles
+int tgk_mesh_create(int kind, const double* nodes, int64_t n_nodes, const int64_t* elems,
+                    int64_t n_elems, tgk_mesh** out) {
+    if (!out) return set_error(TGK_ERR_INPUT, "tgk_mesh_create: null out");
+    if (kind != TGK_TRI3 && kind != TGK_TET4 && kind != TGK_QUAD4)
+        return set_error(TGK_ERR_INPUT, "unknown element kind");
+    if (n_nodes > INT32_MAX) return set_error(TGK_ERR_INPUT, "mesh has more than 2^31-1 nodes");
+    TGK_TRY(host_ensure_device());
+    auto* m = new tgk_mesh();
+    m->kind = kind;
+    m->d = element_dim(kind);
+    m->k = element_nodes(kind);
+    m->N = n_nodes;
+    m->E = n_elems;
+    m->owned = true;
+    if (cudaMalloc(&m->nodes, sizeof(double) * std::max<int64_t>(1, n_nodes * m->d)) != cudaSuccess ||
+        cudaMalloc(&m->conn, sizeof(int32_t) * std::max<int64_t>(1, n_elems * m->k)) != cudaSuccess) {
+        tgk_mesh_destroy(m);
+        return set_error(TGK_ERR_CUDA, "tgk_mesh_create: cudaMalloc failed");
+    }
+    int rc = tgk_mesh_upload(m, nodes, elems, nullptr);
+    if (rc != TGK_OK) {
+        tgk_mesh_destroy(m);
+        return rc;
+    }
+    *out = m;
+    return TGK_OK;
+}
+
+int tgk_mesh_create_d(int kind, const double* d_nodes, int64_t n_nodes, const int32_t* d_elems,
+                      int64_t n_elems, tgk_mesh** out) {
+    if (!out) return set_error(TGK_ERR_INPUT, "tgk_mesh_create_d: null out");
+    auto* m = new tgk_mesh();
+    m->kind = kind;
+    m->d = element_dim(kind);
+    m->k = element_nodes(kind);
+    m->N = n_nodes;
+    m->E = n_elems;
+    m->nodes = const_cast<double*>(d_nodes);
+    m->conn = const_cast<int32_t*>(d_elems);
+    m->owned = false;
+    *out = m;
+    return TGK_OK;
+}
+
+int tgk_mesh_upload(tgk_mesh* m, const double* nodes, const int64_t* elems, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (nodes)
+        HCUDA(cudaMemcpyAsync(m->nodes, nodes, sizeof(double) * m->N * m->d, cudaMemcpyHostToDevice, st));
+    if (elems) {
+        // int64 connectivity goes over PCIe as is and is narrowed (and range
+        // checked, mesh.cpp:61-64) by a device kernel
+        const int64_t n = m->E * m->k;
+        if (!m->staging) HCUDA(cudaMalloc(&m->staging, sizeof(int64_t) * std::max<int64_t>(1, n)));
+        HCUDA(cudaMemcpyAsync(m->staging, elems, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+        int64_t bad = -1;
+        TGK_TRY(narrow_connectivity(m->staging, n, m->N, m->conn, &bad, st));
+        if (bad >= 0)
+            return set_error(TGK_ERR_INPUT, "element " + std::to_string(bad / m->k) + " references node " +
+                                                std::to_string(elems[bad]) + " outside [0," +
+                                                std::to_string(m->N) + ")");
+    } else {
+        HCUDA(cudaStreamSynchronize(st));
+    }
+    return TGK_OK;
+}
+
+void tgk_mesh_destroy(tgk_mesh* m) {
+    if (!m) return;
+    if (m->owned) {
+        if (m->nodes) cudaFree(m->nodes);
+        if (m->conn) cudaFree(m->conn);
+    }
+    if (m->staging) cudaFree(m->staging);
+    delete m;
+}
+
+int tgk_mesh_info(const tgk_mesh* m, int* kind, int64_t* n_nodes, int64_t* n_elems,
+                  const double** d_nodes, const int32_t** d_elems) {
+    if (!m) return set_error(TGK_ERR_INPUT, "null mesh");
+    if (kind) *kind = m->kind;
+    if (n_nodes) *n_nodes = m->N;
+    if (n_elems) *n_elems = m->E;
+    if (d_nodes) *d_nodes = m->nodes;
+    if (d_elems) *d_elems = m->conn;
+    return TGK_OK;
+}
+
+// Restrict the fused assembly to the owned scalar rows [lo, hi) (row-owning
+// partitions); other rows of the outputs are left untouched.
+int tgk_routing_set_owned_rows(tgk_routing* r, int64_t lo, int64_t hi) {
+    tgk_routing* s = r->scalar ? r->scalar : r;
+    if (lo < 0 || hi > s->N || lo > hi) return set_error(TGK_ERR_INPUT, "owned row range out of bounds");
+    if (s->has_plan && s->own_lo == lo && s->own_hi == hi) return TGK_OK;
+    if (s->has_plan) {
+        for (void* p : {(void*)s->plan.row_off, (void*)s->plan.rows, (void*)s->plan.halo_off,
+                        (void*)s->plan.halo, (void*)s->plan.chunk_off, (void*)s->plan.chunk_rec_off,
+                        (void*)s->plan.chunk_cnt, (void*)s->plan.recs})
+            if (p) cudaFree(p);
+        s->plan = PlanDev{};
+        s->has_plan = false;
+    }
+    s->own_lo = lo;
+    s->own_hi = hi;
+    return TGK_OK;
+}
+
+// Plan statistics: blocks, halo elements (recompute factor = halo / E), records, bytes.
+int tgk_routing_plan_stats(tgk_routing* r, int64_t* n_blocks, int64_t* n_halo, int64_t* n_records,
+                           int64_t* bytes) {
+    TGK_TRY(ensure_plan(r));
+    tgk_routing* s = r->scalar ? r->scalar : r;
+    if (n_blocks) *n_blocks = s->plan.n_blocks;
+    if (n_halo) *n_halo = s->plan.n_halo;
+    if (n_records) *n_records = s->plan.n_records;
+    if (bytes) *bytes = s->plan.bytes;
+    return TGK_OK;
+}
+
+// routing cache in the reference layout (routing.cpp:178-209)
+int tgk_routing_save(const tgk_routing* r, uint64_t mesh_hash, const char* path) {
+    if (!r->mat_offsets || !r->vec_offsets)
+        return set_error(TGK_ERR_INPUT, "tgk_routing_save: routing built without TGK_ROUTING_SEGMENTS");
+    const size_t Ek = static_cast<size_t>(r->E) * r->k;
+    std::vector<int64_t> off(r->N + 1), cols(r->nnz);
+    std::vector<uint32_t> vo(r->N + 1), vs(Ek), mo(r->nnz + 1), ms(Ek * r->k);
+    TGK_TRY(tgk_routing_copy(r, off.data(), cols.data(), nullptr, vo.data(), vs.data(), mo.data(), ms.data()));
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return set_error(TGK_ERR_INPUT, std::string("cannot open routing cache for writing: ") + path);
+    const int64_t header[6] = {static_cast<int64_t>(0x74672d726f757432ull), static_cast<int64_t>(mesh_hash),
+                               r->N, r->E, r->k, r->nnz};
+    std::fwrite(header, sizeof header, 1, f);
+    std::fwrite(off.data(), 8, off.size(), f);
+    std::fwrite(cols.data(), 8, cols.size(), f);
+    std::fwrite(vo.data(), 4, vo.size(), f);
+    std::fwrite(vs.data(), 4, vs.size(), f);
+    std::fwrite(mo.data(), 4, mo.size(), f);
+    std::fwrite(ms.data(), 4, ms.size(), f);
+    std::fclose(f);
+    return TGK_OK;
+}
+
+}  // extern "C"
+
+namespace tgk {
+
+// Build (once) and upload the fused row-block plan of a scalar routing.
+int ensure_plan(tgk_routing* rr) {
+    tgk_routing* r = rr->scalar ? rr->scalar : rr;
+    if (r->has_plan) return TGK_OK;
+    const tgk_mesh* m = r->mesh;
+    const int k = m->k, d = m->d;
+    std::vector<double> nodes(m->N * d);
+    std::vector<int32_t> conn(m->E * k);
+    std::vector<int64_t> row_ptr(r->N + 1);
+    std::vector<uint32_t> vo(r->N + 1), vs(r->E * k), slot(r->E * k * k);
+    HCUDA(cudaMemcpy(nodes.data(), m->nodes, nodes.size() * 8, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(conn.data(), m->conn, conn.size() * 4, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(row_ptr.data(), r->row_ptr, row_ptr.size() * 8, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(vo.data(), r->vec_offsets, vo.size() * 4, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(vs.data(), r->vec_slots, vs.size() * 4, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(slot.data(), r->slot_of, slot.size() * 4, cudaMemcpyDeviceToHost));
+    PlanHost P;
+    const int64_t lo = r->own_hi < 0 ? 0 : r->own_lo, hi = r->own_hi < 0 ? r->N : r->own_hi;
+    TGK_TRY(build_plan(m->kind, m->N, m->E, nodes.data(), conn.data(), row_ptr.data(), vo.data(),
+                       vs.data(), slot.data(), lo, hi, P));
+    PlanDev& D = r->plan;
+    D.n_blocks = P.n_blocks;
+    D.lmax = P.lmax;
+    D.n_halo = static_cast<int64_t>(P.halo.size());
+    D.n_records = static_cast<int64_t>(P.recs.size());
+    auto up = [&D](auto*& dst, const auto& v) -> int {
+        using T = typename std::remove_reference<decltype(v)>::type::value_type;
+        const size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+        HCUDA(cudaMalloc(reinterpret_cast<void**>(&dst), bytes));
+        if (!v.empty()) HCUDA(cudaMemcpy(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+        D.bytes += static_cast<int64_t>(bytes);
+        return TGK_OK;
+    };
+    TGK_TRY(up(D.row_off, P.row_off));
+    TGK_TRY(up(D.rows, P.rows));
+    TGK_TRY(up(D.halo_off, P.halo_off));
+    TGK_TRY(up(D.halo, P.halo));
+    TGK_TRY(up(D.chunk_off, P.chunk_off));
+    TGK_TRY(up(D.chunk_rec_off, P.chunk_rec_off));
+    TGK_TRY(up(D.chunk_cnt, P.chunk_cnt));
+    TGK_TRY(up(D.recs, P.recs));
+    r->has_plan = true;
+    return TGK_OK;
+}
+
+static int check_field(const tgk_field& f, const tgk_mesh* m, const char* what) {
+    if (f.type == TGK_FIELD_CONSTANT) return TGK_OK;
+    if (f.type == TGK_FIELD_ELEMENT) {
+        if (f.n != m->E)
+            return set_error(TGK_ERR_INPUT, std::string(what) + ": per-element coefficient: expected " +
+                                                std::to_string(m->E) + " values, got " + std::to_string(f.n));
+        return TGK_OK;
+    }
+    if (f.type == TGK_FIELD_NODAL) {
+        if (f.n != m->N)
+            return set_error(TGK_ERR_INPUT, std::string(what) + ": nodal field: expected " +
+                                                std::to_string(m->N) + " values, got " + std::to_string(f.n));
+        return TGK_OK;
+    }
+    return set_error(TGK_ERR_INPUT, std::string(what) + ": unknown field type");
+}
+
+// tg::assemble (physics.cpp:10-75) on device buffers
+int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
+                 double* M, cudaStream_t st, unsigned long long* d_bad) {
+    if (!p || !m || !r) return set_error(TGK_ERR_INPUT, "tgk_assemble: null argument");
+    if (m->kind != TGK_TRI3 && m->kind != TGK_TET4)
+        return set_error(TGK_ERR_INPUT, "P1 assembly supports TRI3 and TET4 meshes only");
+    const int comps = p->kind == TGK_ELASTICITY ? m->d : 1;
+    if (r->components != comps)
+        return set_error(TGK_ERR_INPUT, "assemble: dofmap component count does not match problem kind");
+    TGK_TRY(check_field(p->diffusion, m, "diffusion"));
+    if (p->kind == TGK_ELASTICITY) {
+        TGK_TRY(check_field(p->lambda, m, "lambda"));
+        TGK_TRY(check_field(p->mu, m, "mu"));
+        if (p->n_source > 0 && p->n_source != m->d)
+            return set_error(TGK_ERR_INPUT, "elasticity body force needs one component per dimension");
+    }
+    for (int s = 0; s < std::min(p->n_source, 3); ++s) TGK_TRY(check_field(p->source[s], m, "source"));
+    if (p->with_mass && comps != 1)
+        return set_error(TGK_ERR_INPUT, "mass matrix assembly only supported for scalar fields");
+    TGK_TRY(host_ensure_device());
+    if (p->kind == TGK_ELASTICITY) return elasticity_assemble(p, m, r, K, F, st);
+    return fused_scalar_assemble(p, m, r, K, F, M, st, d_bad);
+}
+
+}  // namespace tgk
+
+extern "C" {
+
+int tgk_assemble_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, double* d_K,
+                   double* d_F, double* d_M, void* stream) {
+    return tgk::assemble_dev(p, m, const_cast<tgk_routing*>(r), d_K, d_F, d_M,
+                             static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int tgk_assemble_async_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r,
+                         double* d_K, double* d_F, double* d_M, unsigned long long* d_bad,
+                         void* stream) {
+    if (!d_bad) return set_error(TGK_ERR_INPUT, "tgk_assemble_async_d: d_bad is required");
+    if (p && p->kind == TGK_ELASTICITY)
+        return set_error(TGK_ERR_INPUT, "tgk_assemble_async_d: scalar problems only");
+    return tgk::assemble_dev(p, m, const_cast<tgk_routing*>(r), d_K, d_F, d_M,
+                             static_cast<cudaStream_t>(stream), d_bad);
+}
+
+// Host-buffer variant: field data and outputs on the host; copies inside.
+int tgk_assemble(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, double* K,
+                 double* F, double* M) {
+    if (!p || !m || !r) return set_error(TGK_ERR_INPUT, "tgk_assemble: null argument");
+    TGK_TRY(host_ensure_device());
+    tgk_problem pd = *p;
+    std::vector<void*> bufs;
+    auto cleanup = [&bufs] {
+        for (void* b : bufs) cudaFree(b);
+    };
+    auto upload = [&](tgk_field& f) -> int {
+        if (f.type == TGK_FIELD_CONSTANT || !f.data) return TGK_OK;
+        void* d = nullptr;
+        HCUDA(cudaMalloc(&d, sizeof(double) * std::max<int64_t>(1, f.n)));
+        bufs.push_back(d);
+        HCUDA(cudaMemcpy(d, f.data, sizeof(double) * f.n, cudaMemcpyHostToDevice));
+        f.data = static_cast<const double*>(d);
+        return TGK_OK;
+    };
+    int rc = TGK_OK;
+    rc = rc ? rc : upload(pd.diffusion);
+    rc = rc ? rc : upload(pd.lambda);
+    rc = rc ? rc : upload(pd.mu);
+    for (int s = 0; s < std::min(pd.n_source, 3) && !rc; ++s) rc = upload(pd.source[s]);
+    tgk_routing* rw = const_cast<tgk_routing*>(r);
+    auto scratch = [&](double*& buf, int64_t n) -> int {
+        if (buf) return TGK_OK;
+        HCUDA(cudaMalloc(&buf, sizeof(double) * std::max<int64_t>(1, n)));
+        return TGK_OK;
+    };
+    if (!rc) rc = scratch(rw->scratch_K, r->nnz);
+    if (!rc) rc = scratch(rw->scratch_F, r->N);
+    if (!rc && p->with_mass) rc = scratch(rw->scratch_M, r->nnz);
+    double *dK = rw->scratch_K, *dF = rw->scratch_F, *dM = p->with_mass ? rw->scratch_M : nullptr;
+    if (!rc) rc = tgk::assemble_dev(&pd, m, rw, dK, dF, dM, nullptr, nullptr);
+    if (!rc && K && cudaMemcpy(K, dK, sizeof(double) * r->nnz, cudaMemcpyDeviceToHost) != cudaSuccess) rc = set_error(TGK_ERR_CUDA, "copy K");
+    if (!rc && F && cudaMemcpy(F, dF, sizeof(double) * r->N, cudaMemcpyDeviceToHost) != cudaSuccess) rc = set_error(TGK_ERR_CUDA, "copy F");
+    if (!rc && M && dM && cudaMemcpy(M, dM, sizeof(double) * r->nnz, cudaMemcpyDeviceToHost) != cudaSuccess) rc = set_error(TGK_ERR_CUDA, "copy M");
+    cleanup();
+    return rc;
+}
+
+}  // extern "C"

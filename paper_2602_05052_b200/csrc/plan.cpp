@@ -1,0 +1,187 @@
+// Host construction of the fused-assembly row-block plan (see tgk_internal.hpp).
+//
+// Inputs are the scalar routing arrays (bit-identical to the reference's
+// build_routing): row_ptr (CsrPattern::offsets), the node incidence CSR
+// vec_offsets/vec_slots (ascending slot e*k+a per node, routing.cpp:47-62) and
+// the element-to-slot map slot_of.  Steps:
+//  1. order nodes along a Morton curve of their coordinates and cut the order
+//     into blocks of kRowsPerBlock nodes (compact in space => small halos);
+//  2. per block, the halo = sorted unique elements incident to its nodes;
+//  3. per block and halo chunk, one packed record per (owned row, incident
+//     element): element index within the chunk, local node a, and the CSR
+//     position (t - row_ptr[row]) of each of the element's nodes in the row.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+#include "tgk_internal.hpp"
+
+namespace tgk {
+
+namespace {
+
+uint64_t spread3(uint64_t x) {  // 21 bits -> every third bit
+    x &= 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+uint64_t spread2(uint64_t x) {  // 32 bits -> every second bit
+    x &= 0xffffffffull;
+    x = (x | x << 16) & 0x0000ffff0000ffffull;
+    x = (x | x << 8) & 0x00ff00ff00ff00ffull;
+    x = (x | x << 4) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | x << 2) & 0x3333333333333333ull;
+    x = (x | x << 1) & 0x5555555555555555ull;
+    return x;
+}
+
+}  // namespace
+
+int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
+               const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
+               const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, PlanHost& P) {
+    const int d = element_dim(kind), k = element_nodes(kind);
+    (void)E;
+    (void)conn;
+    // --- 1. Morton order of the nodes
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int64_t i = 0; i < N; ++i)
+        for (int c = 0; c < d; ++c) {
+            lo[c] = std::min(lo[c], nodes[i * d + c]);
+            hi[c] = std::max(hi[c], nodes[i * d + c]);
+        }
+    const double span = [&] {
+        double s = 0;
+        for (int c = 0; c < d; ++c) s = std::max(s, hi[c] - lo[c]);
+        return s > 0 ? s : 1.0;
+    }();
+    const double scale = (d == 3 ? double((1u << 21) - 1) : double(0xffffffffu)) / span;
+    // only the owned row range [row_lo, row_hi) gets blocks (row-owning partitions)
+    std::vector<std::pair<uint64_t, uint32_t>> key;
+    key.reserve(static_cast<size_t>(row_hi - row_lo));
+    for (int64_t i = row_lo; i < row_hi; ++i) {
+        uint64_t m = 0;
+        for (int c = 0; c < d; ++c) {
+            const uint64_t q = static_cast<uint64_t>((nodes[i * d + c] - lo[c]) * scale);
+            m |= (d == 3 ? spread3(q) : spread2(q)) << c;
+        }
+        key.push_back({m, static_cast<uint32_t>(i)});
+    }
+    const int64_t n_owned = static_cast<int64_t>(key.size());
+    std::sort(key.begin(), key.end());
+
+    int lmax = 0;
+    for (int64_t i = 0; i < N; ++i) lmax = std::max<int>(lmax, static_cast<int>(row_ptr[i + 1] - row_ptr[i]));
+    if (lmax > kMaxRowLen)
+        return set_error(TGK_ERR_INPUT, "fused plan: CSR row longer than " +
+                                            std::to_string(kMaxRowLen) + " entries");
+    P.lmax = lmax;
+    const int64_t nb = (n_owned + kRowsPerBlock - 1) / kRowsPerBlock;
+    P.n_blocks = nb;
+    P.row_off.resize(nb + 1);
+    P.rows.resize(n_owned);
+    for (int64_t b = 0; b <= nb; ++b) P.row_off[b] = std::min<int64_t>(b * kRowsPerBlock, n_owned);
+    for (int64_t b = 0; b < nb; ++b) {
+        for (int64_t i = P.row_off[b]; i < P.row_off[b + 1]; ++i) P.rows[i] = key[i].second;
+        std::sort(P.rows.begin() + P.row_off[b], P.rows.begin() + P.row_off[b + 1]);
+    }
+    key.clear();
+    key.shrink_to_fit();
+
+    // --- 2/3. halos and records, blocks in parallel
+    struct BlockOut {
+        std::vector<uint32_t> halo;
+        std::vector<uint8_t> cnt;   // nch x kRowsPerBlock
+        std::vector<uint32_t> recs;
+        std::vector<int64_t> chunk_sizes;
+    };
+    std::vector<BlockOut> out(nb);
+    auto work = [&](int64_t b_begin, int64_t b_end) {
+        std::vector<uint32_t> tmp;
+        for (int64_t b = b_begin; b < b_end; ++b) {
+            BlockOut& o = out[b];
+            const int64_t rs = P.row_off[b], re = P.row_off[b + 1];
+            tmp.clear();
+            for (int64_t i = rs; i < re; ++i) {
+                const uint32_t row = P.rows[i];
+                for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s)
+                    tmp.push_back(vec_slots[s] / k);
+            }
+            std::sort(tmp.begin(), tmp.end());
+            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+            o.halo = tmp;
+            const int64_t nh = static_cast<int64_t>(o.halo.size());
+            const int64_t nch = (nh + kChunk - 1) / kChunk;
+            o.cnt.assign(nch * kRowsPerBlock, 0);
+            // records grouped chunk-major, then row, ascending element within a row
+            std::vector<std::vector<uint32_t>> per_chunk(nch);
+            for (int64_t i = rs; i < re; ++i) {
+                const int lr = static_cast<int>(i - rs);
+                const uint32_t row = P.rows[i];
+                const int64_t rp = row_ptr[row];
+                int64_t hpos = 0;
+                for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s) {
+                    const uint32_t slot = vec_slots[s];
+                    const uint32_t e = slot / k;
+                    const int a = static_cast<int>(slot % k);
+                    while (o.halo[hpos] != e) ++hpos;  // both ascending
+                    const int64_t ch = hpos / kChunk;
+                    int pos[4] = {0, 0, 0, 0};
+                    for (int bb = 0; bb < k; ++bb)
+                        pos[bb] = static_cast<int>(slot_of[static_cast<int64_t>(slot) * k + bb] - rp);
+                    per_chunk[ch].push_back(pack_rec(static_cast<int>(hpos % kChunk), a, pos, k));
+                    ++o.cnt[ch * kRowsPerBlock + lr];
+                }
+            }
+            o.chunk_sizes.resize(nch);
+            for (int64_t ch = 0; ch < nch; ++ch) {
+                // per_chunk[ch] was appended row by row in ascending row order: already grouped
+                o.chunk_sizes[ch] = static_cast<int64_t>(per_chunk[ch].size());
+                o.recs.insert(o.recs.end(), per_chunk[ch].begin(), per_chunk[ch].end());
+            }
+        }
+    };
+    const int nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    {
+        std::vector<std::thread> pool;
+        const int64_t per = (nb + nthreads - 1) / nthreads;
+        for (int t = 0; t < nthreads; ++t) {
+            const int64_t b0 = t * per, b1 = std::min(nb, b0 + per);
+            if (b0 < b1) pool.emplace_back(work, b0, b1);
+        }
+        for (auto& th : pool) th.join();
+    }
+    // --- concatenate
+    P.halo_off.assign(nb + 1, 0);
+    P.chunk_off.assign(nb + 1, 0);
+    for (int64_t b = 0; b < nb; ++b) {
+        P.halo_off[b + 1] = P.halo_off[b] + static_cast<int64_t>(out[b].halo.size());
+        P.chunk_off[b + 1] = P.chunk_off[b] + static_cast<int64_t>(out[b].chunk_sizes.size());
+    }
+    const int64_t total_chunks = P.chunk_off[nb];
+    P.halo.resize(P.halo_off[nb]);
+    P.chunk_cnt.resize(total_chunks * kRowsPerBlock);
+    P.chunk_rec_off.assign(total_chunks + 1, 0);
+    int64_t nrec = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        std::copy(out[b].halo.begin(), out[b].halo.end(), P.halo.begin() + P.halo_off[b]);
+        std::copy(out[b].cnt.begin(), out[b].cnt.end(), P.chunk_cnt.begin() + P.chunk_off[b] * kRowsPerBlock);
+        for (size_t ch = 0; ch < out[b].chunk_sizes.size(); ++ch) {
+            P.chunk_rec_off[P.chunk_off[b] + ch] = nrec;
+            nrec += out[b].chunk_sizes[ch];
+        }
+    }
+    P.chunk_rec_off[total_chunks] = nrec;
+    P.recs.resize(nrec);
+    for (int64_t b = 0; b < nb; ++b)
+        std::copy(out[b].recs.begin(), out[b].recs.end(), P.recs.begin() + P.chunk_rec_off[P.chunk_off[b]]);
+    return TGK_OK;
+}
+
+}  // namespace tgk

@@ -1,0 +1,460 @@
+// Materialised Stage I (Map) and Stage II (Reduce) kernels: the drop-in for
+// the reference's public batch.hpp / routing.hpp functions that hand whole
+// E x ... arrays across the API (batch.cpp:56-312, routing.cpp:87-125).  The
+// fused path (fused.cu) never materialises these; they exist for API parity
+// and for the parity tests of each stage.
+//
+// Arithmetic follows the reference literally (FMA disabled), one thread per
+// element (Map) or per output (Reduce, ascending-slot left fold).
+#include <climits>
+
+#include "cuda_util.cuh"
+#include "element.cuh"
+#include "tgk_internal.hpp"
+
+namespace tgk {
+
+__device__ __forceinline__ void flag_bad(unsigned long long* bad, int64_t e) {
+    atomicMin(bad, static_cast<unsigned long long>(e));
+}
+
+// Host-side bad-element check after a kernel (batch.cpp:124-126 message).
+int check_bad(unsigned long long* d_bad, cudaStream_t st) {
+    unsigned long long h = ULLONG_MAX;
+    CUDA_TRY(cudaMemcpyAsync(&h, d_bad, sizeof h, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (h != ULLONG_MAX)
+        return set_error(TGK_ERR_INPUT, "element " + std::to_string(h) +
+                                            " has non-positive Jacobian determinant");
+    return TGK_OK;
+}
+
+namespace {
+
+template <int KIND>
+__device__ __forceinline__ void load_element(const double* nodes, const int32_t* conn, int64_t e,
+                                             double (&X)[P1<KIND>::k][P1<KIND>::d]) {
+    constexpr int k = P1<KIND>::k, d = P1<KIND>::d;
+#pragma unroll
+    for (int a = 0; a < k; ++a) {
+        const int64_t n = conn[e * k + a];
+#pragma unroll
+        for (int c = 0; c < d; ++c) X[a][c] = nodes[n * d + c];
+    }
+}
+
+// batch_geometry + push_forward, literal reference sequence (batch.cpp:76-152)
+template <int KIND, int DEG>
+__global__ void k_geometry(const double* nodes, const int32_t* conn, int64_t E, double* jac,
+                           double* det_out, double* jinv, double* qpts, double* grads,
+                           unsigned long long* bad) {
+    constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    double X[k][d];
+    load_element<KIND>(nodes, conn, e, X);
+    // reference gradients Ghat (reference.cpp:59-71)
+    auto ghat = [](int a, int j) -> double { return a == 0 ? -1.0 : (j == a - 1 ? 1.0 : 0.0); };
+    double J[d * d];
+#pragma unroll
+    for (int i = 0; i < d * d; ++i) J[i] = 0.0;
+#pragma unroll
+    for (int a = 0; a < k; ++a)
+#pragma unroll
+        for (int i = 0; i < d; ++i)
+#pragma unroll
+            for (int j = 0; j < d; ++j) J[i * d + j] += X[a][i] * ghat(a, j);
+    double det;
+    double T[d * d];
+    if constexpr (d == 2) {
+        det = J[0] * J[3] - J[1] * J[2];
+        T[0] = J[3] / det; T[1] = -J[2] / det; T[2] = -J[1] / det; T[3] = J[0] / det;
+    } else {
+        det = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
+              J[2] * (J[3] * J[7] - J[4] * J[6]);
+        const double c00 = J[4] * J[8] - J[5] * J[7];
+        const double c01 = J[5] * J[6] - J[3] * J[8];
+        const double c02 = J[3] * J[7] - J[4] * J[6];
+        const double c10 = J[2] * J[7] - J[1] * J[8];
+        const double c11 = J[0] * J[8] - J[2] * J[6];
+        const double c12 = J[1] * J[6] - J[0] * J[7];
+        const double c20 = J[1] * J[5] - J[2] * J[4];
+        const double c21 = J[2] * J[3] - J[0] * J[5];
+        const double c22 = J[0] * J[4] - J[1] * J[3];
+        T[0] = c00 / det; T[1] = c01 / det; T[2] = c02 / det;
+        T[3] = c10 / det; T[4] = c11 / det; T[5] = c12 / det;
+        T[6] = c20 / det; T[7] = c21 / det; T[8] = c22 / det;
+    }
+    if (det <= 0.0) flag_bad(bad, e);
+    double G[k * d];
+#pragma unroll
+    for (int a = 0; a < k; ++a)
+#pragma unroll
+        for (int i = 0; i < d; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < d; ++j) s += T[i * d + j] * ghat(a, j);
+            G[a * d + i] = s;
+        }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int64_t eq = e * Q + q;
+        if (jac)
+            for (int i = 0; i < d * d; ++i) jac[eq * d * d + i] = J[i];
+        if (det_out) det_out[eq] = det;
+        if (jinv)
+            for (int i = 0; i < d * d; ++i) jinv[eq * d * d + i] = T[i];
+        if (qpts)
+#pragma unroll
+            for (int c = 0; c < d; ++c) {
+                double x = 0.0;
+#pragma unroll
+                for (int a = 0; a < k; ++a) x += basis<KIND, DEG>(q, a) * X[a][c];
+                qpts[eq * d + c] = x;
+            }
+        if (grads)
+            for (int i = 0; i < k * d; ++i) grads[eq * k * d + i] = G[i];
+    }
+}
+
+// local kernels (batch.cpp:156-312); `what` as tgk_local_* entry points
+enum { L_DIFF = 0, L_ELAST = 1, L_MASS = 2, L_LOAD = 3, L_LOADV = 4 };
+
+template <int KIND, int DEG, int WHAT>
+__global__ void k_local(const double* nodes, const int32_t* conn, int64_t E, const double* c1,
+                        const double* c2, double* out, unsigned long long* bad) {
+    constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q;
+    using R = Rule<KIND, DEG>;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    double X[k][d];
+    load_element<KIND>(nodes, conn, e, X);
+    double det;
+    double G[k][d];
+    if (!simplex_geometry<KIND>(X, det, G)) {
+        flag_bad(bad, e);
+        return;
+    }
+    if constexpr (WHAT == L_DIFF) {
+        double Ke[k * k];
+#pragma unroll
+        for (int i = 0; i < k * k; ++i) Ke[i] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const double scale = R::w(q) * det * c1[e * Q + q];
+#pragma unroll
+            for (int a = 0; a < k; ++a)
+#pragma unroll
+                for (int b = 0; b < k; ++b) Ke[a * k + b] += scale * gdot<KIND>(G, a, b);
+        }
+        for (int i = 0; i < k * k; ++i) out[e * k * k + i] = Ke[i];
+    } else if constexpr (WHAT == L_MASS) {
+        double Me[k * k];
+#pragma unroll
+        for (int i = 0; i < k * k; ++i) Me[i] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const double scale = R::w(q) * det * c1[e * Q + q];
+#pragma unroll
+            for (int a = 0; a < k; ++a)
+#pragma unroll
+                for (int b = 0; b < k; ++b)
+                    Me[a * k + b] += scale * basis<KIND, DEG>(q, a) * basis<KIND, DEG>(q, b);
+        }
+        for (int i = 0; i < k * k; ++i) out[e * k * k + i] = Me[i];
+    } else if constexpr (WHAT == L_LOAD) {
+        double Fe[k];
+#pragma unroll
+        for (int a = 0; a < k; ++a) Fe[a] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const double scale = R::w(q) * det * c1[e * Q + q];
+#pragma unroll
+            for (int a = 0; a < k; ++a) Fe[a] += scale * basis<KIND, DEG>(q, a);
+        }
+        for (int a = 0; a < k; ++a) out[e * k + a] = Fe[a];
+    } else if constexpr (WHAT == L_LOADV) {
+        double Fe[k * d];
+#pragma unroll
+        for (int a = 0; a < k * d; ++a) Fe[a] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const double scale = R::w(q) * det;
+#pragma unroll
+            for (int a = 0; a < k; ++a)
+#pragma unroll
+                for (int c = 0; c < d; ++c)
+                    Fe[a * d + c] += scale * basis<KIND, DEG>(q, a) * c1[(e * Q + q) * d + c];
+        }
+        for (int a = 0; a < k * d; ++a) out[e * k * d + a] = Fe[a];
+    } else {  // L_ELAST: batch.cpp:198-246, literal (B and DB with their zeros)
+        constexpr int kk = k * d, ns = d == 2 ? 3 : 6;
+        double* Ke = out + e * kk * kk;
+        for (int i = 0; i < kk * kk; ++i) Ke[i] = 0.0;
+        for (int q = 0; q < Q; ++q) {
+            double B[ns * kk], DB[ns * kk];
+            for (int i = 0; i < ns * kk; ++i) B[i] = 0.0;
+            if constexpr (d == 2) {
+                for (int a = 0; a < k; ++a) {
+                    const double gx = G[a][0], gy = G[a][1];
+                    B[0 * kk + a * 2 + 0] = gx;
+                    B[1 * kk + a * 2 + 1] = gy;
+                    B[2 * kk + a * 2 + 0] = gy;
+                    B[2 * kk + a * 2 + 1] = gx;
+                }
+            } else {
+                for (int a = 0; a < k; ++a) {
+                    const double gx = G[a][0], gy = G[a][1], gz = G[a][2];
+                    B[0 * kk + a * 3 + 0] = gx;
+                    B[1 * kk + a * 3 + 1] = gy;
+                    B[2 * kk + a * 3 + 2] = gz;
+                    B[3 * kk + a * 3 + 0] = gy;
+                    B[3 * kk + a * 3 + 1] = gx;
+                    B[4 * kk + a * 3 + 1] = gz;
+                    B[4 * kk + a * 3 + 2] = gy;
+                    B[5 * kk + a * 3 + 0] = gz;
+                    B[5 * kk + a * 3 + 2] = gx;
+                }
+            }
+            const double lam = c1[e * Q + q], mu = c2[e * Q + q];
+            for (int col = 0; col < kk; ++col) {
+                double tr = 0.0;
+                for (int i = 0; i < d; ++i) tr += B[i * kk + col];
+                for (int i = 0; i < d; ++i) DB[i * kk + col] = lam * tr + 2.0 * mu * B[i * kk + col];
+                for (int i = d; i < ns; ++i) DB[i * kk + col] = mu * B[i * kk + col];
+            }
+            const double scale = R::w(q) * det;
+            for (int a = 0; a < kk; ++a)
+                for (int b = 0; b < kk; ++b) {
+                    double s = 0.0;
+                    for (int i = 0; i < ns; ++i) s += B[i * kk + a] * DB[i * kk + b];
+                    Ke[a * kk + b] += scale * s;
+                }
+        }
+    }
+}
+
+// CoefficientField::evaluate (coefficient.cpp:34-55) -> E x Q
+template <int KIND, int DEG>
+__global__ void k_evaluate(const int32_t* conn, int64_t E, int type, double value,
+                           const double* data, double* out) {
+    constexpr int k = P1<KIND>::k, Q = Rule<KIND, DEG>::Q;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= E) return;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        double v;
+        if (type == TGK_FIELD_CONSTANT) {
+            v = value;
+        } else if (type == TGK_FIELD_ELEMENT) {
+            v = data[e];
+        } else {  // interpolate_nodal (batch.cpp:321-330)
+            v = 0.0;
+#pragma unroll
+            for (int a = 0; a < k; ++a) v += basis<KIND, DEG>(q, a) * data[conn[e * k + a]];
+        }
+        out[e * Q + q] = v;
+    }
+}
+
+// reduce_matrix / reduce_vector (routing.cpp:92-99, 117-124)
+__global__ void k_segment_reduce(const uint32_t* off, const uint32_t* slots, int64_t n,
+                                 const double* local, double* out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double s = 0.0;
+    for (uint32_t u = off[t]; u < off[t + 1]; ++u) s += local[slots[u]];
+    out[t] = s;
+}
+
+template <int KIND, template <int, int> class Launch, class... Args>
+int dispatch_degree(int degree, Args... args) {
+    switch (degree) {
+        case 1: return Launch<KIND, 1>::run(args...);
+        case 2: return Launch<KIND, 2>::run(args...);
+        case 3: return Launch<KIND, 3>::run(args...);
+        case 4: return Launch<KIND, 4>::run(args...);
+    }
+    return set_error(TGK_ERR_INPUT, "quadrature degree " + std::to_string(degree) +
+                                        " unsupported; supported degrees: 1,2,3,4");
+}
+
+template <int KIND, int DEG>
+struct GeomLaunch {
+    static int run(const tgk_mesh* m, double* jac, double* det, double* jinv, double* qp,
+                   double* gr, unsigned long long* bad, cudaStream_t st) {
+        k_geometry<KIND, DEG><<<grid_for(m->E, 128), 128, 0, st>>>(m->nodes, m->conn, m->E, jac, det,
+                                                                  jinv, qp, gr, bad);
+        KERNEL_CHECK("geometry");
+        return TGK_OK;
+    }
+};
+
+template <int WHAT>
+struct LocalOf {
+    template <int KIND, int DEG>
+    struct L {
+        static int run(const tgk_mesh* m, const double* c1, const double* c2, double* out,
+                       unsigned long long* bad, cudaStream_t st) {
+            const int block = WHAT == L_ELAST ? 64 : 128;
+            k_local<KIND, DEG, WHAT><<<grid_for(m->E, block), block, 0, st>>>(m->nodes, m->conn, m->E,
+                                                                             c1, c2, out, bad);
+            KERNEL_CHECK("local");
+            return TGK_OK;
+        }
+    };
+};
+
+template <int KIND, int DEG>
+struct EvalLaunch {
+    static int run(const tgk_mesh* m, const tgk_field* f, double* out, cudaStream_t st) {
+        k_evaluate<KIND, DEG><<<grid_for(m->E, 256), 256, 0, st>>>(m->conn, m->E, f->type, f->value,
+                                                                  f->data, out);
+        KERNEL_CHECK("evaluate");
+        return TGK_OK;
+    }
+};
+
+int check_mesh(const tgk_mesh* m) {
+    if (!m) return set_error(TGK_ERR_INPUT, "null mesh");
+    if (m->kind != TGK_TRI3 && m->kind != TGK_TET4)
+        return set_error(TGK_ERR_INPUT, "P1 kernels support TRI3 and TET4 meshes only");
+    return ensure_device();
+}
+
+template <int WHAT>
+int run_local(const tgk_mesh* m, int degree, const double* c1, const double* c2, double* out,
+              void* stream) {
+    TGK_TRY(check_mesh(m));
+    cudaStream_t st = as_stream(stream);
+    DevBuf<unsigned long long> bad;
+    TGK_TRY(bad.alloc(1));
+    CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    if (m->kind == TGK_TET4)
+        TGK_TRY((dispatch_degree<TGK_TET4, LocalOf<WHAT>::template L>(degree, m, c1, c2, out, bad.p, st)));
+    else
+        TGK_TRY((dispatch_degree<TGK_TRI3, LocalOf<WHAT>::template L>(degree, m, c1, c2, out, bad.p, st)));
+    return check_bad(bad.p, st);
+}
+
+__global__ void k_narrow(const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst,
+                         unsigned long long* bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = src[i];
+        if (v < 0 || v >= n_nodes) atomicMin(bad, static_cast<unsigned long long>(i));
+        dst[i] = static_cast<int32_t>(v);
+    }
+}
+
+}  // namespace
+
+int narrow_connectivity(const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
+                        cudaStream_t st) {
+    DevBuf<unsigned long long> flag;
+    TGK_TRY(flag.alloc(1));
+    CUDA_TRY(cudaMemsetAsync(flag.p, 0xff, sizeof(unsigned long long), st));
+    k_narrow<<<std::min<unsigned>(grid_for(n, 256), 148 * 16), 256, 0, st>>>(src, n, n_nodes, dst, flag.p);
+    KERNEL_CHECK("narrow_connectivity");
+    unsigned long long h = ULLONG_MAX;
+    CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    *bad = h == ULLONG_MAX ? -1 : static_cast<int64_t>(h);
+    return TGK_OK;
+}
+
+}  // namespace tgk
+
+extern "C" {
+
+int tgk_geometry_d(const tgk_mesh* m, int degree, double* d_jac, double* d_det,
+                   double* d_jac_invT, double* d_qpts, double* d_grads, void* stream) {
+    using namespace tgk;
+    TGK_TRY(check_mesh(m));
+    cudaStream_t st = as_stream(stream);
+    DevBuf<unsigned long long> bad;
+    TGK_TRY(bad.alloc(1));
+    CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    if (m->kind == TGK_TET4)
+        TGK_TRY((dispatch_degree<TGK_TET4, GeomLaunch>(degree, m, d_jac, d_det, d_jac_invT, d_qpts,
+                                                       d_grads, bad.p, st)));
+    else
+        TGK_TRY((dispatch_degree<TGK_TRI3, GeomLaunch>(degree, m, d_jac, d_det, d_jac_invT, d_qpts,
+                                                       d_grads, bad.p, st)));
+    return check_bad(bad.p, st);
+}
+
+int tgk_local_stiffness_diffusion_d(const tgk_mesh* m, int degree, const double* c, double* out,
+                                    void* stream) {
+    return tgk::run_local<tgk::L_DIFF>(m, degree, c, nullptr, out, stream);
+}
+
+int tgk_local_stiffness_elasticity_d(const tgk_mesh* m, int degree, const double* lam,
+                                     const double* mu, double* out, void* stream) {
+    using namespace tgk;
+    TGK_TRY(check_mesh(m));
+    // batch.cpp:194-195: mu <= 0 anywhere is an input error
+    const int64_t n = m->E * (m->kind == TGK_TET4 ? (degree == 1 ? 1 : degree == 2 ? 4 : degree == 3 ? 5 : 11)
+                                                   : (degree == 1 ? 1 : degree == 2 ? 3 : degree == 3 ? 4 : 6));
+    std::vector<double> h(n);
+    CUDA_TRY(cudaMemcpy(h.data(), mu, n * sizeof(double), cudaMemcpyDeviceToHost));
+    for (double v : h)
+        if (v <= 0.0) return set_error(TGK_ERR_INPUT, "elasticity requires mu > 0");
+    return run_local<L_ELAST>(m, degree, lam, mu, out, stream);
+}
+
+int tgk_local_mass_d(const tgk_mesh* m, int degree, const double* c, double* out, void* stream) {
+    return tgk::run_local<tgk::L_MASS>(m, degree, c, nullptr, out, stream);
+}
+
+int tgk_local_load_d(const tgk_mesh* m, int degree, const double* src, double* out, void* stream) {
+    return tgk::run_local<tgk::L_LOAD>(m, degree, src, nullptr, out, stream);
+}
+
+int tgk_local_load_vector_d(const tgk_mesh* m, int degree, const double* src, double* out,
+                            void* stream) {
+    return tgk::run_local<tgk::L_LOADV>(m, degree, src, nullptr, out, stream);
+}
+
+int tgk_evaluate_field_d(const tgk_mesh* m, int degree, const tgk_field* f, double* out,
+                         void* stream) {
+    using namespace tgk;
+    TGK_TRY(check_mesh(m));
+    if (!f) return set_error(TGK_ERR_INPUT, "null field");
+    if (f->type == TGK_FIELD_ELEMENT && f->n != m->E)
+        return set_error(TGK_ERR_INPUT, "per-element coefficient: expected " + std::to_string(m->E) +
+                                            " values, got " + std::to_string(f->n));
+    if (f->type == TGK_FIELD_NODAL && f->n != m->N)
+        return set_error(TGK_ERR_INPUT, "nodal field: expected " + std::to_string(m->N) +
+                                            " values, got " + std::to_string(f->n));
+    cudaStream_t st = as_stream(stream);
+    if (m->kind == TGK_TET4)
+        TGK_TRY((dispatch_degree<TGK_TET4, EvalLaunch>(degree, m, f, out, st)));
+    else
+        TGK_TRY((dispatch_degree<TGK_TRI3, EvalLaunch>(degree, m, f, out, st)));
+    return TGK_OK;
+}
+
+int tgk_reduce_matrix_d(const tgk_routing* r, const double* local, double* values, void* stream) {
+    using namespace tgk;
+    if (!r || !r->mat_offsets)
+        return set_error(TGK_ERR_INPUT, "reduce_matrix: routing built without TGK_ROUTING_SEGMENTS");
+    TGK_TRY(ensure_device());
+    k_segment_reduce<<<grid_for(r->nnz, 256), 256, 0, as_stream(stream)>>>(
+        r->mat_offsets, r->mat_slots, r->nnz, local, values);
+    KERNEL_CHECK("reduce_matrix");
+    return TGK_OK;
+}
+
+int tgk_reduce_vector_d(const tgk_routing* r, const double* local, double* F, void* stream) {
+    using namespace tgk;
+    if (!r || !r->vec_offsets)
+        return set_error(TGK_ERR_INPUT, "reduce_vector: routing built without TGK_ROUTING_SEGMENTS");
+    TGK_TRY(ensure_device());
+    k_segment_reduce<<<grid_for(r->N, 256), 256, 0, as_stream(stream)>>>(r->vec_offsets, r->vec_slots,
+                                                                         r->N, local, F);
+    KERNEL_CHECK("reduce_vector");
+    return TGK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,321 @@
+"""Device-resident API over libtgk.so, with torch tensors as the buffers.
+
+PyTorch supplies CUDA memory and streams only; every computation runs in the
+hand-written sm_100a kernels of libtgk.so.  Names follow the reference's C++
+API (tg::assemble, build_routing, reduce_matrix, gradient_products, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._native import check, lib
+
+_DEV = torch.device("cuda")
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _cuda_f64(x, n=None):
+    t = torch.as_tensor(x, dtype=torch.float64, device=_DEV).contiguous()
+    if n is not None and t.numel() != n:
+        raise N.InputError(f"expected {n} values, got {t.numel()}")
+    return t
+
+
+def field(spec, keep):
+    """float | ('element', values) | ('nodal', values) -> (Field, keepalive list)."""
+    if spec is None:
+        return N.Field(N.FIELD_CONSTANT, 1.0, None, 0)
+    if isinstance(spec, (int, float)):
+        return N.Field(N.FIELD_CONSTANT, float(spec), None, 0)
+    kind, vals = spec
+    t = _cuda_f64(vals).reshape(-1)
+    keep.append(t)
+    ftype = {"element": N.FIELD_ELEMENT, "nodal": N.FIELD_NODAL}[kind]
+    return N.Field(ftype, 0.0, C.c_void_p(t.data_ptr()), t.numel())
+
+
+class DeviceMesh:
+    """A tg::Mesh resident on the GPU (fp64 node-major coordinates, int32 connectivity)."""
+
+    def __init__(self, kind, nodes, elements):
+        self.kind = kind.lower() if isinstance(kind, str) else N.KIND_NAMES[kind].lower()
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+        elements = np.ascontiguousarray(elements, dtype=np.int64)
+        self.N, self.dim = nodes.shape
+        self.E, self.k = elements.shape
+        h = C.c_void_p()
+        check(lib().tgk_mesh_create(N.KINDS[self.kind], nodes.ctypes.data, self.N,
+                                    elements.ctypes.data, self.E, C.byref(h)))
+        self._h = h
+        self._keep = None
+
+    @classmethod
+    def from_device(cls, kind, nodes: torch.Tensor, conn: torch.Tensor):
+        """Wrap device tensors (float64 N x d, int32 E x k) without copying."""
+        self = cls.__new__(cls)
+        self.kind = kind
+        nodes = nodes.contiguous()
+        conn = conn.to(torch.int32).contiguous()
+        self.N, self.dim = nodes.shape
+        self.E, self.k = conn.shape
+        h = C.c_void_p()
+        check(lib().tgk_mesh_create_d(N.KINDS[kind], nodes.data_ptr(), self.N, conn.data_ptr(),
+                                      self.E, C.byref(h)))
+        self._h = h
+        self._keep = (nodes, conn)
+        return self
+
+    def upload(self, nodes=None, elements=None, stream=None):
+        """Host -> device copy of new coordinates / connectivity (same sizes)."""
+        np_n = None if nodes is None else np.ascontiguousarray(nodes, dtype=np.float64)
+        np_e = None if elements is None else np.ascontiguousarray(elements, dtype=np.int64)
+        check(lib().tgk_mesh_upload(self._h, None if np_n is None else np_n.ctypes.data,
+                                    None if np_e is None else np_e.ctypes.data, _stream(stream)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().tgk_mesh_destroy(h)
+            self._h = None
+
+
+class Routing:
+    """build_dofmap + build_routing on the GPU (routing.cpp:12-85), bit-identical."""
+
+    def __init__(self, mesh: DeviceMesh, components=1, segments=False, stream=None):
+        self.mesh = mesh
+        h = C.c_void_p()
+        check(lib().tgk_routing_build(mesh._h, int(components), N.ROUTING_SEGMENTS if segments else 0,
+                                      _stream(stream), C.byref(h)))
+        self._h = h
+        v = N.RoutingView()
+        check(lib().tgk_routing_get_view(h, C.byref(v)))
+        self.N, self.E, self.nnz, self.k = v.N, v.E, v.nnz, v.k
+        self.components = v.components
+        self.has_segments = bool(v.mat_offsets)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().tgk_routing_destroy(h)
+            self._h = None
+
+    def host_arrays(self, slot_of=True, segments=None):
+        """Reference-layout arrays copied to host numpy (RoutingMatrices + CsrPattern)."""
+        segments = self.has_segments if segments is None else segments
+        Ek = self.E * self.k
+        out = dict(offsets=np.zeros(self.N + 1, np.int64), cols=np.zeros(self.nnz, np.int64))
+        want_slot = slot_of and self.components == 1
+        if want_slot:
+            out["slot_of"] = np.zeros(Ek * self.k, np.uint32)
+        if segments:
+            out.update(vec_offsets=np.zeros(self.N + 1, np.uint32), vec_slots=np.zeros(Ek, np.uint32),
+                       mat_offsets=np.zeros(self.nnz + 1, np.uint32),
+                       mat_slots=np.zeros(Ek * self.k, np.uint32))
+        g = lambda k: out[k].ctypes.data if k in out else None  # noqa: E731
+        check(lib().tgk_routing_copy(self._h, g("offsets"), g("cols"), g("slot_of"), g("vec_offsets"),
+                                     g("vec_slots"), g("mat_offsets"), g("mat_slots")))
+        return out
+
+    def save(self, mesh_hash, path):
+        check(lib().tgk_routing_save(self._h, C.c_uint64(mesh_hash), str(path).encode()))
+
+
+def make_problem(kind="poisson", diffusion=1.0, lam=1.0, mu=1.0, plane_stress=False, sources=(),
+                 with_mass=False, mode="exact", keep=None):
+    keep = [] if keep is None else keep
+    p = N.Problem()
+    p.kind = {"poisson": N.POISSON, "elasticity": N.ELASTICITY, "mass": N.MASS}[kind]
+    p.diffusion = field(diffusion, keep)
+    p.lam = field(lam, keep)
+    p.mu = field(mu, keep)
+    p.plane_stress = int(bool(plane_stress))
+    p.n_source = len(sources)
+    for i, s in enumerate(sources):
+        p.source[i] = field(s, keep)
+    p.with_mass = int(bool(with_mass))
+    p.mode = {"exact": N.MODE_EXACT, "fast": N.MODE_FAST}[mode]
+    return p, keep
+
+
+def assemble(mesh: DeviceMesh, routing: Routing, kind="poisson", diffusion=1.0, lam=1.0, mu=1.0,
+             plane_stress=False, sources=(), with_mass=False, mode="exact", out=None, stream=None):
+    """tg::assemble (physics.cpp:10-75) on the GPU.  Returns (K values, F, M values | None)."""
+    p, keep = make_problem(kind, diffusion, lam, mu, plane_stress, sources, with_mass, mode)
+    if out is None:
+        K = torch.empty(routing.nnz, dtype=torch.float64, device=_DEV)
+        F = torch.empty(routing.N, dtype=torch.float64, device=_DEV)
+        M = torch.empty(routing.nnz, dtype=torch.float64, device=_DEV) if with_mass else None
+    else:
+        K, F, M = out
+    check(lib().tgk_assemble_d(C.byref(p), mesh._h, routing._h, _ptr(K), _ptr(F), _ptr(M),
+                               _stream(stream)))
+    del keep
+    return K, F, M
+
+
+def assemble_host(mesh: DeviceMesh, routing: Routing, kind="poisson", diffusion=1.0, lam=1.0,
+                  mu=1.0, plane_stress=False, sources=(), with_mass=False, mode="exact", out=None):
+    """Same as assemble() through the host-buffer C-ABI entry (copies inside the call)."""
+    keep = []
+
+    def hfield(spec):
+        if spec is None or isinstance(spec, (int, float)):
+            return N.Field(N.FIELD_CONSTANT, 1.0 if spec is None else float(spec), None, 0)
+        kind_, vals = spec
+        a = np.ascontiguousarray(vals, dtype=np.float64).reshape(-1)
+        keep.append(a)
+        return N.Field({"element": N.FIELD_ELEMENT, "nodal": N.FIELD_NODAL}[kind_], 0.0,
+                       a.ctypes.data, a.size)
+
+    p = N.Problem()
+    p.kind = {"poisson": N.POISSON, "elasticity": N.ELASTICITY, "mass": N.MASS}[kind]
+    p.diffusion, p.lam, p.mu = hfield(diffusion), hfield(lam), hfield(mu)
+    p.plane_stress = int(bool(plane_stress))
+    p.n_source = len(sources)
+    for i, s in enumerate(sources):
+        p.source[i] = hfield(s)
+    p.with_mass = int(bool(with_mass))
+    p.mode = {"exact": N.MODE_EXACT, "fast": N.MODE_FAST}[mode]
+    if out is None:
+        K = np.empty(routing.nnz)
+        F = np.empty(routing.N)
+        M = np.empty(routing.nnz) if with_mass else None
+    else:
+        K, F, M = out
+    check(lib().tgk_assemble(C.byref(p), mesh._h, routing._h, K.ctypes.data, F.ctypes.data,
+                             None if M is None else M.ctypes.data))
+    return K, F, M
+
+
+# ---------------------------------------------------------------- Stage I / II, materialised
+def quadrature_count(kind, degree):
+    Q = C.c_int()
+    check(lib().tgk_tables(N.KINDS[kind], degree, C.byref(Q), None, None, None, None))
+    return Q.value
+
+
+def geometry(mesh: DeviceMesh, degree, stream=None):
+    """batch_geometry + push_forward (batch.cpp:56-154): dict of E x Q x ... tensors."""
+    Q = quadrature_count(mesh.kind, degree)
+    E, d, k = mesh.E, mesh.dim, mesh.k
+    z = lambda *s: torch.empty(*s, dtype=torch.float64, device=_DEV)  # noqa: E731
+    out = dict(jac=z(E, Q, d, d), det=z(E, Q), jac_invT=z(E, Q, d, d), qpts=z(E, Q, d),
+               grads=z(E, Q, k, d))
+    check(lib().tgk_geometry_d(mesh._h, degree, _ptr(out["jac"]), _ptr(out["det"]),
+                               _ptr(out["jac_invT"]), _ptr(out["qpts"]), _ptr(out["grads"]),
+                               _stream(stream)))
+    return out
+
+
+def _table(x, mesh, degree, per=1):
+    Q = quadrature_count(mesh.kind, degree)
+    return _cuda_f64(x, mesh.E * Q * per)
+
+
+def local_stiffness_diffusion(mesh, degree, coeff_eq, stream=None):
+    c = _table(coeff_eq, mesh, degree)
+    out = torch.empty(mesh.E, mesh.k, mesh.k, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_local_stiffness_diffusion_d(mesh._h, degree, _ptr(c), _ptr(out), _stream(stream)))
+    return out
+
+
+def local_stiffness_elasticity(mesh, degree, lam_eq, mu_eq, stream=None):
+    lam = _table(lam_eq, mesh, degree)
+    mu = _table(mu_eq, mesh, degree)
+    kk = mesh.k * mesh.dim
+    out = torch.empty(mesh.E, kk, kk, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_local_stiffness_elasticity_d(mesh._h, degree, _ptr(lam), _ptr(mu), _ptr(out),
+                                                 _stream(stream)))
+    return out
+
+
+def local_mass(mesh, degree, coeff_eq, stream=None):
+    c = _table(coeff_eq, mesh, degree)
+    out = torch.empty(mesh.E, mesh.k, mesh.k, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_local_mass_d(mesh._h, degree, _ptr(c), _ptr(out), _stream(stream)))
+    return out
+
+
+def local_load(mesh, degree, source_eq, stream=None):
+    s = _table(source_eq, mesh, degree)
+    out = torch.empty(mesh.E, mesh.k, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_local_load_d(mesh._h, degree, _ptr(s), _ptr(out), _stream(stream)))
+    return out
+
+
+def local_load_vector(mesh, degree, source_eqc, stream=None):
+    s = _table(source_eqc, mesh, degree, per=mesh.dim)
+    out = torch.empty(mesh.E, mesh.k * mesh.dim, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_local_load_vector_d(mesh._h, degree, _ptr(s), _ptr(out), _stream(stream)))
+    return out
+
+
+def evaluate_field(mesh, degree, spec, stream=None):
+    keep = []
+    f = field(spec, keep)
+    Q = quadrature_count(mesh.kind, degree)
+    out = torch.empty(mesh.E, Q, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_evaluate_field_d(mesh._h, degree, C.byref(f), _ptr(out), _stream(stream)))
+    return out
+
+
+def reduce_matrix(routing: Routing, local, stream=None):
+    loc = _cuda_f64(local, routing.E * routing.k * routing.k)
+    out = torch.empty(routing.nnz, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_reduce_matrix_d(routing._h, _ptr(loc), _ptr(out), _stream(stream)))
+    return out
+
+
+def reduce_vector(routing: Routing, local, stream=None):
+    loc = _cuda_f64(local, routing.E * routing.k)
+    out = torch.empty(routing.N, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_reduce_vector_d(routing._h, _ptr(loc), _ptr(out), _stream(stream)))
+    return out
+
+
+# ---------------------------------------------------------------- batched + adjoint
+def assemble_batched(mesh, routing, rho, source=1.0, with_load=True, mode="exact", stream=None):
+    """B per-element coefficient fields (B x E) -> K values (B x nnz) [+ one F (N)]."""
+    rho = _cuda_f64(rho).reshape(-1, mesh.E)
+    B = rho.shape[0]
+    K = torch.empty(B, routing.nnz, dtype=torch.float64, device=_DEV)
+    F = torch.empty(routing.N, dtype=torch.float64, device=_DEV) if with_load else None
+    check(lib().tgk_assemble_batched_d(mesh._h, routing._h, B, _ptr(rho), float(source), _ptr(K),
+                                       _ptr(F), {"exact": 0, "fast": 1}[mode], _stream(stream)))
+    return K, F
+
+
+def gradient_products(routing, lam, U, stream=None):
+    """gradient_products (adjoint.cpp:68-82), batched: lam, U (B x N) -> dK (B x nnz), dF (B x N)."""
+    lam = _cuda_f64(lam).reshape(-1, routing.N)
+    U = _cuda_f64(U).reshape(-1, routing.N)
+    B = lam.shape[0]
+    dK = torch.empty(B, routing.nnz, dtype=torch.float64, device=_DEV)
+    dF = torch.empty(B, routing.N, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_gradient_products_d(routing._h, B, _ptr(lam), _ptr(U), _ptr(dK), _ptr(dF),
+                                        _stream(stream)))
+    return dK, dF
+
+
+def adjoint_gather(mesh, routing, lam, U, degree=1, stream=None):
+    """dGamma/drho[b,e] = lambda_e^T K0_e U_e (tg_main.cpp:846-850), K0 recomputed in registers."""
+    lam = _cuda_f64(lam).reshape(-1, routing.N)
+    U = _cuda_f64(U).reshape(-1, routing.N)
+    B = lam.shape[0]
+    out = torch.empty(B, mesh.E, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_adjoint_gather_d(mesh._h, routing._h, B, _ptr(lam), _ptr(U), _ptr(out),
+                                     int(degree), _stream(stream)))
+    return out
