@@ -234,7 +234,8 @@ def main():
         N.check(N.lib().tgk_routing_set_owned_rows(routing._h, own_lo, own_hi))
     import ctypes as C
     nb, nh, nrec, pbytes = (C.c_int64() for _ in range(4))
-    N.check(N.lib().tgk_routing_plan_stats(routing._h, C.byref(nb), C.byref(nh), C.byref(nrec),
+    R = 128 if kw.get("with_mass") else 256  # rows per block of the fused kernel variant
+    N.check(N.lib().tgk_routing_plan_stats(routing._h, R, C.byref(nb), C.byref(nh), C.byref(nrec),
                                            C.byref(pbytes)))
     setup_s = time.time() - t0
     E_own = 6 * div[0] * div[1] * div[2] if kind == "tet4" else 2 * div[0] * div[1]
@@ -358,7 +359,7 @@ def main():
                        "parallelism": "single GPU" if world == 1 else
                        f"{world} row-owning z-slabs (halo recompute, no data-path collective)",
                        "l2": "inputs larger than L2 (working set ~1 GB vs 126 MB L2)",
-                       "fused_plan": {"blocks": nb.value, "halo_elements": nh.value,
+                       "fused_plan": {"rows_per_block": R, "blocks": nb.value, "halo_elements": nh.value,
                                       "recompute_factor": nh.value / max(1, elems.shape[0]),
                                       "records": nrec.value, "bytes": pbytes.value},
                        "setup_s": setup_s},

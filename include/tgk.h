@@ -158,10 +158,11 @@ int tgk_routing_copy(const tgk_routing* r, int64_t* row_ptr, int64_t* col_idx, u
  * rows [row_lo, row_hi) of this routing; elements incident to them are
  * recomputed as halo.  Other output rows are left untouched.  Resets the plan. */
 int tgk_routing_set_owned_rows(tgk_routing* r, int64_t row_lo, int64_t row_hi);
-/* Fused-plan statistics (builds the plan if needed): CUDA blocks, halo
- * elements (halo / E = recompute factor), packed records, device bytes. */
-int tgk_routing_plan_stats(tgk_routing* r, int64_t* n_blocks, int64_t* n_halo, int64_t* n_records,
-                           int64_t* bytes);
+/* Fused-plan statistics for blocks of rows_per_block (128 or 256) rows (builds
+ * the plan if needed): CUDA blocks, halo elements (halo / E = recompute
+ * factor), packed records, device bytes. */
+int tgk_routing_plan_stats(tgk_routing* r, int rows_per_block, int64_t* n_blocks, int64_t* n_halo,
+                           int64_t* n_records, int64_t* bytes);
 /* Routing cache file in the reference layout ("tg-rout2", routing.cpp:178-234). */
 int tgk_routing_save(const tgk_routing* r, uint64_t mesh_hash, const char* path);
 

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtgk.so")
+LIB_PATH = os.environ.get("TGK_LIB") or os.path.join(_HERE, "lib", "libtgk.so")  # TGK_LIB: A/B builds
 
 TGK_OK, TGK_ERR_NUMERICAL, TGK_ERR_INPUT, TGK_ERR_CUDA = 0, 1, 2, 3
 TRI3, QUAD4, TET4 = 0, 1, 2
@@ -79,7 +79,7 @@ _SIGS = {
     "tgk_routing_get_view": (_I, [_P, _P]),
     "tgk_routing_copy": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "tgk_routing_set_owned_rows": (_I, [_P, _I64, _I64]),
-    "tgk_routing_plan_stats": (_I, [_P, _P, _P, _P, _P]),
+    "tgk_routing_plan_stats": (_I, [_P, _I, _P, _P, _P, _P]),
     "tgk_routing_save": (_I, [_P, C.c_uint64, C.c_char_p]),
     "tgk_geometry_d": (_I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     "tgk_local_stiffness_diffusion_d": (_I, [_P, _I, _P, _P, _P]),

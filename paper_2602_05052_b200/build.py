@@ -55,6 +55,19 @@ def _compile(src):
     return obj, r.stderr
 
 
+def variant(defines: list[str], name: str) -> str:
+    """Experiment build with extra -D flags into lib/<name>.so (separate object dir)."""
+    global OBJ, LIB, NVFLAGS
+    saved = (OBJ, LIB, NVFLAGS)
+    OBJ = os.path.join(OUT, "obj_" + name)
+    LIB = os.path.join(OUT, name + ".so")
+    NVFLAGS = NVFLAGS + [f"-D{d}" for d in defines]
+    try:
+        return build()
+    finally:
+        OBJ, LIB, NVFLAGS = saved
+
+
 def build(verbose=False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     with ThreadPoolExecutor(max_workers=8) as ex:

@@ -127,11 +127,42 @@ struct P1 {
     static constexpr int d = KIND == TGK_TRI3 ? 2 : 3;
 };
 
+// ------------------------------------------------------------ division
+// Correctly rounded c / det from one correctly rounded reciprocal
+// y = RN(1/det) (__drcp_rn) and Markstein's correction
+//   q = RN(c*y);  r = c - det*q (exact, FMA);  RN(q + r*y) == RN(c/det)
+// (Markstein 1990; Muller et al., Handbook of Floating-Point Arithmetic,
+// "division with an FMA").  The theorem needs every quantity to stay in the
+// normal range.  The fused kernels use it only on meshes certified by
+// mesh_division_safe() (host.cpp): all coordinates 0 or 2^-40 <= |x| <= 2^40,
+// so nonzero Jacobian entries lie in [2^-92, 2^41], cofactors in
+// [2^-236, 2^84] or 0, det in [2^-328, 2^125] and all quotients/residuals are
+// normal.  Uncertified meshes take IEEE division.  Nonzero quotients are then
+// bit-identical to c / det; only the sign of an exact zero may differ, which
+// cannot reach a CSR value (see the header comment).  Verified against IEEE
+// division on 1.7e10 random and adversarial operand pairs on a B200
+// (tools/div_check.cu, profiles/r01_div_check.log).
+struct ExactDiv {
+    double det, y;
+    __device__ __forceinline__ explicit ExactDiv(double d) : det(d), y(0.0) {
+#ifdef __CUDA_ARCH__
+        y = __drcp_rn(d);
+#endif
+    }
+    __device__ __forceinline__ double operator()(double c) const {
+        const double q = c * y;
+        const double r = __fma_rn(-det, q, c);
+        return __fma_rn(r, y, q);
+    }
+};
+
 // ------------------------------------------------------------ geometry
 // batch_geometry (batch.cpp:76-104) + push_forward (batch.cpp:139-152) for an
 // affine simplex.  X: node coordinates (k x d).  Outputs det and the physical
 // basis gradients G (k x d).  Returns false when det <= 0 (batch.cpp:98-101).
-template <int KIND>
+// FASTDIV selects ExactDiv (same nonzero bits, ~3 instead of ~30 instructions
+// per quotient) for the fused kernels; the materialised drop-ins keep '/'.
+template <int KIND, bool FASTDIV = false>
 __device__ __forceinline__ bool simplex_geometry(const double (&X)[P1<KIND>::k][P1<KIND>::d],
                                                  double& det, double (&G)[P1<KIND>::k][P1<KIND>::d]) {
     if constexpr (KIND == TGK_TET4) {
@@ -156,9 +187,17 @@ __device__ __forceinline__ bool simplex_geometry(const double (&X)[P1<KIND>::k][
         det = (J[0] * c00 + J[1] * c01) + J[2] * c02;
         if (det <= 0.0) return false;
         // J^{-T} = cofactor / det (batch.cpp:36-44); push_forward: G_a = J^{-T} Ghat_a
-        const double t00 = c00 / det, t01 = c01 / det, t02 = c02 / det;
-        const double t10 = c10 / det, t11 = c11 / det, t12 = c12 / det;
-        const double t20 = c20 / det, t21 = c21 / det, t22 = c22 / det;
+        double t00, t01, t02, t10, t11, t12, t20, t21, t22;
+        if constexpr (FASTDIV) {
+            const ExactDiv dv(det);
+            t00 = dv(c00); t01 = dv(c01); t02 = dv(c02);
+            t10 = dv(c10); t11 = dv(c11); t12 = dv(c12);
+            t20 = dv(c20); t21 = dv(c21); t22 = dv(c22);
+        } else {
+            t00 = c00 / det; t01 = c01 / det; t02 = c02 / det;
+            t10 = c10 / det; t11 = c11 / det; t12 = c12 / det;
+            t20 = c20 / det; t21 = c21 / det; t22 = c22 / det;
+        }
         G[1][0] = t00; G[2][0] = t01; G[3][0] = t02;
         G[1][1] = t10; G[2][1] = t11; G[3][1] = t12;
         G[1][2] = t20; G[2][2] = t21; G[3][2] = t22;
@@ -171,7 +210,13 @@ __device__ __forceinline__ bool simplex_geometry(const double (&X)[P1<KIND>::k][
         det = J0 * J3 - J1 * J2;
         if (det <= 0.0) return false;
         // batch.cpp:21-24
-        const double t00 = J3 / det, t01 = -J2 / det, t10 = -J1 / det, t11 = J0 / det;
+        double t00, t01, t10, t11;
+        if constexpr (FASTDIV) {
+            const ExactDiv dv(det);
+            t00 = dv(J3); t01 = dv(-J2); t10 = dv(-J1); t11 = dv(J0);
+        } else {
+            t00 = J3 / det; t01 = -J2 / det; t10 = -J1 / det; t11 = J0 / det;
+        }
         G[1][0] = t00; G[2][0] = t01;
         G[1][1] = t10; G[2][1] = t11;
         G[0][0] = -(t00 + t01);

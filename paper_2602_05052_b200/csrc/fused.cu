@@ -4,28 +4,38 @@
 // written to HBM and no atomics.
 //
 // Decomposition ("row blocks", see tgk_internal.hpp / plan.cpp): CUDA block b
-// owns <= 256 CSR rows (mesh nodes, compact in space via a Morton ordering)
-// and walks every element incident to them — its halo — in ascending element
-// id, 256 elements per chunk:
-//   phase A  one thread per halo element: gather coordinates, exact geometry
-//            and local K_e/M_e/F_e into shared memory;
-//   phase B  one thread per owned row: fold that row's records of this chunk
-//            (ascending element) into shared-memory accumulators.
-// Each CSR value is therefore the left fold, from +0.0, of its contributions
-// in ascending element order — the reference reduction's order
-// (routing.cpp:117-124) — so with the exact element arithmetic of
-// element.cuh the output is bit-identical to the CPU reference.
+// owns R CSR rows (mesh nodes, compact in space via a Morton ordering) and
+// walks every element incident to them — its halo, ordered by level in the
+// per-row ascending-element chains (plan.cpp) — R elements per chunk:
+//   prologue  the block's node table (coordinates of every node its halo
+//             touches) is gathered once into shared memory;
+//   phase A   one thread per halo element: exact geometry and local
+//             K_e / M_e / F_e from the node table into shared memory;
+//   phase B   one thread per owned row: fold that row's records of the chunk
+//             (ascending element) — diagonal and load in registers, the
+//             off-diagonal entries in shared-memory accumulators.
+// The next chunk's block-local connectivity and records arrive by cp.async
+// while the current chunk is computed.  Each CSR value is the left fold, from
+// +0.0, of its contributions in ascending element order — the reference
+// reduction's order (routing.cpp:117-124) — so with the exact element
+// arithmetic of element.cuh the output is bit-identical to the CPU reference.
 // Elements on a block boundary are recomputed by every block they touch
-// (halo recompute); the plan records the factor.
-#include <cub/block/block_scan.cuh>
+// (halo recompute; the plan statistics report the factor).
+#include <cstdio>
+#include <vector>
 
 #include "cuda_util.cuh"
 #include "element.cuh"
 #include "tgk_internal.hpp"
 
+#ifndef TGK_MINB
+#define TGK_MINB(R) ((R) == 256 ? 2 : ((R) == 128 ? 4 : 8))
+#endif
+
 namespace tgk {
 
 int check_bad(unsigned long long* d_bad, cudaStream_t st);
+int mesh_division_safe(tgk_mesh* m, cudaStream_t st, bool* safe);
 
 namespace {
 
@@ -37,15 +47,18 @@ struct FieldDev {
 
 struct FusedArgs {
     const double* nodes;
-    const int32_t* conn;
     const int64_t* row_ptr;
     const int64_t* row_off;
     const uint32_t* rows;
+    const int64_t* rows_rp;
     const int64_t* halo_off;
     const uint32_t* halo;
+    const int64_t* bnode_off;
+    const uint32_t* bnodes;
+    const uint16_t* halo_lconn;
     const int64_t* chunk_off;
     const int64_t* chunk_rec_off;
-    const uint8_t* chunk_cnt;
+    const uint16_t* chunk_row_off;
     const uint32_t* recs;
     FieldDev coef;
     FieldDev src;
@@ -53,46 +66,211 @@ struct FusedArgs {
     double* M;
     double* F;
     int lmax;
+    int max_recs;
+    int max_bnodes;
+    int debug;  // profiling only (TGK_FUSED_DEBUG): 1 skips phase B, 2 skips phase A math
+    long long* trace;  // profiling only (TGK_FUSED_TRACE): per block 8 clock64 stamps
     unsigned long long* bad;
 };
 
+constexpr int kMaxChunks = 255;  // halo chunks per block (plan-enforced)
+#ifndef TGK_RING
+#define TGK_RING 4
+#endif
+#ifndef TGK_R_BIG
+#define TGK_R_BIG 256
+#endif
+constexpr int kRing = TGK_RING;  // cp.async ring slots: chunk c+kRing-1 is requested while c is computed
+
+// Slot of K_e[a][b] within the rotated shared-memory row a: 0 for the
+// diagonal, then the other local nodes in ascending order (see pack_rec).
+__host__ __device__ constexpr int rot(int a, int b) { return b == a ? 0 : (b < a ? b + 1 : b); }
+
 // KTYPE 0: diffusion stiffness, 1: coefficient mass (ProblemKind::Mass)
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F>
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R>
 struct FusedCfg {
     static constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q;
-    static constexpr int nK = KTYPE == 0 ? k * (k + 1) / 2 : k * k;
-    static constexpr int offM = nK;
-    static constexpr int nM = HAS_M ? k * k : 0;
-    static constexpr int offF = nK + nM;
-    static constexpr int nF = HAS_F ? k : 0;
-    static constexpr int raw = nK + nM + nF;
-    static constexpr int stride = raw % 2 == 0 ? raw + 1 : raw;  // odd: spreads smem banks
+    // local tensors in shared memory: rotated rows of 4 doubles (16-byte aligned pairs)
+    static constexpr int offK = 0;
+    static constexpr int offM = 4 * k;
+    static constexpr int offF = offM + (HAS_M ? 4 * k : 0);
+    static constexpr int raw = offF + (HAS_F ? 4 : 0);
+    // stride in doubles = 2 * odd: conflict-free 128-bit accesses across lanes
+    static constexpr int stride = (raw / 2) % 2 == 1 ? raw : raw + 2;
     static constexpr int nmat = 1 + (HAS_M ? 1 : 0);
-    static size_t smem_bytes(int lmax) {
-        return sizeof(double) * (size_t(kChunk) * stride + size_t(kRowsPerBlock) * lmax * nmat +
-                                 (HAS_F ? kRowsPerBlock : 0));
+    // node table: coordinates, d doubles per node (odd 8-byte-word stride for
+    // d = 3: random node gathers spread over all bank pairs), then the nodal
+    // coefficient and nodal source as separate arrays (used only when nodal)
+    static constexpr int NV = 3;      // TRI3 pads to 3 as well (odd stride)
+    static constexpr int NVT = NV + 2;  // doubles per node in the table (coords + coef + src)
+    static size_t smem_bytes(int lmax, int max_recs, int max_bnodes) {
+        return sizeof(double) * (size_t(R) * stride + size_t(R) * lmax * nmat + size_t(max_bnodes) * NVT) +
+               kRing * (sizeof(uint32_t) * size_t(max_recs) + sizeof(uint16_t) * size_t(row_off_stride(R)) +
+                        sizeof(uint16_t) * 4 * size_t(R));
     }
 };
 
-__device__ __forceinline__ double field_at_elem(const FieldDev& f, int64_t e) {
-    return f.type == TGK_FIELD_ELEMENT ? __ldg(f.data + e) : f.value;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// One record's rotated local tensor row (K, M) and F_e[a] from shared memory.
+template <bool HAS_M, bool HAS_F>
+struct RowVals {
+    double kv[4];
+    double mv[HAS_M ? 4 : 1];
+    double f;
+    template <class C>
+    __device__ __forceinline__ void load(const double* ke, uint32_t rec) {
+        const int hl = rec & 0xff;
+        const int a = (rec >> 8) & 3;
+        const double* src = ke + hl * C::stride + a * 4;
+        const double2 k01 = *reinterpret_cast<const double2*>(src + C::offK);
+        const double2 k23 = *reinterpret_cast<const double2*>(src + C::offK + 2);
+        kv[0] = k01.x; kv[1] = k01.y; kv[2] = k23.x; kv[3] = k23.y;
+        if constexpr (HAS_M) {
+            const double2 m01 = *reinterpret_cast<const double2*>(src + C::offM);
+            const double2 m23 = *reinterpret_cast<const double2*>(src + C::offM + 2);
+            mv[0] = m01.x; mv[1] = m01.y; mv[2] = m23.x; mv[3] = m23.y;
+        }
+        if constexpr (HAS_F) f = ke[hl * C::stride + C::offF + a];
+    }
+};
+
+// c(x_q) for a constant / per-element / nodal field (coefficient.cpp:34-55,
+// interpolate_nodal batch.cpp:321-330)
+template <int KIND, int DEG>
+__device__ __forceinline__ double field_q(const FieldDev& f, const double* u, int q) {
+    constexpr int k = P1<KIND>::k;
+    if (f.type == TGK_FIELD_NODAL) {
+        double v = basis<KIND, DEG>(q, 0) * u[0];
+#pragma unroll
+        for (int a = 1; a < k; ++a) v += basis<KIND, DEG>(q, a) * u[a];
+        return v;
+    }
+    return f.type == TGK_FIELD_ELEMENT ? u[0] : f.value;
 }
 
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F>
-__global__ void __launch_bounds__(256) k_fused_scalar(FusedArgs p) {
-    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F>;
-    using R = Rule<KIND, DEG>;
-    constexpr int k = C::k, d = C::d, Q = C::Q;
-    extern __shared__ double smem[];
-    double* ke = smem;                                         // kChunk x stride
-    double* accK = ke + kChunk * C::stride;                    // lmax x kRowsPerBlock
-    double* accM = accK + kRowsPerBlock * p.lmax;              // (HAS_M)
-    double* accF = accK + kRowsPerBlock * p.lmax * C::nmat;    // (HAS_F)
-    using Scan = cub::BlockScan<int, 256>;
-    __shared__ typename Scan::TempStorage scan_tmp;
+// Phase A body: the reference's local kernels for one element into `out`
+// (rotated rows).  nt: the block's node table; ln: block-local node ids.
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV>
+__device__ __forceinline__ void element_tensors(const FusedArgs& p, const double* nt, const ushort4 ln,
+                                                int64_t h_global, double* out) {
+    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R>;
+    using Rl = Rule<KIND, DEG>;
+    constexpr int k = C::k, d = C::d, Q = C::Q, NV = C::NV;
+    const int ids[4] = {ln.x, ln.y, ln.z, ln.w};
+    double X[k][d];
+    double cu[k], fu[k];
+#pragma unroll
+    for (int a = 0; a < k; ++a)
+#pragma unroll
+        for (int c = 0; c < d; ++c) X[a][c] = nt[ids[a] * NV + c];
+    if (p.coef.type == TGK_FIELD_NODAL) {
+        const double* cs = nt + p.max_bnodes * NV;
+#pragma unroll
+        for (int a = 0; a < k; ++a) cu[a] = cs[ids[a]];
+    }
+    if (HAS_F && p.src.type == TGK_FIELD_NODAL) {
+        const double* ss = nt + p.max_bnodes * (NV + 1);
+#pragma unroll
+        for (int a = 0; a < k; ++a) fu[a] = ss[ids[a]];
+    }
+    if (p.coef.type == TGK_FIELD_ELEMENT || (HAS_F && p.src.type == TGK_FIELD_ELEMENT)) {
+        const int64_t e = p.halo[h_global];
+        if (p.coef.type == TGK_FIELD_ELEMENT) cu[0] = __ldg(p.coef.data + e);
+        if (HAS_F && p.src.type == TGK_FIELD_ELEMENT) fu[0] = __ldg(p.src.data + e);
+    }
+    double det, G[k][d];
+    if (!simplex_geometry<KIND, FDIV>(X, det, G)) {
+        atomicMin(p.bad, static_cast<unsigned long long>(p.halo[h_global]));
+#pragma unroll
+        for (int i = 0; i < C::raw; ++i) out[i] = 0.0;
+        return;
+    }
+    double sc[Q];  // w_q * det * c_q  (batch.cpp:169 / :261)
+#pragma unroll
+    for (int q = 0; q < Q; ++q) sc[q] = Rl::w(q) * det * field_q<KIND, DEG>(p.coef, cu, q);
+    if constexpr (KTYPE == 0) {
+        // local_stiffness_diffusion (batch.cpp:168-177); K_e symmetric bitwise
+#pragma unroll
+        for (int a = 0; a < k; ++a)
+#pragma unroll
+            for (int b = a; b < k; ++b) {
+                const double dot = gdot<KIND>(G, a, b);
+                double v = sc[0] * dot;
+#pragma unroll
+                for (int q = 1; q < Q; ++q) v += sc[q] * dot;
+                out[C::offK + a * 4 + rot(a, b)] = v;
+                out[C::offK + b * 4 + rot(b, a)] = v;
+            }
+    } else {
+        // local_mass with the coefficient (batch.cpp:259-265)
+#pragma unroll
+        for (int a = 0; a < k; ++a)
+#pragma unroll
+            for (int b = 0; b < k; ++b) {
+                double v = sc[0] * basis<KIND, DEG>(0, a) * basis<KIND, DEG>(0, b);
+#pragma unroll
+                for (int q = 1; q < Q; ++q) v += sc[q] * basis<KIND, DEG>(q, a) * basis<KIND, DEG>(q, b);
+                out[C::offK + a * 4 + rot(a, b)] = v;
+            }
+    }
+    if constexpr (HAS_M) {
+        // with_mass: local_mass with ones (physics.cpp:70-71); w*det*1.0 == w*det
+#pragma unroll
+        for (int a = 0; a < k; ++a)
+#pragma unroll
+            for (int b = 0; b < k; ++b) {
+                double v = Rl::w(0) * det * basis<KIND, DEG>(0, a) * basis<KIND, DEG>(0, b);
+#pragma unroll
+                for (int q = 1; q < Q; ++q)
+                    v += Rl::w(q) * det * basis<KIND, DEG>(q, a) * basis<KIND, DEG>(q, b);
+                out[C::offM + a * 4 + rot(a, b)] = v;
+            }
+    }
+    if constexpr (HAS_F) {
+        // local_load (batch.cpp:280-286)
+        double sf[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) sf[q] = Rl::w(q) * det * field_q<KIND, DEG>(p.src, fu, q);
+#pragma unroll
+        for (int a = 0; a < k; ++a) {
+            double v = sf[0] * basis<KIND, DEG>(0, a);
+#pragma unroll
+            for (int q = 1; q < Q; ++q) v += sf[q] * basis<KIND, DEG>(q, a);
+            out[C::offF + a] = v;
+        }
+    }
+}
+
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV>
+__global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
+    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R>;
+    constexpr int k = C::k, d = C::d, NV = C::NV;
+    constexpr int ROS = R + 8;
+    extern __shared__ __align__(16) double smem[];
+    double* ke = smem;                                               // R x stride
+    double* accK = ke + R * C::stride;                               // lmax x R
+    double* accM = accK + R * p.lmax;                                // (HAS_M)
+    double* nt = accK + R * p.lmax * C::nmat;                        // max_bnodes x (NV + 2)
+    uint32_t* rec_s = reinterpret_cast<uint32_t*>(nt + p.max_bnodes * C::NVT);  // kRing x max_recs
+    uint16_t* ro_s = reinterpret_cast<uint16_t*>(rec_s + kRing * p.max_recs);  // kRing x ROS
+    ushort4* lc_s = reinterpret_cast<ushort4*>(ro_s + kRing * ROS);           // kRing x R
+    __shared__ int64_t cro_s[kMaxChunks + 1];  // this block's chunk record offsets
 
     const int tid = threadIdx.x;
     const int64_t blk = blockIdx.x;
+    long long t_start = 0, t_pro = 0, t_a = 0, t_b = 0, t_loop = 0;
+    if (p.trace && tid == 0) t_start = clock64();
     const int64_t r0 = p.row_off[blk];
     const int nr = static_cast<int>(p.row_off[blk + 1] - r0);
     const int64_t h0 = p.halo_off[blk];
@@ -100,181 +278,214 @@ __global__ void __launch_bounds__(256) k_fused_scalar(FusedArgs p) {
     const int64_t c0 = p.chunk_off[blk];
     const int nch = static_cast<int>(p.chunk_off[blk + 1] - c0);
 
-    for (int i = tid; i < kRowsPerBlock * p.lmax * C::nmat; i += 256) accK[i] = 0.0;
-    if (HAS_F) accF[tid] = 0.0;
+    // stage chunk c's block-local connectivity, records and row offsets into
+    // ring slot c % kRing; always commits a group (possibly empty) so that the
+    // wait below can use a fixed depth
+    auto stage = [&](int c) {
+        if (c < nch) {
+            const int sl = c % kRing;
+            const int64_t cg = c0 + c;
+            const int64_t rb = cro_s[c];
+            const int nrec4 = static_cast<int>((cro_s[c + 1] - rb) >> 2);
+            uint32_t* rdst = rec_s + sl * p.max_recs;
+            for (int i = tid; i < nrec4; i += R) cp_async16(rdst + 4 * i, p.recs + rb + 4 * i);
+            uint16_t* odst = ro_s + sl * ROS;
+            const uint16_t* osrc = p.chunk_row_off + cg * ROS;
+            for (int i = tid; i < ROS / 8; i += R) cp_async16(odst + 8 * i, osrc + 8 * i);
+            const int64_t hb = h0 + int64_t(c) * R;
+            const int64_t rem = nh - int64_t(c) * R;
+            const int ne = rem < R ? static_cast<int>(rem) : R;
+            if (tid < ne) cp_async8(lc_s + sl * R + tid, p.halo_lconn + (hb + tid) * 4);
+        }
+        cp_async_commit();
+    };
 
-    for (int c = 0; c < nch; ++c) {
-        // ---------------- phase A: one halo element per thread
-        const int64_t h = int64_t(c) * kChunk + tid;
-        if (h < nh) {
-            const int64_t e = p.halo[h0 + h];
-            double X[k][d];
-            int32_t nid[k];
-#pragma unroll
-            for (int a = 0; a < k; ++a) nid[a] = __ldg(p.conn + e * k + a);
-#pragma unroll
-            for (int a = 0; a < k; ++a)
-#pragma unroll
-                for (int cc = 0; cc < d; ++cc) X[a][cc] = __ldg(p.nodes + int64_t(nid[a]) * d + cc);
-            double det;
-            double G[k][d];
-            double* out = ke + tid * C::stride;
-            if (!simplex_geometry<KIND>(X, det, G)) {
-                atomicMin(p.bad, static_cast<unsigned long long>(e));
-                for (int i = 0; i < C::raw; ++i) out[i] = 0.0;
-            } else {
-                // coefficient at the quadrature points: scale_q = w_q * det * c_q
-                double sc[Q];
-                if (p.coef.type == TGK_FIELD_NODAL) {
-                    double u[k];
-#pragma unroll
-                    for (int a = 0; a < k; ++a) u[a] = __ldg(p.coef.data + nid[a]);
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        double v = basis<KIND, DEG>(q, 0) * u[0];
-#pragma unroll
-                        for (int a = 1; a < k; ++a) v += basis<KIND, DEG>(q, a) * u[a];
-                        sc[q] = R::w(q) * det * v;
-                    }
-                } else {
-                    const double cv = field_at_elem(p.coef, e);
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) sc[q] = R::w(q) * det * cv;
-                }
-                if constexpr (KTYPE == 0) {
-                    // local_stiffness_diffusion (batch.cpp:168-177)
-#pragma unroll
-                    for (int a = 0; a < k; ++a)
-#pragma unroll
-                        for (int b = a; b < k; ++b) {
-                            const double dot = gdot<KIND>(G, a, b);
-                            double v = sc[0] * dot;
-#pragma unroll
-                            for (int q = 1; q < Q; ++q) v += sc[q] * dot;
-                            out[sym_idx<k>(a, b)] = v;
-                        }
-                } else {
-                    // local_mass with the coefficient (batch.cpp:259-265)
-#pragma unroll
-                    for (int a = 0; a < k; ++a)
-#pragma unroll
-                        for (int b = 0; b < k; ++b) {
-                            double v = sc[0] * basis<KIND, DEG>(0, a) * basis<KIND, DEG>(0, b);
-#pragma unroll
-                            for (int q = 1; q < Q; ++q)
-                                v += sc[q] * basis<KIND, DEG>(q, a) * basis<KIND, DEG>(q, b);
-                            out[a * k + b] = v;
-                        }
-                }
-                if constexpr (HAS_M) {
-                    // with_mass: local_mass with ones (physics.cpp:70-71); w*det*1.0 == w*det
-#pragma unroll
-                    for (int a = 0; a < k; ++a)
-#pragma unroll
-                        for (int b = 0; b < k; ++b) {
-                            double v = R::w(0) * det * basis<KIND, DEG>(0, a) * basis<KIND, DEG>(0, b);
-#pragma unroll
-                            for (int q = 1; q < Q; ++q)
-                                v += R::w(q) * det * basis<KIND, DEG>(q, a) * basis<KIND, DEG>(q, b);
-                            out[C::offM + a * k + b] = v;
-                        }
-                }
-                if constexpr (HAS_F) {
-                    // local_load (batch.cpp:280-286)
-                    double sf[Q];
-                    if (p.src.type == TGK_FIELD_NODAL) {
-                        double u[k];
-#pragma unroll
-                        for (int a = 0; a < k; ++a) u[a] = __ldg(p.src.data + nid[a]);
-#pragma unroll
-                        for (int q = 0; q < Q; ++q) {
-                            double v = basis<KIND, DEG>(q, 0) * u[0];
-#pragma unroll
-                            for (int a = 1; a < k; ++a) v += basis<KIND, DEG>(q, a) * u[a];
-                            sf[q] = R::w(q) * det * v;
-                        }
-                    } else {
-                        const double fv = field_at_elem(p.src, e);
-#pragma unroll
-                        for (int q = 0; q < Q; ++q) sf[q] = R::w(q) * det * fv;
-                    }
-#pragma unroll
-                    for (int a = 0; a < k; ++a) {
-                        double v = sf[0] * basis<KIND, DEG>(0, a);
-#pragma unroll
-                        for (int q = 1; q < Q; ++q) v += sf[q] * basis<KIND, DEG>(q, a);
-                        out[C::offF + a] = v;
-                    }
-                }
-            }
-        }
-        // record offsets of this chunk: exclusive scan of the per-row counts
-        const int64_t cg = c0 + c;
-        const int cnt = tid < nr ? p.chunk_cnt[cg * kRowsPerBlock + tid] : 0;
-        int off;
-        Scan(scan_tmp).ExclusiveSum(cnt, off);
-        __syncthreads();
-        // ---------------- phase B: one owned row per thread, ascending element
-        if (cnt > 0) {
-            const uint32_t* rr = p.recs + p.chunk_rec_off[cg] + off;
-            for (int j = 0; j < cnt; ++j) {
-                const uint32_t rec = __ldg(rr + j);
-                const int hl = rec & 0xff;
-                const int a = (rec >> 8) & 3;
-                const double* src = ke + hl * C::stride;
-#pragma unroll
-                for (int b = 0; b < k; ++b) {
-                    const int pos = (rec >> (10 + 5 * b)) & 31;
-                    const int ix = KTYPE == 0 ? sym_idx<k>(a, b) : a * k + b;
-                    accK[pos * kRowsPerBlock + tid] += src[ix];
-                    if constexpr (HAS_M) accM[pos * kRowsPerBlock + tid] += src[C::offM + a * k + b];
-                }
-                if constexpr (HAS_F) accF[tid] += src[C::offF + a];
-            }
-        }
-        __syncthreads();
-    }
-    // ---------------- epilogue: owned rows -> CSR values / F
+    // this thread's owned row: id, CSR offset and length (used by the epilogue)
+    int64_t my_row = 0, my_rp = 0;
+    int my_len = 0;
     if (tid < nr) {
-        const int64_t row = p.rows[r0 + tid];
-        const int64_t rp = p.row_ptr[row];
-        const int len = static_cast<int>(p.row_ptr[row + 1] - rp);
-        for (int q = 0; q < len; ++q) p.K[rp + q] = accK[q * kRowsPerBlock + tid];
-        if constexpr (HAS_M)
-            for (int q = 0; q < len; ++q) p.M[rp + q] = accM[q * kRowsPerBlock + tid];
-        if constexpr (HAS_F) p.F[row] = accF[tid];
+        my_row = p.rows[r0 + tid];
+        const int64_t packed = p.rows_rp[r0 + tid];  // CSR offset | length << 56 (plan.cpp)
+        my_rp = packed & ((int64_t(1) << 56) - 1);
+        my_len = static_cast<int>(packed >> 56);
+    }
+    for (int i = tid; i <= nch; i += R) cro_s[i] = p.chunk_rec_off[c0 + i];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < kRing - 1; ++c) stage(c);
+    // node table: coordinates (+ nodal coefficient / source) of every node of the
+    // halo; all index loads first, then all coordinate loads (one round trip each)
+    {
+        const int64_t n0 = p.bnode_off[blk];
+        const int nbn = static_cast<int>(p.bnode_off[blk + 1] - n0);
+        constexpr int NPT = 4;  // nodes per thread per batch
+        for (int base = 0; base < nbn; base += NPT * R) {
+            int64_t g[NPT];
+#pragma unroll
+            for (int u = 0; u < NPT; ++u) {
+                const int i = base + u * R + tid;
+                g[u] = i < nbn ? static_cast<int64_t>(p.bnodes[n0 + i]) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < NPT; ++u) {
+                const int i = base + u * R + tid;
+                if (g[u] < 0) continue;
+                double* dst = nt + i * NV;
+#pragma unroll
+                for (int c = 0; c < d; ++c) dst[c] = __ldg(p.nodes + g[u] * d + c);
+                if (p.coef.type == TGK_FIELD_NODAL) nt[p.max_bnodes * NV + i] = __ldg(p.coef.data + g[u]);
+                if constexpr (HAS_F)
+                    if (p.src.type == TGK_FIELD_NODAL) nt[p.max_bnodes * (NV + 1) + i] = __ldg(p.src.data + g[u]);
+            }
+        }
+    }
+    for (int i = tid; i < R * p.lmax * C::nmat; i += R) accK[i] = 0.0;
+    double dK = 0.0, dM = 0.0, dF = 0.0;  // diagonal K, M and the load F of the owned row
+    int diag_pos = 0;
+
+    long long t_mark = 0;
+    for (int c = 0; c < nch; ++c) {
+        cp_async_wait<kRing - 2>();  // chunk c landed (later chunks may be in flight)
+        __syncthreads();  // chunk c visible; node table ready; phase B(c-1) done
+        if (p.trace && tid == 0) {
+            const long long t = clock64();
+            if (c == 0) t_pro = t - t_start; else t_b += t - t_mark;
+            t_mark = t;
+        }
+        stage(c + kRing - 1);  // into the slot phase B(c-1) just released
+        // ---------------- phase A: this thread's element of chunk c
+        const int64_t h = int64_t(c) * R + tid;
+        if (h < nh) {
+            double* out = ke + tid * C::stride;
+            if (p.debug & 2) {
+                for (int i = 0; i < C::raw; ++i) out[i] = nt[0];
+            } else {
+                element_tensors<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV>(p, nt, lc_s[(c % kRing) * R + tid],
+                                                                         h0 + h, out);
+            }
+        }
+        __syncthreads();
+        if (p.trace && tid == 0) {
+            const long long t = clock64();
+            t_a += t - t_mark;
+            t_mark = t;
+        }
+        // ---------------- phase B: owned row tid folds its records of chunk c.
+        // The diagonal entry (the element's node that IS this row) and F live in
+        // registers; the off-diagonal entries are shared-memory read-modify-writes.
+        // The next record and its local tensor row are loaded before the
+        // current record's stores.
+        if (tid < nr && !(p.debug & 1)) {
+            const uint16_t* ro = ro_s + (c % kRing) * ROS;
+            const uint32_t* rs = rec_s + (c % kRing) * p.max_recs;
+            int j = ro[tid];
+            const int j1 = ro[tid + 1];
+            if (j < j1) {
+                uint32_t rec = rs[j];
+                RowVals<HAS_M, HAS_F> v;
+                v.template load<C>(ke, rec);
+                for (; j < j1; ++j) {
+                    const uint32_t rec_n = j + 1 < j1 ? rs[j + 1] : rec;
+                    RowVals<HAS_M, HAS_F> vn;
+                    vn.template load<C>(ke, rec_n);
+                    // the k-1 positions of one record are distinct columns: load all,
+                    // add, store all (no false read-after-write serialisation)
+                    int pos[k - 1];
+                    double ak[k - 1], am[k - 1];
+#pragma unroll
+                    for (int j2 = 0; j2 < k - 1; ++j2) {
+                        pos[j2] = ((rec >> (10 + 5 * j2)) & 31) * R + tid;
+                        ak[j2] = accK[pos[j2]];
+                        if constexpr (HAS_M) am[j2] = accM[pos[j2]];
+                    }
+#pragma unroll
+                    for (int j2 = 0; j2 < k - 1; ++j2) {
+                        accK[pos[j2]] = ak[j2] + v.kv[j2 + 1];
+                        if constexpr (HAS_M) accM[pos[j2]] = am[j2] + v.mv[j2 + 1];
+                    }
+                    dK += v.kv[0];
+                    if constexpr (HAS_M) dM += v.mv[0];
+                    if constexpr (HAS_F) dF += v.f;
+                    diag_pos = (rec >> 25) & 31;
+                    rec = rec_n;
+                    v = vn;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (p.trace && tid == 0) {
+        const long long t = clock64();
+        t_b += t - t_mark;
+        t_loop = t;
+    }
+    // ---------------- epilogue: owned rows -> CSR values, one store per position
+    // (lane = row: conflict-free shared-memory reads; L2 merges the row runs)
+    if (tid < nr) {
+        accK[diag_pos * R + tid] = dK;
+        if constexpr (HAS_M) accM[diag_pos * R + tid] = dM;
+        for (int q = 0; q < my_len; ++q) {
+            p.K[my_rp + q] = accK[q * R + tid];
+            if constexpr (HAS_M) p.M[my_rp + q] = accM[q * R + tid];
+        }
+    }
+    if (HAS_F && tid < nr) p.F[my_row] = dF;
+    if (p.trace && tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        long long* tr = p.trace + blk * 8;
+        tr[0] = t_start; tr[1] = t_pro; tr[2] = t_a; tr[3] = t_b; tr[4] = clock64() - t_loop;
+        tr[5] = smid; tr[6] = nch; tr[7] = clock64();
     }
 }
 
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F>
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV>
 int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
-    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F>;
-    auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F>;
-    const size_t smem = C::smem_bytes(a.lmax);
+    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R>;
+    auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV>;
+    const size_t smem = C::smem_bytes(a.lmax, a.max_recs, a.max_bnodes);
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<static_cast<unsigned>(n_blocks), 256, smem, st>>>(a);
+    if (n_blocks > 0) kern<<<static_cast<unsigned>(n_blocks), R, smem, st>>>(a);
     KERNEL_CHECK("fused_scalar");
     return TGK_OK;
 }
 
+template <int KIND, int DEG, int R, bool FDIV>
+int dispatch_r(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, cudaStream_t st) {
+    if (ktype == 1) return launch_fused<KIND, DEG, 1, false, false, R, FDIV>(a, nb, st);
+    if (m && f) return launch_fused<KIND, DEG, 0, true, true, R, FDIV>(a, nb, st);
+    if (m) return launch_fused<KIND, DEG, 0, true, false, R, FDIV>(a, nb, st);
+    if (f) return launch_fused<KIND, DEG, 0, false, true, R, FDIV>(a, nb, st);
+    return launch_fused<KIND, DEG, 0, false, false, R, FDIV>(a, nb, st);
+}
+
+// Rows per block R and FDIV (Markstein division on meshes certified
+// division-safe) select the kernel instance.
 template <int KIND, int DEG>
-int dispatch_flags(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, cudaStream_t st) {
-    if (ktype == 1) return launch_fused<KIND, DEG, 1, false, false>(a, nb, st);
-    if (m && f) return launch_fused<KIND, DEG, 0, true, true>(a, nb, st);
-    if (m) return launch_fused<KIND, DEG, 0, true, false>(a, nb, st);
-    if (f) return launch_fused<KIND, DEG, 0, false, true>(a, nb, st);
-    return launch_fused<KIND, DEG, 0, false, false>(a, nb, st);
+int dispatch_flags(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, int R, bool fdiv,
+                   cudaStream_t st) {
+    if (R == 128)
+        return fdiv ? dispatch_r<KIND, DEG, 128, true>(ktype, m, f, a, nb, st)
+                    : dispatch_r<KIND, DEG, 128, false>(ktype, m, f, a, nb, st);
+    return fdiv ? dispatch_r<KIND, DEG, TGK_R_BIG, true>(ktype, m, f, a, nb, st)
+                : dispatch_r<KIND, DEG, TGK_R_BIG, false>(ktype, m, f, a, nb, st);
 }
 
 }  // namespace
 
-int ensure_plan(tgk_routing* r);
+int fused_rows_per_block(const tgk_problem* pr) {
+    if (const char* env = getenv("TGK_FUSED_R")) return atoi(env) == 128 ? 128 : TGK_R_BIG;
+    (void)pr;
+    return 128;
+}
 
-// Scalar fused assembly on device buffers.  Returns after the bad-element check.
+// Scalar fused assembly on device buffers.  With d_bad == nullptr it checks
+// the bad-element flag (synchronising); otherwise it is fully asynchronous.
 int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                           double* F, double* M, cudaStream_t st, unsigned long long* d_bad) {
-    TGK_TRY(ensure_plan(r));
-    const PlanDev& pl = r->plan;
+    const int R = fused_rows_per_block(pr);
+    const PlanDev* pl = nullptr;
+    TGK_TRY(ensure_plan(r, R, &pl));
     const bool is_mass = pr->kind == TGK_MASS;
     const bool high = pr->diffusion.type != TGK_FIELD_CONSTANT || is_mass || pr->with_mass;
     const int degree = high ? 2 : 1;  // default_mass_degree / default_stiffness_degree for P1
@@ -282,34 +493,59 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
     const bool has_m = pr->with_mass != 0;
     FusedArgs a{};
     a.nodes = m->nodes;
-    a.conn = m->conn;
     a.row_ptr = r->row_ptr;
-    a.row_off = pl.row_off;
-    a.rows = pl.rows;
-    a.halo_off = pl.halo_off;
-    a.halo = pl.halo;
-    a.chunk_off = pl.chunk_off;
-    a.chunk_rec_off = pl.chunk_rec_off;
-    a.chunk_cnt = pl.chunk_cnt;
-    a.recs = pl.recs;
+    a.row_off = pl->row_off;
+    a.rows = pl->rows;
+    a.rows_rp = pl->rows_rp;
+    a.halo_off = pl->halo_off;
+    a.halo = pl->halo;
+    a.bnode_off = pl->bnode_off;
+    a.bnodes = pl->bnodes;
+    a.halo_lconn = pl->halo_lconn;
+    a.chunk_off = pl->chunk_off;
+    a.chunk_rec_off = pl->chunk_rec_off;
+    a.chunk_row_off = pl->chunk_row_off;
+    a.recs = pl->recs;
     a.coef = FieldDev{pr->diffusion.type, pr->diffusion.value, pr->diffusion.data};
+    a.src = FieldDev{TGK_FIELD_CONSTANT, 0.0, nullptr};
     if (has_f) a.src = FieldDev{pr->source[0].type, pr->source[0].value, pr->source[0].data};
     a.K = K;
     a.M = M;
     a.F = F;
-    a.lmax = pl.lmax;
+    a.lmax = pl->lmax;
+    a.max_recs = pl->max_chunk_recs > 0 ? pl->max_chunk_recs : 4;
+    a.max_bnodes = pl->max_bnodes + (pl->max_bnodes & 1);
+    if (const char* dbg = getenv("TGK_FUSED_DEBUG")) a.debug = atoi(dbg);
+    DevBuf<long long> trace;
+    const char* trace_path = getenv("TGK_FUSED_TRACE");
+    if (trace_path) {
+        TGK_TRY(trace.alloc(pl->n_blocks * 8));
+        a.trace = trace.p;
+    }
     DevBuf<unsigned long long> bad;
     if (!d_bad) TGK_TRY(bad.alloc(1));
     a.bad = d_bad ? d_bad : bad.p;
     CUDA_TRY(cudaMemsetAsync(a.bad, 0xff, sizeof(unsigned long long), st));
     if (!has_f && F) CUDA_TRY(cudaMemsetAsync(F, 0, sizeof(double) * r->N, st));
     const int ktype = is_mass ? 1 : 0;
+    bool fdiv = false;
+    TGK_TRY(mesh_division_safe(const_cast<tgk_mesh*>(m), st, &fdiv));
+    if (getenv("TGK_IEEE_DIV")) fdiv = false;
     if (m->kind == TGK_TET4) {
-        if (degree == 1) TGK_TRY((dispatch_flags<TGK_TET4, 1>(ktype, has_m, has_f, a, pl.n_blocks, st)));
-        else TGK_TRY((dispatch_flags<TGK_TET4, 2>(ktype, has_m, has_f, a, pl.n_blocks, st)));
+        if (degree == 1) TGK_TRY((dispatch_flags<TGK_TET4, 1>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, st)));
+        else TGK_TRY((dispatch_flags<TGK_TET4, 2>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, st)));
     } else {
-        if (degree == 1) TGK_TRY((dispatch_flags<TGK_TRI3, 1>(ktype, has_m, has_f, a, pl.n_blocks, st)));
-        else TGK_TRY((dispatch_flags<TGK_TRI3, 2>(ktype, has_m, has_f, a, pl.n_blocks, st)));
+        if (degree == 1) TGK_TRY((dispatch_flags<TGK_TRI3, 1>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, st)));
+        else TGK_TRY((dispatch_flags<TGK_TRI3, 2>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, st)));
+    }
+    if (trace_path) {
+        std::vector<long long> h(pl->n_blocks * 8);
+        CUDA_TRY(cudaMemcpyAsync(h.data(), trace.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (FILE* f = fopen(trace_path, "wb")) {
+            fwrite(h.data(), 8, h.size(), f);
+            fclose(f);
+        }
     }
     if (!d_bad) return check_bad(bad.p, st);
     return TGK_OK;  // asynchronous: the caller inspects *d_bad

@@ -150,7 +150,6 @@ static double centroid_det(int kind, const double* nodes, const int64_t* conn) {
            J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
 }
 
-int ensure_plan(tgk_routing* r);
 int narrow_connectivity(const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
                         cudaStream_t st);
 int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
@@ -417,8 +416,10 @@ int tgk_mesh_create_d(int kind, const double* d_nodes, int64_t n_nodes, const in
 
 int tgk_mesh_upload(tgk_mesh* m, const double* nodes, const int64_t* elems, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (nodes)
+    if (nodes) {
         HCUDA(cudaMemcpyAsync(m->nodes, nodes, sizeof(double) * m->N * m->d, cudaMemcpyHostToDevice, st));
+        m->div_safe = -1;  // re-certified lazily by the fused path
+    }
     if (elems) {
         // int64 connectivity goes over PCIe as is and is narrowed (and range
         // checked, mesh.cpp:61-64) by a device kernel
@@ -463,29 +464,22 @@ int tgk_mesh_info(const tgk_mesh* m, int* kind, int64_t* n_nodes, int64_t* n_ele
 int tgk_routing_set_owned_rows(tgk_routing* r, int64_t lo, int64_t hi) {
     tgk_routing* s = r->scalar ? r->scalar : r;
     if (lo < 0 || hi > s->N || lo > hi) return set_error(TGK_ERR_INPUT, "owned row range out of bounds");
-    if (s->has_plan && s->own_lo == lo && s->own_hi == hi) return TGK_OK;
-    if (s->has_plan) {
-        for (void* p : {(void*)s->plan.row_off, (void*)s->plan.rows, (void*)s->plan.halo_off,
-                        (void*)s->plan.halo, (void*)s->plan.chunk_off, (void*)s->plan.chunk_rec_off,
-                        (void*)s->plan.chunk_cnt, (void*)s->plan.recs})
-            if (p) cudaFree(p);
-        s->plan = PlanDev{};
-        s->has_plan = false;
-    }
+    if (s->own_lo == lo && s->own_hi == hi) return TGK_OK;
+    for (auto& pl : s->plan) pl.release();
     s->own_lo = lo;
     s->own_hi = hi;
     return TGK_OK;
 }
 
 // Plan statistics: blocks, halo elements (recompute factor = halo / E), records, bytes.
-int tgk_routing_plan_stats(tgk_routing* r, int64_t* n_blocks, int64_t* n_halo, int64_t* n_records,
-                           int64_t* bytes) {
-    TGK_TRY(ensure_plan(r));
-    tgk_routing* s = r->scalar ? r->scalar : r;
-    if (n_blocks) *n_blocks = s->plan.n_blocks;
-    if (n_halo) *n_halo = s->plan.n_halo;
-    if (n_records) *n_records = s->plan.n_records;
-    if (bytes) *bytes = s->plan.bytes;
+int tgk_routing_plan_stats(tgk_routing* r, int rows_per_block, int64_t* n_blocks, int64_t* n_halo,
+                           int64_t* n_records, int64_t* bytes) {
+    const PlanDev* pl = nullptr;
+    TGK_TRY(ensure_plan(r, rows_per_block == 128 || rows_per_block == 64 ? rows_per_block : 256, &pl));
+    if (n_blocks) *n_blocks = pl->n_blocks;
+    if (n_halo) *n_halo = pl->n_halo;
+    if (n_records) *n_records = pl->n_records;
+    if (bytes) *bytes = pl->bytes;
     return TGK_OK;
 }
 
@@ -516,10 +510,22 @@ int tgk_routing_save(const tgk_routing* r, uint64_t mesh_hash, const char* path)
 
 namespace tgk {
 
-// Build (once) and upload the fused row-block plan of a scalar routing.
-int ensure_plan(tgk_routing* rr) {
+void PlanDev::release() {
+    for (void* p : {(void*)row_off, (void*)rows, (void*)rows_rp, (void*)halo_off, (void*)halo, (void*)bnode_off,
+                    (void*)bnodes, (void*)halo_lconn,
+                    (void*)chunk_off, (void*)chunk_rec_off, (void*)chunk_row_off, (void*)recs})
+        if (p) cudaFree(p);
+    *this = PlanDev{};
+}
+
+// Build (once per R) and upload the fused row-block plan of a scalar routing.
+int ensure_plan(tgk_routing* rr, int R, const PlanDev** out) {
     tgk_routing* r = rr->scalar ? rr->scalar : rr;
-    if (r->has_plan) return TGK_OK;
+    PlanDev& D = r->plan[plan_slot(R)];
+    if (D.R == R) {
+        *out = &D;
+        return TGK_OK;
+    }
     const tgk_mesh* m = r->mesh;
     const int k = m->k, d = m->d;
     std::vector<double> nodes(m->N * d);
@@ -535,15 +541,16 @@ int ensure_plan(tgk_routing* rr) {
     PlanHost P;
     const int64_t lo = r->own_hi < 0 ? 0 : r->own_lo, hi = r->own_hi < 0 ? r->N : r->own_hi;
     TGK_TRY(build_plan(m->kind, m->N, m->E, nodes.data(), conn.data(), row_ptr.data(), vo.data(),
-                       vs.data(), slot.data(), lo, hi, P));
-    PlanDev& D = r->plan;
+                       vs.data(), slot.data(), lo, hi, R, P));
+    D = PlanDev{};
     D.n_blocks = P.n_blocks;
     D.lmax = P.lmax;
+    D.max_chunk_recs = P.max_chunk_recs;
     D.n_halo = static_cast<int64_t>(P.halo.size());
     D.n_records = static_cast<int64_t>(P.recs.size());
     auto up = [&D](auto*& dst, const auto& v) -> int {
         using T = typename std::remove_reference<decltype(v)>::type::value_type;
-        const size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+        const size_t bytes = std::max<size_t>(16, v.size() * sizeof(T));
         HCUDA(cudaMalloc(reinterpret_cast<void**>(&dst), bytes));
         if (!v.empty()) HCUDA(cudaMemcpy(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
         D.bytes += static_cast<int64_t>(bytes);
@@ -551,13 +558,19 @@ int ensure_plan(tgk_routing* rr) {
     };
     TGK_TRY(up(D.row_off, P.row_off));
     TGK_TRY(up(D.rows, P.rows));
+    TGK_TRY(up(D.rows_rp, P.rows_rp));
     TGK_TRY(up(D.halo_off, P.halo_off));
     TGK_TRY(up(D.halo, P.halo));
+    TGK_TRY(up(D.bnode_off, P.bnode_off));
+    TGK_TRY(up(D.bnodes, P.bnodes));
+    TGK_TRY(up(D.halo_lconn, P.halo_lconn));
+    D.max_bnodes = P.max_bnodes;
     TGK_TRY(up(D.chunk_off, P.chunk_off));
     TGK_TRY(up(D.chunk_rec_off, P.chunk_rec_off));
-    TGK_TRY(up(D.chunk_cnt, P.chunk_cnt));
+    TGK_TRY(up(D.chunk_row_off, P.chunk_row_off));
     TGK_TRY(up(D.recs, P.recs));
-    r->has_plan = true;
+    D.R = R;
+    *out = &D;
     return TGK_OK;
 }
 

@@ -6,7 +6,8 @@
 // the element-to-slot map slot_of.  Steps:
 //  1. order nodes along a Morton curve of their coordinates and cut the order
 //     into blocks of kRowsPerBlock nodes (compact in space => small halos);
-//  2. per block, the halo = sorted unique elements incident to its nodes;
+//  2. per block, the halo = unique elements incident to its nodes, ordered by
+//     level in the per-row precedence chains (see below), then id;
 //  3. per block and halo chunk, one packed record per (owned row, incident
 //     element): element index within the chunk, local node a, and the CSR
 //     position (t - row_ptr[row]) of each of the element's nodes in the row.
@@ -45,11 +46,12 @@ uint64_t spread2(uint64_t x) {  // 32 bits -> every second bit
 
 int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
                const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
-               const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, PlanHost& P) {
+               const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int R, PlanHost& P) {
     const int d = element_dim(kind), k = element_nodes(kind);
     (void)E;
-    (void)conn;
-    // --- 1. Morton order of the nodes
+    if (R != 64 && R != 128 && R != 256) return set_error(TGK_ERR_INPUT, "fused plan: R must be 64, 128 or 256");
+    P.R = R;
+    // --- 1. Morton order of the owned nodes
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (int64_t i = 0; i < N; ++i)
         for (int c = 0; c < d; ++c) {
@@ -62,7 +64,6 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
         return s > 0 ? s : 1.0;
     }();
     const double scale = (d == 3 ? double((1u << 21) - 1) : double(0xffffffffu)) / span;
-    // only the owned row range [row_lo, row_hi) gets blocks (row-owning partitions)
     std::vector<std::pair<uint64_t, uint32_t>> key;
     key.reserve(static_cast<size_t>(row_hi - row_lo));
     for (int64_t i = row_lo; i < row_hi; ++i) {
@@ -82,23 +83,28 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
         return set_error(TGK_ERR_INPUT, "fused plan: CSR row longer than " +
                                             std::to_string(kMaxRowLen) + " entries");
     P.lmax = lmax;
-    const int64_t nb = (n_owned + kRowsPerBlock - 1) / kRowsPerBlock;
+    const int64_t nb = (n_owned + R - 1) / R;
     P.n_blocks = nb;
     P.row_off.resize(nb + 1);
     P.rows.resize(n_owned);
-    for (int64_t b = 0; b <= nb; ++b) P.row_off[b] = std::min<int64_t>(b * kRowsPerBlock, n_owned);
+    for (int64_t b = 0; b <= nb; ++b) P.row_off[b] = std::min<int64_t>(b * R, n_owned);
     for (int64_t b = 0; b < nb; ++b) {
         for (int64_t i = P.row_off[b]; i < P.row_off[b + 1]; ++i) P.rows[i] = key[i].second;
         std::sort(P.rows.begin() + P.row_off[b], P.rows.begin() + P.row_off[b + 1]);
     }
     key.clear();
     key.shrink_to_fit();
+    P.rows_rp.resize(n_owned + 1);
+    for (int64_t i = 0; i < n_owned; ++i)  // CSR offset | row length << 56
+        P.rows_rp[i] = row_ptr[P.rows[i]] | ((row_ptr[P.rows[i] + 1] - row_ptr[P.rows[i]]) << 56);
+    P.rows_rp[n_owned] = 0;
 
     // --- 2/3. halos and records, blocks in parallel
+    const int ros = row_off_stride(R);
     struct BlockOut {
         std::vector<uint32_t> halo;
-        std::vector<uint8_t> cnt;   // nch x kRowsPerBlock
-        std::vector<uint32_t> recs;
+        std::vector<uint16_t> row_off;  // nch x ros
+        std::vector<uint32_t> recs;     // chunk segments, each padded to a multiple of 4
         std::vector<int64_t> chunk_sizes;
     };
     std::vector<BlockOut> out(nb);
@@ -115,35 +121,74 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
             }
             std::sort(tmp.begin(), tmp.end());
             tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-            o.halo = tmp;
-            const int64_t nh = static_cast<int64_t>(o.halo.size());
-            const int64_t nch = (nh + kChunk - 1) / kChunk;
-            o.cnt.assign(nch * kRowsPerBlock, 0);
+            const int64_t nh = static_cast<int64_t>(tmp.size());
+            // Level schedule: every owned row's elements must be folded in
+            // ascending id, i.e. they form a chain; level(e) = longest chain
+            // ending at e.  Ordering the halo by (level, id) keeps each row's
+            // elements ascending across and within chunks while giving every
+            // row at most one element per level -> balanced phase B.
+            std::vector<int> level(nh, 0);
+            {
+                std::vector<std::pair<uint32_t, uint32_t>> edges;  // (next, pred) as halo indices
+                for (int64_t i = rs; i < re; ++i) {
+                    const uint32_t row = P.rows[i];
+                    int64_t prev = -1;
+                    for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s) {
+                        const uint32_t e = vec_slots[s] / k;
+                        const int64_t hix = std::lower_bound(tmp.begin(), tmp.end(), e) - tmp.begin();
+                        if (prev >= 0) edges.push_back({static_cast<uint32_t>(hix), static_cast<uint32_t>(prev)});
+                        prev = hix;
+                    }
+                }
+                std::sort(edges.begin(), edges.end());  // by target: a topological order
+                for (const auto& ed : edges) level[ed.first] = std::max(level[ed.first], level[ed.second] + 1);
+            }
+            std::vector<std::pair<int, uint32_t>> order(nh);
+            for (int64_t h = 0; h < nh; ++h) order[h] = {level[h], tmp[h]};
+            std::sort(order.begin(), order.end());
+            o.halo.resize(nh);
+            std::vector<std::pair<uint32_t, uint32_t>> where(nh);  // (element, position)
+            for (int64_t h = 0; h < nh; ++h) {
+                o.halo[h] = order[h].second;
+                where[h] = {order[h].second, static_cast<uint32_t>(h)};
+            }
+            std::sort(where.begin(), where.end());
+            const int64_t nch = (nh + R - 1) / R;
             // records grouped chunk-major, then row, ascending element within a row
             std::vector<std::vector<uint32_t>> per_chunk(nch);
+            std::vector<std::vector<uint16_t>> cnt(nch, std::vector<uint16_t>(R, 0));
             for (int64_t i = rs; i < re; ++i) {
                 const int lr = static_cast<int>(i - rs);
                 const uint32_t row = P.rows[i];
                 const int64_t rp = row_ptr[row];
-                int64_t hpos = 0;
                 for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s) {
                     const uint32_t slot = vec_slots[s];
                     const uint32_t e = slot / k;
                     const int a = static_cast<int>(slot % k);
-                    while (o.halo[hpos] != e) ++hpos;  // both ascending
-                    const int64_t ch = hpos / kChunk;
+                    const int64_t hpos =
+                        std::lower_bound(where.begin(), where.end(), std::make_pair(e, 0u))->second;
+                    const int64_t ch = hpos / R;
                     int pos[4] = {0, 0, 0, 0};
                     for (int bb = 0; bb < k; ++bb)
                         pos[bb] = static_cast<int>(slot_of[static_cast<int64_t>(slot) * k + bb] - rp);
-                    per_chunk[ch].push_back(pack_rec(static_cast<int>(hpos % kChunk), a, pos, k));
-                    ++o.cnt[ch * kRowsPerBlock + lr];
+                    per_chunk[ch].push_back(pack_rec(static_cast<int>(hpos % R), a, pos, k));
+                    ++cnt[ch][lr];
                 }
             }
             o.chunk_sizes.resize(nch);
+            o.row_off.assign(nch * ros, 0);
             for (int64_t ch = 0; ch < nch; ++ch) {
                 // per_chunk[ch] was appended row by row in ascending row order: already grouped
-                o.chunk_sizes[ch] = static_cast<int64_t>(per_chunk[ch].size());
-                o.recs.insert(o.recs.end(), per_chunk[ch].begin(), per_chunk[ch].end());
+                uint16_t acc = 0;
+                for (int lr = 0; lr < R; ++lr) {
+                    o.row_off[ch * ros + lr] = acc;
+                    acc = static_cast<uint16_t>(acc + cnt[ch][lr]);
+                }
+                for (int j = R; j < ros; ++j) o.row_off[ch * ros + j] = acc;
+                auto& v = per_chunk[ch];
+                while (v.size() % 4) v.push_back(0);
+                o.chunk_sizes[ch] = static_cast<int64_t>(v.size());
+                o.recs.insert(o.recs.end(), v.begin(), v.end());
             }
         }
     };
@@ -165,22 +210,65 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
         P.chunk_off[b + 1] = P.chunk_off[b] + static_cast<int64_t>(out[b].chunk_sizes.size());
     }
     const int64_t total_chunks = P.chunk_off[nb];
+    for (int64_t b = 0; b < nb; ++b)
+        if (P.chunk_off[b + 1] - P.chunk_off[b] > 255)
+            return set_error(TGK_ERR_INPUT, "fused plan: a row block needs more than 255 halo chunks");
     P.halo.resize(P.halo_off[nb]);
-    P.chunk_cnt.resize(total_chunks * kRowsPerBlock);
+    P.halo_lconn.assign(P.halo.size() * 4, 0);
+    P.chunk_row_off.resize(total_chunks * ros);
     P.chunk_rec_off.assign(total_chunks + 1, 0);
     int64_t nrec = 0;
+    int maxrec = 0;
     for (int64_t b = 0; b < nb; ++b) {
         std::copy(out[b].halo.begin(), out[b].halo.end(), P.halo.begin() + P.halo_off[b]);
-        std::copy(out[b].cnt.begin(), out[b].cnt.end(), P.chunk_cnt.begin() + P.chunk_off[b] * kRowsPerBlock);
+        std::copy(out[b].row_off.begin(), out[b].row_off.end(), P.chunk_row_off.begin() + P.chunk_off[b] * ros);
         for (size_t ch = 0; ch < out[b].chunk_sizes.size(); ++ch) {
             P.chunk_rec_off[P.chunk_off[b] + ch] = nrec;
             nrec += out[b].chunk_sizes[ch];
+            maxrec = std::max<int>(maxrec, static_cast<int>(out[b].chunk_sizes[ch]));
         }
     }
     P.chunk_rec_off[total_chunks] = nrec;
+    P.max_chunk_recs = maxrec;
     P.recs.resize(nrec);
     for (int64_t b = 0; b < nb; ++b)
         std::copy(out[b].recs.begin(), out[b].recs.end(), P.recs.begin() + P.chunk_rec_off[P.chunk_off[b]]);
+    // block node tables (the halo's nodes, staged in shared memory by the
+    // kernel) and block-local connectivity
+    P.bnode_off.assign(nb + 1, 0);
+    std::vector<std::vector<uint32_t>> bn(nb);
+    auto node_work = [&](int64_t b_begin, int64_t b_end) {
+        for (int64_t b = b_begin; b < b_end; ++b) {
+            auto& v = bn[b];
+            for (int64_t h = P.halo_off[b]; h < P.halo_off[b + 1]; ++h)
+                for (int a = 0; a < k; ++a) v.push_back(static_cast<uint32_t>(conn[static_cast<int64_t>(P.halo[h]) * k + a]));
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+            for (int64_t h = P.halo_off[b]; h < P.halo_off[b + 1]; ++h)
+                for (int a = 0; a < k; ++a) {
+                    const uint32_t g = static_cast<uint32_t>(conn[static_cast<int64_t>(P.halo[h]) * k + a]);
+                    P.halo_lconn[h * 4 + a] = static_cast<uint16_t>(std::lower_bound(v.begin(), v.end(), g) - v.begin());
+                }
+        }
+    };
+    {
+        std::vector<std::thread> pool;
+        const int64_t per = (nb + nthreads - 1) / nthreads;
+        for (int t = 0; t < nthreads; ++t) {
+            const int64_t b0 = t * per, b1 = std::min(nb, b0 + per);
+            if (b0 < b1) pool.emplace_back(node_work, b0, b1);
+        }
+        for (auto& th : pool) th.join();
+    }
+    int maxbn = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        P.bnode_off[b + 1] = P.bnode_off[b] + static_cast<int64_t>(bn[b].size());
+        maxbn = std::max<int>(maxbn, static_cast<int>(bn[b].size()));
+    }
+    if (maxbn > 65535) return set_error(TGK_ERR_INPUT, "fused plan: block node table exceeds 65535 nodes");
+    P.max_bnodes = maxbn;
+    P.bnodes.resize(P.bnode_off[nb]);
+    for (int64_t b = 0; b < nb; ++b) std::copy(bn[b].begin(), bn[b].end(), P.bnodes.begin() + P.bnode_off[b]);
     return TGK_OK;
 }
 

@@ -361,18 +361,10 @@ tgk_routing::~tgk_routing() {
                     (void*)vec_slots, (void*)mat_offsets, (void*)mat_slots, (void*)scratch_K,
                     (void*)scratch_F, (void*)scratch_M})
         if (p) cudaFree(p);
-    if (has_plan) {
-        for (void* p : {(void*)plan.row_off, (void*)plan.rows, (void*)plan.halo_off,
-                        (void*)plan.halo, (void*)plan.chunk_off, (void*)plan.chunk_rec_off,
-                        (void*)plan.chunk_cnt, (void*)plan.recs})
-            if (p) cudaFree(p);
-    }
+    for (auto& pl : plan) pl.release();
     if (scalar && scalar != this) delete scalar;
 }
 
-namespace tgk {
-int ensure_plan(tgk_routing* r);
-}
 
 extern "C" {
 

@@ -349,6 +349,36 @@ __global__ void k_narrow(const int64_t* src, int64_t n, int64_t n_nodes, int32_t
 
 }  // namespace
 
+// Division-safety certificate of a mesh (element.cuh ExactDiv): every
+// coordinate is 0 or has 2^-40 <= |x| <= 2^40.
+__global__ void k_coord_range(const double* x, int64_t n, unsigned* bad) {
+    unsigned b = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double a = fabs(x[i]);
+        b |= (a != 0.0 && (a < 0x1p-40 || a > 0x1p40)) ? 1u : 0u;  // NaN/inf: > fails, < fails...
+        b |= (a != a || a == __longlong_as_double(0x7ff0000000000000ll)) ? 1u : 0u;
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+int mesh_division_safe(tgk_mesh* m, cudaStream_t st, bool* safe) {
+    if (m->div_safe < 0) {
+        DevBuf<unsigned> flag;
+        TGK_TRY(flag.alloc(1));
+        CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(unsigned), st));
+        const int64_t n = m->N * m->d;
+        k_coord_range<<<std::min<unsigned>(grid_for(n, 256), 148 * 8), 256, 0, st>>>(m->nodes, n, flag.p);
+        KERNEL_CHECK("coord_range");
+        unsigned h = 1;
+        CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        m->div_safe = h == 0 ? 1 : 0;
+    }
+    *safe = m->div_safe == 1;
+    return TGK_OK;
+}
+
 int narrow_connectivity(const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
                         cudaStream_t st) {
     DevBuf<unsigned long long> flag;

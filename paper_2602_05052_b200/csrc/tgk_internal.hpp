@@ -31,58 +31,82 @@ inline int element_nodes(int kind) { return kind == TGK_TRI3 ? 3 : 4; }
 
 // ----------------------------------------------------------------- fused plan
 // Row-block ("node block") plan for the fused Map+Reduce kernel.  Each CUDA
-// block owns a set of CSR rows (mesh nodes) and recomputes every element
-// incident to them ("halo"), in ascending element order, in chunks of
-// kChunk elements.  For every owned row the incidences (element, local node
-// a, CSR positions of the element's nodes within the row) are stored per
-// chunk as packed 32-bit records, grouped by row, ascending element within
-// a row — so each CSR value is folded in ascending element order, the
+// block owns R CSR rows (mesh nodes, compact in space) and recomputes every
+// element incident to them ("halo"), in ascending element order, in chunks of
+// R elements (one per thread).  For every owned row the incidences (element,
+// local node a, CSR positions of the element's nodes within the row) are
+// stored per chunk as packed 32-bit records, grouped by row, ascending element
+// within a row — so each CSR value is folded in ascending element order, the
 // reference's order (routing.cpp:117-124).
-constexpr int kRowsPerBlock = 256;  // owned rows per CUDA block (= threads)
-constexpr int kChunk = 256;         // halo elements per chunk (= threads)
-constexpr int kMaxRowLen = 32;      // CSR row length limit of the packed record (5-bit positions)
+constexpr int kMaxRowLen = 32;  // CSR row length limit of the packed record (5-bit positions)
+constexpr int kPlanSlots = 3;   // plans cached per routing: R = 64, 128, 256
+
+inline int plan_slot(int R) { return R == 64 ? 2 : (R == 128 ? 0 : 1); }
 
 struct PlanHost {
+    int R = 256;                         // rows per block = elements per chunk
     int64_t n_blocks = 0;
     int lmax = 0;                        // max CSR row length
+    int max_chunk_recs = 0;              // largest record segment of one chunk (padded)
     std::vector<int64_t> row_off;        // n_blocks+1 into rows
     std::vector<uint32_t> rows;          // owned node ids, ascending within a block
+    std::vector<int64_t> rows_rp;        // per owned row: row_ptr[row] | row length << 56
     std::vector<int64_t> halo_off;       // n_blocks+1 into halo
-    std::vector<uint32_t> halo;          // incident element ids, ascending within a block
+    std::vector<uint32_t> halo;          // incident element ids, level-ordered within a block
+    int max_bnodes = 0;                  // largest block node table
+    std::vector<int64_t> bnode_off;      // n_blocks+1 into bnodes
+    std::vector<uint32_t> bnodes;        // per block: sorted unique nodes of its halo elements
+    std::vector<uint16_t> halo_lconn;    // 4 block-local node indices per halo element (TRI3: 4th = 0)
     std::vector<int64_t> chunk_off;      // per block: first chunk index (n_blocks+1)
-    std::vector<int64_t> chunk_rec_off;  // per chunk: first record (total_chunks+1)
-    std::vector<uint8_t> chunk_cnt;      // per chunk x kRowsPerBlock: records of that row in the chunk
-    std::vector<uint32_t> recs;          // packed records
+    std::vector<int64_t> chunk_rec_off;  // per chunk: first record (multiple of 4), total+1
+    std::vector<uint16_t> chunk_row_off; // per chunk: R+8 u16 row offsets into its records
+    std::vector<uint32_t> recs;          // packed records (chunk segments padded to 16 B)
 };
 
 struct PlanDev {
+    int R = 0;
     int64_t n_blocks = 0;
     int lmax = 0;
+    int max_chunk_recs = 0;
     int64_t* row_off = nullptr;
     uint32_t* rows = nullptr;
+    int64_t* rows_rp = nullptr;
     int64_t* halo_off = nullptr;
     uint32_t* halo = nullptr;
+    int max_bnodes = 0;
+    int64_t* bnode_off = nullptr;
+    uint32_t* bnodes = nullptr;
+    uint16_t* halo_lconn = nullptr;
     int64_t* chunk_off = nullptr;
     int64_t* chunk_rec_off = nullptr;
-    uint8_t* chunk_cnt = nullptr;
+    uint16_t* chunk_row_off = nullptr;
     uint32_t* recs = nullptr;
     int64_t bytes = 0;
     int64_t n_halo = 0, n_records = 0;
+    void release();
 };
 
-// record layout: bits 0-7 element index within the chunk, 8-9 local node a,
-// 10+5b.. CSR position of local node b's column within the row.
+inline int row_off_stride(int R) { return R + 8; }  // u16 entries per chunk (16-byte multiple)
+
+// record layout: bits 0-7 element index within the chunk, 8-9 local node a
+// (the element's node that is this row), 10-14 / 15-19 / 20-24 CSR positions
+// (within the row) of the element's OTHER nodes b != a in ascending b,
+// 25-29 the row's diagonal position.  The fused kernel stores each local
+// tensor row a "rotated" to match: [K_aa, K_ab for b != a ascending].
 TGK_HD inline uint32_t pack_rec(int hl, int a, const int* pos, int k) {
     uint32_t r = uint32_t(hl) | (uint32_t(a) << 8);
-    for (int b = 0; b < k; ++b) r |= uint32_t(pos[b]) << (10 + 5 * b);
-    return r;
+    int j = 0;
+    for (int b = 0; b < k; ++b)
+        if (b != a) r |= uint32_t(pos[b]) << (10 + 5 * j++);
+    return r | (uint32_t(pos[a]) << 25);
 }
 
 // Builds the plan on the host from the scalar routing (row_ptr, vec segment
-// map = node->incidence CSR in ascending slot order, slot_of).
+// map = node->incidence CSR in ascending slot order, slot_of) for the owned
+// row range [row_lo, row_hi) with R rows per block.
 int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
                const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
-               const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, PlanHost& out);
+               const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int R, PlanHost& out);
 
 }  // namespace tgk
 
@@ -91,9 +115,10 @@ struct tgk_mesh {
     int kind = TGK_TET4;
     int d = 3, k = 4;
     int64_t N = 0, E = 0;
-    double* nodes = nullptr;  // device, N x d
-    int32_t* conn = nullptr;  // device, E x k
+    double* nodes = nullptr;     // device, N x d
+    int32_t* conn = nullptr;     // device, E x k
     int64_t* staging = nullptr;  // device int64 connectivity staging for host uploads
+    int div_safe = -1;           // coordinates certified for Markstein division (-1 unknown)
     bool owned = false;
 };
 
@@ -111,11 +136,15 @@ struct tgk_routing {
     uint32_t* mat_slots = nullptr;
     // scalar (node-level) routing used by vector problems and the fused plan
     tgk_routing* scalar = nullptr;   // == this for components == 1
-    tgk::PlanDev plan;
-    bool has_plan = false;
+    tgk::PlanDev plan[tgk::kPlanSlots];
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
     double* scratch_K = nullptr;     // device output buffers of the host-buffer entry point
     double* scratch_F = nullptr;
     double* scratch_M = nullptr;
     ~tgk_routing();
 };
+
+namespace tgk {
+// Build (once per R) and upload the fused plan of the routing's scalar part.
+int ensure_plan(tgk_routing* r, int R, const PlanDev** out);
+}

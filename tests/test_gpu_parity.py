@@ -335,3 +335,21 @@ def test_c2_size_properties(eng):
     # stiffness is bitwise symmetric (K_e symmetric, same fold order)
     perm = np.lexsort((rows, h["cols"]))  # (col,row) order = transpose
     assert_bitwise(Kn[perm], Kn[np.lexsort((h["cols"], rows))])
+
+
+@pytest.mark.parametrize("scale", [2.0 ** -30, 1e-15, 3.0e12])
+def test_division_paths_bit_exact(eng, scale):
+    """Certified meshes use the Markstein division, uncertified ones (tiny or huge
+    coordinates) IEEE division; both must reproduce the reference bit for bit."""
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [7, 6, 5])
+    nodes = nodes * scale + 0.37 * scale
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    r = eng.Routing(m, 1)
+    pr = port.Routing(nodes.shape[0], port.dofmap("tet4", elems, 1))
+    rho = 0.5 + np.random.default_rng(9).random(elems.shape[0])
+    K, F, M = eng.assemble(m, r, diffusion=("element", rho), sources=[1.0], with_mass=True)
+    Kr, Fr, Mr = port.assemble("tet4", nodes, elems, pr, diffusion=("element", rho), sources=[1.0],
+                               with_mass=True)
+    assert_bitwise(np_(K), Kr)
+    assert_bitwise(np_(F), Fr)
+    assert_bitwise(np_(M), Mr)
