@@ -44,6 +44,35 @@ uint64_t spread2(uint64_t x) {  // 32 bits -> every second bit
 
 }  // namespace
 
+// Owned rows [row_lo, row_hi) in Morton order of their coordinates.
+std::vector<uint32_t> morton_order(int kind, int64_t N, const double* nodes, int64_t row_lo, int64_t row_hi) {
+    const int d = element_dim(kind);
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int64_t i = 0; i < N; ++i)
+        for (int c = 0; c < d; ++c) {
+            lo[c] = std::min(lo[c], nodes[i * d + c]);
+            hi[c] = std::max(hi[c], nodes[i * d + c]);
+        }
+    double span = 0;
+    for (int c = 0; c < d; ++c) span = std::max(span, hi[c] - lo[c]);
+    if (!(span > 0)) span = 1.0;
+    const double scale = (d == 3 ? double((1u << 21) - 1) : double(0xffffffffu)) / span;
+    std::vector<std::pair<uint64_t, uint32_t>> key;
+    key.reserve(static_cast<size_t>(row_hi - row_lo));
+    for (int64_t i = row_lo; i < row_hi; ++i) {
+        uint64_t m = 0;
+        for (int c = 0; c < d; ++c) {
+            const uint64_t q = static_cast<uint64_t>((nodes[i * d + c] - lo[c]) * scale);
+            m |= (d == 3 ? spread3(q) : spread2(q)) << c;
+        }
+        key.push_back({m, static_cast<uint32_t>(i)});
+    }
+    std::sort(key.begin(), key.end());
+    std::vector<uint32_t> out(key.size());
+    for (size_t i = 0; i < key.size(); ++i) out[i] = key[i].second;
+    return out;
+}
+
 int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
                const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
                const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int R, PlanHost& P) {

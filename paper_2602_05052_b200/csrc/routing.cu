@@ -362,6 +362,7 @@ tgk_routing::~tgk_routing() {
                     (void*)scratch_F, (void*)scratch_M})
         if (p) cudaFree(p);
     for (auto& pl : plan) pl.release();
+    plan4.release();
     if (scalar && scalar != this) delete scalar;
 }
 
