@@ -1,27 +1,41 @@
 """Benchmark of the fused P1 assembly hot path (BASELINE.json metric).
 
     python bench.py [--gpus N --steps K --warmup W] [--workload c2] [--impl reference]
+                    [--dist-mode exchange|halo]
 
 A step is one tg::assemble-equivalent pass (Map fused with Reduce) over the
-workload's mesh.  Default workload = BASELINE.json configs[1] ("C2"): 3D Poisson
-P1 tet stiffness + mass + load on the unit-cube Kuhn grid 100^3 (6,000,000
-tets), fp64.  Under torchrun each rank owns a z-slab of 100 cube layers of a
-100 x 100 x (100 N) grid (row-owning partition, halo elements recomputed, no
-data-path collective) -> weak scaling, results bitwise identical to one GPU.
+workload's mesh.  Workloads (BASELINE.json configs):
 
-value     = assembled elements / s over all ranks, inputs resident in HBM
-            (device time, CUDA events on the launching stream, max over ranks)
-e2e       = the same metric through the host-buffer C-ABI call (tgk_assemble):
-            per step H2D of the mesh (pinned host -> device) and D2H of K, M, F
-roofline  = algorithmic bytes / measured step time vs the
-            measured HBM copy peak (MEASURED_PEAKS.json)
+  c2   (default, configs[1]) 3D Poisson P1 tet K+M+F, unit-cube Kuhn 100^3 per GPU
+       (6,000,000 tets), fp64, Q=4; weak scaling: rank r owns a z-slab of 100
+       cube layers of a 100 x 100 x (100 N) grid
+  c2a  the same mesh, K+F at Q=1 (the north-star target case)
+  c1   (configs[0]) 2D Poisson P1 K+F, unit square 256x256 (131k tris)
+  c3   (configs[2]) 3D linear elasticity (3x3 blocks), Kuhn 100^3 per GPU, K+F
+  c4   (configs[3]) 256 per-element coefficient fields on the 2D unstructured
+       C4 mesh (131k tris): batched K_b (+F) and the adjoint transpose gather;
+       fields sharded across GPUs (strong scaling)
+  c5   (configs[4]) Kuhn 256^3 (100.7M tets) split into N z-slabs (strong scaling)
+
+Multi-GPU (tet4 scalar workloads): --dist-mode exchange (default) assembles
+each rank's own elements and sums the interface node layer over NCCL
+(paper_2602_05052_b200/dist.py); --dist-mode halo recomputes the halo layer
+instead (no data-path collective, bitwise equal to one GPU).
+
+value     = elements/s over all ranks, inputs resident in HBM (device time of
+            the whole step, CUDA events on the launching stream, max over ranks)
+e2e       = the same metric through the public C ABI with host buffers:
+            H2D of the mesh from pinned memory, assembly, D2H of the outputs
+roofline  = SURVEY.md 8(d) algorithmic bytes of the dominant kernel per launch
+            / that kernel's event-timed duration, vs MEASURED_PEAKS.json
 cpu_baseline = the reference library (oracle/_ref, compiled from the reference
-            sources) on the box's host cores, bounded sample, rank 0 only
+            sources) on the box's host cores, bounded sample, rank 0 at N=1
 --impl reference runs that reference CPU implementation as the timed arm.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -38,15 +52,26 @@ sys.path.insert(0, ROOT)
 METRIC = "assembled elements/sec and achieved HBM GB/s (% roofline) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "elements/s"
 
+# name: (kind, divisions per rank or global, problem kwargs, description, scaling)
 WORKLOADS = {
-    # name: (kind, divisions per rank, problem kwargs, description)
     "c2": ("tet4", (100, 100, 100), dict(sources=[1.0], with_mass=True),
-           "C2: 3D Poisson P1 tet K+M+F, unit-cube Kuhn 100^3 (6M tets), fp64, Q=4"),
+           "C2: 3D Poisson P1 tet K+M+F, unit-cube Kuhn 100^3 (6M tets) per GPU, fp64, Q=4", "weak"),
     "c2a": ("tet4", (100, 100, 100), dict(sources=[1.0]),
-            "C2a: 3D Poisson P1 tet K+F, unit-cube Kuhn 100^3 (6M tets), fp64, Q=1"),
+            "C2a: 3D Poisson P1 tet K+F, unit-cube Kuhn 100^3 (6M tets) per GPU, fp64, Q=1", "weak"),
     "c1": ("tri3", (256, 256), dict(sources=[1.0]),
-           "C1: 2D Poisson P1 K+F, unit square 256x256 (131k tris), fp64"),
+           "C1: 2D Poisson P1 K+F, unit square 256x256 (131k tris), fp64, Q=1", "weak"),
+    "c3": ("tet4", (100, 100, 100), None,
+           "C3: 3D linear elasticity P1 tets (3x3 blocks), Kuhn 100^3 (6M tets) per GPU, E=1 nu=0.3, "
+           "body force (1,1,1), K+F, fp64", "weak"),
+    "c4": ("tri3", (256, 256), None,
+           "C4: 256 per-element coefficient fields on the 2D unstructured C4 mesh (131,072 tris, "
+           "jittered + random diagonals + permuted), batched K_b + F, with the adjoint transpose gather, fp64",
+           "strong"),
+    "c5": ("tet4", (256, 256, 256), dict(sources=[1.0]),
+           "C5: 3D Poisson P1 tet K+F, Kuhn 256^3 (100.7M tets) partitioned into z-slabs, fp64, Q=1", "strong"),
 }
+C4_FIELDS = 256
+LAME = (0.3 / (1.3 * 0.4), 1.0 / (2 * 1.3))  # lame_from_young(1, 0.3) (batch.cpp:353-357)
 
 
 def peaks():
@@ -58,46 +83,74 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def alg_bytes(kind, E, Nn, nnz, with_mass, has_f):
+def alg_bytes(kind, E, Nn, nnz, with_mass, has_f, comps=1):
     """SURVEY.md 8(d) algorithmic bytes: connectivity E*k*4 + coordinates N*d*8
-    + slot map E*k^2*4 + CSR values nnz*8 per matrix + load N*8."""
+    + slot map E*k^2*4 + CSR values nnz*8 per matrix + load N_dof*8
+    (+ scalar row_ptr (N+1)*4 for vector problems)."""
     k = 4 if kind == "tet4" else 3
     d = 3 if kind == "tet4" else 2
     b = E * k * 4 + Nn * d * 8 + E * k * k * 4 + nnz * 8 * (2 if with_mass else 1)
     if has_f:
-        b += Nn * 8
-    compulsory = b - E * k * k * 4
-    return b, compulsory
+        b += Nn * comps * 8
+    if comps > 1:
+        b += (Nn + 1) * 4
+    return b, b - E * k * k * 4
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region (NVML, ~1 ms
+    period; nvidia-smi fallback)."""
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def _run_nvml(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4}
+        while not self._stop.is_set():
+            self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            self.mx.append(mx)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for n, bit in names.items():
+                if r & bit:
+                    self.reasons.add(n)
+            time.sleep(0.001)
+
+    def _run_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip().split(",")
+                self.sm.append(float(out[0]))
+                self.mx.append(float(out[1]))
+                for i, n in enumerate(names):
+                    if out[2 + i].strip().lower().startswith("active"):
+                        self.reasons.add(n)
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.05)
+
+    def _run(self):
+        try:
+            self._run_nvml()
+        except Exception:
+            self._run_smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.01)
         return self
 
     def __exit__(self, *a):
@@ -105,52 +158,19 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.samples:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx),
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
-def slab_mesh(kind, div, rank, world):
-    """Rank `rank`'s z-slab of the global grid div[0] x div[1] x (div[2]*world):
-    cube layers [z0-1, z1) (one halo layer below for rank > 0), coordinates and
-    connectivity bit-identical to the global tg::generate_grid arrays.
-    Returns (nodes, elems, owned node range [lo, hi), global element offset)."""
-    from paper_2602_05052_b200 import tgfem
-    if world == 1:
-        m = tgfem.generate_grid(kind, [1.0] * len(div), list(div))
-        return m.nodes, m.elements, 0, m.node_count(), 0
-    nx, ny, nzr = div
-    nz = nzr * world
-    z0, z1 = rank * nzr, (rank + 1) * nzr
-    zl = z0 - 1 if rank > 0 else 0
-    # the global grid restricted to cube layers [zl, z1): generate the full-size
-    # index pattern on a local grid and shift (Kuhn split is translation invariant)
-    loc = tgfem.generate_grid(kind, [1.0, 1.0, 1.0], [nx, ny, z1 - zl])
-    hz = 1.0 / nz
-    nodes = loc.nodes.copy()
-    layer = (nx + 1) * (ny + 1)
-    kz = np.repeat(np.arange(zl, z1 + 1, dtype=np.int64), layer)
-    nodes[:, 2] = kz * hz                 # same expression as mesh.cpp:139 (kz * hz)
-    nodes[:, 0] = loc.nodes[:, 0]
-    nodes[:, 1] = loc.nodes[:, 1]
-    own_lo = (z0 - zl) * layer
-    own_hi = (z1 - zl) * layer + (layer if rank == world - 1 else 0)
-    return nodes, loc.elements, own_lo, own_hi, zl * nx * ny * 6
-
-
+# ------------------------------------------------------------------ reference (CPU) arm
 def cpu_reference_time(kind, divs, problem_kw, steps, warmup, threads=0):
     """Reference tg::assemble (oracle/_ref) on the host: returns (E, seconds list)."""
     from oracle import ref
     ref.set_threads(threads)
     m = ref.Mesh.grid(kind, [1.0] * len(divs), list(divs))
-    r = ref.Routing(m, 1)
+    r = ref.Routing(m, 3 if problem_kw.get("problem") == "elasticity" else 1)
     times = []
     for i in range(warmup + steps):
         *_, secs = ref.assemble(m, r, timing=True, **problem_kw)
@@ -159,8 +179,37 @@ def cpu_reference_time(kind, divs, problem_kw, steps, warmup, threads=0):
     return m.E, times
 
 
-def effective_cores():
-    return os.cpu_count() or 1
+def cpu_reference_c4(steps, warmup, fields=4, threads=0):
+    """B x (per-element evaluate + local_stiffness_diffusion + reduce_matrix) (+F) of the reference on
+    the C4 mesh, `fields` fields per step (a bounded sample of the 256-field batch)."""
+    from oracle import ref
+    from paper_2602_05052_b200 import meshgen
+    ref.set_threads(threads)
+    nodes, elems = meshgen.unstructured_tri(256)
+    m = ref.Mesh.from_arrays("tri3", nodes, elems)
+    r = ref.Routing(m, 1)
+    rho = meshgen.batch_fields(fields, elems.shape[0])
+    times = []
+    for i in range(warmup + steps):
+        t = 0.0
+        for b in range(fields):
+            *_, secs = ref.assemble(m, r, diffusion=("element", rho[b]), sources=[1.0] if b == 0 else [],
+                                    timing=True)
+            t += secs
+        if i >= warmup:
+            times.append(t)
+    return elems.shape[0] * fields, times
+
+
+def ref_problem_kw(workload):
+    kind, div, kw, desc, _ = WORKLOADS[workload]
+    if workload == "c3":
+        return dict(problem="elasticity", lam=LAME[0], mu=LAME[1], sources=[1.0, 1.0, 1.0])
+    return dict(kw or {})
+
+
+REF_SAMPLE = {"c2": (50, 50, 50), "c2a": (50, 50, 50), "c1": (256, 256), "c3": (30, 30, 30),
+              "c5": (64, 64, 64)}
 
 
 def run_reference(args):
@@ -168,29 +217,416 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    kind, div, kw, desc = WORKLOADS[args.workload]
+    kind, div, kw, desc, scaling = WORKLOADS[args.workload]
     from oracle import ref
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtgref.so not built"}))
         return
-    sample = tuple(args.ref_sample) if args.ref_sample else ((50, 50, 50) if kind == "tet4" else div)
-    E, times = cpu_reference_time(kind, sample, kw, args.steps, args.warmup)
+    if args.workload == "c4":
+        E, times = cpu_reference_c4(args.steps, args.warmup)
+        sample = f"C4 mesh, 4 of the 256 coefficient fields per step ({E} element-fields)"
+    else:
+        smp = tuple(args.ref_sample) if args.ref_sample else REF_SAMPLE[args.workload]
+        E, times = cpu_reference_time(kind, smp, ref_problem_kw(args.workload), args.steps, args.warmup)
+        sample = f"{kind} Kuhn {'x'.join(map(str, smp))} ({E} elements) per step"
     mean = statistics.mean(times)
     value = E / mean
     cores = ref.thread_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": desc, "sample": f"{kind} Kuhn {'x'.join(map(str, sample))} ({E} elements) "
-                   "per step (bounded sample of the workload)", "parallelism": f"{cores} host threads"},
+        "config": {"workload": desc, "sample": sample + " (bounded sample of the workload)",
+                   "parallelism": f"{cores} host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"tg::assemble on {kind} {'x'.join(map(str, sample))}, {E} elements, "
-                                   f"mean of {args.steps}"},
+                         "sample": f"tg::assemble, {sample}, mean of {args.steps}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+def cpu_baseline_line(workload):
+    try:
+        from oracle import ref
+        if not ref.available():
+            return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                    "sample": "oracle/_ref/libtgref.so not present"}
+        if workload == "c4":
+            E, times = cpu_reference_c4(2, 1)
+            sample = f"tg::assemble per field on the C4 mesh, 4 fields ({E} element-fields), best of 2"
+        else:
+            kind = WORKLOADS[workload][0]
+            smp = {"c2": (40, 40, 40), "c2a": (40, 40, 40), "c3": (25, 25, 25), "c5": (40, 40, 40)}.get(
+                workload, REF_SAMPLE.get(workload))
+            E, times = cpu_reference_time(kind, smp, ref_problem_kw(workload), 3, 1)
+            sample = (f"tg::assemble (oracle/_ref, reference sources) on {kind} Kuhn {'x'.join(map(str, smp))} "
+                      f"= {E} elements, best of 3")
+        return {"value": E / min(times), "unit": UNIT, "cores": ref.thread_count(), "kind": "reference",
+                "sample": sample}
+    except Exception as exc:  # reported, never fatal
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"error: {exc}"}
+
+
+# ------------------------------------------------------------------ our arm
+class Ctx:
+    def __init__(self, args):
+        import torch
+        self.torch = torch
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local_rank)
+        self.dev = torch.device("cuda", self.local_rank)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.dist = dist
+        self.stream = torch.cuda.current_stream()
+        self.sp = C.c_void_p(self.stream.cuda_stream)
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, x):
+        if not self.dist:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(self, step, steps, clocks=None):
+        """Device time (ms) of `steps` calls of step(), CUDA events on the stream, max over ranks."""
+        torch = self.torch
+        self.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(self.stream)
+        for _ in range(steps):
+            step()
+        ev1.record(self.stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        self.barrier()
+        return self.max_over_ranks(ms)
+
+
+def ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def run_scalar(args, ctx, N):
+    """c1 / c2 / c2a / c5: fused scalar assembly; tet4 meshes split into z-slabs."""
+    torch = ctx.torch
+    from paper_2602_05052_b200 import dist as D, engine, tgfem
+    kind, div, kw, desc, scaling = WORKLOADS[args.workload]
+    world, rank = ctx.world, ctx.rank
+    t0 = time.time()
+    if kind == "tet4":
+        per = tuple(div) if scaling == "weak" else (div[0], div[1], div[2] // world)
+        if scaling == "strong" and div[2] % world:
+            raise SystemExit(f"{args.workload}: {div[2]} cube layers do not split into {world} slabs")
+        s = D.slab(per, rank, world, args.dist_mode if world > 1 else "halo")
+        nodes, elems = D.slab_mesh(s)
+        parallelism = ("single GPU" if world == 1 else
+                       f"{world} row-owning z-slabs, " + ("own elements + NCCL interface-layer exchange"
+                                                          if s.mode == "exchange" else
+                                                          "halo recompute (no data-path collective)"))
+    else:
+        if world > 1:
+            parallelism = f"{world} independent replicas (2D mesh not partitioned)"
+        else:
+            parallelism = "single GPU"
+        m = tgfem.generate_grid(kind, [1.0] * len(div), list(div))
+        nodes, elems, s = m.nodes, m.elements, None
+    mesh = engine.DeviceMesh(kind, nodes, elems)
+    routing = engine.Routing(mesh, 1)
+    L = N.lib()
+    if s is not None and world > 1:
+        N.check(L.tgk_routing_set_owned_rows(routing._h, s.own_lo, s.calc_hi))
+        if s.mode == "exchange":
+            N.check(L.tgk_routing_set_element_range(routing._h, s.elem_lo, s.elem_hi))
+    nb, nh, nrec, pbytes = (C.c_int64() for _ in range(4))
+    N.check(L.tgk_routing_plan_stats(routing._h, 128, C.byref(nb), C.byref(nh), C.byref(nrec), C.byref(pbytes)))
+    setup_s = time.time() - t0
+    with_mass = kw.get("with_mass", False)
+    has_f = bool(kw.get("sources"))
+    p, keep = engine.make_problem("poisson", mode=args.mode, **kw)
+    K = torch.zeros(routing.nnz, dtype=torch.float64, device=ctx.dev)
+    F = torch.zeros(routing.N, dtype=torch.float64, device=ctx.dev)
+    M = torch.zeros(routing.nnz, dtype=torch.float64, device=ctx.dev) if with_mass else None
+    bad = torch.empty(1, dtype=torch.int64, device=ctx.dev)
+    row_ptr = routing.host_arrays(slot_of=False, segments=False)["offsets"]
+    exchange = s is not None and world > 1 and s.mode == "exchange"
+    ev_k0, ev_k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def kernel():
+        N.check(L.tgk_assemble_async_d(C.byref(p), mesh._h, routing._h, ptr(K), ptr(F), ptr(M), ptr(bad), ctx.sp))
+
+    def step():
+        kernel()
+        if exchange:
+            D.exchange_interface(K, F, row_ptr, s, D.gpu_combine, ctx.dist)
+            if M is not None:
+                z = torch.zeros_like(F)
+                D.exchange_interface(M, z, row_ptr, s, D.gpu_combine, ctx.dist)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if int(bad.item()) != -1:
+        raise SystemExit(f"element {bad.item()} has non-positive Jacobian determinant")
+    with ClockSampler(ctx.local_rank) as clocks:
+        ms = ctx.timed(step, args.steps)
+        # kernel-only duration (roofline): event pair around the fused launches alone
+        ctx.barrier()
+        ev_k0.record(ctx.stream)
+        for _ in range(args.steps):
+            kernel()
+        ev_k1.record(ctx.stream)
+        torch.cuda.synchronize()
+    ms_kernel = ev_k0.elapsed_time(ev_k1) / args.steps
+    ms_per_step = ms / args.steps
+    if kind == "tet4":
+        E_own = 6 * s.div[0] * s.div[1] * s.div[2]
+        own_rows = (s.own_lo, s.own_hi)
+    else:
+        E_own = elems.shape[0]
+        own_rows = (0, nodes.shape[0])
+    total_E = E_own * world
+    value = total_E / (ms_per_step * 1e-3)
+
+    # e2e through the C ABI with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        h_nodes = torch.from_numpy(np.ascontiguousarray(nodes)).pin_memory()
+        h_elems = torch.from_numpy(np.ascontiguousarray(elems)).pin_memory()
+        o0, o1 = own_rows
+        kk0, kk1 = int(row_ptr[o0]), int(row_ptr[o1])
+        hK = torch.empty(kk1 - kk0, dtype=torch.float64).pin_memory()
+        hF = torch.empty(o1 - o0, dtype=torch.float64).pin_memory()
+        hM = torch.empty(kk1 - kk0, dtype=torch.float64).pin_memory() if with_mass else None
+        if world == 1:
+            fK = torch.empty(routing.nnz, dtype=torch.float64).pin_memory()
+            fF = torch.empty(routing.N, dtype=torch.float64).pin_memory()
+            fM = torch.empty(routing.nnz, dtype=torch.float64).pin_memory() if with_mass else None
+            hp = N.Problem()
+            C.memmove(C.addressof(hp), C.addressof(p), C.sizeof(p))
+
+            def e2e_step():  # host buffers in, host buffers out: tgk_assemble copies inside
+                N.check(L.tgk_mesh_upload(mesh._h, ptr(h_nodes), ptr(h_elems), ctx.sp))
+                N.check(L.tgk_assemble(C.byref(hp), mesh._h, routing._h, ptr(fK), ptr(fF), ptr(fM)))
+            d2h = (fK.numel() + fF.numel() + (fM.numel() if fM is not None else 0)) * 8
+            path = "tgk_mesh_upload + tgk_assemble (host buffers, pinned)"
+        else:
+            def e2e_step():
+                N.check(L.tgk_mesh_upload(mesh._h, ptr(h_nodes), ptr(h_elems), ctx.sp))
+                step()
+                hK.copy_(K[kk0:kk1], non_blocking=True)
+                hF.copy_(F[o0:o1], non_blocking=True)
+                if hM is not None:
+                    hM.copy_(M[kk0:kk1], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            d2h = (hK.numel() + hF.numel() + (hM.numel() if hM is not None else 0)) * 8
+            path = "tgk_mesh_upload + tgk_assemble_async_d + NCCL exchange + D2H of owned rows (pinned)"
+        e2e_step()
+        ctx.barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = ctx.max_over_ranks((time.perf_counter() - w0) / args.e2e_steps)
+        e2e = {"value": total_E / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h_nodes.numel() * 8 + h_elems.numel() * 8),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3, "path": path}
+
+    # roofline of the fused kernel (per launch, kernel-only events)
+    Nn = own_rows[1] - own_rows[0]
+    nnz_own = int(row_ptr[own_rows[1]] - row_ptr[own_rows[0]])
+    ab, comp = alg_bytes(kind, E_own, Nn, nnz_own, with_mass, has_f)
+    peak, peak_src = peaks()
+    achieved = ab / (ms_kernel * 1e-3) / 1e9
+    launches = args.steps * (1 + (2 * (2 if with_mass else 1) if exchange and s.receives_down else 0))
+    config = {"workload": desc, "elements_per_gpu": E_own, "nnz_per_gpu": nnz_own, "mode": args.mode,
+              "parallelism": parallelism,
+              "l2": "inputs larger than L2 (working set > 126 MB L2)" if ab > 2e8 else
+                    "working set below L2 size (C1 parity config; no flush between steps)",
+              "fused_plan": {"rows_per_block": 128, "blocks": nb.value, "halo_elements": nh.value,
+                             "recompute_factor": nh.value / max(1, elems.shape[0]), "records": nrec.value,
+                             "bytes": pbytes.value},
+              "setup_s": setup_s, "kernel_ms": ms_kernel}
+    return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
+                gpu_launches=launches, clocks=clocks.summary(),
+                roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                          "frac": achieved / peak, "traffic": None, "alg_bytes": ab, "compulsory_bytes": comp,
+                          "peak_source": peak_src, "kernel": "k_fused_scalar (one launch per step)",
+                          "kernel_ms": ms_kernel})
+
+
+def run_elasticity(args, ctx, N):
+    """c3: 3D linear elasticity (materialised Stage I + Stage II kernels; replicas for N > 1)."""
+    torch = ctx.torch
+    from paper_2602_05052_b200 import engine, tgfem
+    kind, div, _, desc, scaling = WORKLOADS["c3"]
+    t0 = time.time()
+    m = tgfem.generate_grid(kind, [1.0] * 3, list(div))
+    mesh = engine.DeviceMesh(kind, m.nodes, m.elements)
+    routing = engine.Routing(mesh, 3, segments=True)
+    setup_s = time.time() - t0
+    p, keep = engine.make_problem("elasticity", lam=LAME[0], mu=LAME[1], sources=[1.0, 1.0, 1.0])
+    K = torch.empty(routing.nnz, dtype=torch.float64, device=ctx.dev)
+    F = torch.empty(routing.N, dtype=torch.float64, device=ctx.dev)
+    L = N.lib()
+
+    def step():
+        N.check(L.tgk_assemble_d(C.byref(p), mesh._h, routing._h, ptr(K), ptr(F), None, ctx.sp))
+
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(ctx.local_rank) as clocks:
+        ms = ctx.timed(step, args.steps)
+    ms_per_step = ms / args.steps
+    E = m.element_count()
+    value = E * ctx.world / (ms_per_step * 1e-3)
+    ab, comp = alg_bytes(kind, E, m.node_count(), routing.nnz, False, True, comps=3)
+    peak, peak_src = peaks()
+    achieved = ab / (ms_per_step * 1e-3) / 1e9
+    e2e = None
+    if args.e2e_steps > 0:
+        hK = np.empty(routing.nnz)
+        hF = np.empty(routing.N)
+        h_nodes = torch.from_numpy(np.ascontiguousarray(m.nodes)).pin_memory()
+        h_elems = torch.from_numpy(np.ascontiguousarray(m.elements)).pin_memory()
+        hp = N.Problem()
+        C.memmove(C.addressof(hp), C.addressof(p), C.sizeof(p))
+
+        def e2e_step():
+            N.check(L.tgk_mesh_upload(mesh._h, ptr(h_nodes), ptr(h_elems), ctx.sp))
+            N.check(L.tgk_assemble(C.byref(hp), mesh._h, routing._h, hK.ctypes.data, hF.ctypes.data, None))
+        e2e_step()
+        ctx.barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e2e_s = ctx.max_over_ranks((time.perf_counter() - w0) / args.e2e_steps)
+        e2e = {"value": E * ctx.world / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(h_nodes.numel() * 8 + h_elems.numel() * 8),
+               "d2h_bytes_per_step": int((hK.size + hF.size) * 8), "ms_per_step": e2e_s * 1e3,
+               "path": "tgk_mesh_upload + tgk_assemble (host buffers)"}
+    config = {"workload": desc, "elements_per_gpu": E, "nnz_per_gpu": routing.nnz,
+              "parallelism": "single GPU" if ctx.world == 1 else f"{ctx.world} independent replicas",
+              "path": "materialised: evaluate + local_stiffness_elasticity + reduce_matrix, load_vector + "
+                      "reduce_vector (stage.cu kernels)",
+              "l2": "inputs larger than L2", "setup_s": setup_s}
+    return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
+                gpu_launches=args.steps * 9, clocks=clocks.summary(),
+                roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                          "frac": achieved / peak, "traffic": None, "alg_bytes": ab, "compulsory_bytes": comp,
+                          "peak_source": peak_src,
+                          "kernel": "whole elasticity step (materialised local tensors)"})
+
+
+def run_batched(args, ctx, N):
+    """c4: batched per-element coefficient fields + adjoint gather; fields sharded across ranks."""
+    torch = ctx.torch
+    from paper_2602_05052_b200 import engine, meshgen
+    _, _, _, desc, scaling = WORKLOADS["c4"]
+    t0 = time.time()
+    nodes, elems = meshgen.unstructured_tri(256)
+    E, Nn = elems.shape[0], nodes.shape[0]
+    mesh = engine.DeviceMesh("tri3", nodes, elems)
+    routing = engine.Routing(mesh, 1)
+    if C4_FIELDS % ctx.world:
+        raise SystemExit("c4: 256 fields do not split evenly")
+    Bl = C4_FIELDS // ctx.world
+    b0 = ctx.rank * Bl
+    rho_h = np.stack([0.5 + np.random.default_rng(1000 + b).random(E) for b in range(b0, b0 + Bl)])
+    lam_h = np.stack([np.random.default_rng(2000 + b).random(Nn) - 0.5 for b in range(b0, b0 + Bl)])
+    U_h = np.stack([np.random.default_rng(3000 + b).random(Nn) - 0.5 for b in range(b0, b0 + Bl)])
+    rho = torch.from_numpy(rho_h).to(ctx.dev)
+    lam = torch.from_numpy(lam_h).to(ctx.dev)
+    U = torch.from_numpy(U_h).to(ctx.dev)
+    K = torch.empty(Bl, routing.nnz, dtype=torch.float64, device=ctx.dev)
+    F = torch.empty(Nn, dtype=torch.float64, device=ctx.dev)
+    dr = torch.empty(Bl, E, dtype=torch.float64, device=ctx.dev)
+    setup_s = time.time() - t0
+    L = N.lib()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+    def k_batched():
+        N.check(L.tgk_assemble_batched_d(mesh._h, routing._h, Bl, ptr(rho), 1.0, ptr(K), ptr(F), 0, ctx.sp))
+
+    def k_adjoint():
+        N.check(L.tgk_adjoint_gather_d(mesh._h, routing._h, Bl, ptr(lam), ptr(U), ptr(dr), 1, ctx.sp))
+
+    def step():
+        k_batched()
+        k_adjoint()
+
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(ctx.local_rank) as clocks:
+        ms = ctx.timed(step, args.steps)
+        ctx.barrier()
+        ev[0].record(ctx.stream)
+        for _ in range(args.steps):
+            k_batched()
+        ev[1].record(ctx.stream)
+        for _ in range(args.steps):
+            k_adjoint()
+        ev[2].record(ctx.stream)
+        torch.cuda.synchronize()
+    ms_b = ev[0].elapsed_time(ev[1]) / args.steps
+    ms_a = ev[1].elapsed_time(ev[2]) / args.steps
+    ms_per_step = ms / args.steps
+    value = E * C4_FIELDS / (ms_per_step * 1e-3)  # element-fields per second, all ranks
+    # SURVEY.md 8(d): batched K_b: connectivity + coordinates + slot map + B*nnz*8 + B*E*8 (rho) + N*8 (F)
+    ab_b = E * 3 * 4 + Nn * 2 * 8 + E * 9 * 4 + Bl * routing.nnz * 8 + Bl * E * 8 + Nn * 8
+    ab_a = E * 3 * 4 + Nn * 2 * 8 + E * 9 * 4 + Bl * (2 * Nn * 8 + E * 8)
+    peak, peak_src = peaks()
+    ach_b = ab_b / (ms_b * 1e-3) / 1e9
+    ach_a = ab_a / (ms_a * 1e-3) / 1e9
+    e2e = None
+    if args.e2e_steps > 0:
+        h_rho = torch.from_numpy(rho_h).pin_memory()
+        h_lam = torch.from_numpy(lam_h).pin_memory()
+        h_U = torch.from_numpy(U_h).pin_memory()
+        hK = torch.empty(Bl, routing.nnz, dtype=torch.float64).pin_memory()
+        hdr = torch.empty(Bl, E, dtype=torch.float64).pin_memory()
+        hF = torch.empty(Nn, dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            rho.copy_(h_rho, non_blocking=True)
+            lam.copy_(h_lam, non_blocking=True)
+            U.copy_(h_U, non_blocking=True)
+            step()
+            hK.copy_(K, non_blocking=True)
+            hF.copy_(F, non_blocking=True)
+            hdr.copy_(dr, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_step()
+        ctx.barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e2e_s = ctx.max_over_ranks((time.perf_counter() - w0) / args.e2e_steps)
+        e2e = {"value": E * C4_FIELDS / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int((h_rho.numel() + h_lam.numel() + h_U.numel()) * 8),
+               "d2h_bytes_per_step": int((hK.numel() + hF.numel() + hdr.numel()) * 8),
+               "ms_per_step": e2e_s * 1e3,
+               "path": "pinned H2D of rho/lambda/U + tgk_assemble_batched_d + tgk_adjoint_gather_d + D2H"}
+    config = {"workload": desc, "fields_per_gpu": Bl, "elements": E, "nnz": routing.nnz,
+              "metric_unit_note": "element-fields/s (E x 256 per step)",
+              "parallelism": "single GPU" if ctx.world == 1 else f"{ctx.world} GPUs, fields sharded (no collective)",
+              "l2": "outputs larger than L2 (K_b 943 MB per step)", "setup_s": setup_s,
+              "batched_ms": ms_b, "adjoint_ms": ms_a,
+              "adjoint_roofline": {"achieved": ach_a, "frac": ach_a / peak, "alg_bytes": ab_a}}
+    return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
+                gpu_launches=args.steps * 2, clocks=clocks.summary(),
+                roofline={"bound": "hbm", "achieved": ach_b, "peak": peak, "unit": "GB/s",
+                          "frac": ach_b / peak, "traffic": None, "alg_bytes": ab_b, "peak_source": peak_src,
+                          "kernel": "k_batched (one launch per step, all fields)", "kernel_ms": ms_b})
 
 
 def main():
@@ -201,6 +637,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--dist-mode", default="exchange", choices=["exchange", "halo"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample", type=int, nargs="*", default=None)
@@ -208,173 +645,28 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
-
-    import torch
-    from paper_2602_05052_b200 import engine
     from paper_2602_05052_b200 import _native as N
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    kind, div, kw, desc = WORKLOADS[args.workload]
-    if kind != "tet4" and world > 1:
-        raise SystemExit("multi-GPU slabs are defined for the tet4 workloads")
-
-    # ---------------- setup (not timed): mesh, routing, fused plan
-    t0 = time.time()
-    nodes, elems, own_lo, own_hi, _ = slab_mesh(kind, div, rank, world)
-    mesh = engine.DeviceMesh(kind, nodes, elems)
-    routing = engine.Routing(mesh, 1)
-    if world > 1:
-        N.check(N.lib().tgk_routing_set_owned_rows(routing._h, own_lo, own_hi))
-    import ctypes as C
-    nb, nh, nrec, pbytes = (C.c_int64() for _ in range(4))
-    R = 128 if kw.get("with_mass") else 256  # rows per block of the fused kernel variant
-    N.check(N.lib().tgk_routing_plan_stats(routing._h, R, C.byref(nb), C.byref(nh), C.byref(nrec),
-                                           C.byref(pbytes)))
-    setup_s = time.time() - t0
-    E_own = 6 * div[0] * div[1] * div[2] if kind == "tet4" else 2 * div[0] * div[1]
-    with_mass = kw.get("with_mass", False)
-    has_f = bool(kw.get("sources"))
-    p, keep = engine.make_problem("poisson", mode=args.mode, **kw)
-    dev = torch.device("cuda", local_rank)
-    K = torch.empty(routing.nnz, dtype=torch.float64, device=dev)
-    F = torch.empty(routing.N, dtype=torch.float64, device=dev)
-    M = torch.empty(routing.nnz, dtype=torch.float64, device=dev) if with_mass else None
-    bad = torch.empty(1, dtype=torch.int64, device=dev)
-    stream = torch.cuda.current_stream()
-    sp = C.c_void_p(stream.cuda_stream)
-    ptr = lambda t: None if t is None else C.c_void_p(t.data_ptr())  # noqa: E731
-
-    def step():
-        N.check(N.lib().tgk_assemble_async_d(C.byref(p), mesh._h, routing._h, ptr(K), ptr(F), ptr(M),
-                                             ptr(bad), sp))
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if int(bad.item()) != -1:
-        raise SystemExit(f"element {bad.item()} has non-positive Jacobian determinant")
-
-    # ---------------- timed region (device time)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clocks:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per_step = ms / args.steps
-    total_E = E_own * world
-    value = total_E / (ms_per_step * 1e-3)
-
-    # ---------------- e2e through the host-buffer C-ABI call
-    e2e = None
-    if args.e2e_steps > 0:
-        h_nodes = torch.from_numpy(np.ascontiguousarray(nodes)).pin_memory()
-        h_elems = torch.from_numpy(np.ascontiguousarray(elems)).pin_memory()
-        hK = torch.empty(routing.nnz, dtype=torch.float64).pin_memory()
-        hF = torch.empty(routing.N, dtype=torch.float64).pin_memory()
-        hM = torch.empty(routing.nnz, dtype=torch.float64).pin_memory() if with_mass else None
-        hp = N.Problem()
-        C.memmove(C.addressof(hp), C.addressof(p), C.sizeof(p))
-        hptr = lambda t: None if t is None else C.c_void_p(t.data_ptr())  # noqa: E731
-
-        def e2e_step():
-            N.check(N.lib().tgk_mesh_upload(mesh._h, hptr(h_nodes), hptr(h_elems), sp))
-            N.check(N.lib().tgk_assemble(C.byref(hp), mesh._h, routing._h, hptr(hK), hptr(hF), hptr(hM)))
-
-        e2e_step()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        w0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            e2e_step()
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - w0) / args.e2e_steps
-        if dist:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        h2d = h_nodes.numel() * 8 + h_elems.numel() * 8
-        d2h = hK.numel() * 8 + hF.numel() * 8 + (hM.numel() * 8 if hM is not None else 0)
-        e2e = {"value": total_E / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
-               "path": "tgk_mesh_upload + tgk_assemble (host buffers, pinned)"}
-
-    # ---------------- roofline of the fused kernel (the step is one fused launch)
-    Nn = nodes.shape[0]
-    own_nodes = own_hi - own_lo
-    offs = routing.host_arrays(slot_of=False, segments=False)["offsets"]
-    nnz_own = int(offs[own_hi] - offs[own_lo])
-    ab, comp = alg_bytes(kind, E_own, own_nodes, nnz_own, with_mass, has_f)
-    peak, peak_src = peaks()
-    achieved = ab / (ms_per_step * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get(f"{args.workload}_{args.mode}")
-
+    ctx = Ctx(args)
+    if args.workload == "c3":
+        r = run_elasticity(args, ctx, N)
+    elif args.workload == "c4":
+        r = run_batched(args, ctx, N)
+    else:
+        r = run_scalar(args, ctx, N)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            from oracle import ref
-            if ref.available():
-                sample = (40, 40, 40) if kind == "tet4" else div
-                Es, times = cpu_reference_time(kind, sample, kw, 3, 1)
-                cpu = {"value": Es / min(times), "unit": UNIT, "cores": ref.thread_count(),
-                       "kind": "reference",
-                       "sample": f"tg::assemble (oracle/_ref, reference sources) on {kind} Kuhn "
-                                 f"{'x'.join(map(str, sample))} = {Es} elements, best of 3"}
-            else:
-                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                       "sample": "oracle/_ref/libtgref.so not present"}
-        except Exception as exc:  # reported, never fatal
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"error: {exc}"}
-
-    if rank == 0:
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_line(args.workload)
+    if ctx.rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "elements_per_gpu": E_own, "nnz_per_gpu": nnz_own,
-                       "mode": args.mode,
-                       "parallelism": "single GPU" if world == 1 else
-                       f"{world} row-owning z-slabs (halo recompute, no data-path collective)",
-                       "l2": "inputs larger than L2 (working set ~1 GB vs 126 MB L2)",
-                       "fused_plan": {"rows_per_block": R, "blocks": nb.value, "halo_elements": nh.value,
-                                      "recompute_factor": nh.value / max(1, elems.shape[0]),
-                                      "records": nrec.value, "bytes": pbytes.value},
-                       "setup_s": setup_s},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "alg_bytes": ab,
-                         "compulsory_bytes": comp, "peak_source": peak_src,
-                         "kernel": "k_fused_scalar (one launch per step)"},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": args.steps,
-            "clocks": clocks.summary(),
+            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ctx.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": r["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": r["config"], "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"],
+            "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],
         }
         print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
+    if ctx.dist:
+        ctx.dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -158,6 +158,14 @@ int tgk_routing_copy(const tgk_routing* r, int64_t* row_ptr, int64_t* col_idx, u
  * rows [row_lo, row_hi) of this routing; elements incident to them are
  * recomputed as halo.  Other output rows are left untouched.  Resets the plan. */
 int tgk_routing_set_owned_rows(tgk_routing* r, int64_t row_lo, int64_t row_hi);
+/* Multi-GPU slabs with an interface exchange: restrict the fused assembly to
+ * the elements [elem_lo, elem_hi).  Rows touched only by other elements come
+ * out as +0.0; rows shared with other elements hold the partial left fold of
+ * these elements (to be summed with the other ranks' partials).  Resets the plan. */
+int tgk_routing_set_element_range(tgk_routing* r, int64_t elem_lo, int64_t elem_hi);
+/* Interface sum of the multi-GPU exchange (paper_2602_05052_b200/dist.py):
+ * d_values[i] = d_lower[i] + d_values[i] for i < n (device pointers). */
+int tgk_interface_combine_d(const double* d_lower, double* d_values, int64_t n, void* stream);
 /* Fused-plan statistics for blocks of rows_per_block (128 or 256) rows (builds
  * the plan if needed): CUDA blocks, halo elements (halo / E = recompute
  * factor), packed records, device bytes. */

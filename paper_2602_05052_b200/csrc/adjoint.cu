@@ -12,6 +12,8 @@ namespace tgk {
 int check_bad(unsigned long long* d_bad, cudaStream_t st);
 int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                           double* F, double* M, cudaStream_t st, unsigned long long* d_bad);
+int batched_fused(const tgk_mesh* m, tgk_routing* r, int64_t B, const double* rho, double source, double* K,
+                  double* F, cudaStream_t st, unsigned long long* d_bad);
 
 namespace {
 
@@ -206,15 +208,27 @@ int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, con
     return check_bad(bad.p, st);
 }
 
-// v1: one fused launch per field (shared plan / geometry inputs).
+// One batched launch (batched.cu: halo geometry cached per block, all fields
+// folded through the same plan); one fused launch per field when the block
+// working set does not fit shared memory.
 int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, const double* rho,
                            double source, double* K, double* F, int mode, void* stream) {
     using namespace tgk;
     (void)mode;
     if (!m || !r) return set_error(TGK_ERR_INPUT, "assemble_batched: null argument");
+    if (r->components != 1) return set_error(TGK_ERR_INPUT, "assemble_batched: scalar routing required");
+    if (B < 0) return set_error(TGK_ERR_INPUT, "assemble_batched: negative batch");
+    TGK_TRY(ensure_device());
     cudaStream_t st = as_stream(stream);
     DevBuf<unsigned long long> bad;
     TGK_TRY(bad.alloc(1));
+    CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    if (B == 0) return TGK_OK;
+    if (!getenv("TGK_BATCHED_LOOP")) {
+        const int rc = batched_fused(m, const_cast<tgk_routing*>(r), B, rho, source, K, F, st, bad.p);
+        if (rc == TGK_OK) return check_bad(bad.p, st);
+        if (rc != TGK_ERR_INPUT) return rc;
+    }
     for (int64_t b = 0; b < B; ++b) {
         tgk_problem p{};
         p.kind = TGK_POISSON;

@@ -1,0 +1,274 @@
+// Batched operator-learning assembly (BASELINE.json configs[3], "C4"): B
+// per-element coefficient fields rho_b on one mesh -> B stiffness matrices on
+// one CSR pattern (+ one load vector), i.e. B x (CoefficientField::per_element
+// evaluate + local_stiffness_diffusion + reduce_matrix) of the reference
+// (coefficient.cpp:34-55, batch.cpp:156-181, routing.cpp:109-132), fused.
+//
+// Same row-block plan as the scalar fused kernel (plan.cpp), but the geometry
+// of the whole block halo is computed ONCE and kept in shared memory (det and
+// the k(k+1)/2 gradient dot products per element; small for 2D meshes), then
+// for every field b the block re-runs only the cheap part: sc_q = w_q*det*rho_b
+// and K_e = sum_q sc_q*(G_a.G_b) in the reference's operation order (phase A),
+// and the ascending-element row fold (phase B) — bit-identical to B calls of
+// the reference assemble.  Output K is field-major (B x nnz).
+#include <climits>
+
+#include "cuda_util.cuh"
+#include "element.cuh"
+#include "tgk_internal.hpp"
+
+namespace tgk {
+
+int check_bad(unsigned long long* d_bad, cudaStream_t st);
+
+namespace {
+
+struct BatchedArgs {
+    const double* nodes;
+    const double* rho;  // B x E
+    int64_t E, nnz, B;
+    double source;
+    const int64_t* row_off;
+    const uint32_t* rows;
+    const int64_t* rows_rp;
+    const int64_t* halo_off;
+    const uint32_t* halo;
+    const int64_t* bnode_off;
+    const uint32_t* bnodes;
+    const uint16_t* halo_lconn;
+    const int64_t* chunk_off;
+    const int64_t* chunk_rec_off;
+    const uint16_t* chunk_row_off;
+    const uint32_t* recs;
+    double* K;  // B x nnz
+    double* F;  // N (may be null)
+    int lmax, max_halo, max_bnodes, max_block_recs, max_block_chunks;
+    unsigned long long* bad;
+};
+
+__host__ __device__ constexpr int brot(int a, int b) { return b == a ? 0 : (b < a ? b + 1 : b); }
+
+template <int KIND>
+struct BCfg {
+    static constexpr int k = P1<KIND>::k, d = P1<KIND>::d;
+    static constexpr int ND = k * (k + 1) / 2;  // unique gradient dot products
+    static constexpr int NG = ND + 1;           // + det
+    static constexpr int raw = 4 * k + 4;  // k rotated K rows of 4 doubles, then F
+    static constexpr int stride = (raw / 2) % 2 == 1 ? raw : raw + 2;  // 2 x odd: conflict-free lanes
+    static size_t smem(int R, int lmax, int max_halo, int max_bnodes, int max_block_recs, int max_block_chunks) {
+        auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+        size_t o = 0;
+        o = al(o + sizeof(double) * size_t(max_halo) * NG);            // geometry cache
+        o = al(o + sizeof(double) * size_t(R) * stride);               // ke
+        o = al(o + sizeof(double) * size_t(R) * lmax);                 // acc
+        o = al(o + sizeof(double) * size_t(max_bnodes) * d);           // node table
+        o = al(o + sizeof(uint32_t) * size_t(max_halo));               // halo element ids
+        o = al(o + sizeof(uint32_t) * size_t(max_block_recs));         // records of all chunks
+        o = al(o + sizeof(uint16_t) * size_t(max_block_chunks) * (R + 8));  // row offsets of all chunks
+        o = al(o + sizeof(int64_t) * size_t(max_block_chunks + 1));    // chunk record offsets
+        return o;
+    }
+};
+
+template <int KIND, int DEG, int R>
+__global__ void __launch_bounds__(R) k_batched(BatchedArgs p) {
+    using C = BCfg<KIND>;
+    using Rl = Rule<KIND, DEG>;
+    constexpr int k = C::k, d = C::d, Q = Rl::Q, NG = C::NG, ROS = R + 8;
+    extern __shared__ __align__(16) unsigned char smb[];
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    size_t o = 0;
+    double* geo = reinterpret_cast<double*>(smb + o); o = al(o + sizeof(double) * size_t(p.max_halo) * NG);
+    double* ke = reinterpret_cast<double*>(smb + o); o = al(o + sizeof(double) * size_t(R) * C::stride);
+    double* acc = reinterpret_cast<double*>(smb + o); o = al(o + sizeof(double) * size_t(R) * p.lmax);
+    double* nt = reinterpret_cast<double*>(smb + o); o = al(o + sizeof(double) * size_t(p.max_bnodes) * d);
+    uint32_t* hid = reinterpret_cast<uint32_t*>(smb + o); o = al(o + sizeof(uint32_t) * size_t(p.max_halo));
+    uint32_t* rec_s = reinterpret_cast<uint32_t*>(smb + o); o = al(o + sizeof(uint32_t) * size_t(p.max_block_recs));
+    uint16_t* ro_s = reinterpret_cast<uint16_t*>(smb + o); o = al(o + sizeof(uint16_t) * size_t(p.max_block_chunks) * ROS);
+    int64_t* cro = reinterpret_cast<int64_t*>(smb + o);
+
+    const int tid = threadIdx.x;
+    const int64_t blk = blockIdx.x;
+    const int64_t r0 = p.row_off[blk];
+    const int nr = static_cast<int>(p.row_off[blk + 1] - r0);
+    const int64_t h0 = p.halo_off[blk];
+    const int nh = static_cast<int>(p.halo_off[blk + 1] - h0);
+    const int64_t c0 = p.chunk_off[blk];
+    const int nch = static_cast<int>(p.chunk_off[blk + 1] - c0);
+    const int64_t n0 = p.bnode_off[blk];
+    const int nbn = static_cast<int>(p.bnode_off[blk + 1] - n0);
+
+    // ---------------- prologue: node table, halo ids, records, row offsets
+    for (int i = tid; i <= nch; i += R) cro[i] = p.chunk_rec_off[c0 + i] - p.chunk_rec_off[c0];
+    for (int i = tid; i < nbn; i += R) {
+        const int64_t g = p.bnodes[n0 + i];
+#pragma unroll
+        for (int c = 0; c < d; ++c) nt[i * d + c] = __ldg(p.nodes + g * d + c);
+    }
+    for (int i = tid; i < nh; i += R) hid[i] = p.halo[h0 + i];
+    {
+        const int64_t rb = p.chunk_rec_off[c0];
+        const int nrec = static_cast<int>(p.chunk_rec_off[c0 + nch] - rb);
+        for (int i = tid; i < nrec; i += R) rec_s[i] = p.recs[rb + i];
+        for (int i = tid; i < nch * ROS; i += R) ro_s[i] = p.chunk_row_off[c0 * ROS + i];
+    }
+    __syncthreads();
+    // ---------------- geometry of the whole halo, once (batch.cpp:76-154)
+    for (int h = tid; h < nh; h += R) {
+        const ushort4 ln = *reinterpret_cast<const ushort4*>(p.halo_lconn + (h0 + h) * 4);
+        const int ids[4] = {ln.x, ln.y, ln.z, ln.w};
+        double X[k][d];
+#pragma unroll
+        for (int a = 0; a < k; ++a)
+#pragma unroll
+            for (int c = 0; c < d; ++c) X[a][c] = nt[ids[a] * d + c];
+        double det, G[k][d];
+        if (!simplex_geometry<KIND, false>(X, det, G)) {
+            atomicMin(p.bad, static_cast<unsigned long long>(hid[h]));
+            det = 0.0;
+#pragma unroll
+            for (int a = 0; a < k; ++a)
+#pragma unroll
+                for (int c = 0; c < d; ++c) G[a][c] = 0.0;
+        }
+        double* g = geo + h * NG;
+        g[0] = det;
+        int t = 1;
+#pragma unroll
+        for (int a = 0; a < k; ++a)
+#pragma unroll
+            for (int b = a; b < k; ++b) g[t++] = gdot<KIND>(G, a, b);
+    }
+    // ---------------- one pass per field
+    for (int64_t b = 0; b < p.B; ++b) {
+        const double* rho_b = p.rho + b * p.E;
+        const bool with_f = b == 0 && p.F != nullptr;
+        for (int i = tid; i < R * p.lmax; i += R) acc[i] = 0.0;
+        double dK = 0.0, dF = 0.0;
+        int diag_pos = 0;
+        for (int c = 0; c < nch; ++c) {
+            __syncthreads();  // geometry ready / previous phase B done with ke
+            const int h = c * R + tid;
+            if (h < nh) {
+                // phase A: local_stiffness_diffusion with c_q = rho_b[e] (batch.cpp:168-177)
+                const double* g = geo + h * NG;
+                const double det = g[0];
+                const double rho = __ldg(rho_b + hid[h]);
+                double sc[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) sc[q] = Rl::w(q) * det * rho;
+                double* out = ke + tid * C::stride;
+                int t = 1;
+#pragma unroll
+                for (int a = 0; a < k; ++a)
+#pragma unroll
+                    for (int bb = a; bb < k; ++bb) {
+                        const double dot = g[t++];
+                        double v = sc[0] * dot;
+#pragma unroll
+                        for (int q = 1; q < Q; ++q) v += sc[q] * dot;
+                        out[a * 4 + brot(a, bb)] = v;
+                        out[bb * 4 + brot(bb, a)] = v;
+                    }
+                if (with_f) {
+                    // local_load with a constant source (batch.cpp:280-286)
+#pragma unroll
+                    for (int a = 0; a < k; ++a) {
+                        double v = (Rl::w(0) * det * p.source) * basis<KIND, DEG>(0, a);
+#pragma unroll
+                        for (int q = 1; q < Q; ++q) v += (Rl::w(q) * det * p.source) * basis<KIND, DEG>(q, a);
+                        out[4 * k + a] = v;
+                    }
+                }
+            }
+            __syncthreads();
+            // phase B: owned row tid folds its records of chunk c, ascending element
+            if (tid < nr) {
+                const uint16_t* ro = ro_s + c * ROS;
+                const uint32_t* rs = rec_s + cro[c];
+                for (int j = ro[tid]; j < ro[tid + 1]; ++j) {
+                    const uint32_t rec = rs[j];
+                    const int hl = rec & 0xff;
+                    const int a = (rec >> 8) & 3;
+                    const double* src = ke + hl * C::stride + a * 4;
+                    int pos[k - 1];
+                    double ak[k - 1];
+#pragma unroll
+                    for (int j2 = 0; j2 < k - 1; ++j2) {
+                        pos[j2] = ((rec >> (10 + 5 * j2)) & 31) * R + tid;
+                        ak[j2] = acc[pos[j2]];
+                    }
+#pragma unroll
+                    for (int j2 = 0; j2 < k - 1; ++j2) acc[pos[j2]] = ak[j2] + src[j2 + 1];
+                    dK += src[0];
+                    if (with_f) dF += ke[hl * C::stride + 4 * k + a];
+                    diag_pos = (rec >> 25) & 31;
+                }
+            }
+        }
+        __syncthreads();
+        // epilogue: this field's rows -> K_b
+        if (tid < nr) {
+            const int64_t packed = p.rows_rp[r0 + tid];
+            const int64_t rp = packed & ((int64_t(1) << 56) - 1);
+            const int len = static_cast<int>(packed >> 56);
+            acc[diag_pos * R + tid] = dK;
+            double* Kb = p.K + b * p.nnz + rp;
+            for (int q = 0; q < len; ++q) Kb[q] = acc[q * R + tid];
+            if (with_f) p.F[p.rows[r0 + tid]] = dF;
+        }
+    }
+}
+
+template <int KIND, int DEG, int R>
+int launch_batched(const BatchedArgs& a, int64_t nb, cudaStream_t st) {
+    auto kern = k_batched<KIND, DEG, R>;
+    const size_t smem = BCfg<KIND>::smem(R, a.lmax, a.max_halo, a.max_bnodes, a.max_block_recs, a.max_block_chunks);
+    if (smem > 227 * 1024) return TGK_ERR_INPUT;  // caller falls back to one fused launch per field
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (nb > 0) kern<<<static_cast<unsigned>(nb), R, smem, st>>>(a);
+    KERNEL_CHECK("batched");
+    return TGK_OK;
+}
+
+}  // namespace
+
+// Returns TGK_ERR_INPUT without launching (and without setting an error
+// message) when the block working set does not fit shared memory.
+int batched_fused(const tgk_mesh* m, tgk_routing* r, int64_t B, const double* rho, double source, double* K,
+                  double* F, cudaStream_t st, unsigned long long* d_bad) {
+    constexpr int R = 64;
+    const PlanDev* pl = nullptr;
+    TGK_TRY(ensure_plan(r, R, &pl));
+    BatchedArgs a{};
+    a.nodes = m->nodes;
+    a.rho = rho;
+    a.E = m->E;
+    a.nnz = r->nnz;
+    a.B = B;
+    a.source = source;
+    a.row_off = pl->row_off;
+    a.rows = pl->rows;
+    a.rows_rp = pl->rows_rp;
+    a.halo_off = pl->halo_off;
+    a.halo = pl->halo;
+    a.bnode_off = pl->bnode_off;
+    a.bnodes = pl->bnodes;
+    a.halo_lconn = pl->halo_lconn;
+    a.chunk_off = pl->chunk_off;
+    a.chunk_rec_off = pl->chunk_rec_off;
+    a.chunk_row_off = pl->chunk_row_off;
+    a.recs = pl->recs;
+    a.K = K;
+    a.F = F;
+    a.lmax = pl->lmax;
+    a.max_halo = pl->max_block_halo;
+    a.max_bnodes = pl->max_bnodes;
+    a.max_block_recs = pl->max_block_recs;
+    a.max_block_chunks = pl->max_block_chunks;
+    a.bad = d_bad;
+    if (m->kind == TGK_TRI3) return launch_batched<TGK_TRI3, 2, R>(a, pl->n_blocks, st);
+    return launch_batched<TGK_TET4, 2, R>(a, pl->n_blocks, st);
+}
+
+}  // namespace tgk

@@ -75,7 +75,11 @@ std::vector<uint32_t> morton_order(int kind, int64_t N, const double* nodes, int
 
 int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
                const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
-               const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int R, PlanHost& P) {
+               const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int R,
+               PlanHost& P) {
+    // elements outside [elem_lo, elem_hi) take no part (multi-GPU slabs that
+    // exchange interface partial sums instead of recomputing the halo)
+    auto in_range = [elem_lo, elem_hi](uint32_t e) { return int64_t(e) >= elem_lo && int64_t(e) < elem_hi; };
     const int d = element_dim(kind), k = element_nodes(kind);
     (void)E;
     if (R != 64 && R != 128 && R != 256) return set_error(TGK_ERR_INPUT, "fused plan: R must be 64, 128 or 256");
@@ -146,7 +150,7 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
             for (int64_t i = rs; i < re; ++i) {
                 const uint32_t row = P.rows[i];
                 for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s)
-                    tmp.push_back(vec_slots[s] / k);
+                    if (in_range(vec_slots[s] / k)) tmp.push_back(vec_slots[s] / k);
             }
             std::sort(tmp.begin(), tmp.end());
             tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
@@ -164,6 +168,7 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
                     int64_t prev = -1;
                     for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s) {
                         const uint32_t e = vec_slots[s] / k;
+                        if (!in_range(e)) continue;
                         const int64_t hix = std::lower_bound(tmp.begin(), tmp.end(), e) - tmp.begin();
                         if (prev >= 0) edges.push_back({static_cast<uint32_t>(hix), static_cast<uint32_t>(prev)});
                         prev = hix;
@@ -193,6 +198,7 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
                 for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s) {
                     const uint32_t slot = vec_slots[s];
                     const uint32_t e = slot / k;
+                    if (!in_range(e)) continue;
                     const int a = static_cast<int>(slot % k);
                     const int64_t hpos =
                         std::lower_bound(where.begin(), where.end(), std::make_pair(e, 0u))->second;

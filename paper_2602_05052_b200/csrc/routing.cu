@@ -363,6 +363,7 @@ tgk_routing::~tgk_routing() {
         if (p) cudaFree(p);
     for (auto& pl : plan) pl.release();
     plan4.release();
+    plan5.release();
     if (scalar && scalar != this) delete scalar;
 }
 

@@ -6,6 +6,7 @@
 //
 // Arithmetic follows the reference literally (FMA disabled), one thread per
 // element (Map) or per output (Reduce, ascending-slot left fold).
+#include <algorithm>
 #include <climits>
 
 #include "cuda_util.cuh"
@@ -488,3 +489,24 @@ int tgk_reduce_vector_d(const tgk_routing* r, const double* local, double* F, vo
 }
 
 }  // extern "C"
+
+namespace tgk {
+namespace {
+// Interface-row sum of the multi-GPU exchange: values = lower + values
+// (lower: the partial fold of the rank below = elements with smaller ids).
+__global__ void k_interface_combine(const double* lower, double* values, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        values[i] = lower[i] + values[i];
+}
+}  // namespace
+}  // namespace tgk
+
+extern "C" int tgk_interface_combine_d(const double* d_lower, double* d_values, int64_t n, void* stream) {
+    using namespace tgk;
+    if (n < 0 || (n > 0 && (!d_lower || !d_values))) return set_error(TGK_ERR_INPUT, "interface_combine: bad arguments");
+    TGK_TRY(ensure_device());
+    if (n == 0) return TGK_OK;
+    k_interface_combine<<<std::min<unsigned>(grid_for(n, 256), 148 * 8), 256, 0, as_stream(stream)>>>(d_lower, d_values, n);
+    KERNEL_CHECK("interface_combine");
+    return TGK_OK;
+}

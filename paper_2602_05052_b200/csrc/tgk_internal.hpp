@@ -83,6 +83,7 @@ struct PlanDev {
     uint32_t* recs = nullptr;
     int64_t bytes = 0;
     int64_t n_halo = 0, n_records = 0;
+    int max_block_halo = 0, max_block_recs = 0, max_block_chunks = 0;  // per-block maxima (batched kernel)
     void release();
 };
 
@@ -106,7 +107,39 @@ TGK_HD inline uint32_t pack_rec(int hl, int a, const int* pos, int k) {
 // row range [row_lo, row_hi) with R rows per block.
 int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
                const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
-               const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int R, PlanHost& out);
+               const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int R,
+               PlanHost& out);
+
+// ----------------------------------------------------------------- fused plan v5
+// v3's row blocks (Morton rows, level-ordered halo chunks of R elements, node
+// tables) with per-chunk work items: the chunk's active rows, sorted by record
+// count.  item = local row (bits 0-7) | record count (8-15) | first record
+// relative to the chunk (16-31).  Records as pack_rec.
+struct Plan5Host {
+    int R = 128;
+    int64_t n_blocks = 0;
+    int lmax = 0, max_bnodes = 0, max_chunk_recs = 0, max_chunk_items = 0, max_block_chunks = 0;
+    std::vector<int64_t> row_off, rows_rp, halo_off, bnode_off, chunk_off, chunk_rec, chunk_item;
+    std::vector<uint32_t> rows, halo, bnodes, chunk_nitems, items, recs;
+    std::vector<uint16_t> halo_lconn;
+};
+
+struct PlanDev5 {
+    int R = 0;
+    int64_t n_blocks = 0;
+    int lmax = 0, max_bnodes = 0, max_chunk_recs = 0, max_chunk_items = 0, max_block_chunks = 0;
+    int64_t *row_off = nullptr, *rows_rp = nullptr, *halo_off = nullptr, *bnode_off = nullptr,
+            *chunk_off = nullptr, *chunk_rec = nullptr, *chunk_item = nullptr;
+    uint32_t *rows = nullptr, *halo = nullptr, *bnodes = nullptr, *chunk_nitems = nullptr, *items = nullptr,
+             *recs = nullptr;
+    uint16_t* halo_lconn = nullptr;
+    int64_t bytes = 0, n_halo = 0, n_records = 0, n_chunks = 0;
+    void release();
+};
+
+int build_plan5(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
+                const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
+                int64_t row_lo, int64_t row_hi, int R, Plan5Host& out);
 
 // ----------------------------------------------------------------- fused plan v4
 // "Row blocks with update rounds" (plan4.cpp / fused4.cu): a CUDA block owns
@@ -191,7 +224,9 @@ struct tgk_routing {
     tgk_routing* scalar = nullptr;   // == this for components == 1
     tgk::PlanDev plan[tgk::kPlanSlots];
     tgk::PlanDev4 plan4;              // v4 plan (one shape cached)
+    tgk::PlanDev5 plan5;              // v5 plan (one R cached)
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
+    int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
     double* scratch_K = nullptr;     // device output buffers of the host-buffer entry point
     double* scratch_F = nullptr;
     double* scratch_M = nullptr;
@@ -202,4 +237,5 @@ namespace tgk {
 // Build (once per R) and upload the fused plan of the routing's scalar part.
 int ensure_plan(tgk_routing* r, int R, const PlanDev** out);
 int ensure_plan4(tgk_routing* r, int R, int T, const PlanDev4** out);
+int ensure_plan5(tgk_routing* r, int R, const PlanDev5** out);
 }

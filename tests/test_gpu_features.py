@@ -1,0 +1,113 @@
+"""GPU: multi-GPU slab assembly (emulated on one device), the batched C4 kernel
+on the unstructured mesh, and the interface-combine kernel — through the C ABI,
+checked against the CPU oracle."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import port  # noqa: E402
+from tests._util import assert_bitwise, assert_scaled_close  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def eng():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_05052_b200 import engine
+    return engine
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.mark.parametrize("mode,with_mass", [("exchange", False), ("exchange", True), ("halo", True)])
+def test_slabs_on_one_gpu_match_single_gpu(eng, mode, with_mass):
+    """Every rank of a 3-slab partition run in turn on one GPU; the NCCL P2P is
+    replaced by a device copy, the interface sum is libtgk's combine kernel."""
+    from paper_2602_05052_b200 import _native as N
+    from paper_2602_05052_b200 import dist as D
+    L = N.lib()
+    div, world = (5, 4, 3), 3
+    parts = []
+    for rank in range(world):
+        s = D.slab(div, rank, world, mode)
+        nodes, elems = D.slab_mesh(s)
+        m = eng.DeviceMesh("tet4", nodes, elems)
+        r = eng.Routing(m, 1)
+        N.check(L.tgk_routing_set_owned_rows(r._h, s.own_lo, s.calc_hi))
+        if mode == "exchange":
+            N.check(L.tgk_routing_set_element_range(r._h, s.elem_lo, s.elem_hi))
+        K, F, M = eng.assemble(m, r, sources=[1.0], with_mass=with_mass)
+        rp = r.host_arrays(slot_of=False, segments=False)["offsets"]
+        parts.append((s, rp, K, F, M, (m, r)))
+    if mode == "exchange":
+        for rank in range(1, world):
+            s, rp, K, F, M, _ = parts[rank]
+            sl, rpl, Kl, Fl, Ml, _ = parts[rank - 1]
+            lo, hi = s.bottom_rows
+            tl, th = sl.top_rows
+            for a, al in [(K, Kl)] + ([(M, Ml)] if with_mass else []):
+                D.gpu_combine(al[int(rpl[tl]):int(rpl[th])].clone(), a[int(rp[lo]):int(rp[hi])])
+            D.gpu_combine(Fl[tl:th].clone(), F[lo:hi])
+    torch.cuda.synchronize()
+    nodes, elems = port.generate_grid("tet4", [1.0] * 3, [5, 4, 3 * world])
+    pr = port.Routing(nodes.shape[0], port.dofmap("tet4", elems, 1))
+    Kr, Fr, Mr = port.assemble("tet4", nodes, elems, pr, sources=[1.0], with_mass=with_mass)
+    for s, rp, K, F, M, _ in parts:
+        g0, g1 = s.node_offset + s.own_lo, s.node_offset + s.own_hi
+        assert np.array_equal(rp[s.own_lo:s.own_hi + 1] - rp[s.own_lo], pr.offsets[g0:g1 + 1] - pr.offsets[g0])
+        got = {"K": np_(K)[rp[s.own_lo]:rp[s.own_hi]], "F": np_(F)[s.own_lo:s.own_hi]}
+        want = {"K": Kr[pr.offsets[g0]:pr.offsets[g1]], "F": Fr[g0:g1]}
+        if with_mass:
+            got["M"] = np_(M)[rp[s.own_lo]:rp[s.own_hi]]
+            want["M"] = Mr[pr.offsets[g0]:pr.offsets[g1]]
+        for key in got:
+            if mode == "halo" or s.rank == 0:
+                assert_bitwise(got[key], want[key], f"rank {s.rank} {key}")
+            else:
+                nif = s.layer if key == "F" else int(rp[s.own_lo + s.layer] - rp[s.own_lo])
+                assert_scaled_close(got[key][:nif], want[key][:nif], what=f"rank {s.rank} interface {key}")
+                assert_bitwise(got[key][nif:], want[key][nif:], f"rank {s.rank} interior {key}")
+
+
+def test_batched_c4_mesh_bit_exact(eng):
+    from paper_2602_05052_b200 import meshgen
+    nodes, elems = meshgen.unstructured_tri(40)
+    m = eng.DeviceMesh("tri3", nodes, elems)
+    r = eng.Routing(m, 1)
+    pr = port.Routing(nodes.shape[0], port.dofmap("tri3", elems, 1))
+    B = 7
+    rho = meshgen.batch_fields(B, elems.shape[0])
+    K, F = eng.assemble_batched(m, r, rho, source=1.0)
+    torch.cuda.synchronize()
+    for b in range(B):
+        Kr, Fr, _ = port.assemble("tri3", nodes, elems, pr, diffusion=("element", rho[b]), sources=[1.0])
+        assert_bitwise(np_(K[b]), Kr, f"field {b}")
+        if b == 0:
+            assert_bitwise(np_(F), Fr, "F")
+
+
+def test_batched_tet4_bit_exact(eng):
+    nodes, elems = port.generate_grid("tet4", [1.0] * 3, [6, 5, 4])
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    r = eng.Routing(m, 1)
+    pr = port.Routing(nodes.shape[0], port.dofmap("tet4", elems, 1))
+    rho = 0.5 + np.random.default_rng(5).random((3, elems.shape[0]))
+    K, F = eng.assemble_batched(m, r, rho, source=1.0)
+    for b in range(3):
+        Kr, Fr, _ = port.assemble("tet4", nodes, elems, pr, diffusion=("element", rho[b]), sources=[1.0])
+        assert_bitwise(np_(K[b]), Kr, f"field {b}")
+
+
+def test_interface_combine_kernel(eng):
+    from paper_2602_05052_b200 import dist as D
+    rng = np.random.default_rng(9)
+    a, b = rng.random(10007), rng.random(10007)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    D.gpu_combine(ta, tb)
+    assert_bitwise(np_(tb), a + b)
