@@ -14,6 +14,9 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
                           double* F, double* M, cudaStream_t st, unsigned long long* d_bad);
 int batched_fused(const tgk_mesh* m, tgk_routing* r, int64_t B, const double* rho, double source, double* K,
                   double* F, cudaStream_t st, unsigned long long* d_bad);
+int local_elasticity_nocheck(const tgk_mesh* m, int degree, const double* lam, const double* mu, double* out,
+                             cudaStream_t st);
+int routing_scratch(tgk_routing* r, int slot, size_t n, double** out);
 
 namespace {
 
@@ -123,42 +126,41 @@ int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r
     int Q = 0;
     TGK_TRY(tgk_tables(m->kind, degree, &Q, nullptr, nullptr, nullptr, nullptr));
     const int64_t nq = m->E * Q;
-    DevBuf<double> lam, mu, local;
-    TGK_TRY(lam.alloc(nq));
-    TGK_TRY(mu.alloc(nq));
-    TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->lambda, lam.p, st));
-    TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->mu, mu.p, st));
+    const int kk = m->k * d;
+    double *lam, *mu, *local, *src, *comp;  // cached on the routing: no per-call cudaMalloc of E*kk*kk doubles
+    TGK_TRY(routing_scratch(r, 0, nq, &lam));
+    TGK_TRY(routing_scratch(r, 1, nq, &mu));
+    TGK_TRY(routing_scratch(r, 2, size_t(m->E) * kk * kk, &local));
+    TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->lambda, lam, st));
+    TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->mu, mu, st));
     if (d == 2 && pr->plane_stress) {
-        k_plane_stress<<<grid_for(nq, 256), 256, 0, st>>>(lam.p, mu.p, nq);
+        k_plane_stress<<<grid_for(nq, 256), 256, 0, st>>>(lam, mu, nq);
         KERNEL_CHECK("plane_stress");
     }
     {
         DevBuf<unsigned long long> flag;
         TGK_TRY(flag.alloc(1));
         CUDA_TRY(cudaMemsetAsync(flag.p, 0xff, sizeof(unsigned long long), st));
-        k_min_value<<<grid_for(nq, 256), 256, 0, st>>>(mu.p, nq, flag.p);
+        k_min_value<<<grid_for(nq, 256), 256, 0, st>>>(mu, nq, flag.p);
         KERNEL_CHECK("mu_check");
         unsigned long long h = ULLONG_MAX;
         CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof h, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
         if (h != ULLONG_MAX) return set_error(TGK_ERR_INPUT, "elasticity requires mu > 0");
     }
-    const int kk = m->k * d;
-    TGK_TRY(local.alloc(m->E * kk * kk));
-    TGK_TRY(tgk_local_stiffness_elasticity_d(m, degree, lam.p, mu.p, local.p, st));
-    TGK_TRY(tgk_reduce_matrix_d(r, local.p, K, st));
+    TGK_TRY(local_elasticity_nocheck(m, degree, lam, mu, local, st));
+    TGK_TRY(tgk_reduce_matrix_d(r, local, K, st));
     if (F) {
         if (pr->n_source > 0) {
-            DevBuf<double> src, comp;
-            TGK_TRY(src.alloc(nq * d));
-            TGK_TRY(comp.alloc(nq));
+            TGK_TRY(routing_scratch(r, 3, size_t(nq) * d, &src));
+            TGK_TRY(routing_scratch(r, 4, nq, &comp));
             for (int c = 0; c < d; ++c) {
-                TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->source[c], comp.p, st));
-                k_interleave<<<grid_for(nq, 256), 256, 0, st>>>(comp.p, nq, d, c, src.p);
+                TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->source[c], comp, st));
+                k_interleave<<<grid_for(nq, 256), 256, 0, st>>>(comp, nq, d, c, src);
                 KERNEL_CHECK("interleave");
             }
-            TGK_TRY(tgk_local_load_vector_d(m, degree, src.p, local.p, st));
-            TGK_TRY(tgk_reduce_vector_d(r, local.p, F, st));
+            TGK_TRY(tgk_local_load_vector_d(m, degree, src, local, st));
+            TGK_TRY(tgk_reduce_vector_d(r, local, F, st));
         } else {
             CUDA_TRY(cudaMemsetAsync(F, 0, sizeof(double) * r->N, st));
         }

@@ -11,7 +11,9 @@
 // and K_e = sum_q sc_q*(G_a.G_b) in the reference's operation order (phase A),
 // and the ascending-element row fold (phase B) — bit-identical to B calls of
 // the reference assemble.  Output K is field-major (B x nnz).
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "cuda_util.cuh"
 #include "element.cuh"
@@ -43,6 +45,7 @@ struct BatchedArgs {
     double* K;  // B x nnz
     double* F;  // N (may be null)
     int lmax, max_halo, max_bnodes, max_block_recs, max_block_chunks;
+    int64_t fields_per_block;  // blockIdx.y selects a group of fields (fills the GPU for few row blocks)
     unsigned long long* bad;
 };
 
@@ -140,7 +143,9 @@ __global__ void __launch_bounds__(R) k_batched(BatchedArgs p) {
             for (int b = a; b < k; ++b) g[t++] = gdot<KIND>(G, a, b);
     }
     // ---------------- one pass per field
-    for (int64_t b = 0; b < p.B; ++b) {
+    const int64_t bf0 = int64_t(blockIdx.y) * p.fields_per_block;
+    const int64_t bf1 = bf0 + p.fields_per_block < p.B ? bf0 + p.fields_per_block : p.B;
+    for (int64_t b = bf0; b < bf1; ++b) {
         const double* rho_b = p.rho + b * p.E;
         const bool with_f = b == 0 && p.F != nullptr;
         for (int i = tid; i < R * p.lmax; i += R) acc[i] = 0.0;
@@ -226,7 +231,8 @@ int launch_batched(const BatchedArgs& a, int64_t nb, cudaStream_t st) {
     const size_t smem = BCfg<KIND>::smem(R, a.lmax, a.max_halo, a.max_bnodes, a.max_block_recs, a.max_block_chunks);
     if (smem > 227 * 1024) return TGK_ERR_INPUT;  // caller falls back to one fused launch per field
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (nb > 0) kern<<<static_cast<unsigned>(nb), R, smem, st>>>(a);
+    const dim3 grid(static_cast<unsigned>(nb), static_cast<unsigned>((a.B + a.fields_per_block - 1) / a.fields_per_block));
+    if (nb > 0) kern<<<grid, R, smem, st>>>(a);
     KERNEL_CHECK("batched");
     return TGK_OK;
 }
@@ -267,6 +273,10 @@ int batched_fused(const tgk_mesh* m, tgk_routing* r, int64_t B, const double* rh
     a.max_block_recs = pl->max_block_recs;
     a.max_block_chunks = pl->max_block_chunks;
     a.bad = d_bad;
+    // field groups: about 16 resident blocks' worth of work per SM in total
+    const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(B, (148 * 16 + pl->n_blocks - 1) / std::max<int64_t>(1, pl->n_blocks)));
+    a.fields_per_block = (B + groups - 1) / groups;
+    if (const char* e = getenv("TGK_BATCHED_FPB")) a.fields_per_block = std::max(1, atoi(e));
     if (m->kind == TGK_TRI3) return launch_batched<TGK_TRI3, 2, R>(a, pl->n_blocks, st);
     return launch_batched<TGK_TET4, 2, R>(a, pl->n_blocks, st);
 }

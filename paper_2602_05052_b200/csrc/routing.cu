@@ -362,6 +362,8 @@ tgk_routing::~tgk_routing() {
                     (void*)scratch_F, (void*)scratch_M})
         if (p) cudaFree(p);
     for (auto& pl : plan) pl.release();
+    for (double* p : scr)
+        if (p) cudaFree(p);
     plan4.release();
     plan5.release();
     if (scalar && scalar != this) delete scalar;

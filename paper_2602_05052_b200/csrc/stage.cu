@@ -235,6 +235,106 @@ __global__ void k_local(const double* nodes, const int32_t* conn, int64_t E, con
     }
 }
 
+
+// ------------------------------------------------------------------ elasticity local kernel
+// local_stiffness_elasticity (batch.cpp:183-248) with the reference's
+// operation order but only over the STRUCTURAL nonzeros of the Voigt B and
+// D*B (batch.cpp:205-236): every skipped term is a product with an exact
+// structural zero (+-0.0), and adding +-0.0 to a partial sum that starts at
+// +0.0 never changes it, so all values are bit-identical to the literal loop.
+// Warp per 32 elements; each row of K_e is staged in shared memory and written
+// by the warp as contiguous runs (coalesced element-major output).
+template <int D>
+__host__ __device__ constexpr int bcomp(int i, int c) {
+    // gradient component carried by B[i][a*D + c] (Voigt row i), -1 if structurally zero
+    if (D == 3) {
+        return i == 0 ? (c == 0 ? 0 : -1)
+             : i == 1 ? (c == 1 ? 1 : -1)
+             : i == 2 ? (c == 2 ? 2 : -1)
+             : i == 3 ? (c == 0 ? 1 : (c == 1 ? 0 : -1))   // gamma_xy
+             : i == 4 ? (c == 1 ? 2 : (c == 2 ? 1 : -1))   // gamma_yz
+             : (c == 0 ? 2 : (c == 2 ? 0 : -1));           // gamma_xz
+    }
+    return i == 0 ? (c == 0 ? 0 : -1) : i == 1 ? (c == 1 ? 1 : -1) : (c == 0 ? 1 : (c == 1 ? 0 : -1));
+}
+
+template <int KIND, int DEG>
+__global__ void __launch_bounds__(32) k_local_elasticity(const double* nodes, const int32_t* conn, int64_t E,
+                                                         const double* lam_eq, const double* mu_eq, double* out,
+                                                         unsigned long long* bad) {
+    constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q;
+    constexpr int kk = k * d, ns = d == 2 ? 3 : 6;
+    using R = Rule<KIND, DEG>;
+    __shared__ double tile[32 * (kk + 1)];
+    const int lane = threadIdx.x;
+    const int64_t e0 = int64_t(blockIdx.x) * 32;
+    const int64_t e = e0 + lane;
+    const bool valid = e < E;
+    double G[k][d];
+    double det = 0.0;
+    bool ok = false;
+    if (valid) {
+        double X[k][d];
+        load_element<KIND>(nodes, conn, e, X);
+        ok = simplex_geometry<KIND>(X, det, G);
+        if (!ok) flag_bad(bad, e);
+    }
+    if (!ok) {
+#pragma unroll
+        for (int a = 0; a < k; ++a)
+#pragma unroll
+            for (int c = 0; c < d; ++c) G[a][c] = 0.0;
+    }
+    const int nvalid = E - e0 < 32 ? static_cast<int>(E - e0) : 32;
+#pragma unroll
+    for (int ar = 0; ar < kk; ++ar) {
+        const int a = ar / d, c = ar % d;  // compile-time after unrolling
+        double row[kk];
+#pragma unroll
+        for (int j = 0; j < kk; ++j) row[j] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const double lam = valid ? lam_eq[e * Q + q] : 0.0;
+            const double mu = valid ? mu_eq[e * Q + q] : 1.0;
+            const double two_mu = 2.0 * mu;
+            const double scale = R::w(q) * det;
+#pragma unroll
+            for (int b = 0; b < k; ++b)
+#pragma unroll
+                for (int cp = 0; cp < d; ++cp) {
+                    const double g = G[b][cp];
+                    const double tr = 0.0 + g;  // the column's only normal entry (batch.cpp:232)
+                    double s = 0.0;
+#pragma unroll
+                    for (int i = 0; i < ns; ++i) {
+                        const int ga = bcomp<d>(i, c);
+                        if (ga < 0) continue;  // B[i][a*d+c] structurally zero
+                        const double Ba = G[a][ga];
+                        double DB;
+                        if (i < d) {
+                            DB = i == cp ? lam * tr + two_mu * g : lam * tr + two_mu * 0.0;  // batch.cpp:233
+                        } else {
+                            const int gb = bcomp<d>(i, cp);
+                            if (gb < 0) continue;  // mu * 0.0 (batch.cpp:234)
+                            DB = mu * G[b][gb];
+                        }
+                        s += Ba * DB;
+                    }
+                    row[b * d + cp] += scale * s;  // batch.cpp:240-242
+                }
+        }
+#pragma unroll
+        for (int j = 0; j < kk; ++j) tile[lane * (kk + 1) + j] = row[j];
+        __syncwarp();
+        // coalesced store of row ar of the warp's (up to) 32 elements
+        for (int f = lane; f < nvalid * kk; f += 32) {
+            const int el = f / kk, col = f % kk;
+            out[(e0 + el) * kk * kk + ar * kk + col] = tile[el * (kk + 1) + col];
+        }
+        __syncwarp();
+    }
+}
+
 // CoefficientField::evaluate (coefficient.cpp:34-55) -> E x Q
 template <int KIND, int DEG>
 __global__ void k_evaluate(const int32_t* conn, int64_t E, int type, double value,
@@ -297,9 +397,14 @@ struct LocalOf {
     struct L {
         static int run(const tgk_mesh* m, const double* c1, const double* c2, double* out,
                        unsigned long long* bad, cudaStream_t st) {
-            const int block = WHAT == L_ELAST ? 64 : 128;
-            k_local<KIND, DEG, WHAT><<<grid_for(m->E, block), block, 0, st>>>(m->nodes, m->conn, m->E,
-                                                                             c1, c2, out, bad);
+            if constexpr (WHAT == L_ELAST) {
+                k_local_elasticity<KIND, DEG><<<grid_for(m->E, 32), 32, 0, st>>>(m->nodes, m->conn, m->E, c1, c2,
+                                                                                  out, bad);
+                KERNEL_CHECK("local_elasticity");
+                return TGK_OK;
+            }
+            k_local<KIND, DEG, WHAT><<<grid_for(m->E, 128), 128, 0, st>>>(m->nodes, m->conn, m->E,
+                                                                         c1, c2, out, bad);
             KERNEL_CHECK("local");
             return TGK_OK;
         }
@@ -349,6 +454,25 @@ __global__ void k_narrow(const int64_t* src, int64_t n, int64_t n_nodes, int32_t
 }
 
 }  // namespace
+
+// local_stiffness_elasticity without the host-side mu check (the caller checked mu on the device)
+int local_elasticity_nocheck(const tgk_mesh* m, int degree, const double* lam, const double* mu, double* out,
+                             cudaStream_t st) {
+    return run_local<L_ELAST>(m, degree, lam, mu, out, st);
+}
+
+// Cached device scratch of a routing handle (slot < 6, grows on demand).
+int routing_scratch(tgk_routing* r, int slot, size_t n, double** out) {
+    if (r->scr_n[slot] < n) {
+        if (r->scr[slot]) cudaFree(r->scr[slot]);
+        r->scr[slot] = nullptr;
+        r->scr_n[slot] = 0;
+        CUDA_TRY(cudaMalloc(&r->scr[slot], sizeof(double) * std::max<size_t>(1, n)));
+        r->scr_n[slot] = n;
+    }
+    *out = r->scr[slot];
+    return TGK_OK;
+}
 
 // Division-safety certificate of a mesh (element.cuh ExactDiv): every
 // coordinate is 0 or has 2^-40 <= |x| <= 2^40.

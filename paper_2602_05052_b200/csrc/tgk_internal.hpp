@@ -227,6 +227,8 @@ struct tgk_routing {
     tgk::PlanDev5 plan5;              // v5 plan (one R cached)
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
     int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
+    double* scr[6] = {};             // cached device scratch (materialised elasticity path)
+    size_t scr_n[6] = {};
     double* scratch_K = nullptr;     // device output buffers of the host-buffer entry point
     double* scratch_F = nullptr;
     double* scratch_M = nullptr;
