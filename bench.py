@@ -472,7 +472,7 @@ def run_elasticity(args, ctx, N):
     t0 = time.time()
     m = tgfem.generate_grid(kind, [1.0] * 3, list(div))
     mesh = engine.DeviceMesh(kind, m.nodes, m.elements)
-    routing = engine.Routing(mesh, 3, segments=True)
+    routing = engine.Routing(mesh, 3)
     setup_s = time.time() - t0
     p, keep = engine.make_problem("elasticity", lam=LAME[0], mu=LAME[1], sources=[1.0, 1.0, 1.0])
     K = torch.empty(routing.nnz, dtype=torch.float64, device=ctx.dev)
@@ -516,15 +516,14 @@ def run_elasticity(args, ctx, N):
                "path": "tgk_mesh_upload + tgk_assemble (host buffers)"}
     config = {"workload": desc, "elements_per_gpu": E, "nnz_per_gpu": routing.nnz,
               "parallelism": "single GPU" if ctx.world == 1 else f"{ctx.world} independent replicas",
-              "path": "materialised: evaluate + local_stiffness_elasticity + reduce_matrix, load_vector + "
-                      "reduce_vector (stage.cu kernels)",
+              "path": "fused row-block elasticity kernel (fused_elast.cu): one launch per step",
               "l2": "inputs larger than L2", "setup_s": setup_s}
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
-                gpu_launches=args.steps * 9, clocks=clocks.summary(),
+                gpu_launches=args.steps, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                           "frac": achieved / peak, "traffic": None, "alg_bytes": ab, "compulsory_bytes": comp,
                           "peak_source": peak_src,
-                          "kernel": "whole elasticity step (materialised local tensors)"})
+                          "kernel": "k_fused_elast (one launch per step)"})
 
 
 def run_batched(args, ctx, N):

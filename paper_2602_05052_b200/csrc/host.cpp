@@ -160,6 +160,8 @@ int fused4_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing
                            double* M, cudaStream_t st, unsigned long long* d_bad);
 int fused5_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
                            double* M, cudaStream_t st, unsigned long long* d_bad);
+int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
+                              cudaStream_t st);
 
 // Fused kernel generation: 3 (row-thread fold, default) or 4 (element-thread
 // updates in plan rounds; TGK_FUSED_V=4).  Both are bit-identical to the
@@ -827,7 +829,13 @@ int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double
     if (p->with_mass && comps != 1)
         return set_error(TGK_ERR_INPUT, "mass matrix assembly only supported for scalar fields");
     TGK_TRY(host_ensure_device());
-    if (p->kind == TGK_ELASTICITY) return elasticity_assemble(p, m, r, K, F, st);
+    if (p->kind == TGK_ELASTICITY) {
+        // fused row-block kernel (fused_elast.cu); the materialised Stage I + II
+        // path (evaluate -> local_stiffness_elasticity -> reduce_matrix) remains
+        // behind TGK_ELAST_MATERIALISED=1 (needs a routing with segment maps)
+        if (getenv("TGK_ELAST_MATERIALISED")) return elasticity_assemble(p, m, r, K, F, st);
+        return fused_elasticity_assemble(p, m, r, K, F, st);
+    }
     const tgk_routing* rs = r->scalar ? r->scalar : r;
     if (fused_version() != 3 && rs->elem_hi >= 0)
         return set_error(TGK_ERR_INPUT, "element ranges need the v3 fused kernel");
