@@ -349,7 +349,8 @@ def run_scalar(args, ctx, N):
         if s.mode == "exchange":
             N.check(L.tgk_routing_set_element_range(routing._h, s.elem_lo, s.elem_hi))
     nb, nh, nrec, pbytes = (C.c_int64() for _ in range(4))
-    N.check(L.tgk_routing_plan_stats(routing._h, 128, C.byref(nb), C.byref(nh), C.byref(nrec), C.byref(pbytes)))
+    R_plan = 64 if kw.get("with_mass") else 128  # rows per block of the fused kernel variant (fused.cu)
+    N.check(L.tgk_routing_plan_stats(routing._h, R_plan, C.byref(nb), C.byref(nh), C.byref(nrec), C.byref(pbytes)))
     setup_s = time.time() - t0
     with_mass = kw.get("with_mass", False)
     has_f = bool(kw.get("sources"))
@@ -452,7 +453,7 @@ def run_scalar(args, ctx, N):
               "parallelism": parallelism,
               "l2": "inputs larger than L2 (working set > 126 MB L2)" if ab > 2e8 else
                     "working set below L2 size (C1 parity config; no flush between steps)",
-              "fused_plan": {"rows_per_block": 128, "blocks": nb.value, "halo_elements": nh.value,
+              "fused_plan": {"rows_per_block": R_plan, "blocks": nb.value, "halo_elements": nh.value,
                              "recompute_factor": nh.value / max(1, elems.shape[0]), "records": nrec.value,
                              "bytes": pbytes.value},
               "setup_s": setup_s, "kernel_ms": ms_kernel}

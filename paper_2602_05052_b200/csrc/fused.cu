@@ -68,6 +68,7 @@ struct FusedArgs {
     int lmax;
     int max_recs;
     int max_bnodes;
+    int ntcols;  // doubles per node-table entry: 3 coordinates [+ nodal coefficient] [+ nodal source]
     int debug;  // profiling only (TGK_FUSED_DEBUG): 1 skips phase B, 2 skips phase A math
     long long* trace;  // profiling only (TGK_FUSED_TRACE): per block 8 clock64 stamps
     unsigned long long* bad;
@@ -75,7 +76,7 @@ struct FusedArgs {
 
 constexpr int kMaxChunks = 255;  // halo chunks per block (plan-enforced)
 #ifndef TGK_RING
-#define TGK_RING 4
+#define TGK_RING 2
 #endif
 #ifndef TGK_R_BIG
 #define TGK_R_BIG 256
@@ -102,9 +103,10 @@ struct FusedCfg {
     // d = 3: random node gathers spread over all bank pairs), then the nodal
     // coefficient and nodal source as separate arrays (used only when nodal)
     static constexpr int NV = 3;      // TRI3 pads to 3 as well (odd stride)
-    static constexpr int NVT = NV + 2;  // doubles per node in the table (coords + coef + src)
-    static size_t smem_bytes(int lmax, int max_recs, int max_bnodes) {
-        return sizeof(double) * (size_t(R) * stride + size_t(R) * lmax * nmat + size_t(max_bnodes) * NVT) +
+    // doubles per node in the table: the coordinates, then the nodal
+    // coefficient / source columns only when those fields are nodal (FusedArgs::ntcols)
+    static size_t smem_bytes(int lmax, int max_recs, int max_bnodes, int ntcols) {
+        return sizeof(double) * (size_t(R) * stride + size_t(R) * lmax * nmat + size_t(max_bnodes) * ntcols) +
                kRing * (sizeof(uint32_t) * size_t(max_recs) + sizeof(uint16_t) * size_t(row_off_stride(R)) +
                         sizeof(uint16_t) * 4 * size_t(R));
     }
@@ -180,7 +182,7 @@ __device__ __forceinline__ void element_tensors(const FusedArgs& p, const double
         for (int a = 0; a < k; ++a) cu[a] = cs[ids[a]];
     }
     if (HAS_F && p.src.type == TGK_FIELD_NODAL) {
-        const double* ss = nt + p.max_bnodes * (NV + 1);
+        const double* ss = nt + p.max_bnodes * (NV + (p.coef.type == TGK_FIELD_NODAL ? 1 : 0));
 #pragma unroll
         for (int a = 0; a < k; ++a) fu[a] = ss[ids[a]];
     }
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
     double* accK = ke + R * C::stride;                               // lmax x R
     double* accM = accK + R * p.lmax;                                // (HAS_M)
     double* nt = accK + R * p.lmax * C::nmat;                        // max_bnodes x (NV + 2)
-    uint32_t* rec_s = reinterpret_cast<uint32_t*>(nt + p.max_bnodes * C::NVT);  // kRing x max_recs
+    uint32_t* rec_s = reinterpret_cast<uint32_t*>(nt + p.max_bnodes * p.ntcols);  // kRing x max_recs
     uint16_t* ro_s = reinterpret_cast<uint16_t*>(rec_s + kRing * p.max_recs);  // kRing x ROS
     ushort4* lc_s = reinterpret_cast<ushort4*>(ro_s + kRing * ROS);           // kRing x R
     __shared__ int64_t cro_s[kMaxChunks + 1];  // this block's chunk record offsets
@@ -335,7 +337,8 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
                 for (int c = 0; c < d; ++c) dst[c] = __ldg(p.nodes + g[u] * d + c);
                 if (p.coef.type == TGK_FIELD_NODAL) nt[p.max_bnodes * NV + i] = __ldg(p.coef.data + g[u]);
                 if constexpr (HAS_F)
-                    if (p.src.type == TGK_FIELD_NODAL) nt[p.max_bnodes * (NV + 1) + i] = __ldg(p.src.data + g[u]);
+                    if (p.src.type == TGK_FIELD_NODAL)
+                        nt[p.max_bnodes * (NV + (p.coef.type == TGK_FIELD_NODAL ? 1 : 0)) + i] = __ldg(p.src.data + g[u]);
             }
         }
     }
@@ -443,7 +446,7 @@ template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV
 int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
     using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R>;
     auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV>;
-    const size_t smem = C::smem_bytes(a.lmax, a.max_recs, a.max_bnodes);
+    const size_t smem = C::smem_bytes(a.lmax, a.max_recs, a.max_bnodes, a.ntcols);
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (n_blocks > 0) kern<<<static_cast<unsigned>(n_blocks), R, smem, st>>>(a);
     KERNEL_CHECK("fused_scalar");
@@ -467,6 +470,9 @@ int dispatch_flags(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, in
     if (R == 128)
         return fdiv ? dispatch_r<KIND, DEG, 128, true>(ktype, m, f, a, nb, st)
                     : dispatch_r<KIND, DEG, 128, false>(ktype, m, f, a, nb, st);
+    if (R == 64)
+        return fdiv ? dispatch_r<KIND, DEG, 64, true>(ktype, m, f, a, nb, st)
+                    : dispatch_r<KIND, DEG, 64, false>(ktype, m, f, a, nb, st);
     return fdiv ? dispatch_r<KIND, DEG, TGK_R_BIG, true>(ktype, m, f, a, nb, st)
                 : dispatch_r<KIND, DEG, TGK_R_BIG, false>(ktype, m, f, a, nb, st);
 }
@@ -474,9 +480,14 @@ int dispatch_flags(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, in
 }  // namespace
 
 int fused_rows_per_block(const tgk_problem* pr) {
-    if (const char* env = getenv("TGK_FUSED_R")) return atoi(env) == 128 ? 128 : TGK_R_BIG;
-    (void)pr;
-    return 128;
+    if (const char* env = getenv("TGK_FUSED_R")) {
+        const int r = atoi(env);
+        return r == 64 || r == 128 ? r : TGK_R_BIG;
+    }
+    // measured on B200 (profiles/r01_fused_experiments.txt): K+F best at 128
+    // rows per block; with the unit mass the larger per-element working set
+    // fits more resident blocks at 64 rows
+    return pr->with_mass ? 64 : 128;
 }
 
 // Scalar fused assembly on device buffers.  With d_bad == nullptr it checks
@@ -515,6 +526,7 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
     a.lmax = pl->lmax;
     a.max_recs = pl->max_chunk_recs > 0 ? pl->max_chunk_recs : 4;
     a.max_bnodes = pl->max_bnodes + (pl->max_bnodes & 1);
+    a.ntcols = 3 + (a.coef.type == TGK_FIELD_NODAL ? 1 : 0) + (has_f && a.src.type == TGK_FIELD_NODAL ? 1 : 0);
     if (const char* dbg = getenv("TGK_FUSED_DEBUG")) a.debug = atoi(dbg);
     DevBuf<long long> trace;
     const char* trace_path = getenv("TGK_FUSED_TRACE");
