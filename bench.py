@@ -97,6 +97,16 @@ def alg_bytes(kind, E, Nn, nnz, with_mass, has_f, comps=1):
     return b, b - E * k * k * 4
 
 
+def ncu_traffic(workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel per launch, from the
+    committed ncu --set full capture of this workload (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(workload, {}).get("bytes")
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """SM clocks + throttle reasons sampled DURING the timed region (NVML, ~1 ms
     period; nvidia-smi fallback)."""
@@ -460,7 +470,8 @@ def run_scalar(args, ctx, N):
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
                 gpu_launches=launches, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                          "frac": achieved / peak, "traffic": None, "alg_bytes": ab, "compulsory_bytes": comp,
+                          "frac": achieved / peak, "traffic": ncu_traffic(args.workload) if world == 1 else None,
+                          "alg_bytes": ab, "compulsory_bytes": comp,
                           "peak_source": peak_src, "kernel": "k_fused_scalar (one launch per step)",
                           "kernel_ms": ms_kernel})
 
@@ -522,8 +533,8 @@ def run_elasticity(args, ctx, N):
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
                 gpu_launches=args.steps, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                          "frac": achieved / peak, "traffic": None, "alg_bytes": ab, "compulsory_bytes": comp,
-                          "peak_source": peak_src,
+                          "frac": achieved / peak, "traffic": ncu_traffic("c3") if ctx.world == 1 else None,
+                          "alg_bytes": ab, "compulsory_bytes": comp, "peak_source": peak_src,
                           "kernel": "k_fused_elast (one launch per step)"})
 
 
@@ -625,7 +636,8 @@ def run_batched(args, ctx, N):
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
                 gpu_launches=args.steps * 2, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": ach_b, "peak": peak, "unit": "GB/s",
-                          "frac": ach_b / peak, "traffic": None, "alg_bytes": ab_b, "peak_source": peak_src,
+                          "frac": ach_b / peak, "traffic": ncu_traffic("c4") if ctx.world == 1 else None,
+                          "alg_bytes": ab_b, "peak_source": peak_src,
                           "kernel": "k_batched (one launch per step, all fields)", "kernel_ms": ms_b})
 
 

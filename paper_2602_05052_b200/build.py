@@ -27,8 +27,8 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler",
 CXXFLAGS = ["-O3", "-fPIC", "-std=c++17", "-Wall", "-Wno-unused-function",
             f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}", f"-I{os.path.join(CUDA, 'include')}"]
 
-CU = ["routing.cu", "stage.cu", "fused.cu", "fused4.cu", "fused5.cu", "batched.cu", "fused_elast.cu", "adjoint.cu"]
-CPP = ["host.cpp", "plan.cpp", "plan4.cpp", "plan5.cpp"]
+CU = ["routing.cu", "stage.cu", "fused.cu", "batched.cu", "fused_elast.cu", "adjoint.cu"]
+CPP = ["host.cpp", "plan.cpp"]
 HEADERS = ["tgk_internal.hpp", "element.cuh", "cuda_util.cuh"]
 
 

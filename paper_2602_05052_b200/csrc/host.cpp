@@ -156,24 +156,8 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
                           double* F, double* M, cudaStream_t st, unsigned long long* d_bad);
 int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                         double* F, cudaStream_t st);
-int fused4_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
-                           double* M, cudaStream_t st, unsigned long long* d_bad);
-int fused5_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
-                           double* M, cudaStream_t st, unsigned long long* d_bad);
 int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
                               cudaStream_t st);
-
-// Fused kernel generation: 3 (row-thread fold, default) or 4 (element-thread
-// updates in plan rounds; TGK_FUSED_V=4).  Both are bit-identical to the
-// reference; v4 measured slower on Kuhn grids.
-static int fused_version() {
-    static const int v = [] {
-        const char* e = getenv("TGK_FUSED_V");
-        const int x = e ? atoi(e) : 3;
-        return x == 4 || x == 5 ? x : 3;
-    }();
-    return v;
-}
 
 }  // namespace tgk
 
@@ -484,8 +468,6 @@ int tgk_routing_set_owned_rows(tgk_routing* r, int64_t lo, int64_t hi) {
     if (lo < 0 || hi > s->N || lo > hi) return set_error(TGK_ERR_INPUT, "owned row range out of bounds");
     if (s->own_lo == lo && s->own_hi == hi) return TGK_OK;
     for (auto& pl : s->plan) pl.release();
-    s->plan4.release();
-    s->plan5.release();
     s->own_lo = lo;
     s->own_hi = hi;
     return TGK_OK;
@@ -499,8 +481,6 @@ int tgk_routing_set_element_range(tgk_routing* r, int64_t lo, int64_t hi) {
     if (lo < 0 || hi > s->E || lo > hi) return set_error(TGK_ERR_INPUT, "element range out of bounds");
     if (s->elem_lo == lo && s->elem_hi == hi) return TGK_OK;
     for (auto& pl : s->plan) pl.release();
-    s->plan4.release();
-    s->plan5.release();
     s->elem_lo = lo;
     s->elem_hi = hi;
     return TGK_OK;
@@ -616,182 +596,6 @@ int ensure_plan(tgk_routing* rr, int R, const PlanDev** out) {
     return TGK_OK;
 }
 
-void PlanDev4::release() {
-    for (void* p : {(void*)row_off, (void*)rows, (void*)rows_rp, (void*)bnode_off, (void*)bnodes, (void*)halo_off,
-                    (void*)halo, (void*)hconn, (void*)chunk_off, (void*)chunk_rec, (void*)chunk_meta,
-                    (void*)chunk_wbase, (void*)recs})
-        if (p) cudaFree(p);
-    *this = PlanDev4{};
-}
-
-void PlanDev5::release() {
-    for (void* p : {(void*)row_off, (void*)rows_rp, (void*)halo_off, (void*)bnode_off, (void*)chunk_off,
-                    (void*)chunk_rec, (void*)chunk_item, (void*)rows, (void*)halo, (void*)bnodes,
-                    (void*)chunk_nitems, (void*)items, (void*)recs, (void*)halo_lconn})
-        if (p) cudaFree(p);
-    *this = PlanDev5{};
-}
-
-// Host copies of the scalar routing inputs of the plan builders.
-struct PlanInputs {
-    std::vector<double> nodes;
-    std::vector<int32_t> conn;
-    std::vector<int64_t> row_ptr;
-    std::vector<uint32_t> vo, vs, slot;
-};
-static int plan_inputs(const tgk_routing* r, PlanInputs& I) {
-    const tgk_mesh* m = r->mesh;
-    const int k = m->k, d = m->d;
-    I.nodes.resize(m->N * d);
-    I.conn.resize(m->E * k);
-    I.row_ptr.resize(r->N + 1);
-    I.vo.resize(r->N + 1);
-    I.vs.resize(r->E * k);
-    I.slot.resize(r->E * k * k);
-    HCUDA(cudaMemcpy(I.nodes.data(), m->nodes, I.nodes.size() * 8, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(I.conn.data(), m->conn, I.conn.size() * 4, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(I.row_ptr.data(), r->row_ptr, I.row_ptr.size() * 8, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(I.vo.data(), r->vec_offsets, I.vo.size() * 4, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(I.vs.data(), r->vec_slots, I.vs.size() * 4, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(I.slot.data(), r->slot_of, I.slot.size() * 4, cudaMemcpyDeviceToHost));
-    return TGK_OK;
-}
-
-template <class D, class V>
-static int upload_vec(D*& dst, const V& v, int64_t& bytes_acc) {
-    using T_ = typename V::value_type;
-    const size_t bytes = std::max<size_t>(16, v.size() * sizeof(T_));
-    HCUDA(cudaMalloc(reinterpret_cast<void**>(&dst), bytes));
-    if (!v.empty()) HCUDA(cudaMemcpy(dst, v.data(), v.size() * sizeof(T_), cudaMemcpyHostToDevice));
-    bytes_acc += static_cast<int64_t>(bytes);
-    return TGK_OK;
-}
-
-// Build (once per R) and upload the v5 fused plan of a scalar routing.
-int ensure_plan5(tgk_routing* rr, int R, const PlanDev5** out) {
-    tgk_routing* r = rr->scalar ? rr->scalar : rr;
-    PlanDev5& D = r->plan5;
-    if (D.R == R) {
-        *out = &D;
-        return TGK_OK;
-    }
-    D.release();
-    PlanInputs I;
-    TGK_TRY(plan_inputs(r, I));
-    Plan5Host P;
-    const int64_t lo = r->own_hi < 0 ? 0 : r->own_lo, hi = r->own_hi < 0 ? r->N : r->own_hi;
-    TGK_TRY(build_plan5(r->mesh->kind, r->mesh->N, I.nodes.data(), I.conn.data(), I.row_ptr.data(), I.vo.data(),
-                        I.vs.data(), I.slot.data(), lo, hi, R, P));
-    D.n_blocks = P.n_blocks;
-    D.lmax = P.lmax;
-    D.max_bnodes = P.max_bnodes;
-    D.max_chunk_recs = P.max_chunk_recs;
-    D.max_chunk_items = P.max_chunk_items;
-    D.max_block_chunks = P.max_block_chunks;
-    D.n_halo = static_cast<int64_t>(P.halo.size());
-    D.n_records = static_cast<int64_t>(P.recs.size());
-    D.n_chunks = static_cast<int64_t>(P.chunk_nitems.size());
-    int64_t& B = D.bytes;
-    TGK_TRY(upload_vec(D.row_off, P.row_off, B));
-    TGK_TRY(upload_vec(D.rows_rp, P.rows_rp, B));
-    TGK_TRY(upload_vec(D.halo_off, P.halo_off, B));
-    TGK_TRY(upload_vec(D.bnode_off, P.bnode_off, B));
-    TGK_TRY(upload_vec(D.chunk_off, P.chunk_off, B));
-    TGK_TRY(upload_vec(D.chunk_rec, P.chunk_rec, B));
-    TGK_TRY(upload_vec(D.chunk_item, P.chunk_item, B));
-    TGK_TRY(upload_vec(D.rows, P.rows, B));
-    TGK_TRY(upload_vec(D.halo, P.halo, B));
-    TGK_TRY(upload_vec(D.bnodes, P.bnodes, B));
-    TGK_TRY(upload_vec(D.chunk_nitems, P.chunk_nitems, B));
-    TGK_TRY(upload_vec(D.items, P.items, B));
-    TGK_TRY(upload_vec(D.recs, P.recs, B));
-    TGK_TRY(upload_vec(D.halo_lconn, P.halo_lconn, B));
-    D.R = R;
-    if (getenv("TGK_PLAN_STATS")) {
-        double items = 0;
-        for (uint32_t v : P.chunk_nitems) items += v;
-        fprintf(stderr, "plan5 R=%d blocks=%lld halo=%lld chunks=%lld items/chunk=%.1f records=%lld max_bnodes=%d "
-                        "max_recs=%d max_items=%d bytes=%lld\n",
-                R, (long long)P.n_blocks, (long long)D.n_halo, (long long)D.n_chunks,
-                items / std::max<int64_t>(1, D.n_chunks), (long long)D.n_records, P.max_bnodes, P.max_chunk_recs,
-                P.max_chunk_items, (long long)D.bytes);
-    }
-    *out = &D;
-    return TGK_OK;
-}
-
-// Build (once per block shape) and upload the v4 fused plan of a scalar routing.
-int ensure_plan4(tgk_routing* rr, int R, int T, const PlanDev4** out) {
-    tgk_routing* r = rr->scalar ? rr->scalar : rr;
-    PlanDev4& D = r->plan4;
-    if (D.R == R && D.T == T) {
-        *out = &D;
-        return TGK_OK;
-    }
-    D.release();
-    const tgk_mesh* m = r->mesh;
-    const int k = m->k, d = m->d;
-    std::vector<double> nodes(m->N * d);
-    std::vector<int32_t> conn(m->E * k);
-    std::vector<int64_t> row_ptr(r->N + 1);
-    std::vector<uint32_t> vo(r->N + 1), vs(r->E * k), slot(r->E * k * k);
-    HCUDA(cudaMemcpy(nodes.data(), m->nodes, nodes.size() * 8, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(conn.data(), m->conn, conn.size() * 4, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(row_ptr.data(), r->row_ptr, row_ptr.size() * 8, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(vo.data(), r->vec_offsets, vo.size() * 4, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(vs.data(), r->vec_slots, vs.size() * 4, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(slot.data(), r->slot_of, slot.size() * 4, cudaMemcpyDeviceToHost));
-    Plan4Host P;
-    const int64_t lo = r->own_hi < 0 ? 0 : r->own_lo, hi = r->own_hi < 0 ? r->N : r->own_hi;
-    TGK_TRY(build_plan4(m->kind, m->N, nodes.data(), conn.data(), row_ptr.data(), vo.data(), vs.data(),
-                        slot.data(), lo, hi, R, T, P));
-    D.n_blocks = P.n_blocks;
-    D.lmax = P.lmax;
-    D.max_bnodes = P.max_bnodes;
-    D.max_chunk_recs = P.max_chunk_recs;
-    D.max_rounds = P.max_rounds;
-    D.n_halo = static_cast<int64_t>(P.halo.size());
-    D.n_records = static_cast<int64_t>(P.recs.size());
-    D.n_chunks = static_cast<int64_t>(P.chunk_meta.size());
-    for (int64_t b = 0; b < P.n_blocks; ++b)
-        D.max_block_chunks = std::max<int>(D.max_block_chunks, static_cast<int>(P.chunk_off[b + 1] - P.chunk_off[b]));
-    auto up = [&D](auto*& dst, const auto& v) -> int {
-        using T_ = typename std::remove_reference<decltype(v)>::type::value_type;
-        const size_t bytes = std::max<size_t>(16, v.size() * sizeof(T_));
-        HCUDA(cudaMalloc(reinterpret_cast<void**>(&dst), bytes));
-        if (!v.empty()) HCUDA(cudaMemcpy(dst, v.data(), v.size() * sizeof(T_), cudaMemcpyHostToDevice));
-        D.bytes += static_cast<int64_t>(bytes);
-        return TGK_OK;
-    };
-    TGK_TRY(up(D.row_off, P.row_off));
-    TGK_TRY(up(D.rows, P.rows));
-    TGK_TRY(up(D.rows_rp, P.rows_rp));
-    TGK_TRY(up(D.bnode_off, P.bnode_off));
-    TGK_TRY(up(D.bnodes, P.bnodes));
-    TGK_TRY(up(D.halo_off, P.halo_off));
-    TGK_TRY(up(D.halo, P.halo));
-    TGK_TRY(up(D.hconn, P.hconn));
-    TGK_TRY(up(D.chunk_off, P.chunk_off));
-    TGK_TRY(up(D.chunk_rec, P.chunk_rec));
-    TGK_TRY(up(D.chunk_meta, P.chunk_meta));
-    TGK_TRY(up(D.chunk_wbase, P.chunk_wbase));
-    TGK_TRY(up(D.recs, P.recs));
-    D.R = R;
-    D.T = T;
-    if (getenv("TGK_PLAN_STATS")) {
-        double rounds = 0;
-        for (uint32_t v : P.chunk_meta) rounds += v;
-        fprintf(stderr,
-                "plan4 R=%d T=%d blocks=%lld halo=%lld chunks=%lld (%.2f/block) rounds/chunk=%.2f max_rounds=%d "
-                "records=%lld max_bnodes=%d max_recs=%d lmax=%d bytes=%lld\n",
-                R, T, (long long)P.n_blocks, (long long)D.n_halo, (long long)D.n_chunks,
-                double(D.n_chunks) / std::max<int64_t>(1, P.n_blocks), rounds / std::max<size_t>(1, P.chunk_meta.size()),
-                P.max_rounds, (long long)D.n_records, P.max_bnodes, P.max_chunk_recs, P.lmax, (long long)D.bytes);
-    }
-    *out = &D;
-    return TGK_OK;
-}
-
 static int check_field(const tgk_field& f, const tgk_mesh* m, const char* what) {
     if (f.type == TGK_FIELD_CONSTANT) return TGK_OK;
     if (f.type == TGK_FIELD_ELEMENT) {
@@ -836,11 +640,6 @@ int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double
         if (getenv("TGK_ELAST_MATERIALISED")) return elasticity_assemble(p, m, r, K, F, st);
         return fused_elasticity_assemble(p, m, r, K, F, st);
     }
-    const tgk_routing* rs = r->scalar ? r->scalar : r;
-    if (fused_version() != 3 && rs->elem_hi >= 0)
-        return set_error(TGK_ERR_INPUT, "element ranges need the v3 fused kernel");
-    if (fused_version() == 4) return fused4_scalar_assemble(p, m, r, K, F, M, st, d_bad);
-    if (fused_version() == 5) return fused5_scalar_assemble(p, m, r, K, F, M, st, d_bad);
     return fused_scalar_assemble(p, m, r, K, F, M, st, d_bad);
 }
 

@@ -364,8 +364,6 @@ tgk_routing::~tgk_routing() {
     for (auto& pl : plan) pl.release();
     for (double* p : scr)
         if (p) cudaFree(p);
-    plan4.release();
-    plan5.release();
     if (scalar && scalar != this) delete scalar;
 }
 

@@ -110,90 +110,6 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
                const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int R,
                PlanHost& out);
 
-// ----------------------------------------------------------------- fused plan v5
-// v3's row blocks (Morton rows, level-ordered halo chunks of R elements, node
-// tables) with per-chunk work items: the chunk's active rows, sorted by record
-// count.  item = local row (bits 0-7) | record count (8-15) | first record
-// relative to the chunk (16-31).  Records as pack_rec.
-struct Plan5Host {
-    int R = 128;
-    int64_t n_blocks = 0;
-    int lmax = 0, max_bnodes = 0, max_chunk_recs = 0, max_chunk_items = 0, max_block_chunks = 0;
-    std::vector<int64_t> row_off, rows_rp, halo_off, bnode_off, chunk_off, chunk_rec, chunk_item;
-    std::vector<uint32_t> rows, halo, bnodes, chunk_nitems, items, recs;
-    std::vector<uint16_t> halo_lconn;
-};
-
-struct PlanDev5 {
-    int R = 0;
-    int64_t n_blocks = 0;
-    int lmax = 0, max_bnodes = 0, max_chunk_recs = 0, max_chunk_items = 0, max_block_chunks = 0;
-    int64_t *row_off = nullptr, *rows_rp = nullptr, *halo_off = nullptr, *bnode_off = nullptr,
-            *chunk_off = nullptr, *chunk_rec = nullptr, *chunk_item = nullptr;
-    uint32_t *rows = nullptr, *halo = nullptr, *bnodes = nullptr, *chunk_nitems = nullptr, *items = nullptr,
-             *recs = nullptr;
-    uint16_t* halo_lconn = nullptr;
-    int64_t bytes = 0, n_halo = 0, n_records = 0, n_chunks = 0;
-    void release();
-};
-
-int build_plan5(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
-                const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
-                int64_t row_lo, int64_t row_hi, int R, Plan5Host& out);
-
-// ----------------------------------------------------------------- fused plan v4
-// "Row blocks with update rounds" (plan4.cpp / fused4.cu): a CUDA block owns
-// up to R rows and walks their halo in chunks of T elements, one per thread;
-// each element thread adds its local tensor rows straight into the block's
-// shared-memory row accumulators, in plan-computed rounds (ascending element
-// order per row), with no intermediate element-tensor buffer.
-constexpr int kMaxChunks4 = 1024;  // chunks per block (the kernel stages the chunk table in shared memory)
-
-struct Plan4Host {
-    int R = 256, T = 128;
-    int64_t n_blocks = 0;
-    int lmax = 0, max_bnodes = 0, max_chunk_recs = 0, max_rounds = 0;
-    std::vector<int64_t> row_off;      // n_blocks+1 into rows
-    std::vector<uint32_t> rows;        // owned rows, ascending within a block
-    std::vector<int64_t> rows_rp;      // per owned row: row_ptr[row] | row length << 56
-    std::vector<int64_t> bnode_off;    // n_blocks+1 into bnodes
-    std::vector<uint32_t> bnodes;      // per block: owned rows (local ids 0..nr-1), then other halo nodes
-    std::vector<int64_t> halo_off;     // n_blocks+1 into halo / hconn
-    std::vector<uint32_t> halo;        // halo element ids in (level, id) order
-    std::vector<uint64_t> hconn;       // 4 block-local node ids (16 bits each) per halo element
-    std::vector<int64_t> chunk_off;    // n_blocks+1: first chunk of each block
-    std::vector<int64_t> chunk_rec;    // per chunk: first record (multiple of 4); total at the end
-    std::vector<uint32_t> chunk_meta;  // per chunk: number of update rounds
-    std::vector<uint16_t> chunk_wbase; // per chunk: 8 warp record bases (relative to the chunk)
-    std::vector<uint32_t> recs;        // bits 5b..5b+4: CSR position of node b in row a; 24-28: round
-};
-
-struct PlanDev4 {
-    int R = 0, T = 0;
-    int64_t n_blocks = 0;
-    int lmax = 0, max_bnodes = 0, max_chunk_recs = 0, max_rounds = 0;
-    int64_t* row_off = nullptr;
-    uint32_t* rows = nullptr;
-    int64_t* rows_rp = nullptr;
-    int64_t* bnode_off = nullptr;
-    uint32_t* bnodes = nullptr;
-    int64_t* halo_off = nullptr;
-    uint32_t* halo = nullptr;
-    uint64_t* hconn = nullptr;
-    int64_t* chunk_off = nullptr;
-    int64_t* chunk_rec = nullptr;
-    uint32_t* chunk_meta = nullptr;
-    uint16_t* chunk_wbase = nullptr;
-    uint32_t* recs = nullptr;
-    int max_block_chunks = 0;
-    int64_t bytes = 0, n_halo = 0, n_records = 0, n_chunks = 0;
-    void release();
-};
-
-int build_plan4(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
-                const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
-                int64_t row_lo, int64_t row_hi, int R, int T, Plan4Host& out);
-
 }  // namespace tgk
 
 // ----------------------------------------------------------------- handles
@@ -223,8 +139,6 @@ struct tgk_routing {
     // scalar (node-level) routing used by vector problems and the fused plan
     tgk_routing* scalar = nullptr;   // == this for components == 1
     tgk::PlanDev plan[tgk::kPlanSlots];
-    tgk::PlanDev4 plan4;              // v4 plan (one shape cached)
-    tgk::PlanDev5 plan5;              // v5 plan (one R cached)
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
     int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
     double* scr[6] = {};             // cached device scratch (materialised elasticity path)
@@ -238,6 +152,4 @@ struct tgk_routing {
 namespace tgk {
 // Build (once per R) and upload the fused plan of the routing's scalar part.
 int ensure_plan(tgk_routing* r, int R, const PlanDev** out);
-int ensure_plan4(tgk_routing* r, int R, int T, const PlanDev4** out);
-int ensure_plan5(tgk_routing* r, int R, const PlanDev5** out);
 }
