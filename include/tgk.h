@@ -231,6 +231,15 @@ int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B,
                            const double* d_rho, double source, double* d_K, double* d_F,
                            int mode, void* stream);
 
+/* Allen-Cahn Newton re-assembly (AllenCahnStepper::step, timestep.cpp:144-178;
+ * SURVEY.md 8(f) rank 1), fused in one pass at the mass degree for the nodal
+ * state u (N values, device):
+ *   d_T = reduce_matrix(local_mass(reaction_tangent_coefficient(u, eps)))  (nnz)
+ *   d_F = reduce_vector(local_reaction_load(u, eps))                       (N; may be NULL)
+ * (batch.cpp:314-351).  Bit-identical to the reference. */
+int tgk_allen_cahn_d(const tgk_mesh* m, const tgk_routing* r, const double* d_u, double eps, double* d_T,
+                     double* d_F, void* stream);
+
 /* ------------------------------------------------------------------ adjoint */
 /* gradient_products (adjoint.cpp:68-82): dK[t] = lambda_i U_cols[t] on the
  * pattern, dF = -lambda.  Batched over B fields (lambda, U: B x N). */

@@ -66,6 +66,7 @@ def lib():
         L.tgr_assemble.argtypes = [P, P, C.c_int, P, P, P, C.c_int, C.c_int, P, C.c_int, P, P, P, P]
         L.tgr_gradient_products.argtypes = [P] * 5
         L.tgr_simp_sensitivity.argtypes = [P, P, P, C.c_double, C.c_double, C.c_double, P, P, P]
+        L.tgr_allen_cahn.argtypes = [P, P, P, C.c_double, P, P]
         _lib = L
     return _lib
 
@@ -239,6 +240,15 @@ def local(mesh: Mesh, degree, what, c1, c2=None):
     c2 = None if c2 is None else np.ascontiguousarray(c2, dtype=np.float64)
     _check(lib().tgr_local(mesh._h, degree, what, _p(c1), _p(c2), _p(out)))
     return out
+
+
+def allen_cahn(mesh: Mesh, routing: Routing, u, eps):
+    """AllenCahnStepper re-assembly (timestep.cpp:144-178): (T values, reaction load F)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    T = np.zeros(routing.nnz)
+    F = np.zeros(routing.N)
+    _check(lib().tgr_allen_cahn(mesh._h, routing._h, _p(u), C.c_double(eps), _p(T), _p(F)))
+    return T, F
 
 
 def assemble(mesh: Mesh, routing: Routing, problem="poisson", diffusion=1.0, lam=1.0, mu=1.0,

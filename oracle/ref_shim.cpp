@@ -249,6 +249,25 @@ int tgr_local(void* mp, int degree, int what, const double* c1, const double* c2
     });
 }
 
+// Allen-Cahn Newton re-assembly exactly as AllenCahnStepper does it
+// (timestep.cpp:118-135 tables/geometry at the mass degree, :144-146 reaction
+// load, :177-178 tangent): T = reduce_matrix(local_mass(reaction_tangent_coefficient(u))),
+// F = reduce_vector(local_reaction_load(u)).
+int tgr_allen_cahn(void* mp, void* rp, const double* u, double eps, double* T, double* F) {
+    return guarded([&] {
+        const auto& m = *static_cast<Mesh*>(mp);
+        const auto& r = static_cast<RefRouting*>(rp)->routing;
+        const auto t = reference_tables(m.kind, default_mass_degree(m.kind));
+        const auto g = batch_geometry(m, t);
+        const std::vector<double> un(u, u + m.node_count());
+        const auto tc = reaction_tangent_coefficient(g, m, un, eps, t);    // batch.cpp:344-351
+        const auto Tm = reduce_matrix(r, local_mass(g, tc, t));
+        const auto Fv = reduce_vector(r, local_reaction_load(g, m, un, eps, t));  // batch.cpp:335-342
+        std::memcpy(T, Tm.values.data(), Tm.values.size() * 8);
+        std::memcpy(F, Fv.data(), Fv.size() * 8);
+    });
+}
+
 // ---------------------------------------------------------------- stage II
 int tgr_reduce_matrix(void* rp, const double* local, double* values) {  // routing.cpp:109-125
     return guarded([&] {

@@ -147,15 +147,32 @@ struct RowVals {
     }
 };
 
+// Internal field types of the Allen-Cahn Newton re-assembly (tgk_allen_cahn_d):
+// nodal state u interpolated at q, then the reaction tangent coefficient
+// -e2 (3 v^2 - 1) (batch.cpp:344-351) or the reaction source -e2 v (v^2 - 1)
+// (batch.cpp:335-342), e2 = eps^2 with eps in FieldDev::value.
+constexpr int kFieldAcTangent = 100, kFieldAcReaction = 101;
+__host__ __device__ inline bool nodal_like(int type) {
+    return type == TGK_FIELD_NODAL || type == kFieldAcTangent || type == kFieldAcReaction;
+}
+
 // c(x_q) for a constant / per-element / nodal field (coefficient.cpp:34-55,
 // interpolate_nodal batch.cpp:321-330)
 template <int KIND, int DEG>
 __device__ __forceinline__ double field_q(const FieldDev& f, const double* u, int q) {
     constexpr int k = P1<KIND>::k;
-    if (f.type == TGK_FIELD_NODAL) {
+    if (nodal_like(f.type)) {
         double v = basis<KIND, DEG>(q, 0) * u[0];
 #pragma unroll
         for (int a = 1; a < k; ++a) v += basis<KIND, DEG>(q, a) * u[a];
+        if (f.type == kFieldAcTangent) {
+            const double e2 = f.value * f.value;
+            return -e2 * (3.0 * v * v - 1.0);
+        }
+        if (f.type == kFieldAcReaction) {
+            const double e2 = f.value * f.value;
+            return -e2 * v * (v * v - 1.0);
+        }
         return v;
     }
     return f.type == TGK_FIELD_ELEMENT ? u[0] : f.value;
@@ -176,13 +193,13 @@ __device__ __forceinline__ void element_tensors(const FusedArgs& p, const double
     for (int a = 0; a < k; ++a)
 #pragma unroll
         for (int c = 0; c < d; ++c) X[a][c] = nt[ids[a] * NV + c];
-    if (p.coef.type == TGK_FIELD_NODAL) {
+    if (nodal_like(p.coef.type)) {
         const double* cs = nt + p.max_bnodes * NV;
 #pragma unroll
         for (int a = 0; a < k; ++a) cu[a] = cs[ids[a]];
     }
-    if (HAS_F && p.src.type == TGK_FIELD_NODAL) {
-        const double* ss = nt + p.max_bnodes * (NV + (p.coef.type == TGK_FIELD_NODAL ? 1 : 0));
+    if (HAS_F && nodal_like(p.src.type)) {
+        const double* ss = nt + p.max_bnodes * (NV + (nodal_like(p.coef.type) ? 1 : 0));
 #pragma unroll
         for (int a = 0; a < k; ++a) fu[a] = ss[ids[a]];
     }
@@ -335,10 +352,10 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
                 double* dst = nt + i * NV;
 #pragma unroll
                 for (int c = 0; c < d; ++c) dst[c] = __ldg(p.nodes + g[u] * d + c);
-                if (p.coef.type == TGK_FIELD_NODAL) nt[p.max_bnodes * NV + i] = __ldg(p.coef.data + g[u]);
+                if (nodal_like(p.coef.type)) nt[p.max_bnodes * NV + i] = __ldg(p.coef.data + g[u]);
                 if constexpr (HAS_F)
-                    if (p.src.type == TGK_FIELD_NODAL)
-                        nt[p.max_bnodes * (NV + (p.coef.type == TGK_FIELD_NODAL ? 1 : 0)) + i] = __ldg(p.src.data + g[u]);
+                    if (nodal_like(p.src.type))
+                        nt[p.max_bnodes * (NV + (nodal_like(p.coef.type) ? 1 : 0)) + i] = __ldg(p.src.data + g[u]);
             }
         }
     }
@@ -455,7 +472,8 @@ int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
 
 template <int KIND, int DEG, int R, bool FDIV>
 int dispatch_r(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, cudaStream_t st) {
-    if (ktype == 1) return launch_fused<KIND, DEG, 1, false, false, R, FDIV>(a, nb, st);
+    if (ktype == 1) return f ? launch_fused<KIND, DEG, 1, false, true, R, FDIV>(a, nb, st)
+                             : launch_fused<KIND, DEG, 1, false, false, R, FDIV>(a, nb, st);
     if (m && f) return launch_fused<KIND, DEG, 0, true, true, R, FDIV>(a, nb, st);
     if (m) return launch_fused<KIND, DEG, 0, true, false, R, FDIV>(a, nb, st);
     if (f) return launch_fused<KIND, DEG, 0, false, true, R, FDIV>(a, nb, st);
@@ -490,18 +508,13 @@ int fused_rows_per_block(const tgk_problem* pr) {
     return pr->with_mass ? 64 : 128;
 }
 
-// Scalar fused assembly on device buffers.  With d_bad == nullptr it checks
-// the bad-element flag (synchronising); otherwise it is fully asynchronous.
-int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
-                          double* F, double* M, cudaStream_t st, unsigned long long* d_bad) {
-    const int R = fused_rows_per_block(pr);
+// Fused scalar assembly core: ktype 0 (diffusion stiffness) / 1 (coefficient
+// mass), quadrature degree, optional unit mass M and load F.
+static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int degree, bool has_m, bool has_f,
+                      FieldDev coef, FieldDev src, double* K, double* F, double* M, cudaStream_t st,
+                      unsigned long long* d_bad) {
     const PlanDev* pl = nullptr;
     TGK_TRY(ensure_plan(r, R, &pl));
-    const bool is_mass = pr->kind == TGK_MASS;
-    const bool high = pr->diffusion.type != TGK_FIELD_CONSTANT || is_mass || pr->with_mass;
-    const int degree = high ? 2 : 1;  // default_mass_degree / default_stiffness_degree for P1
-    const bool has_f = !is_mass && pr->n_source > 0;
-    const bool has_m = pr->with_mass != 0;
     FusedArgs a{};
     a.nodes = m->nodes;
     a.row_ptr = r->row_ptr;
@@ -517,16 +530,15 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
     a.chunk_rec_off = pl->chunk_rec_off;
     a.chunk_row_off = pl->chunk_row_off;
     a.recs = pl->recs;
-    a.coef = FieldDev{pr->diffusion.type, pr->diffusion.value, pr->diffusion.data};
-    a.src = FieldDev{TGK_FIELD_CONSTANT, 0.0, nullptr};
-    if (has_f) a.src = FieldDev{pr->source[0].type, pr->source[0].value, pr->source[0].data};
+    a.coef = coef;
+    a.src = has_f ? src : FieldDev{TGK_FIELD_CONSTANT, 0.0, nullptr};
     a.K = K;
     a.M = M;
     a.F = F;
     a.lmax = pl->lmax;
     a.max_recs = pl->max_chunk_recs > 0 ? pl->max_chunk_recs : 4;
     a.max_bnodes = pl->max_bnodes + (pl->max_bnodes & 1);
-    a.ntcols = 3 + (a.coef.type == TGK_FIELD_NODAL ? 1 : 0) + (has_f && a.src.type == TGK_FIELD_NODAL ? 1 : 0);
+    a.ntcols = 3 + (nodal_like(a.coef.type) ? 1 : 0) + (has_f && nodal_like(a.src.type) ? 1 : 0);
     if (const char* dbg = getenv("TGK_FUSED_DEBUG")) a.debug = atoi(dbg);
     DevBuf<long long> trace;
     const char* trace_path = getenv("TGK_FUSED_TRACE");
@@ -539,7 +551,6 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
     a.bad = d_bad ? d_bad : bad.p;
     CUDA_TRY(cudaMemsetAsync(a.bad, 0xff, sizeof(unsigned long long), st));
     if (!has_f && F) CUDA_TRY(cudaMemsetAsync(F, 0, sizeof(double) * r->N, st));
-    const int ktype = is_mass ? 1 : 0;
     bool fdiv = false;
     TGK_TRY(mesh_division_safe(const_cast<tgk_mesh*>(m), st, &fdiv));
     if (getenv("TGK_IEEE_DIV")) fdiv = false;
@@ -561,6 +572,30 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
     }
     if (!d_bad) return check_bad(bad.p, st);
     return TGK_OK;  // asynchronous: the caller inspects *d_bad
+}
+
+// Scalar fused assembly on device buffers.  With d_bad == nullptr it checks
+// the bad-element flag (synchronising); otherwise it is fully asynchronous.
+int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
+                          double* F, double* M, cudaStream_t st, unsigned long long* d_bad) {
+    const bool is_mass = pr->kind == TGK_MASS;
+    const bool high = pr->diffusion.type != TGK_FIELD_CONSTANT || is_mass || pr->with_mass;
+    const int degree = high ? 2 : 1;  // default_mass_degree / default_stiffness_degree for P1
+    const bool has_f = !is_mass && pr->n_source > 0;
+    const FieldDev coef{pr->diffusion.type, pr->diffusion.value, pr->diffusion.data};
+    const FieldDev src = has_f ? FieldDev{pr->source[0].type, pr->source[0].value, pr->source[0].data}
+                               : FieldDev{TGK_FIELD_CONSTANT, 0.0, nullptr};
+    return fused_core(m, r, fused_rows_per_block(pr), is_mass ? 1 : 0, degree, pr->with_mass != 0, has_f, coef, src,
+                      K, F, M, st, d_bad);
+}
+
+// Allen-Cahn Newton re-assembly (AllenCahnStepper::step, timestep.cpp:144-178)
+// in one fused pass at the mass degree: T = reduce_matrix(local_mass(
+// reaction_tangent_coefficient(u))) and F = reduce_vector(local_reaction_load(u)).
+int fused_allen_cahn(const tgk_mesh* m, tgk_routing* r, const double* u, double eps, double* T, double* F,
+                     cudaStream_t st) {
+    const FieldDev tang{kFieldAcTangent, eps, u}, react{kFieldAcReaction, eps, u};
+    return fused_core(m, r, 128, 1, 2, false, F != nullptr, tang, react, T, F, nullptr, st, nullptr);
 }
 
 }  // namespace tgk

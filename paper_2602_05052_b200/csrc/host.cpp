@@ -158,6 +158,8 @@ int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r
                         double* F, cudaStream_t st);
 int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
                               cudaStream_t st);
+int fused_allen_cahn(const tgk_mesh* m, tgk_routing* r, const double* u, double eps, double* T, double* F,
+                     cudaStream_t st);
 
 }  // namespace tgk
 
@@ -651,6 +653,16 @@ int tgk_assemble_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r
                    double* d_F, double* d_M, void* stream) {
     return tgk::assemble_dev(p, m, const_cast<tgk_routing*>(r), d_K, d_F, d_M,
                              static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int tgk_allen_cahn_d(const tgk_mesh* m, const tgk_routing* r, const double* d_u, double eps, double* d_T,
+                     double* d_F, void* stream) {
+    if (!m || !r || !d_u || !d_T) return set_error(TGK_ERR_INPUT, "tgk_allen_cahn_d: null argument");
+    if (m->kind != TGK_TRI3 && m->kind != TGK_TET4)
+        return set_error(TGK_ERR_INPUT, "P1 assembly supports TRI3 and TET4 meshes only");
+    if (r->components != 1) return set_error(TGK_ERR_INPUT, "AllenCahnStepper: scalar fields only");  // timestep.cpp:137
+    TGK_TRY(host_ensure_device());
+    return tgk::fused_allen_cahn(m, const_cast<tgk_routing*>(r), d_u, eps, d_T, d_F, static_cast<cudaStream_t>(stream));
 }
 
 int tgk_assemble_async_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r,

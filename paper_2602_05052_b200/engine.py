@@ -87,7 +87,10 @@ class DeviceMesh:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().tgk_mesh_destroy(h)
+            try:
+                lib().tgk_mesh_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self._h = None
 
 
@@ -109,7 +112,10 @@ class Routing:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().tgk_routing_destroy(h)
+            try:
+                lib().tgk_routing_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self._h = None
 
     def host_arrays(self, slot_of=True, segments=None):
@@ -319,3 +325,13 @@ def adjoint_gather(mesh, routing, lam, U, degree=1, stream=None):
     check(lib().tgk_adjoint_gather_d(mesh._h, routing._h, B, _ptr(lam), _ptr(U), _ptr(out),
                                      int(degree), _stream(stream)))
     return out
+
+
+def allen_cahn(mesh, routing, u, eps, with_load=True, stream=None):
+    """AllenCahnStepper Newton re-assembly (timestep.cpp:144-178), fused: tangent-mass values T
+    (nnz) and reaction load F (N) for the nodal state u."""
+    u = _cuda_f64(u, routing.N)
+    T = torch.empty(routing.nnz, dtype=torch.float64, device=_DEV)
+    F = torch.empty(routing.N, dtype=torch.float64, device=_DEV) if with_load else None
+    check(lib().tgk_allen_cahn_d(mesh._h, routing._h, _ptr(u), float(eps), _ptr(T), _ptr(F), _stream(stream)))
+    return T, F

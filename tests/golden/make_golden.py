@@ -117,6 +117,15 @@ def small_mesh(tag, kind, ext, div, seed):
     save(f"mesh_{tag}.npz", **out)
 
 
+def allen_cahn(tag, kind, ext, div, seed, eps):
+    """AllenCahnStepper Newton re-assembly (timestep.cpp:144-178) through the reference code."""
+    m = ref.Mesh.grid(kind, ext, div)
+    r = ref.Routing(m, 1)
+    u = 2.0 * u01(MT64(seed), m.N) - 1.0
+    T, F = ref.allen_cahn(m, r, u, eps)
+    save(f"allen_cahn_{tag}.npz", nodes=m.nodes, elements=m.elements, u=u, eps=np.float64(eps), T=T, F=F)
+
+
 if __name__ == "__main__":
     ref_triangle()
     tri3_1x1()
@@ -124,3 +133,5 @@ if __name__ == "__main__":
     small_mesh("tri3_7x5", "tri3", [1.0, 0.5], [7, 5], 12)
     small_mesh("tet4_2x2x2", "tet4", [1.0, 1.0, 1.0], [2, 2, 2], 13)
     small_mesh("tet4_3x2x4", "tet4", [1.3, 0.7, 1.1], [3, 2, 4], 14)
+    allen_cahn("tri3_7x5", "tri3", [1.0, 0.5], [7, 5], 21, 0.8)
+    allen_cahn("tet4_3x2x4", "tet4", [1.3, 0.7, 1.1], [3, 2, 4], 22, 0.35)
