@@ -41,6 +41,7 @@ class Mesh:
         self._nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, self.dim)
         self._elements = np.ascontiguousarray(elements, dtype=np.int64).reshape(-1, k)
         self._boundary = None if boundary_nodes is None else np.asarray(boundary_nodes, np.int64)
+        self.boundary_tags = {}  # gmsh entity tag -> sorted node ids (mesh.hpp boundary_tags)
         self._dev = {}
 
     @property
@@ -172,12 +173,146 @@ def compliance(F, U):
     return s
 
 
+_GMSH_DIM = {1: 1, 2: 2, 3: 2, 4: 3, 15: 0}      # gmsh_io.cpp kind_dim
+_GMSH_NODES = {1: 2, 2: 3, 3: 4, 4: 4, 15: 1}    # gmsh_io.cpp kind_nodes
+_GMSH_KIND = {2: "tri3", 3: "quad4", 4: "tet4"}
+
+
 def load_gmsh(path):
-    raise NotImplementedError("gmsh I/O is outside the accelerated assembly path (SURVEY.md 8(f))")
+    """tg::load_gmsh (gmsh_io.cpp:64-221): MSH 4.x ASCII; node tags re-packed to
+    0-based indices in ascending tag order, one volume element kind, lower-
+    dimensional elements become boundary tag groups; Mesh::validate at the end.
+    The input-side half of SURVEY.md 8(c)'s identical-input rule."""
+    try:
+        f = open(path)
+    except OSError:
+        raise InputError(f"cannot open mesh file: {path}") from None
+    lines = []
+    with f:
+        for raw in f:
+            ln = raw.rstrip("\n")
+            if ln.endswith("\r"):
+                ln = ln[:-1]
+            if ln:
+                lines.append(ln)
+    pos = 0
+
+    def nxt(what):
+        nonlocal pos
+        if pos >= len(lines):
+            raise InputError(f"{path}:{pos}: unexpected end of file in {what}")
+        pos += 1
+        return lines[pos - 1]
+
+    nodes_by_tag, raw_elems, saw_format = {}, [], False
+    while pos < len(lines):
+        ln = nxt("file")
+        if not ln.startswith("$"):
+            continue
+        section = ln[1:]
+        if section == "MeshFormat":
+            head = nxt("$MeshFormat").split()
+            try:
+                version, binary = float(head[0]), int(head[1])
+            except (IndexError, ValueError):
+                raise InputError(f"{path}: unsupported mesh format (need MSH 4.x ASCII)") from None
+            if version < 4.0 or version >= 5.0 or binary != 0:
+                raise InputError(f"{path}: unsupported mesh format (need MSH 4.x ASCII)")
+            saw_format = True
+            if nxt("$MeshFormat") != "$EndMeshFormat":
+                raise InputError(f"{path}: missing $EndMeshFormat")
+        elif section == "Nodes":
+            nb = int(nxt("$Nodes").split()[0])
+            for _ in range(nb):
+                _, _, _, count = (int(x) for x in nxt("$Nodes").split()[:4])
+                tags = [int(nxt("node tags").split()[0]) for _ in range(count)]
+                for t in tags:
+                    xs = nxt("node coordinates").split()
+                    nodes_by_tag[t] = (float(xs[0]), float(xs[1]), float(xs[2]))
+            if nxt("$Nodes") != "$EndNodes":
+                raise InputError(f"{path}: missing $EndNodes")
+        elif section == "Elements":
+            nb = int(nxt("$Elements").split()[0])
+            for _ in range(nb):
+                _, etag, etype, count = (int(x) for x in nxt("$Elements").split()[:4])
+                nn = _GMSH_NODES.get(etype)
+                if nn is None:
+                    raise InputError(f"{path}: unsupported element type {etype}")
+                for _ in range(count):
+                    parts = nxt("element list").split()
+                    if len(parts) < 1 + nn:
+                        raise InputError(f"{path}: malformed element connectivity")
+                    raw_elems.append((etype, etag, [int(x) for x in parts[1:1 + nn]]))
+            if nxt("$Elements") != "$EndElements":
+                raise InputError(f"{path}: missing $EndElements")
+        else:  # skip unknown sections ($Entities, $PhysicalNames, ...)
+            end = "$End" + section
+            while nxt(end) != end:
+                pass
+    if not saw_format:
+        raise InputError(f"{path}: not a Gmsh MSH file (no $MeshFormat)")
+    if not nodes_by_tag:
+        raise InputError(f"{path}: no $Nodes section")
+    if not raw_elems:
+        raise InputError(f"{path}: no $Elements section")
+    vol_dim = max(_GMSH_DIM[t] for t, _, _ in raw_elems)
+    vol_types = {t for t, _, _ in raw_elems if _GMSH_DIM[t] == vol_dim}
+    if len(vol_types) > 1:
+        a, b = sorted(vol_types)[:2]
+        raise InputError(f"{path}: mixed volume element kinds (types {a} and {b})")
+    vol_type = vol_types.pop()
+    if vol_type not in _GMSH_KIND:
+        raise InputError(f"{path}: no supported volume elements (TRI3/QUAD4/TET4)")
+    tags = sorted(nodes_by_tag)
+    index_of = {t: i for i, t in enumerate(tags)}
+    nodes = np.array([nodes_by_tag[t][:vol_dim] for t in tags], dtype=np.float64)
+    elems, groups, bnodes = [], {}, set()
+    for etype, etag, conn in raw_elems:
+        try:
+            ids = [index_of[t] for t in conn]
+        except KeyError as exc:
+            raise InputError(f"{path}: element references unknown node tag {exc.args[0]}") from None
+        if _GMSH_DIM[etype] == vol_dim:
+            elems.append(ids)
+        else:
+            groups.setdefault(str(etag), []).extend(ids)
+            bnodes.update(ids)
+    mesh = Mesh(_GMSH_KIND[vol_type], nodes, np.array(elems, dtype=np.int64),
+                boundary_nodes=sorted(bnodes) if bnodes else None)
+    mesh.boundary_tags = {k: sorted(set(v)) for k, v in sorted(groups.items())}
+    mesh.validate()
+    return mesh
+
+
+def _fmt17(x):
+    """std::ostream << double at precision(17) (default floatfield) == printf %.17g."""
+    return "%.17g" % x
 
 
 def write_gmsh(mesh, path):
-    raise NotImplementedError("gmsh I/O is outside the accelerated assembly path (SURVEY.md 8(f))")
+    """tg::write_gmsh (gmsh_io.cpp:223-250): MSH 4.1 ASCII, one node and one element block,
+    tags 1..N / 1..E; byte-identical to the reference writer."""
+    try:
+        out = open(path, "w")
+    except OSError:
+        raise InputError(f"cannot open file for writing: {path}") from None
+    nodes, elems = mesh.nodes, mesh.elements
+    N, E = nodes.shape[0], elems.shape[0]
+    gtype = {"TRI3": 2, "QUAD4": 3, "TET4": 4}[mesh.kind]
+    dim = mesh.dim
+    w = ["$MeshFormat\n4.1 0 8\n$EndMeshFormat\n", f"$Nodes\n1 {N} 1 {N}\n", f"{dim} 1 0 {N}\n"]
+    w.extend(f"{i + 1}\n" for i in range(N))
+    for i in range(N):
+        x = nodes[i]
+        z = x[2] if dim == 3 else 0.0
+        w.append(f"{_fmt17(x[0])} {_fmt17(x[1])} {_fmt17(z)}\n")
+    w.append("$EndNodes\n")
+    w.append(f"$Elements\n1 {E} 1 {E}\n{dim} 1 {gtype} {E}\n")
+    for e in range(E):
+        w.append(str(e + 1) + "".join(f" {int(v) + 1}" for v in elems[e]) + "\n")
+    w.append("$EndElements\n")
+    with out:
+        out.write("".join(w))
 
 
 def solve_poisson(mesh, diffusion=None, source=1.0):
