@@ -171,8 +171,13 @@ int tgk_interface_combine_d(const double* d_lower, double* d_values, int64_t n, 
  * factor), packed records, device bytes. */
 int tgk_routing_plan_stats(tgk_routing* r, int rows_per_block, int64_t* n_blocks, int64_t* n_halo,
                            int64_t* n_records, int64_t* bytes);
-/* Routing cache file in the reference layout ("tg-rout2", routing.cpp:178-234). */
+/* Routing cache file in the reference layout ("tg-rout2", save_routing routing.cpp:194-209). */
 int tgk_routing_save(const tgk_routing* r, uint64_t mesh_hash, const char* path);
+/* load_routing (routing.cpp:211-234): *hit = 0 (status 0) on a missing file or a
+ * magic / mesh-hash / size mismatch, as the reference returns false; else a
+ * device routing bit-identical to the cached arrays in *out. */
+int tgk_routing_load(const tgk_mesh* m, int components, uint64_t mesh_hash, const char* path, void* stream,
+                     int* hit, tgk_routing** out);
 
 /* ------------------------------------------------------------------ Stage I (Map), materialised */
 /* batch_geometry + push_forward (batch.cpp:56-154).  Outputs E x Q x ... like

@@ -82,6 +82,7 @@ _SIGS = {
     "tgk_routing_set_element_range": (_I, [_P, _I64, _I64]),
     "tgk_interface_combine_d": (_I, [_P, _P, _I64, _P]),
     "tgk_allen_cahn_d": (_I, [_P, _P, _P, _D, _P, _P, _P]),
+    "tgk_routing_load": (_I, [_P, _I, C.c_uint64, C.c_char_p, _P, _P, _P]),
     "tgk_routing_plan_stats": (_I, [_P, _I, _P, _P, _P, _P]),
     "tgk_routing_save": (_I, [_P, C.c_uint64, C.c_char_p]),
     "tgk_geometry_d": (_I, [_P, _I, _P, _P, _P, _P, _P, _P]),

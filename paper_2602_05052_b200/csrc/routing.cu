@@ -17,6 +17,10 @@
 // columns {d*j + c' : j in row i}.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
 #include "cuda_util.cuh"
 #include "tgk_internal.hpp"
 
@@ -419,6 +423,87 @@ int tgk_routing_get_view(const tgk_routing* r, tgk_routing_view* v) {
     v->vec_slots = r->vec_slots;
     v->mat_offsets = r->mat_offsets;
     v->mat_slots = r->mat_slots;
+    return TGK_OK;
+}
+
+// load_routing (routing.cpp:211-234): the reference's "tg-rout2" cache file ->
+// a device routing.  *hit = 0 (and TGK_OK) on a missing file, wrong magic,
+// mesh-hash mismatch, size mismatch with the mesh or a short read — the cases
+// in which the reference returns false and the caller rebuilds.
+int tgk_routing_load(const tgk_mesh* m, int components, uint64_t mesh_hash, const char* path, void* stream,
+                     int* hit, tgk_routing** out) {
+    using namespace tgk;
+    if (!m || !path || !hit || !out) return set_error(TGK_ERR_INPUT, "tgk_routing_load: null argument");
+    *hit = 0;
+    *out = nullptr;
+    if (components != 1 && components != m->d)
+        return set_error(TGK_ERR_INPUT, "components per node must be 1 or the mesh dimension");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return TGK_OK;
+    int64_t h[6];
+    auto rd = [f](void* dst, size_t bytes) { return std::fread(dst, 1, bytes, f) == bytes; };
+    if (!rd(h, sizeof h) || static_cast<uint64_t>(h[0]) != 0x74672d726f757432ull ||
+        static_cast<uint64_t>(h[1]) != mesh_hash || h[2] != m->N * components || h[3] != m->E ||
+        h[4] != m->k * components) {
+        std::fclose(f);
+        return TGK_OK;
+    }
+    const int64_t N = h[2], E = h[3], nnz = h[5];
+    const int k = static_cast<int>(h[4]);
+    const size_t Ek = static_cast<size_t>(E) * k;
+    std::vector<int64_t> off(N + 1), cols(nnz);
+    std::vector<uint32_t> vo(N + 1), vs(Ek), mo(nnz + 1), ms(Ek * k);
+    const bool ok = rd(off.data(), off.size() * 8) && rd(cols.data(), cols.size() * 8) && rd(vo.data(), vo.size() * 4) &&
+                    rd(vs.data(), vs.size() * 4) && rd(mo.data(), mo.size() * 4) && rd(ms.data(), ms.size() * 4);
+    std::fclose(f);
+    if (!ok) return TGK_OK;
+    TGK_TRY(ensure_device());
+    cudaStream_t st = as_stream(stream);
+    auto* r = new tgk_routing();
+    r->mesh = m;
+    r->N = N;
+    r->E = E;
+    r->k = k;
+    r->nnz = nnz;
+    r->components = components;
+    int64_t lmax = 0;
+    for (int64_t i = 0; i < N; ++i) lmax = std::max<int64_t>(lmax, off[i + 1] - off[i]);
+    r->lmax = static_cast<int>(lmax);
+    auto up = [](auto*& dst, const auto& v) -> int {
+        using T = typename std::remove_reference<decltype(v)>::type::value_type;
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&dst), std::max<size_t>(1, v.size()) * sizeof(T)));
+        if (!v.empty()) CUDA_TRY(cudaMemcpy(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+        return TGK_OK;
+    };
+    int rc = TGK_OK;
+    if (!rc) rc = up(r->row_ptr, off);
+    if (!rc) rc = up(r->col_idx, cols);
+    if (!rc) rc = up(r->vec_offsets, vo);
+    if (!rc) rc = up(r->vec_slots, vs);
+    if (!rc) rc = up(r->mat_offsets, mo);
+    if (!rc) rc = up(r->mat_slots, ms);
+    if (!rc && components == 1) {
+        // element-to-slot map = inverse of the segment map (slot_of[mat_slots[u]] = t)
+        std::vector<uint32_t> slot(Ek * k);
+        for (int64_t t = 0; t < nnz; ++t)
+            for (uint32_t u = mo[t]; u < mo[t + 1]; ++u) slot[ms[u]] = static_cast<uint32_t>(t);
+        rc = up(r->slot_of, slot);
+        r->scalar = r;
+    } else if (!rc) {
+        // the fused kernels run on the node-level (scalar) routing: rebuild it on the GPU
+        auto* s = new tgk_routing();
+        s->mesh = m;
+        rc = build_scalar(m, 0, st, s);
+        if (rc) delete s;
+        else r->scalar = s;
+    }
+    if (rc) {
+        if (r->scalar == r) r->scalar = nullptr;
+        delete r;
+        return rc;
+    }
+    *hit = 1;
+    *out = r;
     return TGK_OK;
 }
 

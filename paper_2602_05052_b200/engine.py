@@ -136,7 +136,26 @@ class Routing:
         return out
 
     def save(self, mesh_hash, path):
+        """save_routing (routing.cpp:194-209): the reference's "tg-rout2" cache file."""
         check(lib().tgk_routing_save(self._h, C.c_uint64(mesh_hash), str(path).encode()))
+
+    @classmethod
+    def load(cls, mesh: DeviceMesh, mesh_hash, path, components=1, stream=None):
+        """load_routing (routing.cpp:211-234): a Routing, or None on a cache miss."""
+        h, hit = C.c_void_p(), C.c_int(0)
+        check(lib().tgk_routing_load(mesh._h, int(components), C.c_uint64(mesh_hash), str(path).encode(),
+                                     _stream(stream), C.byref(hit), C.byref(h)))
+        if not hit.value:
+            return None
+        self = cls.__new__(cls)
+        self.mesh = mesh
+        self._h = h
+        v = N.RoutingView()
+        check(lib().tgk_routing_get_view(h, C.byref(v)))
+        self.N, self.E, self.nnz, self.k = v.N, v.E, v.nnz, v.k
+        self.components = v.components
+        self.has_segments = bool(v.mat_offsets)
+        return self
 
 
 def make_problem(kind="poisson", diffusion=1.0, lam=1.0, mu=1.0, plane_stress=False, sources=(),

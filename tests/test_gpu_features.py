@@ -111,3 +111,34 @@ def test_interface_combine_kernel(eng):
     ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
     D.gpu_combine(ta, tb)
     assert_bitwise(np_(tb), a + b)
+
+
+@pytest.mark.parametrize("kind,div,comps", [("tri3", [9, 7], 1), ("tet4", [4, 3, 5], 1), ("tet4", [3, 3, 2], 3)])
+def test_routing_cache_round_trip_with_reference(eng, tmp_path, kind, div, comps):
+    """save_routing / load_routing (routing.cpp:194-234): our file is byte-identical to
+    the reference's, the reference's file loads into a routing that assembles identically,
+    and a hash mismatch is a cache miss (the reference returns false)."""
+    from oracle import ref
+    nodes, elems = port.generate_grid(kind, [1.0] * len(div), div)
+    h = port.content_hash(kind, nodes, elems)
+    m = eng.DeviceMesh(kind, nodes, elems)
+    r = eng.Routing(m, comps, segments=True)
+    ours = tmp_path / "ours.bin"
+    r.save(h, ours)
+    if ref.available():
+        rm = ref.Mesh.from_arrays(kind, nodes, elems)
+        theirs = tmp_path / "ref.bin"
+        ref.Routing(rm, comps).save(h, theirs)
+        assert ours.read_bytes() == theirs.read_bytes()
+    r2 = eng.Routing.load(m, h, ours, components=comps)
+    assert r2 is not None
+    a, b = r.host_arrays(), r2.host_arrays()
+    for key in a:
+        assert np.array_equal(a[key], b[key]), key
+    kw = dict(kind="elasticity", lam=0.6, mu=0.4, sources=[1.0] * 3) if comps == 3 else dict(sources=[1.0])
+    K1, F1, _ = eng.assemble(m, r, **kw)
+    K2, F2, _ = eng.assemble(m, r2, **kw)
+    assert_bitwise(np_(K1), np_(K2), "K")
+    assert_bitwise(np_(F1), np_(F2), "F")
+    assert eng.Routing.load(m, h ^ 1, ours, components=comps) is None
+    assert eng.Routing.load(m, h, tmp_path / "missing.bin", components=comps) is None
