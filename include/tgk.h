@@ -260,6 +260,32 @@ int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B,
                          const double* d_lambda, const double* d_U, double* d_out, int degree,
                          void* stream);
 
+/* ------------------------------------------------------------------ consumers of the CSR */
+typedef struct tgk_condensed tgk_condensed;
+/* SparseOperator::apply (sparse.cpp:18-31): y = A x, row sums in column order from +0.0. */
+int tgk_spmv_d(int64_t rows, const int64_t* d_offsets, const int64_t* d_cols, const double* d_values,
+               const double* d_x, double* d_y, void* stream);
+/* condense (solver.cpp:34-85) on device CSR (N rows, CsrPattern offsets/cols, K values, F):
+ * free / constrained DoF lists (ascending), K_ff pattern and values, F_f = F - K_fc g.
+ * Duplicate Dirichlet DoFs: the last value wins (as the reference's assignment loop).
+ * Out-of-range DoF -> status 2 "condense: dirichlet dof out of range". */
+int tgk_condense_d(int64_t N, const int64_t* d_offsets, const int64_t* d_cols, const double* d_K, const double* d_F,
+                   int64_t n_dirichlet, const int64_t* d_dofs, const double* d_values, void* stream,
+                   tgk_condensed** out);
+int tgk_condensed_info(const tgk_condensed* c, int64_t* n_free, int64_t* n_fixed, int64_t* nnz_ff,
+                       const int64_t** d_free_dofs, const int64_t** d_fixed_dofs, const double** d_prescribed,
+                       const int64_t** d_offsets, const int64_t** d_cols, const double** d_values,
+                       const double** d_F_f);
+/* Copy the condensed system to host arrays (any pointer may be NULL). */
+int tgk_condensed_copy(const tgk_condensed* c, int64_t* free_dofs, int64_t* fixed_dofs, double* prescribed,
+                       int64_t* offsets, int64_t* cols, double* values, double* F_f);
+/* restrict_to_free (solver.cpp:87-103): the free-free block of another operator on the same pattern. */
+int tgk_restrict_to_free_d(const tgk_condensed* c, const int64_t* d_offsets, const int64_t* d_cols, const double* d_A,
+                           double* d_out, void* stream);
+/* CondensedSystem::expand (solver.cpp:20-26): full vector from free values + prescribed values. */
+int tgk_expand_d(const tgk_condensed* c, const double* d_u_free, double* d_u, void* stream);
+void tgk_condensed_destroy(tgk_condensed* c);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,8 @@ def lib():
         L.tgr_gradient_products.argtypes = [P] * 5
         L.tgr_simp_sensitivity.argtypes = [P, P, P, C.c_double, C.c_double, C.c_double, P, P, P]
         L.tgr_allen_cahn.argtypes = [P, P, P, C.c_double, P, P]
+        L.tgr_condense.argtypes = [P, P, P, C.c_int64] + [P] * 12
+        L.tgr_spmv.argtypes = [P] * 4
         _lib = L
     return _lib
 
@@ -249,6 +251,32 @@ def allen_cahn(mesh: Mesh, routing: Routing, u, eps):
     F = np.zeros(routing.N)
     _check(lib().tgr_allen_cahn(mesh._h, routing._h, _p(u), C.c_double(eps), _p(T), _p(F)))
     return T, F
+
+
+def condense(routing: Routing, K, F, dofs, values):
+    """condense (solver.cpp:34-85): dict of free_dofs, fixed_dofs, prescribed, offsets, cols, values, F_f."""
+    dofs = np.ascontiguousarray(dofs, dtype=np.int64)
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    K = np.ascontiguousarray(K, dtype=np.float64)
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    N, nnz = routing.N, routing.nnz
+    nf, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+    buf = dict(free_dofs=np.zeros(N, np.int64), fixed_dofs=np.zeros(N, np.int64), prescribed=np.zeros(N),
+               offsets=np.zeros(N + 1, np.int64), cols=np.zeros(nnz, np.int64), values=np.zeros(nnz), F_f=np.zeros(N))
+    _check(lib().tgr_condense(routing._h, _p(K), _p(F), dofs.size, _p(dofs), _p(values), C.byref(nf), C.byref(nc),
+                              C.byref(nz), *[_p(buf[k]) for k in ["free_dofs", "fixed_dofs", "prescribed", "offsets",
+                                                                 "cols", "values", "F_f"]]))
+    n, c, z = nf.value, nc.value, nz.value
+    return dict(free_dofs=buf["free_dofs"][:n], fixed_dofs=buf["fixed_dofs"][:c], prescribed=buf["prescribed"][:c],
+                offsets=buf["offsets"][:n + 1], cols=buf["cols"][:z], values=buf["values"][:z], F_f=buf["F_f"][:n])
+
+
+def spmv(routing: Routing, values, x):
+    """SparseOperator::apply (sparse.cpp:18-31)."""
+    y = np.zeros(routing.N)
+    _check(lib().tgr_spmv(routing._h, _p(np.ascontiguousarray(values, dtype=np.float64)),
+                          _p(np.ascontiguousarray(x, dtype=np.float64)), _p(y)))
+    return y
 
 
 def assemble(mesh: Mesh, routing: Routing, problem="poisson", diffusion=1.0, lam=1.0, mu=1.0,

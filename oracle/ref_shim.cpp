@@ -25,6 +25,7 @@
 #include "tg/physics.hpp"
 #include "tg/reference.hpp"
 #include "tg/routing.hpp"
+#include "tg/solver.hpp"
 #include "tg/sparse.hpp"
 
 using namespace tg;
@@ -265,6 +266,44 @@ int tgr_allen_cahn(void* mp, void* rp, const double* u, double eps, double* T, d
         const auto Fv = reduce_vector(r, local_reaction_load(g, m, un, eps, t));  // batch.cpp:335-342
         std::memcpy(T, Tm.values.data(), Tm.values.size() * 8);
         std::memcpy(F, Fv.data(), Fv.size() * 8);
+    });
+}
+
+// condense (solver.cpp:34-85) of a K on the routing's pattern; outputs sized by
+// the caller: free/fixed lists and F_f (N), K_ff offsets (N+1), cols/values (nnz).
+int tgr_condense(void* rp, const double* K, const double* F, std::int64_t nd, const std::int64_t* dofs,
+                 const double* vals, std::int64_t* n_free, std::int64_t* n_fixed, std::int64_t* nnz_ff,
+                 std::int64_t* free_dofs, std::int64_t* fixed_dofs, double* prescribed, std::int64_t* offsets,
+                 std::int64_t* cols, double* values, double* F_f) {
+    return guarded([&] {
+        const auto& r = static_cast<RefRouting*>(rp)->routing;
+        SparseOperator Kop;
+        Kop.pattern = r.pattern;
+        Kop.values.assign(K, K + r.nnz());
+        const auto sys = condense(Kop, std::vector<double>(F, F + r.N), std::vector<std::int64_t>(dofs, dofs + nd),
+                                  std::vector<double>(vals, vals + nd));
+        *n_free = static_cast<std::int64_t>(sys.free_dofs.size());
+        *n_fixed = static_cast<std::int64_t>(sys.constrained_dofs.size());
+        *nnz_ff = static_cast<std::int64_t>(sys.K_ff.values.size());
+        std::memcpy(free_dofs, sys.free_dofs.data(), sys.free_dofs.size() * 8);
+        std::memcpy(fixed_dofs, sys.constrained_dofs.data(), sys.constrained_dofs.size() * 8);
+        std::memcpy(prescribed, sys.prescribed.data(), sys.prescribed.size() * 8);
+        std::memcpy(offsets, sys.K_ff.pattern->offsets.data(), sys.K_ff.pattern->offsets.size() * 8);
+        std::memcpy(cols, sys.K_ff.pattern->cols.data(), sys.K_ff.pattern->cols.size() * 8);
+        std::memcpy(values, sys.K_ff.values.data(), sys.K_ff.values.size() * 8);
+        std::memcpy(F_f, sys.F_f.data(), sys.F_f.size() * 8);
+    });
+}
+
+// SparseOperator::apply (sparse.cpp:18-31) on the routing's pattern
+int tgr_spmv(void* rp, const double* vals, const double* x, double* y) {
+    return guarded([&] {
+        const auto& r = static_cast<RefRouting*>(rp)->routing;
+        SparseOperator A;
+        A.pattern = r.pattern;
+        A.values.assign(vals, vals + r.nnz());
+        const auto out = A.apply(std::vector<double>(x, x + r.N));
+        std::memcpy(y, out.data(), out.size() * 8);
     });
 }
 

@@ -83,6 +83,13 @@ _SIGS = {
     "tgk_interface_combine_d": (_I, [_P, _P, _I64, _P]),
     "tgk_allen_cahn_d": (_I, [_P, _P, _P, _D, _P, _P, _P]),
     "tgk_routing_load": (_I, [_P, _I, C.c_uint64, C.c_char_p, _P, _P, _P]),
+    "tgk_spmv_d": (_I, [_I64, _P, _P, _P, _P, _P, _P]),
+    "tgk_condense_d": (_I, [_I64, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
+    "tgk_condensed_info": (_I, [_P] * 11),
+    "tgk_restrict_to_free_d": (_I, [_P, _P, _P, _P, _P, _P]),
+    "tgk_expand_d": (_I, [_P, _P, _P, _P]),
+    "tgk_condensed_copy": (_I, [_P] * 8),
+    "tgk_condensed_destroy": (None, [_P]),
     "tgk_routing_plan_stats": (_I, [_P, _I, _P, _P, _P, _P]),
     "tgk_routing_save": (_I, [_P, C.c_uint64, C.c_char_p]),
     "tgk_geometry_d": (_I, [_P, _I, _P, _P, _P, _P, _P, _P]),

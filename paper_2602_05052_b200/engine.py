@@ -354,3 +354,70 @@ def allen_cahn(mesh, routing, u, eps, with_load=True, stream=None):
     F = torch.empty(routing.N, dtype=torch.float64, device=_DEV) if with_load else None
     check(lib().tgk_allen_cahn_d(mesh._h, routing._h, _ptr(u), float(eps), _ptr(T), _ptr(F), _stream(stream)))
     return T, F
+
+
+# ---------------------------------------------------------------- consumers of the CSR
+def _csr_device(routing):
+    if not hasattr(routing, "_csr_dev"):
+        h = routing.host_arrays(slot_of=False, segments=False)
+        routing._csr_dev = (torch.from_numpy(h["offsets"]).to(_DEV), torch.from_numpy(h["cols"]).to(_DEV))
+    return routing._csr_dev
+
+
+def spmv(routing, values, x, stream=None):
+    """SparseOperator::apply (sparse.cpp:18-31) on the routing's pattern."""
+    off, cols = _csr_device(routing)
+    x = _cuda_f64(x, routing.N)
+    y = torch.empty(routing.N, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_spmv_d(routing.N, _ptr(off), _ptr(cols), _ptr(values), _ptr(x), _ptr(y), _stream(stream)))
+    return y
+
+
+class Condensed:
+    """condense (solver.cpp:34-85) on the device: K_ff pattern and values, F_f, free /
+    constrained DoFs and prescribed values, held by a libtgk handle."""
+
+    def __init__(self, routing, K, F, dofs, values, stream=None):
+        off, cols = _csr_device(routing)
+        d = torch.as_tensor(np.asarray(dofs, dtype=np.int64)).to(_DEV)
+        v = _cuda_f64(values, d.numel())
+        h = C.c_void_p()
+        check(lib().tgk_condense_d(routing.N, _ptr(off), _ptr(cols), _ptr(K), _ptr(F), d.numel(), _ptr(d), _ptr(v),
+                                   _stream(stream), C.byref(h)))
+        self._h, self._routing = h, routing
+        nf, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().tgk_condensed_info(h, C.byref(nf), C.byref(nc), C.byref(nz), *([None] * 8)))
+        self.n_free, self.n_fixed, self.nnz_ff = nf.value, nc.value, nz.value
+
+    def arrays(self):
+        """Host copies: free_dofs, fixed_dofs, prescribed, offsets, cols, values, F_f."""
+        out = dict(free_dofs=np.empty(self.n_free, np.int64), fixed_dofs=np.empty(self.n_fixed, np.int64),
+                   prescribed=np.empty(self.n_fixed), offsets=np.empty(self.n_free + 1, np.int64),
+                   cols=np.empty(self.nnz_ff, np.int64), values=np.empty(self.nnz_ff), F_f=np.empty(self.n_free))
+        check(lib().tgk_condensed_copy(self._h, *[out[k].ctypes.data for k in
+                                                  ["free_dofs", "fixed_dofs", "prescribed", "offsets", "cols",
+                                                   "values", "F_f"]]))
+        return out
+
+    def restrict_to_free(self, A, stream=None):
+        """restrict_to_free (solver.cpp:87-103) of another operator on the routing's pattern."""
+        off, cols = _csr_device(self._routing)
+        out = torch.empty(self.nnz_ff, dtype=torch.float64, device=_DEV)
+        check(lib().tgk_restrict_to_free_d(self._h, _ptr(off), _ptr(cols), _ptr(A), _ptr(out), _stream(stream)))
+        return out
+
+    def expand(self, u_free, stream=None):
+        """CondensedSystem::expand (solver.cpp:20-26)."""
+        u_free = _cuda_f64(u_free, self.n_free)
+        u = torch.empty(self._routing.N, dtype=torch.float64, device=_DEV)
+        check(lib().tgk_expand_d(self._h, _ptr(u_free), _ptr(u), _stream(stream)))
+        return u
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().tgk_condensed_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._h = None

@@ -142,3 +142,43 @@ def test_routing_cache_round_trip_with_reference(eng, tmp_path, kind, div, comps
     assert_bitwise(np_(F1), np_(F2), "F")
     assert eng.Routing.load(m, h ^ 1, ours, components=comps) is None
     assert eng.Routing.load(m, h, tmp_path / "missing.bin", components=comps) is None
+
+
+def test_spmv_and_condense_match_reference(eng):
+    """SparseOperator::apply and condense / restrict_to_free / expand (sparse.cpp:18-31,
+    solver.cpp:20-103) on the device, bit-identical to the reference library."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("reference library (oracle/_ref) not built")
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [7, 6, 5])
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    r = eng.Routing(m, 1)
+    rho = 0.5 + np.random.default_rng(3).random(elems.shape[0])
+    K, F, M = eng.assemble(m, r, diffusion=("element", rho), sources=[1.0], with_mass=True)
+    rm = ref.Mesh.from_arrays("tet4", nodes, elems)
+    rr = ref.Routing(rm, 1)
+    x = np.random.default_rng(4).random(nodes.shape[0]) - 0.5
+    assert_bitwise(np_(eng.spmv(r, K, x)), ref.spmv(rr, np_(K), x), "spmv")
+    bnd = rm.boundary_nodes
+    rng = np.random.default_rng(5)
+    dofs = np.concatenate([bnd, bnd[:7]])              # duplicates: the last value wins
+    vals = rng.random(dofs.size)
+    c = eng.Condensed(r, K, F, dofs, vals)
+    got = c.arrays()
+    want = ref.condense(rr, np_(K), np_(F), dofs, vals)
+    for key in want:
+        if want[key].dtype == np.float64:
+            assert_bitwise(got[key], want[key], key)
+        else:
+            assert np.array_equal(got[key], want[key]), key
+    Mff = np_(c.restrict_to_free(M))
+    want_M = ref.condense(rr, np_(M), np_(F), dofs, vals)["values"]
+    assert_bitwise(Mff, want_M, "restrict_to_free")
+    uf = rng.random(c.n_free)
+    u = np_(c.expand(uf))
+    full = np.zeros(nodes.shape[0])
+    full[want["free_dofs"]] = uf
+    full[want["fixed_dofs"]] = want["prescribed"]
+    assert_bitwise(u, full, "expand")
+    with pytest.raises(eng.N.InputError, match="out of range"):
+        eng.Condensed(r, K, F, [nodes.shape[0]], [1.0])
