@@ -285,6 +285,17 @@ int tgk_restrict_to_free_d(const tgk_condensed* c, const int64_t* d_offsets, con
 /* CondensedSystem::expand (solver.cpp:20-26): full vector from free values + prescribed values. */
 int tgk_expand_d(const tgk_condensed* c, const double* d_u_free, double* d_u, void* stream);
 void tgk_condensed_destroy(tgk_condensed* c);
+/* Device-to-device copy on a stream (plumbing for the Python layer). */
+int tgk_copy_d2d(void* dst, const void* src, int64_t nbytes, void* stream);
+/* bicgstab (solver.cpp:105-227): Jacobi-preconditioned BiCGSTAB with up to 8
+ * restarts, divergence rollback and best-iterate fallback, on device CSR.
+ * d_x holds the initial guess and receives the solution.  Dot products are
+ * deterministic fixed-order reductions (the reference folds serially), so
+ * iterates agree with the reference to rounding, not bitwise.
+ * Zero diagonal -> status 1 (NumericalError) like the reference. */
+int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, const double* d_values,
+                   const double* d_b, double* d_x, double tol_rel, double tol_abs, int64_t max_iter,
+                   int64_t* iterations, double* rel_residual, int* converged, void* stream);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,7 @@ def lib():
         L.tgr_allen_cahn.argtypes = [P, P, P, C.c_double, P, P]
         L.tgr_condense.argtypes = [P, P, P, C.c_int64] + [P] * 12
         L.tgr_spmv.argtypes = [P] * 4
+        L.tgr_bicgstab.argtypes = [C.c_int64, P, P, P, P, P, C.c_double, C.c_double, C.c_int64, P, P, P]
         _lib = L
     return _lib
 
@@ -269,6 +270,17 @@ def condense(routing: Routing, K, F, dofs, values):
     n, c, z = nf.value, nc.value, nz.value
     return dict(free_dofs=buf["free_dofs"][:n], fixed_dofs=buf["fixed_dofs"][:c], prescribed=buf["prescribed"][:c],
                 offsets=buf["offsets"][:n + 1], cols=buf["cols"][:z], values=buf["values"][:z], F_f=buf["F_f"][:n])
+
+
+def bicgstab(offsets, cols, values, b, tol_rel=1e-10, tol_abs=1e-10, max_iter=10000):
+    """bicgstab (solver.cpp:105-227) from a zero initial guess: (x, report)."""
+    n = len(offsets) - 1
+    x = np.zeros(n)
+    it, rel, conv = C.c_int64(), C.c_double(), C.c_int()
+    _check(lib().tgr_bicgstab(n, _p(np.ascontiguousarray(offsets, np.int64)), _p(np.ascontiguousarray(cols, np.int64)),
+                              _p(np.ascontiguousarray(values, np.float64)), _p(np.ascontiguousarray(b, np.float64)),
+                              _p(x), tol_rel, tol_abs, max_iter, C.byref(it), C.byref(rel), C.byref(conv)))
+    return x, {"iterations": it.value, "rel_residual": rel.value, "converged": bool(conv.value)}
 
 
 def spmv(routing: Routing, values, x):

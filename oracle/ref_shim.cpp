@@ -295,6 +295,31 @@ int tgr_condense(void* rp, const double* K, const double* F, std::int64_t nd, co
     });
 }
 
+// bicgstab (solver.cpp:105-227) on a CSR given as arrays
+int tgr_bicgstab(std::int64_t n, const std::int64_t* off, const std::int64_t* cols, const double* vals,
+                 const double* b, double* x, double tol_rel, double tol_abs, std::int64_t max_iter,
+                 std::int64_t* iters, double* rel, int* conv) {
+    return guarded([&] {
+        auto pat = std::make_shared<CsrPattern>();
+        pat->rows = n;
+        pat->offsets.assign(off, off + n + 1);
+        pat->cols.assign(cols, cols + off[n]);
+        SparseOperator A;
+        A.pattern = pat;
+        A.values.assign(vals, vals + off[n]);
+        std::vector<double> xv(x, x + n);
+        SolverConfig cfg;
+        cfg.tol_rel = tol_rel;
+        cfg.tol_abs = tol_abs;
+        cfg.max_iter = max_iter;
+        const auto rep = bicgstab(A, std::vector<double>(b, b + n), xv, cfg);
+        std::memcpy(x, xv.data(), n * 8);
+        *iters = rep.iterations;
+        *rel = rep.rel_residual;
+        *conv = rep.converged ? 1 : 0;
+    });
+}
+
 // SparseOperator::apply (sparse.cpp:18-31) on the routing's pattern
 int tgr_spmv(void* rp, const double* vals, const double* x, double* y) {
     return guarded([&] {

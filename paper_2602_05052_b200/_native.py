@@ -90,6 +90,8 @@ _SIGS = {
     "tgk_expand_d": (_I, [_P, _P, _P, _P]),
     "tgk_condensed_copy": (_I, [_P] * 8),
     "tgk_condensed_destroy": (None, [_P]),
+    "tgk_bicgstab_d": (_I, [_I64, _P, _P, _P, _P, _P, _D, _D, _I64, _P, _P, _P, _P]),
+    "tgk_copy_d2d": (_I, [_P, _P, _I64, _P]),
     "tgk_routing_plan_stats": (_I, [_P, _I, _P, _P, _P, _P]),
     "tgk_routing_save": (_I, [_P, C.c_uint64, C.c_char_p]),
     "tgk_geometry_d": (_I, [_P, _I, _P, _P, _P, _P, _P, _P]),

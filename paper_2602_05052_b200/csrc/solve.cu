@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 
 #include "cuda_util.cuh"
 #include "tgk_internal.hpp"
@@ -131,6 +132,100 @@ __global__ void k_expand(int64_t n_free, const int64_t* free_dofs, const double*
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (i < n_free) u[free_dofs[i]] = u_free[i];
         if (i < n_fixed) u[fixed_dofs[i]] = prescribed[i];
+    }
+}
+
+
+// ------------------------------------------------------------------ BiCGSTAB (solver.cpp:105-227)
+constexpr int kDotBlocks = 296, kDotThreads = 256;
+
+// Deterministic dot product: fixed grid, fixed per-thread ranges, fixed tree
+// orders (the reference uses a serial left fold, solver.cpp:11-16; results
+// agree to rounding, run-to-run bitwise reproducible here).
+__global__ void k_dot_partial(const double* a, const double* b, int64_t n, double* part) {
+    __shared__ double sh[kDotThreads];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)kDotThreads + threadIdx.x; i < n; i += (int64_t)kDotBlocks * kDotThreads)
+        s += a[i] * b[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = kDotThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void k_dot_final(const double* part, double* out) {
+    __shared__ double sh[512];
+    sh[threadIdx.x] = threadIdx.x < kDotBlocks ? part[threadIdx.x] : 0.0;
+    __syncthreads();
+    for (int w = 256; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+// SparseOperator::diagonal (sparse.cpp:50-57) -> 1 / d; flags a zero diagonal
+__global__ void k_inv_diag(int64_t n, const int64_t* off, const int64_t* cols, const double* vals, double* inv,
+                           int* zero) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double d = 0.0;
+        int64_t lo = off[i], hi = off[i + 1];
+        while (lo < hi) {  // CsrPattern::find (sparse.cpp:10-16)
+            const int64_t mid = (lo + hi) >> 1;
+            if (cols[mid] < i) lo = mid + 1; else hi = mid;
+        }
+        if (lo < off[i + 1] && cols[lo] == i) d = vals[lo];
+        if (d == 0.0) atomicExch(zero, 1);
+        inv[i] = 1.0 / d;
+    }
+}
+
+// r = b - A x (+ non-finite flag)
+__global__ void k_residual(int64_t n, const int64_t* off, const int64_t* cols, const double* vals, const double* x,
+                           const double* b, double* r, int* nonfinite) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int64_t t = off[i]; t < off[i + 1]; ++t) s += vals[t] * x[cols[t]];
+        const double v = b[i] - s;
+        if (!isfinite(v)) atomicExch(nonfinite, 1);
+        r[i] = v;
+    }
+}
+
+// p = r + beta (p - omega v); phat = inv_diag p
+__global__ void k_bicg_p(int64_t n, const double* r, const double* v, const double* inv, double beta, double omega,
+                         double* p, double* phat) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double pi = r[i] + beta * (p[i] - omega * v[i]);
+        p[i] = pi;
+        phat[i] = inv[i] * pi;
+    }
+}
+
+// s = r - alpha v
+__global__ void k_bicg_s(int64_t n, const double* r, const double* v, double alpha, double* s) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s[i] = r[i] - alpha * v[i];
+}
+
+// y = inv_diag x
+__global__ void k_scale(int64_t n, const double* inv, const double* x, double* y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = inv[i] * x[i];
+}
+
+// x += alpha phat (+ omega shat); r = s - omega t
+__global__ void k_bicg_x(int64_t n, double alpha, const double* phat, double omega, const double* shat,
+                         const double* s, const double* t, double* x, double* r, int full) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (full) {
+            x[i] += alpha * phat[i] + omega * shat[i];
+            r[i] = s[i] - omega * t[i];
+        } else {
+            x[i] += alpha * phat[i];
+        }
     }
 }
 
@@ -299,6 +394,149 @@ int tgk_condensed_copy(const tgk_condensed* c, int64_t* free_dofs, int64_t* fixe
     TGK_TRY(cp(cols, c->cols, sizeof(int64_t) * c->nnz_ff));
     TGK_TRY(cp(values, c->values, sizeof(double) * c->nnz_ff));
     TGK_TRY(cp(F_f, c->F_f, sizeof(double) * c->n_free));
+    return TGK_OK;
+}
+
+
+// Jacobi-preconditioned BiCGSTAB with restarts, divergence rollback and the
+// best-iterate fallback of the reference (solver.cpp:105-227), on device CSR.
+int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, const double* d_values,
+                   const double* d_b, double* d_x, double tol_rel, double tol_abs, int64_t max_iter,
+                   int64_t* iterations, double* rel_residual, int* converged, void* stream) {
+    using namespace tgk;
+    if (n < 0 || (n > 0 && (!d_offsets || !d_cols || !d_values || !d_b || !d_x)))
+        return set_error(TGK_ERR_INPUT, "bicgstab: bad arguments");
+    TGK_TRY(ensure_device());
+    cudaStream_t st = as_stream(stream);
+    int64_t iters = 0;
+    if (iterations) *iterations = 0;
+    if (rel_residual) *rel_residual = 0.0;
+    if (converged) *converged = 0;
+    if (n == 0) {
+        if (converged) *converged = 1;
+        return TGK_OK;
+    }
+    DevBuf<double> r, p, v, phat, shat, s, t, rt, inv, best_x, part, scal;
+    DevBuf<int> flag;
+    for (DevBuf<double>* b : {&r, &p, &v, &phat, &shat, &s, &t, &rt, &inv, &best_x}) TGK_TRY(b->alloc(n));
+    TGK_TRY(part.alloc(kDotBlocks));
+    TGK_TRY(scal.alloc(1));
+    TGK_TRY(flag.alloc(1));
+    const unsigned G = grid_n(n);
+    auto dot = [&](const double* a, const double* b, double* out) -> int {
+        k_dot_partial<<<kDotBlocks, kDotThreads, 0, st>>>(a, b, n, part.p);
+        k_dot_final<<<1, 512, 0, st>>>(part.p, scal.p);
+        CUDA_TRY(cudaMemcpyAsync(out, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return TGK_OK;
+    };
+    auto nrm = [&](const double* a, double* out) -> int {
+        TGK_TRY(dot(a, a, out));
+        *out = std::sqrt(*out);
+        return TGK_OK;
+    };
+    auto residual = [&](double* out_r, bool* finite) -> int {  // out_r = b - A x
+        CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+        k_residual<<<G, 256, 0, st>>>(n, d_offsets, d_cols, d_values, d_x, d_b, out_r, flag.p);
+        int h = 0;
+        CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        *finite = h == 0;
+        return TGK_OK;
+    };
+    double norm_b = 0.0;
+    TGK_TRY(nrm(d_b, &norm_b));
+    if (norm_b == 0.0) {  // solver.cpp:113-117
+        CUDA_TRY(cudaMemsetAsync(d_x, 0, sizeof(double) * n, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (converged) *converged = 1;
+        return TGK_OK;
+    }
+    CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    k_inv_diag<<<G, 256, 0, st>>>(n, d_offsets, d_cols, d_values, inv.p, flag.p);
+    int zero = 0;
+    CUDA_TRY(cudaMemcpyAsync(&zero, flag.p, sizeof zero, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (zero) return set_error(TGK_ERR_NUMERICAL, "Jacobi preconditioner: zero diagonal entry");
+    const double tol = tol_rel * norm_b, eps_bd = 1e-300;
+    const int max_restarts = 8;
+    CUDA_TRY(cudaMemcpyAsync(best_x.p, d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    double best_res = 1e300;
+    for (int pass = 0; pass <= max_restarts && iters < max_iter; ++pass) {
+        bool finite = true;
+        TGK_TRY(residual(r.p, &finite));
+        if (!finite) {  // diverged iterate: roll back to the best one (solver.cpp:140-145)
+            CUDA_TRY(cudaMemcpyAsync(d_x, best_x.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            TGK_TRY(residual(r.p, &finite));
+        }
+        double res = 0.0;
+        TGK_TRY(nrm(r.p, &res));
+        if (res < best_res) {
+            best_res = res;
+            CUDA_TRY(cudaMemcpyAsync(best_x.p, d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        }
+        if (res <= tol) break;
+        CUDA_TRY(cudaMemcpyAsync(rt.p, r.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemsetAsync(p.p, 0, sizeof(double) * n, st));
+        CUDA_TRY(cudaMemsetAsync(v.p, 0, sizeof(double) * n, st));
+        double rho = 1.0, alpha = 1.0, omega = 1.0;
+        while (res > tol && iters < max_iter) {
+            double rho_new = 0.0;
+            TGK_TRY(dot(rt.p, r.p, &rho_new));
+            if (!std::isfinite(rho_new) || std::abs(rho_new) < eps_bd * norm_b * norm_b) break;
+            const double beta = (rho_new / rho) * (alpha / omega);
+            rho = rho_new;
+            k_bicg_p<<<G, 256, 0, st>>>(n, r.p, v.p, inv.p, beta, omega, p.p, phat.p);
+            k_spmv<<<G, 256, 0, st>>>(n, d_offsets, d_cols, d_values, phat.p, v.p);
+            double rtv = 0.0;
+            TGK_TRY(dot(rt.p, v.p, &rtv));
+            alpha = rho / rtv;
+            if (!std::isfinite(alpha)) break;
+            k_bicg_s<<<G, 256, 0, st>>>(n, r.p, v.p, alpha, s.p);
+            double s_norm = 0.0;
+            TGK_TRY(nrm(s.p, &s_norm));
+            ++iters;
+            if (s_norm <= tol) {
+                k_bicg_x<<<G, 256, 0, st>>>(n, alpha, phat.p, 0.0, nullptr, nullptr, nullptr, d_x, nullptr, 0);
+                res = s_norm;
+                break;
+            }
+            k_scale<<<G, 256, 0, st>>>(n, inv.p, s.p, shat.p);
+            k_spmv<<<G, 256, 0, st>>>(n, d_offsets, d_cols, d_values, shat.p, t.p);
+            double tt = 0.0, ts = 0.0;
+            TGK_TRY(dot(t.p, t.p, &tt));
+            TGK_TRY(dot(t.p, s.p, &ts));
+            omega = ts / tt;
+            if (!std::isfinite(omega) || tt < eps_bd) {
+                k_bicg_x<<<G, 256, 0, st>>>(n, alpha, phat.p, 0.0, nullptr, nullptr, nullptr, d_x, nullptr, 0);
+                break;
+            }
+            k_bicg_x<<<G, 256, 0, st>>>(n, alpha, phat.p, omega, shat.p, s.p, t.p, d_x, r.p, 1);
+            TGK_TRY(nrm(r.p, &res));
+            if (!std::isfinite(res)) break;
+        }
+        KERNEL_CHECK("bicgstab");
+    }
+    // report the true residual, roll back to the best iterate if worse (solver.cpp:210-218)
+    bool finite = true;
+    TGK_TRY(residual(r.p, &finite));
+    double fin = 0.0;
+    TGK_TRY(nrm(r.p, &fin));
+    if (!finite || fin > best_res) {
+        CUDA_TRY(cudaMemcpyAsync(d_x, best_x.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        TGK_TRY(residual(r.p, &finite));
+        TGK_TRY(nrm(r.p, &fin));
+    }
+    if (iterations) *iterations = iters;
+    if (rel_residual) *rel_residual = fin / norm_b;
+    if (converged) *converged = (fin / norm_b <= tol_rel || fin <= tol_abs) ? 1 : 0;
+    return TGK_OK;
+}
+
+int tgk_copy_d2d(void* dst, const void* src, int64_t nbytes, void* stream) {
+    using namespace tgk;
+    if (nbytes < 0 || (nbytes > 0 && (!dst || !src))) return set_error(TGK_ERR_INPUT, "copy_d2d: bad arguments");
+    if (nbytes) CUDA_TRY(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDeviceToDevice, as_stream(stream)));
     return TGK_OK;
 }
 

@@ -421,3 +421,38 @@ class Condensed:
             except Exception:  # interpreter shutdown
                 pass
             self._h = None
+
+
+def bicgstab(offsets, cols, values, b, x0=None, tol_rel=1e-10, tol_abs=1e-10, max_iter=10000, stream=None):
+    """bicgstab (solver.cpp:105-227) on a device CSR (offsets, cols, values: torch CUDA tensors).
+    Returns (x, report dict) like tg::SolveReport."""
+    n = offsets.numel() - 1
+    b = _cuda_f64(b, n)
+    x = torch.zeros(n, dtype=torch.float64, device=_DEV) if x0 is None else _cuda_f64(x0, n).clone()
+    it, rel, conv = C.c_int64(), C.c_double(), C.c_int()
+    check(lib().tgk_bicgstab_d(n, _ptr(offsets), _ptr(cols), _ptr(values), _ptr(b), _ptr(x), float(tol_rel),
+                               float(tol_abs), int(max_iter), C.byref(it), C.byref(rel), C.byref(conv),
+                               _stream(stream)))
+    return x, {"iterations": it.value, "rel_residual": rel.value, "converged": bool(conv.value)}
+
+
+def solve_condensed(cond, tol_rel=1e-10, tol_abs=1e-10, max_iter=10000, stream=None):
+    """Solve K_ff u_f = F_f on the device and expand with the prescribed values
+    (solve_condensed solver.cpp:268-292, BiCGSTAB path; the reference switches to a
+    dense LU below 2000 free DoFs, which is not ported)."""
+    off = torch.empty(cond.n_free + 1, dtype=torch.int64, device=_DEV)
+    cols = torch.empty(cond.nnz_ff, dtype=torch.int64, device=_DEV)
+    vals = torch.empty(cond.nnz_ff, dtype=torch.float64, device=_DEV)
+    F_f = torch.empty(cond.n_free, dtype=torch.float64, device=_DEV)
+    ptrs = [C.c_void_p() for _ in range(7)]
+    check(lib().tgk_condensed_info(cond._h, None, None, None, *[C.byref(p) for p in ptrs]))
+    for t, pp, n, es in [(off, ptrs[3], cond.n_free + 1, 8), (cols, ptrs[4], cond.nnz_ff, 8),
+                         (vals, ptrs[5], cond.nnz_ff, 8), (F_f, ptrs[6], cond.n_free, 8)]:
+        if n:
+            _copy_d2d(t, pp.value, n * es)
+    u_f, rep = bicgstab(off, cols, vals, F_f, tol_rel=tol_rel, tol_abs=tol_abs, max_iter=max_iter, stream=stream)
+    return cond.expand(u_f, stream=stream), rep
+
+
+def _copy_d2d(dst, src_ptr, nbytes, stream=None):
+    check(lib().tgk_copy_d2d(_ptr(dst), C.c_void_p(src_ptr), C.c_int64(nbytes), _stream(stream)))

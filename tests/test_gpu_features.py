@@ -182,3 +182,32 @@ def test_spmv_and_condense_match_reference(eng):
     assert_bitwise(u, full, "expand")
     with pytest.raises(eng.N.InputError, match="out of range"):
         eng.Condensed(r, K, F, [nodes.shape[0]], [1.0])
+
+
+def test_device_poisson_solve_matches_reference_bicgstab(eng):
+    """assemble -> condense -> BiCGSTAB -> expand on the device (solver.cpp:34-292) vs the
+    reference's bicgstab on the same condensed system: converged, same solution to
+    solver tolerance (dot products are parallel reductions, not the serial fold)."""
+    from oracle import ref
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [12, 10, 9])
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    r = eng.Routing(m, 1)
+    rho = 0.5 + np.random.default_rng(8).random(elems.shape[0])
+    K, F, _ = eng.assemble(m, r, diffusion=("element", rho), sources=[1.0])
+    from paper_2602_05052_b200 import tgfem
+    bnd = tgfem.Mesh("tet4", nodes, elems).boundary_nodes
+    c = eng.Condensed(r, K, F, bnd, np.zeros(bnd.size))
+    u, rep = eng.solve_condensed(c, tol_rel=1e-12)
+    assert rep["converged"] and rep["rel_residual"] <= 1e-12
+    a = c.arrays()
+    # residual of the full system on the free rows: K u - F == 0 there
+    Ku = np_(eng.spmv(r, K, u))
+    res = (Ku - np_(F))[a["free_dofs"]]
+    assert np.linalg.norm(res) <= 1e-10 * np.linalg.norm(np_(F)[a["free_dofs"]])
+    assert np.all(np_(u)[a["fixed_dofs"]] == 0.0)
+    if ref.available():
+        xr, rr = ref.bicgstab(a["offsets"], a["cols"], a["values"], a["F_f"], tol_rel=1e-12)
+        assert rr["converged"]
+        uf = np_(u)[a["free_dofs"]]
+        assert np.max(np.abs(uf - xr)) <= 1e-9 * np.max(np.abs(xr))
+        assert abs(rep["iterations"] - rr["iterations"]) <= max(3, rr["iterations"] // 5)
