@@ -5,9 +5,9 @@ and out, computed by the sm_100a kernels of libtgk.so.
 
 Differences by design: the device mesh and the routing (pattern + slot map)
 are cached per mesh object instead of being rebuilt on every call
-(module.cpp:116-117 rebuilds build_routing each time).  Solvers and topology
-optimisation (solve_poisson, topopt_cantilever) are outside the accelerated
-path and raise NotImplementedError.
+(module.cpp:116-117 rebuilds build_routing each time).  solve_poisson runs on
+the device (condensation + BiCGSTAB); topology optimisation (topopt_cantilever)
+is outside the accelerated path and raises NotImplementedError.
 """
 from __future__ import annotations
 
@@ -316,7 +316,25 @@ def write_gmsh(mesh, path):
 
 
 def solve_poisson(mesh, diffusion=None, source=1.0):
-    raise NotImplementedError("linear solves are outside the accelerated assembly path (SURVEY.md 8(f))")
+    """Homogeneous-Dirichlet Poisson solve (module.cpp:133-157) on the GPU: fused
+    assembly, condensation of the boundary nodes (solver.cpp:34-85) and Jacobi
+    BiCGSTAB (solver.cpp:105-227); returns {u, iterations, rel_residual}.
+    Difference by design: the reference's dense LU for <= 2000 free DoFs
+    (solver.cpp:274-281) is not ported; BiCGSTAB is used at every size."""
+    from . import engine
+    dm = mesh._device()
+    r = mesh._routing(1, segments=False)
+    coef = 1.0 if diffusion is None else ("element", np.asarray(diffusion, dtype=np.float64))
+    K, F, _ = engine.assemble(dm, r, diffusion=coef, sources=[float(source)])
+    b = mesh.boundary_nodes
+    cond = engine.Condensed(r, K, F, b, np.zeros(b.size))
+    if cond.n_free == 0:
+        return {"u": cond.expand(np.zeros(0)).cpu().numpy(), "iterations": 0, "rel_residual": 0.0}
+    u, rep = engine.solve_condensed(cond)
+    if not rep["converged"]:
+        raise NumericalError(f"linear solve did not converge: rel_residual = {rep['rel_residual']} "
+                             f"after {rep['iterations']} iterations")
+    return {"u": u.cpu().numpy(), "iterations": rep["iterations"], "rel_residual": rep["rel_residual"]}
 
 
 def topopt_cantilever(nx=60, ny=30, iterations=51, vol_frac=0.5):

@@ -211,3 +211,25 @@ def test_device_poisson_solve_matches_reference_bicgstab(eng):
         uf = np_(u)[a["free_dofs"]]
         assert np.max(np.abs(uf - xr)) <= 1e-9 * np.max(np.abs(xr))
         assert abs(rep["iterations"] - rr["iterations"]) <= max(3, rr["iterations"] // 5)
+
+
+def test_tgfem_solve_poisson_device(eng):
+    """module.cpp:133-157 drop-in: residual of the full system on free rows, zero on the
+    boundary, and agreement with a direct sparse solve (scipy) of the same system."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    from paper_2602_05052_b200 import tgfem
+    mesh = tgfem.generate_grid("tri3", [1.0, 1.0], [40, 30])
+    rho = 0.5 + np.random.default_rng(2).random(mesh.element_count())
+    out = tgfem.solve_poisson(mesh, rho, 1.0)
+    u = out["u"]
+    assert out["rel_residual"] <= 1e-10
+    r = port.Routing(mesh.node_count(), port.dofmap("tri3", mesh.elements, 1))
+    K, F, _ = port.assemble("tri3", mesh.nodes, mesh.elements, r, diffusion=("element", rho), sources=[1.0])
+    A = sp.csr_matrix((K, r.cols, r.offsets), shape=(mesh.node_count(),) * 2)
+    b = mesh.boundary_nodes
+    free = np.setdiff1d(np.arange(mesh.node_count()), b)
+    ref_u = np.zeros(mesh.node_count())
+    ref_u[free] = spla.spsolve(A[free][:, free].tocsc(), F[free])
+    assert np.all(u[b] == 0.0)
+    assert np.max(np.abs(u - ref_u)) <= 1e-8 * np.max(np.abs(ref_u))
