@@ -83,15 +83,15 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def alg_bytes(kind, E, Nn, nnz, with_mass, has_f, comps=1):
+def alg_bytes(kind, E, Nn, nnz, with_mass, has_f, comps=1, vbytes=8):
     """SURVEY.md 8(d) algorithmic bytes: connectivity E*k*4 + coordinates N*d*8
     + slot map E*k^2*4 + CSR values nnz*8 per matrix + load N_dof*8
-    (+ scalar row_ptr (N+1)*4 for vector problems)."""
+    (+ scalar row_ptr (N+1)*4 for vector problems); vbytes=4 for the fp32 outputs."""
     k = 4 if kind == "tet4" else 3
     d = 3 if kind == "tet4" else 2
-    b = E * k * 4 + Nn * d * 8 + E * k * k * 4 + nnz * 8 * (2 if with_mass else 1)
+    b = E * k * 4 + Nn * d * 8 + E * k * k * 4 + nnz * vbytes * (2 if with_mass else 1)
     if has_f:
-        b += Nn * comps * 8
+        b += Nn * comps * vbytes
     if comps > 1:
         b += (Nn + 1) * 4
     return b, b - E * k * k * 4
@@ -364,17 +364,22 @@ def run_scalar(args, ctx, N):
     setup_s = time.time() - t0
     with_mass = kw.get("with_mass", False)
     has_f = bool(kw.get("sources"))
-    p, keep = engine.make_problem("poisson", mode=args.mode, **kw)
-    K = torch.zeros(routing.nnz, dtype=torch.float64, device=ctx.dev)
-    F = torch.zeros(routing.N, dtype=torch.float64, device=ctx.dev)
-    M = torch.zeros(routing.nnz, dtype=torch.float64, device=ctx.dev) if with_mass else None
+    p, keep = engine.make_problem("poisson", **kw)
+    f32 = args.precision == "f32"
+    vdt = torch.float32 if f32 else torch.float64
+    K = torch.zeros(routing.nnz, dtype=vdt, device=ctx.dev)
+    F = torch.zeros(routing.N, dtype=vdt, device=ctx.dev)
+    M = torch.zeros(routing.nnz, dtype=vdt, device=ctx.dev) if with_mass else None
     bad = torch.empty(1, dtype=torch.int64, device=ctx.dev)
     row_ptr = routing.host_arrays(slot_of=False, segments=False)["offsets"]
     exchange = s is not None and world > 1 and s.mode == "exchange"
     ev_k0, ev_k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def kernel():
-        N.check(L.tgk_assemble_async_d(C.byref(p), mesh._h, routing._h, ptr(K), ptr(F), ptr(M), ptr(bad), ctx.sp))
+        if f32:
+            N.check(L.tgk_assemble_f32_d(C.byref(p), mesh._h, routing._h, ptr(K), ptr(F), ptr(M), ptr(bad), ctx.sp))
+        else:
+            N.check(L.tgk_assemble_async_d(C.byref(p), mesh._h, routing._h, ptr(K), ptr(F), ptr(M), ptr(bad), ctx.sp))
 
     def step():
         kernel()
@@ -384,6 +389,7 @@ def run_scalar(args, ctx, N):
                 z = torch.zeros_like(F)
                 D.exchange_interface(M, z, row_ptr, s, D.gpu_combine, ctx.dist)
 
+    bad.fill_(-1)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -411,7 +417,7 @@ def run_scalar(args, ctx, N):
 
     # e2e through the C ABI with host buffers
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not f32:
         h_nodes = torch.from_numpy(np.ascontiguousarray(nodes)).pin_memory()
         h_elems = torch.from_numpy(np.ascontiguousarray(elems)).pin_memory()
         o0, o1 = own_rows
@@ -455,11 +461,11 @@ def run_scalar(args, ctx, N):
     # roofline of the fused kernel (per launch, kernel-only events)
     Nn = own_rows[1] - own_rows[0]
     nnz_own = int(row_ptr[own_rows[1]] - row_ptr[own_rows[0]])
-    ab, comp = alg_bytes(kind, E_own, Nn, nnz_own, with_mass, has_f)
+    ab, comp = alg_bytes(kind, E_own, Nn, nnz_own, with_mass, has_f, vbytes=4 if f32 else 8)
     peak, peak_src = peaks()
     achieved = ab / (ms_kernel * 1e-3) / 1e9
     launches = args.steps * (1 + (2 * (2 if with_mass else 1) if exchange and s.receives_down else 0))
-    config = {"workload": desc, "elements_per_gpu": E_own, "nnz_per_gpu": nnz_own, "mode": args.mode,
+    config = {"workload": desc, "elements_per_gpu": E_own, "nnz_per_gpu": nnz_own, "mode": "exact (bit-identical)",
               "parallelism": parallelism,
               "l2": "inputs larger than L2 (working set > 126 MB L2)" if ab > 2e8 else
                     "working set below L2 size (C1 parity config; no flush between steps)",
@@ -648,8 +654,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
     ap.add_argument("--dist-mode", default="exchange", choices=["exchange", "halo"])
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
+                    help="f32: the fp32 variant of the fused scalar kernel (tgk_assemble_f32_d)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample", type=int, nargs="*", default=None)
@@ -672,7 +679,7 @@ def main():
         line = {
             "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ctx.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-            "scaling": r["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": r["scaling"], "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": r["config"], "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"],
             "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],
         }

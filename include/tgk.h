@@ -55,9 +55,10 @@ extern "C" {
 #define TGK_FIELD_ELEMENT 1 /* E values                       */
 #define TGK_FIELD_NODAL 2   /* N_node values, interpolated by the basis (batch.cpp:314-333) */
 
-/* arithmetic modes for the fused path */
-#define TGK_MODE_EXACT 0 /* reference operation order, no FMA: bit-identical CSR values */
-#define TGK_MODE_FAST 1  /* FMA + shared reciprocal: within 1e-13 relative (scaled) */
+/* arithmetic mode of tgk_problem (fp64 entries): the reference operation order,
+ * no FMA contraction, bit-identical CSR values.  The fp32 variant is a separate
+ * entry point (tgk_assemble_f32_d) with float outputs. */
+#define TGK_MODE_EXACT 0
 
 typedef struct tgk_mesh tgk_mesh;
 typedef struct tgk_routing tgk_routing;
@@ -78,7 +79,7 @@ typedef struct {
     int n_source;          /* 0, 1 (scalar) or d (elasticity body force) */
     tgk_field source[3];
     int with_mass;         /* also assemble M (scalar problems only; physics.cpp:68-73) */
-    int mode;              /* TGK_MODE_EXACT (default) or TGK_MODE_FAST */
+    int mode;              /* TGK_MODE_EXACT (the only fp64 mode; other values: status 2) */
 } tgk_problem;
 
 /* Routing description (RoutingMatrices, routing.hpp:16-32).  All pointers are
@@ -224,6 +225,14 @@ int tgk_assemble_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r
 int tgk_assemble_async_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r,
                          double* d_K, double* d_F, double* d_M, unsigned long long* d_bad,
                          void* stream);
+/* fp32 variant of tgk_assemble_d for scalar problems: the same fused kernel in
+ * single precision with float CSR values / load (field data stays fp64 and is
+ * rounded on load).  Accuracy vs the fp64 reference: |dv| <= 1e-5 |v| + 1e-7 max|v|
+ * (north star "1e-5 in fp32"). */
+int tgk_assemble_f32_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, float* d_K,
+                       float* d_F, float* d_M, unsigned long long* d_bad, void* stream);
+/* d_bad: NULL = check the Jacobians synchronously; else asynchronous, the smallest
+ * element with det <= 0 (or ~0ull) lands in the 8-byte device word *d_bad. */
 /* Same call on HOST buffers (field data, outputs), with the copies inside. */
 int tgk_assemble(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, double* K,
                  double* F, double* M);

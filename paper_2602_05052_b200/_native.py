@@ -15,7 +15,7 @@ TGK_OK, TGK_ERR_NUMERICAL, TGK_ERR_INPUT, TGK_ERR_CUDA = 0, 1, 2, 3
 TRI3, QUAD4, TET4 = 0, 1, 2
 POISSON, ELASTICITY, MASS = 0, 1, 2
 FIELD_CONSTANT, FIELD_ELEMENT, FIELD_NODAL = 0, 1, 2
-MODE_EXACT, MODE_FAST = 0, 1
+MODE_EXACT = 0
 ROUTING_SEGMENTS = 1
 KINDS = {"tri3": TRI3, "quad4": QUAD4, "tet4": TET4}
 KIND_NAMES = {v: k.upper() for k, v in KINDS.items()}
@@ -82,6 +82,7 @@ _SIGS = {
     "tgk_routing_set_element_range": (_I, [_P, _I64, _I64]),
     "tgk_interface_combine_d": (_I, [_P, _P, _I64, _P]),
     "tgk_allen_cahn_d": (_I, [_P, _P, _P, _D, _P, _P, _P]),
+    "tgk_assemble_f32_d": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "tgk_routing_load": (_I, [_P, _I, C.c_uint64, C.c_char_p, _P, _P, _P]),
     "tgk_spmv_d": (_I, [_I64, _P, _P, _P, _P, _P, _P]),
     "tgk_condense_d": (_I, [_I64, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),

@@ -216,8 +216,8 @@ int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, con
 int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, const double* rho,
                            double source, double* K, double* F, int mode, void* stream) {
     using namespace tgk;
-    (void)mode;
     if (!m || !r) return set_error(TGK_ERR_INPUT, "assemble_batched: null argument");
+    if (mode != TGK_MODE_EXACT) return set_error(TGK_ERR_INPUT, "assemble_batched: unknown arithmetic mode");
     if (r->components != 1) return set_error(TGK_ERR_INPUT, "assemble_batched: scalar routing required");
     if (B < 0) return set_error(TGK_ERR_INPUT, "assemble_batched: negative batch");
     TGK_TRY(ensure_device());

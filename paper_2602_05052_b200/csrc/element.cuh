@@ -162,32 +162,35 @@ struct ExactDiv {
 // basis gradients G (k x d).  Returns false when det <= 0 (batch.cpp:98-101).
 // FASTDIV selects ExactDiv (same nonzero bits, ~3 instead of ~30 instructions
 // per quotient) for the fused kernels; the materialised drop-ins keep '/'.
-template <int KIND, bool FASTDIV = false>
-__device__ __forceinline__ bool simplex_geometry(const double (&X)[P1<KIND>::k][P1<KIND>::d],
-                                                 double& det, double (&G)[P1<KIND>::k][P1<KIND>::d]) {
+// T = float: the fp32 mode (tgk_assemble_f32_d), same expressions in fp32
+// with IEEE division (FASTDIV is fp64-only).
+template <int KIND, bool FASTDIV = false, typename T = double>
+__device__ __forceinline__ bool simplex_geometry(const T (&X)[P1<KIND>::k][P1<KIND>::d],
+                                                 T& det, T (&G)[P1<KIND>::k][P1<KIND>::d]) {
+    static_assert(!FASTDIV || sizeof(T) == 8, "Markstein division is the fp64 path");
     if constexpr (KIND == TGK_TET4) {
         // J[i][j] = sum_a X[a][i] * Ghat[a][j]; Ghat row 0 = -1, rows 1..3 = e_j
-        double J[9];
+        T J[9];
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int j = 0; j < 3; ++j) J[i * 3 + j] = X[j + 1][i] - X[0][i];
         // invert_transpose cofactors (batch.cpp:26-34)
-        const double c00 = J[4] * J[8] - J[5] * J[7];
-        const double c01 = J[5] * J[6] - J[3] * J[8];
-        const double c02 = J[3] * J[7] - J[4] * J[6];
-        const double c10 = J[2] * J[7] - J[1] * J[8];
-        const double c11 = J[0] * J[8] - J[2] * J[6];
-        const double c12 = J[1] * J[6] - J[0] * J[7];
-        const double c20 = J[1] * J[5] - J[2] * J[4];
-        const double c21 = J[2] * J[3] - J[0] * J[5];
-        const double c22 = J[0] * J[4] - J[1] * J[3];
+        const T c00 = J[4] * J[8] - J[5] * J[7];
+        const T c01 = J[5] * J[6] - J[3] * J[8];
+        const T c02 = J[3] * J[7] - J[4] * J[6];
+        const T c10 = J[2] * J[7] - J[1] * J[8];
+        const T c11 = J[0] * J[8] - J[2] * J[6];
+        const T c12 = J[1] * J[6] - J[0] * J[7];
+        const T c20 = J[1] * J[5] - J[2] * J[4];
+        const T c21 = J[2] * J[3] - J[0] * J[5];
+        const T c22 = J[0] * J[4] - J[1] * J[3];
         // batch.cpp:95-96: J0*(J4J8-J5J7) - J1*(J3J8-J5J6) + J2*(J3J7-J4J6)
         //   == (J0*c00 + J1*c01) + J2*c02 exactly (c01 is the negated middle term)
         det = (J[0] * c00 + J[1] * c01) + J[2] * c02;
-        if (det <= 0.0) return false;
+        if (det <= T(0)) return false;
         // J^{-T} = cofactor / det (batch.cpp:36-44); push_forward: G_a = J^{-T} Ghat_a
-        double t00, t01, t02, t10, t11, t12, t20, t21, t22;
+        T t00, t01, t02, t10, t11, t12, t20, t21, t22;
         if constexpr (FASTDIV) {
             const ExactDiv dv(det);
             t00 = dv(c00); t01 = dv(c01); t02 = dv(c02);
@@ -205,12 +208,12 @@ __device__ __forceinline__ bool simplex_geometry(const double (&X)[P1<KIND>::k][
         G[0][1] = -((t10 + t11) + t12);
         G[0][2] = -((t20 + t21) + t22);
     } else {
-        const double J0 = X[1][0] - X[0][0], J1 = X[2][0] - X[0][0];
-        const double J2 = X[1][1] - X[0][1], J3 = X[2][1] - X[0][1];
+        const T J0 = X[1][0] - X[0][0], J1 = X[2][0] - X[0][0];
+        const T J2 = X[1][1] - X[0][1], J3 = X[2][1] - X[0][1];
         det = J0 * J3 - J1 * J2;
-        if (det <= 0.0) return false;
+        if (det <= T(0)) return false;
         // batch.cpp:21-24
-        double t00, t01, t10, t11;
+        T t00, t01, t10, t11;
         if constexpr (FASTDIV) {
             const ExactDiv dv(det);
             t00 = dv(J3); t01 = dv(-J2); t10 = dv(-J1); t11 = dv(J0);
@@ -226,8 +229,8 @@ __device__ __forceinline__ bool simplex_geometry(const double (&X)[P1<KIND>::k][
 }
 
 // dot_ab of local_stiffness_diffusion (batch.cpp:173-174)
-template <int KIND>
-__device__ __forceinline__ double gdot(const double (&G)[P1<KIND>::k][P1<KIND>::d], int a, int b) {
+template <int KIND, typename T = double>
+__device__ __forceinline__ T gdot(const T (&G)[P1<KIND>::k][P1<KIND>::d], int a, int b) {
     if constexpr (KIND == TGK_TET4)
         return (G[a][0] * G[b][0] + G[a][1] * G[b][1]) + G[a][2] * G[b][2];
     else

@@ -62,9 +62,9 @@ struct FusedArgs {
     const uint32_t* recs;
     FieldDev coef;
     FieldDev src;
-    double* K;
-    double* M;
-    double* F;
+    void* K;  // T* (double, or float in the fp32 mode)
+    void* M;
+    void* F;
     int lmax;
     int max_recs;
     int max_bnodes;
@@ -87,17 +87,20 @@ constexpr int kRing = TGK_RING;  // cp.async ring slots: chunk c+kRing-1 is requ
 // diagonal, then the other local nodes in ascending order (see pack_rec).
 __host__ __device__ constexpr int rot(int a, int b) { return b == a ? 0 : (b < a ? b + 1 : b); }
 
-// KTYPE 0: diffusion stiffness, 1: coefficient mass (ProblemKind::Mass)
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R>
+// KTYPE 0: diffusion stiffness, 1: coefficient mass (ProblemKind::Mass);
+// T: double (exact mode) or float (fp32 mode)
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, typename T = double>
 struct FusedCfg {
     static constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q;
-    // local tensors in shared memory: rotated rows of 4 doubles (16-byte aligned pairs)
+    // local tensors in shared memory: rotated rows of 4 values (16-byte aligned)
     static constexpr int offK = 0;
     static constexpr int offM = 4 * k;
     static constexpr int offF = offM + (HAS_M ? 4 * k : 0);
     static constexpr int raw = offF + (HAS_F ? 4 : 0);
-    // stride in doubles = 2 * odd: conflict-free 128-bit accesses across lanes
-    static constexpr int stride = (raw / 2) % 2 == 1 ? raw : raw + 2;
+    // stride = (16-byte vector) x odd: conflict-free 128-bit accesses across lanes
+    static constexpr int VEC = 16 / int(sizeof(T));
+    static constexpr int stride = ((raw + VEC - 1) / VEC) % 2 == 1 ? (raw + VEC - 1) / VEC * VEC
+                                                                   : (raw + VEC - 1) / VEC * VEC + VEC;
     static constexpr int nmat = 1 + (HAS_M ? 1 : 0);
     // node table: coordinates, d doubles per node (odd 8-byte-word stride for
     // d = 3: random node gathers spread over all bank pairs), then the nodal
@@ -106,7 +109,7 @@ struct FusedCfg {
     // doubles per node in the table: the coordinates, then the nodal
     // coefficient / source columns only when those fields are nodal (FusedArgs::ntcols)
     static size_t smem_bytes(int lmax, int max_recs, int max_bnodes, int ntcols) {
-        return sizeof(double) * (size_t(R) * stride + size_t(R) * lmax * nmat + size_t(max_bnodes) * ntcols) +
+        return sizeof(T) * (size_t(R) * stride + size_t(R) * lmax * nmat + size_t(max_bnodes) * ntcols) +
                kRing * (sizeof(uint32_t) * size_t(max_recs) + sizeof(uint16_t) * size_t(row_off_stride(R)) +
                         sizeof(uint16_t) * 4 * size_t(R));
     }
@@ -124,24 +127,34 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// Four consecutive values of a 16-byte aligned shared-memory row.
+__device__ __forceinline__ void load4(const double* src, double (&v)[4]) {
+    const double2 a = *reinterpret_cast<const double2*>(src);
+    const double2 b = *reinterpret_cast<const double2*>(src + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+__device__ __forceinline__ void load4(const float* src, float (&v)[4]) {
+    const float4 a = *reinterpret_cast<const float4*>(src);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+}
+
 // One record's rotated local tensor row (K, M) and F_e[a] from shared memory.
-template <bool HAS_M, bool HAS_F>
+template <typename T, bool HAS_M, bool HAS_F>
 struct RowVals {
-    double kv[4];
-    double mv[HAS_M ? 4 : 1];
-    double f;
+    T kv[4];
+    T mv[HAS_M ? 4 : 1];
+    T f;
     template <class C>
-    __device__ __forceinline__ void load(const double* ke, uint32_t rec) {
+    __device__ __forceinline__ void load(const T* ke, uint32_t rec) {
         const int hl = rec & 0xff;
         const int a = (rec >> 8) & 3;
-        const double* src = ke + hl * C::stride + a * 4;
-        const double2 k01 = *reinterpret_cast<const double2*>(src + C::offK);
-        const double2 k23 = *reinterpret_cast<const double2*>(src + C::offK + 2);
-        kv[0] = k01.x; kv[1] = k01.y; kv[2] = k23.x; kv[3] = k23.y;
+        const T* src = ke + hl * C::stride + a * 4;
+        load4(src + C::offK, kv);
         if constexpr (HAS_M) {
-            const double2 m01 = *reinterpret_cast<const double2*>(src + C::offM);
-            const double2 m23 = *reinterpret_cast<const double2*>(src + C::offM + 2);
-            mv[0] = m01.x; mv[1] = m01.y; mv[2] = m23.x; mv[3] = m23.y;
+            T m4[4];
+            load4(src + C::offM, m4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) mv[i] = m4[i];
         }
         if constexpr (HAS_F) f = ke[hl * C::stride + C::offF + a];
     }
@@ -158,74 +171,74 @@ __host__ __device__ inline bool nodal_like(int type) {
 
 // c(x_q) for a constant / per-element / nodal field (coefficient.cpp:34-55,
 // interpolate_nodal batch.cpp:321-330)
-template <int KIND, int DEG>
-__device__ __forceinline__ double field_q(const FieldDev& f, const double* u, int q) {
+template <int KIND, int DEG, typename T = double>
+__device__ __forceinline__ T field_q(const FieldDev& f, const T* u, int q) {
     constexpr int k = P1<KIND>::k;
     if (nodal_like(f.type)) {
-        double v = basis<KIND, DEG>(q, 0) * u[0];
+        T v = T(basis<KIND, DEG>(q, 0)) * u[0];
 #pragma unroll
-        for (int a = 1; a < k; ++a) v += basis<KIND, DEG>(q, a) * u[a];
+        for (int a = 1; a < k; ++a) v += T(basis<KIND, DEG>(q, a)) * u[a];
         if (f.type == kFieldAcTangent) {
-            const double e2 = f.value * f.value;
-            return -e2 * (3.0 * v * v - 1.0);
+            const T e2 = T(f.value) * T(f.value);
+            return -e2 * (T(3) * v * v - T(1));
         }
         if (f.type == kFieldAcReaction) {
-            const double e2 = f.value * f.value;
-            return -e2 * v * (v * v - 1.0);
+            const T e2 = T(f.value) * T(f.value);
+            return -e2 * v * (v * v - T(1));
         }
         return v;
     }
-    return f.type == TGK_FIELD_ELEMENT ? u[0] : f.value;
+    return f.type == TGK_FIELD_ELEMENT ? u[0] : T(f.value);
 }
 
 // Phase A body: the reference's local kernels for one element into `out`
 // (rotated rows).  nt: the block's node table; ln: block-local node ids.
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV>
-__device__ __forceinline__ void element_tensors(const FusedArgs& p, const double* nt, const ushort4 ln,
-                                                int64_t h_global, double* out) {
-    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R>;
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV, typename T>
+__device__ __forceinline__ void element_tensors(const FusedArgs& p, const T* nt, const ushort4 ln,
+                                                int64_t h_global, T* out) {
+    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T>;
     using Rl = Rule<KIND, DEG>;
     constexpr int k = C::k, d = C::d, Q = C::Q, NV = C::NV;
     const int ids[4] = {ln.x, ln.y, ln.z, ln.w};
-    double X[k][d];
-    double cu[k], fu[k];
+    T X[k][d];
+    T cu[k], fu[k];
 #pragma unroll
     for (int a = 0; a < k; ++a)
 #pragma unroll
         for (int c = 0; c < d; ++c) X[a][c] = nt[ids[a] * NV + c];
     if (nodal_like(p.coef.type)) {
-        const double* cs = nt + p.max_bnodes * NV;
+        const T* cs = nt + p.max_bnodes * NV;
 #pragma unroll
         for (int a = 0; a < k; ++a) cu[a] = cs[ids[a]];
     }
     if (HAS_F && nodal_like(p.src.type)) {
-        const double* ss = nt + p.max_bnodes * (NV + (nodal_like(p.coef.type) ? 1 : 0));
+        const T* ss = nt + p.max_bnodes * (NV + (nodal_like(p.coef.type) ? 1 : 0));
 #pragma unroll
         for (int a = 0; a < k; ++a) fu[a] = ss[ids[a]];
     }
     if (p.coef.type == TGK_FIELD_ELEMENT || (HAS_F && p.src.type == TGK_FIELD_ELEMENT)) {
         const int64_t e = p.halo[h_global];
-        if (p.coef.type == TGK_FIELD_ELEMENT) cu[0] = __ldg(p.coef.data + e);
-        if (HAS_F && p.src.type == TGK_FIELD_ELEMENT) fu[0] = __ldg(p.src.data + e);
+        if (p.coef.type == TGK_FIELD_ELEMENT) cu[0] = T(__ldg(p.coef.data + e));
+        if (HAS_F && p.src.type == TGK_FIELD_ELEMENT) fu[0] = T(__ldg(p.src.data + e));
     }
-    double det, G[k][d];
-    if (!simplex_geometry<KIND, FDIV>(X, det, G)) {
+    T det, G[k][d];
+    if (!simplex_geometry<KIND, FDIV, T>(X, det, G)) {
         atomicMin(p.bad, static_cast<unsigned long long>(p.halo[h_global]));
 #pragma unroll
-        for (int i = 0; i < C::raw; ++i) out[i] = 0.0;
+        for (int i = 0; i < C::raw; ++i) out[i] = T(0);
         return;
     }
-    double sc[Q];  // w_q * det * c_q  (batch.cpp:169 / :261)
+    T sc[Q];  // w_q * det * c_q  (batch.cpp:169 / :261)
 #pragma unroll
-    for (int q = 0; q < Q; ++q) sc[q] = Rl::w(q) * det * field_q<KIND, DEG>(p.coef, cu, q);
+    for (int q = 0; q < Q; ++q) sc[q] = T(Rl::w(q)) * det * field_q<KIND, DEG, T>(p.coef, cu, q);
     if constexpr (KTYPE == 0) {
         // local_stiffness_diffusion (batch.cpp:168-177); K_e symmetric bitwise
 #pragma unroll
         for (int a = 0; a < k; ++a)
 #pragma unroll
             for (int b = a; b < k; ++b) {
-                const double dot = gdot<KIND>(G, a, b);
-                double v = sc[0] * dot;
+                const T dot = gdot<KIND, T>(G, a, b);
+                T v = sc[0] * dot;
 #pragma unroll
                 for (int q = 1; q < Q; ++q) v += sc[q] * dot;
                 out[C::offK + a * 4 + rot(a, b)] = v;
@@ -237,9 +250,9 @@ __device__ __forceinline__ void element_tensors(const FusedArgs& p, const double
         for (int a = 0; a < k; ++a)
 #pragma unroll
             for (int b = 0; b < k; ++b) {
-                double v = sc[0] * basis<KIND, DEG>(0, a) * basis<KIND, DEG>(0, b);
+                T v = sc[0] * T(basis<KIND, DEG>(0, a)) * T(basis<KIND, DEG>(0, b));
 #pragma unroll
-                for (int q = 1; q < Q; ++q) v += sc[q] * basis<KIND, DEG>(q, a) * basis<KIND, DEG>(q, b);
+                for (int q = 1; q < Q; ++q) v += sc[q] * T(basis<KIND, DEG>(q, a)) * T(basis<KIND, DEG>(q, b));
                 out[C::offK + a * 4 + rot(a, b)] = v;
             }
     }
@@ -249,38 +262,38 @@ __device__ __forceinline__ void element_tensors(const FusedArgs& p, const double
         for (int a = 0; a < k; ++a)
 #pragma unroll
             for (int b = 0; b < k; ++b) {
-                double v = Rl::w(0) * det * basis<KIND, DEG>(0, a) * basis<KIND, DEG>(0, b);
+                T v = T(Rl::w(0)) * det * T(basis<KIND, DEG>(0, a)) * T(basis<KIND, DEG>(0, b));
 #pragma unroll
                 for (int q = 1; q < Q; ++q)
-                    v += Rl::w(q) * det * basis<KIND, DEG>(q, a) * basis<KIND, DEG>(q, b);
+                    v += T(Rl::w(q)) * det * T(basis<KIND, DEG>(q, a)) * T(basis<KIND, DEG>(q, b));
                 out[C::offM + a * 4 + rot(a, b)] = v;
             }
     }
     if constexpr (HAS_F) {
         // local_load (batch.cpp:280-286)
-        double sf[Q];
+        T sf[Q];
 #pragma unroll
-        for (int q = 0; q < Q; ++q) sf[q] = Rl::w(q) * det * field_q<KIND, DEG>(p.src, fu, q);
+        for (int q = 0; q < Q; ++q) sf[q] = T(Rl::w(q)) * det * field_q<KIND, DEG, T>(p.src, fu, q);
 #pragma unroll
         for (int a = 0; a < k; ++a) {
-            double v = sf[0] * basis<KIND, DEG>(0, a);
+            T v = sf[0] * T(basis<KIND, DEG>(0, a));
 #pragma unroll
-            for (int q = 1; q < Q; ++q) v += sf[q] * basis<KIND, DEG>(q, a);
+            for (int q = 1; q < Q; ++q) v += sf[q] * T(basis<KIND, DEG>(q, a));
             out[C::offF + a] = v;
         }
     }
 }
 
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV>
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV, typename T>
 __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
-    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R>;
+    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T>;
     constexpr int k = C::k, d = C::d, NV = C::NV;
     constexpr int ROS = R + 8;
-    extern __shared__ __align__(16) double smem[];
-    double* ke = smem;                                               // R x stride
-    double* accK = ke + R * C::stride;                               // lmax x R
-    double* accM = accK + R * p.lmax;                                // (HAS_M)
-    double* nt = accK + R * p.lmax * C::nmat;                        // max_bnodes x (NV + 2)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* ke = reinterpret_cast<T*>(smem_raw);                          // R x stride
+    T* accK = ke + R * C::stride;                                    // lmax x R
+    T* accM = accK + R * p.lmax;                                     // (HAS_M)
+    T* nt = accK + R * p.lmax * C::nmat;                             // max_bnodes x ntcols
     uint32_t* rec_s = reinterpret_cast<uint32_t*>(nt + p.max_bnodes * p.ntcols);  // kRing x max_recs
     uint16_t* ro_s = reinterpret_cast<uint16_t*>(rec_s + kRing * p.max_recs);  // kRing x ROS
     ushort4* lc_s = reinterpret_cast<ushort4*>(ro_s + kRing * ROS);           // kRing x R
@@ -349,18 +362,18 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
             for (int u = 0; u < NPT; ++u) {
                 const int i = base + u * R + tid;
                 if (g[u] < 0) continue;
-                double* dst = nt + i * NV;
+                T* dst = nt + i * NV;
 #pragma unroll
-                for (int c = 0; c < d; ++c) dst[c] = __ldg(p.nodes + g[u] * d + c);
-                if (nodal_like(p.coef.type)) nt[p.max_bnodes * NV + i] = __ldg(p.coef.data + g[u]);
+                for (int c = 0; c < d; ++c) dst[c] = T(__ldg(p.nodes + g[u] * d + c));
+                if (nodal_like(p.coef.type)) nt[p.max_bnodes * NV + i] = T(__ldg(p.coef.data + g[u]));
                 if constexpr (HAS_F)
                     if (nodal_like(p.src.type))
-                        nt[p.max_bnodes * (NV + (nodal_like(p.coef.type) ? 1 : 0)) + i] = __ldg(p.src.data + g[u]);
+                        nt[p.max_bnodes * (NV + (nodal_like(p.coef.type) ? 1 : 0)) + i] = T(__ldg(p.src.data + g[u]));
             }
         }
     }
-    for (int i = tid; i < R * p.lmax * C::nmat; i += R) accK[i] = 0.0;
-    double dK = 0.0, dM = 0.0, dF = 0.0;  // diagonal K, M and the load F of the owned row
+    for (int i = tid; i < R * p.lmax * C::nmat; i += R) accK[i] = T(0);
+    T dK = T(0), dM = T(0), dF = T(0);  // diagonal K, M and the load F of the owned row
     int diag_pos = 0;
 
     long long t_mark = 0;
@@ -376,11 +389,11 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
         // ---------------- phase A: this thread's element of chunk c
         const int64_t h = int64_t(c) * R + tid;
         if (h < nh) {
-            double* out = ke + tid * C::stride;
+            T* out = ke + tid * C::stride;
             if (p.debug & 2) {
                 for (int i = 0; i < C::raw; ++i) out[i] = nt[0];
             } else {
-                element_tensors<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV>(p, nt, lc_s[(c % kRing) * R + tid],
+                element_tensors<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV, T>(p, nt, lc_s[(c % kRing) * R + tid],
                                                                          h0 + h, out);
             }
         }
@@ -402,16 +415,16 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
             const int j1 = ro[tid + 1];
             if (j < j1) {
                 uint32_t rec = rs[j];
-                RowVals<HAS_M, HAS_F> v;
+                RowVals<T, HAS_M, HAS_F> v;
                 v.template load<C>(ke, rec);
                 for (; j < j1; ++j) {
                     const uint32_t rec_n = j + 1 < j1 ? rs[j + 1] : rec;
-                    RowVals<HAS_M, HAS_F> vn;
+                    RowVals<T, HAS_M, HAS_F> vn;
                     vn.template load<C>(ke, rec_n);
                     // the k-1 positions of one record are distinct columns: load all,
                     // add, store all (no false read-after-write serialisation)
                     int pos[k - 1];
-                    double ak[k - 1], am[k - 1];
+                    T ak[k - 1], am[k - 1];
 #pragma unroll
                     for (int j2 = 0; j2 < k - 1; ++j2) {
                         pos[j2] = ((rec >> (10 + 5 * j2)) & 31) * R + tid;
@@ -444,12 +457,14 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
     if (tid < nr) {
         accK[diag_pos * R + tid] = dK;
         if constexpr (HAS_M) accM[diag_pos * R + tid] = dM;
+        T* Ko = static_cast<T*>(p.K);
+        T* Mo = static_cast<T*>(p.M);
         for (int q = 0; q < my_len; ++q) {
-            p.K[my_rp + q] = accK[q * R + tid];
-            if constexpr (HAS_M) p.M[my_rp + q] = accM[q * R + tid];
+            Ko[my_rp + q] = accK[q * R + tid];
+            if constexpr (HAS_M) Mo[my_rp + q] = accM[q * R + tid];
         }
     }
-    if (HAS_F && tid < nr) p.F[my_row] = dF;
+    if (HAS_F && tid < nr) static_cast<T*>(p.F)[my_row] = dF;
     if (p.trace && tid == 0) {
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -459,10 +474,10 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
     }
 }
 
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV>
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV, typename T>
 int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
-    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R>;
-    auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV>;
+    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T>;
+    auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV, T>;
     const size_t smem = C::smem_bytes(a.lmax, a.max_recs, a.max_bnodes, a.ntcols);
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (n_blocks > 0) kern<<<static_cast<unsigned>(n_blocks), R, smem, st>>>(a);
@@ -470,29 +485,33 @@ int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
     return TGK_OK;
 }
 
-template <int KIND, int DEG, int R, bool FDIV>
+template <int KIND, int DEG, int R, bool FDIV, typename T>
 int dispatch_r(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, cudaStream_t st) {
-    if (ktype == 1) return f ? launch_fused<KIND, DEG, 1, false, true, R, FDIV>(a, nb, st)
-                             : launch_fused<KIND, DEG, 1, false, false, R, FDIV>(a, nb, st);
-    if (m && f) return launch_fused<KIND, DEG, 0, true, true, R, FDIV>(a, nb, st);
-    if (m) return launch_fused<KIND, DEG, 0, true, false, R, FDIV>(a, nb, st);
-    if (f) return launch_fused<KIND, DEG, 0, false, true, R, FDIV>(a, nb, st);
-    return launch_fused<KIND, DEG, 0, false, false, R, FDIV>(a, nb, st);
+    if (ktype == 1) return f ? launch_fused<KIND, DEG, 1, false, true, R, FDIV, T>(a, nb, st)
+                             : launch_fused<KIND, DEG, 1, false, false, R, FDIV, T>(a, nb, st);
+    if (m && f) return launch_fused<KIND, DEG, 0, true, true, R, FDIV, T>(a, nb, st);
+    if (m) return launch_fused<KIND, DEG, 0, true, false, R, FDIV, T>(a, nb, st);
+    if (f) return launch_fused<KIND, DEG, 0, false, true, R, FDIV, T>(a, nb, st);
+    return launch_fused<KIND, DEG, 0, false, false, R, FDIV, T>(a, nb, st);
 }
 
-// Rows per block R and FDIV (Markstein division on meshes certified
-// division-safe) select the kernel instance.
+// Rows per block R, value type (fp64 / fp32) and FDIV (Markstein division on
+// meshes certified division-safe, fp64 only) select the kernel instance.
 template <int KIND, int DEG>
-int dispatch_flags(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, int R, bool fdiv,
+int dispatch_flags(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, int R, bool fdiv, bool f32,
                    cudaStream_t st) {
+    if (f32) {
+        if (R == 64) return dispatch_r<KIND, DEG, 64, false, float>(ktype, m, f, a, nb, st);
+        return dispatch_r<KIND, DEG, 128, false, float>(ktype, m, f, a, nb, st);
+    }
     if (R == 128)
-        return fdiv ? dispatch_r<KIND, DEG, 128, true>(ktype, m, f, a, nb, st)
-                    : dispatch_r<KIND, DEG, 128, false>(ktype, m, f, a, nb, st);
+        return fdiv ? dispatch_r<KIND, DEG, 128, true, double>(ktype, m, f, a, nb, st)
+                    : dispatch_r<KIND, DEG, 128, false, double>(ktype, m, f, a, nb, st);
     if (R == 64)
-        return fdiv ? dispatch_r<KIND, DEG, 64, true>(ktype, m, f, a, nb, st)
-                    : dispatch_r<KIND, DEG, 64, false>(ktype, m, f, a, nb, st);
-    return fdiv ? dispatch_r<KIND, DEG, TGK_R_BIG, true>(ktype, m, f, a, nb, st)
-                : dispatch_r<KIND, DEG, TGK_R_BIG, false>(ktype, m, f, a, nb, st);
+        return fdiv ? dispatch_r<KIND, DEG, 64, true, double>(ktype, m, f, a, nb, st)
+                    : dispatch_r<KIND, DEG, 64, false, double>(ktype, m, f, a, nb, st);
+    return fdiv ? dispatch_r<KIND, DEG, TGK_R_BIG, true, double>(ktype, m, f, a, nb, st)
+                : dispatch_r<KIND, DEG, TGK_R_BIG, false, double>(ktype, m, f, a, nb, st);
 }
 
 }  // namespace
@@ -511,8 +530,8 @@ int fused_rows_per_block(const tgk_problem* pr) {
 // Fused scalar assembly core: ktype 0 (diffusion stiffness) / 1 (coefficient
 // mass), quadrature degree, optional unit mass M and load F.
 static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int degree, bool has_m, bool has_f,
-                      FieldDev coef, FieldDev src, double* K, double* F, double* M, cudaStream_t st,
-                      unsigned long long* d_bad) {
+                      FieldDev coef, FieldDev src, void* K, void* F, void* M, cudaStream_t st,
+                      unsigned long long* d_bad, bool f32 = false) {
     const PlanDev* pl = nullptr;
     TGK_TRY(ensure_plan(r, R, &pl));
     FusedArgs a{};
@@ -537,7 +556,7 @@ static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int d
     a.F = F;
     a.lmax = pl->lmax;
     a.max_recs = pl->max_chunk_recs > 0 ? pl->max_chunk_recs : 4;
-    a.max_bnodes = pl->max_bnodes + (pl->max_bnodes & 1);
+    a.max_bnodes = (pl->max_bnodes + 3) & ~3;  // node table ends 16-byte aligned for fp32 and fp64
     a.ntcols = 3 + (nodal_like(a.coef.type) ? 1 : 0) + (has_f && nodal_like(a.src.type) ? 1 : 0);
     if (const char* dbg = getenv("TGK_FUSED_DEBUG")) a.debug = atoi(dbg);
     DevBuf<long long> trace;
@@ -550,16 +569,16 @@ static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int d
     if (!d_bad) TGK_TRY(bad.alloc(1));
     a.bad = d_bad ? d_bad : bad.p;
     CUDA_TRY(cudaMemsetAsync(a.bad, 0xff, sizeof(unsigned long long), st));
-    if (!has_f && F) CUDA_TRY(cudaMemsetAsync(F, 0, sizeof(double) * r->N, st));
+    if (!has_f && F) CUDA_TRY(cudaMemsetAsync(F, 0, (f32 ? sizeof(float) : sizeof(double)) * r->N, st));
     bool fdiv = false;
     TGK_TRY(mesh_division_safe(const_cast<tgk_mesh*>(m), st, &fdiv));
     if (getenv("TGK_IEEE_DIV")) fdiv = false;
     if (m->kind == TGK_TET4) {
-        if (degree == 1) TGK_TRY((dispatch_flags<TGK_TET4, 1>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, st)));
-        else TGK_TRY((dispatch_flags<TGK_TET4, 2>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, st)));
+        if (degree == 1) TGK_TRY((dispatch_flags<TGK_TET4, 1>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, f32, st)));
+        else TGK_TRY((dispatch_flags<TGK_TET4, 2>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, f32, st)));
     } else {
-        if (degree == 1) TGK_TRY((dispatch_flags<TGK_TRI3, 1>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, st)));
-        else TGK_TRY((dispatch_flags<TGK_TRI3, 2>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, st)));
+        if (degree == 1) TGK_TRY((dispatch_flags<TGK_TRI3, 1>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, f32, st)));
+        else TGK_TRY((dispatch_flags<TGK_TRI3, 2>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, f32, st)));
     }
     if (trace_path) {
         std::vector<long long> h(pl->n_blocks * 8);
@@ -587,6 +606,21 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
                                : FieldDev{TGK_FIELD_CONSTANT, 0.0, nullptr};
     return fused_core(m, r, fused_rows_per_block(pr), is_mass ? 1 : 0, degree, pr->with_mass != 0, has_f, coef, src,
                       K, F, M, st, d_bad);
+}
+
+// fp32 mode (tgk_assemble_f32_d): the same fused kernel in single precision,
+// fp32 CSR values; held to |dv| <= 1e-5 |v_ref| + 1e-7 max|v_ref| against the
+// fp64 reference.
+int fused_scalar_assemble_f32(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, float* K, float* F,
+                              float* M, cudaStream_t st, unsigned long long* d_bad) {
+    const bool is_mass = pr->kind == TGK_MASS;
+    const bool high = pr->diffusion.type != TGK_FIELD_CONSTANT || is_mass || pr->with_mass;
+    const bool has_f = !is_mass && pr->n_source > 0;
+    const FieldDev coef{pr->diffusion.type, pr->diffusion.value, pr->diffusion.data};
+    const FieldDev src = has_f ? FieldDev{pr->source[0].type, pr->source[0].value, pr->source[0].data}
+                               : FieldDev{TGK_FIELD_CONSTANT, 0.0, nullptr};
+    return fused_core(m, r, fused_rows_per_block(pr), is_mass ? 1 : 0, high ? 2 : 1, pr->with_mass != 0, has_f,
+                      coef, src, K, F, M, st, d_bad, true);
 }
 
 // Allen-Cahn Newton re-assembly (AllenCahnStepper::step, timestep.cpp:144-178)

@@ -160,6 +160,8 @@ int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
                               cudaStream_t st);
 int fused_allen_cahn(const tgk_mesh* m, tgk_routing* r, const double* u, double eps, double* T, double* F,
                      cudaStream_t st);
+int fused_scalar_assemble_f32(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, float* K, float* F,
+                              float* M, cudaStream_t st, unsigned long long* d_bad);
 
 }  // namespace tgk
 
@@ -619,6 +621,7 @@ static int check_field(const tgk_field& f, const tgk_mesh* m, const char* what) 
 int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
                  double* M, cudaStream_t st, unsigned long long* d_bad) {
     if (!p || !m || !r) return set_error(TGK_ERR_INPUT, "tgk_assemble: null argument");
+    if (p->mode != TGK_MODE_EXACT) return set_error(TGK_ERR_INPUT, "tgk_assemble: unknown arithmetic mode");
     if (m->kind != TGK_TRI3 && m->kind != TGK_TET4)
         return set_error(TGK_ERR_INPUT, "P1 assembly supports TRI3 and TET4 meshes only");
     const int comps = p->kind == TGK_ELASTICITY ? m->d : 1;
@@ -653,6 +656,20 @@ int tgk_assemble_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r
                    double* d_F, double* d_M, void* stream) {
     return tgk::assemble_dev(p, m, const_cast<tgk_routing*>(r), d_K, d_F, d_M,
                              static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int tgk_assemble_f32_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, float* d_K, float* d_F,
+                       float* d_M, unsigned long long* d_bad, void* stream) {
+    if (!p || !m || !r) return set_error(TGK_ERR_INPUT, "tgk_assemble_f32_d: null argument");
+    if (m->kind != TGK_TRI3 && m->kind != TGK_TET4)
+        return set_error(TGK_ERR_INPUT, "P1 assembly supports TRI3 and TET4 meshes only");
+    if (p->kind == TGK_ELASTICITY || r->components != 1)
+        return set_error(TGK_ERR_INPUT, "tgk_assemble_f32_d: scalar problems only");
+    TGK_TRY(check_field(p->diffusion, m, "diffusion"));
+    for (int s = 0; s < std::min(p->n_source, 3); ++s) TGK_TRY(check_field(p->source[s], m, "source"));
+    TGK_TRY(host_ensure_device());
+    return tgk::fused_scalar_assemble_f32(p, m, const_cast<tgk_routing*>(r), d_K, d_F, d_M,
+                                          static_cast<cudaStream_t>(stream), d_bad);
 }
 
 int tgk_allen_cahn_d(const tgk_mesh* m, const tgk_routing* r, const double* d_u, double eps, double* d_T,

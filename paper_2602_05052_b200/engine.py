@@ -159,7 +159,7 @@ class Routing:
 
 
 def make_problem(kind="poisson", diffusion=1.0, lam=1.0, mu=1.0, plane_stress=False, sources=(),
-                 with_mass=False, mode="exact", keep=None):
+                 with_mass=False, keep=None):
     keep = [] if keep is None else keep
     p = N.Problem()
     p.kind = {"poisson": N.POISSON, "elasticity": N.ELASTICITY, "mass": N.MASS}[kind]
@@ -171,28 +171,32 @@ def make_problem(kind="poisson", diffusion=1.0, lam=1.0, mu=1.0, plane_stress=Fa
     for i, s in enumerate(sources):
         p.source[i] = field(s, keep)
     p.with_mass = int(bool(with_mass))
-    p.mode = {"exact": N.MODE_EXACT, "fast": N.MODE_FAST}[mode]
+    p.mode = N.MODE_EXACT
     return p, keep
 
 
 def assemble(mesh: DeviceMesh, routing: Routing, kind="poisson", diffusion=1.0, lam=1.0, mu=1.0,
-             plane_stress=False, sources=(), with_mass=False, mode="exact", out=None, stream=None):
-    """tg::assemble (physics.cpp:10-75) on the GPU.  Returns (K values, F, M values | None)."""
-    p, keep = make_problem(kind, diffusion, lam, mu, plane_stress, sources, with_mass, mode)
+             plane_stress=False, sources=(), with_mass=False, dtype=torch.float64, out=None, stream=None):
+    """tg::assemble (physics.cpp:10-75) on the GPU.  Returns (K values, F, M values | None).
+    dtype=torch.float32 runs the fp32 variant (tgk_assemble_f32_d, scalar problems)."""
+    p, keep = make_problem(kind, diffusion, lam, mu, plane_stress, sources, with_mass)
     if out is None:
-        K = torch.empty(routing.nnz, dtype=torch.float64, device=_DEV)
-        F = torch.empty(routing.N, dtype=torch.float64, device=_DEV)
-        M = torch.empty(routing.nnz, dtype=torch.float64, device=_DEV) if with_mass else None
+        K = torch.empty(routing.nnz, dtype=dtype, device=_DEV)
+        F = torch.empty(routing.N, dtype=dtype, device=_DEV)
+        M = torch.empty(routing.nnz, dtype=dtype, device=_DEV) if with_mass else None
     else:
         K, F, M = out
-    check(lib().tgk_assemble_d(C.byref(p), mesh._h, routing._h, _ptr(K), _ptr(F), _ptr(M),
-                               _stream(stream)))
+    if dtype == torch.float32:
+        check(lib().tgk_assemble_f32_d(C.byref(p), mesh._h, routing._h, _ptr(K), _ptr(F), _ptr(M), None,
+                                       _stream(stream)))
+    else:
+        check(lib().tgk_assemble_d(C.byref(p), mesh._h, routing._h, _ptr(K), _ptr(F), _ptr(M), _stream(stream)))
     del keep
     return K, F, M
 
 
 def assemble_host(mesh: DeviceMesh, routing: Routing, kind="poisson", diffusion=1.0, lam=1.0,
-                  mu=1.0, plane_stress=False, sources=(), with_mass=False, mode="exact", out=None):
+                  mu=1.0, plane_stress=False, sources=(), with_mass=False, out=None):
     """Same as assemble() through the host-buffer C-ABI entry (copies inside the call)."""
     keep = []
 
@@ -213,7 +217,7 @@ def assemble_host(mesh: DeviceMesh, routing: Routing, kind="poisson", diffusion=
     for i, s in enumerate(sources):
         p.source[i] = hfield(s)
     p.with_mass = int(bool(with_mass))
-    p.mode = {"exact": N.MODE_EXACT, "fast": N.MODE_FAST}[mode]
+    p.mode = N.MODE_EXACT
     if out is None:
         K = np.empty(routing.nnz)
         F = np.empty(routing.N)
@@ -312,14 +316,14 @@ def reduce_vector(routing: Routing, local, stream=None):
 
 
 # ---------------------------------------------------------------- batched + adjoint
-def assemble_batched(mesh, routing, rho, source=1.0, with_load=True, mode="exact", stream=None):
+def assemble_batched(mesh, routing, rho, source=1.0, with_load=True, stream=None):
     """B per-element coefficient fields (B x E) -> K values (B x nnz) [+ one F (N)]."""
     rho = _cuda_f64(rho).reshape(-1, mesh.E)
     B = rho.shape[0]
     K = torch.empty(B, routing.nnz, dtype=torch.float64, device=_DEV)
     F = torch.empty(routing.N, dtype=torch.float64, device=_DEV) if with_load else None
     check(lib().tgk_assemble_batched_d(mesh._h, routing._h, B, _ptr(rho), float(source), _ptr(K),
-                                       _ptr(F), {"exact": 0, "fast": 1}[mode], _stream(stream)))
+                                       _ptr(F), N.MODE_EXACT, _stream(stream)))
     return K, F
 
 

@@ -233,3 +233,32 @@ def test_tgfem_solve_poisson_device(eng):
     ref_u[free] = spla.spsolve(A[free][:, free].tocsc(), F[free])
     assert np.all(u[b] == 0.0)
     assert np.max(np.abs(u - ref_u)) <= 1e-8 * np.max(np.abs(ref_u))
+
+
+@pytest.mark.parametrize("kind,div,kw", [
+    ("tri3", [40, 33], dict(sources=[1.0])),
+    ("tet4", [11, 9, 8], dict(sources=[1.0], with_mass=True)),
+    ("tet4", [9, 8, 7], dict(diffusion="element", sources=["nodal"])),
+    ("tri3", [25, 20], dict(kind="mass", diffusion="nodal")),
+])
+def test_fp32_mode_within_tolerance(eng, kind, div, kw):
+    """tgk_assemble_f32_d vs the fp64 reference: |dv| <= 1e-5 |v| + 1e-7 max|v|."""
+    nodes, elems = port.generate_grid(kind, [1.0] * len(div), div)
+    rng = np.random.default_rng(11)
+    fields = {"element": ("element", 0.5 + rng.random(elems.shape[0])),
+              "nodal": ("nodal", 0.5 + rng.random(nodes.shape[0]))}
+    kw = {k: ([fields.get(x, x) for x in v] if isinstance(v, list) else fields.get(v, v)) for k, v in kw.items()}
+    m = eng.DeviceMesh(kind, nodes, elems)
+    r = eng.Routing(m, 1)
+    K32, F32, M32 = eng.assemble(m, r, dtype=torch.float32, **kw)
+    assert K32.dtype == torch.float32
+    pr = port.Routing(nodes.shape[0], port.dofmap(kind, elems, 1))
+    pkw = dict(kw)
+    if pkw.pop("kind", None) == "mass":
+        pkw["problem"] = "mass"
+    Kr, Fr, Mr = port.assemble(kind, nodes, elems, pr, **pkw)
+    assert_scaled_close(np_(K32).astype(np.float64), Kr, rel=1e-5, floor=1e-7, what="K fp32")
+    if kw.get("sources"):
+        assert_scaled_close(np_(F32).astype(np.float64), Fr, rel=1e-5, floor=1e-7, what="F fp32")
+    if kw.get("with_mass"):
+        assert_scaled_close(np_(M32).astype(np.float64), Mr, rel=1e-5, floor=1e-7, what="M fp32")
