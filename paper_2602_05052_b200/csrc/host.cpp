@@ -538,13 +538,22 @@ void PlanDev::release() {
 }
 
 // Build (once per R) and upload the fused row-block plan of a scalar routing.
-int ensure_plan(tgk_routing* rr, int R, const PlanDev** out) {
+int ensure_plan(tgk_routing* rr, int R, const PlanDev** out, int C) {
     tgk_routing* r = rr->scalar ? rr->scalar : rr;
-    PlanDev& D = r->plan[plan_slot(R)];
-    if (D.R == R) {
-        *out = &D;
-        return TGK_OK;
+    if (C == 0) C = R;
+    PlanDev* cache = nullptr;
+    for (auto& pl : r->plan)
+        if (pl.R == R && pl.C == C) {
+            *out = &pl;
+            return TGK_OK;
+        }
+    for (auto& pl : r->plan)
+        if (pl.R == 0 && !cache) cache = &pl;
+    if (!cache) {  // all slots in use: evict the first
+        cache = &r->plan[0];
+        cache->release();
     }
+    PlanDev& D = *cache;
     const tgk_mesh* m = r->mesh;
     const int k = m->k, d = m->d;
     std::vector<double> nodes(m->N * d);
@@ -561,7 +570,7 @@ int ensure_plan(tgk_routing* rr, int R, const PlanDev** out) {
     const int64_t lo = r->own_hi < 0 ? 0 : r->own_lo, hi = r->own_hi < 0 ? r->N : r->own_hi;
     const int64_t elo = r->elem_hi < 0 ? 0 : r->elem_lo, ehi = r->elem_hi < 0 ? r->E : r->elem_hi;
     TGK_TRY(build_plan(m->kind, m->N, m->E, nodes.data(), conn.data(), row_ptr.data(), vo.data(),
-                       vs.data(), slot.data(), lo, hi, elo, ehi, R, P));
+                       vs.data(), slot.data(), lo, hi, elo, ehi, R, C, P));
     D = PlanDev{};
     D.n_blocks = P.n_blocks;
     D.lmax = P.lmax;
@@ -596,6 +605,7 @@ int ensure_plan(tgk_routing* rr, int R, const PlanDev** out) {
     TGK_TRY(up(D.chunk_row_off, P.chunk_row_off));
     TGK_TRY(up(D.recs, P.recs));
     D.R = R;
+    D.C = C;
     *out = &D;
     return TGK_OK;
 }

@@ -77,14 +77,17 @@ std::vector<uint32_t> morton_order(int kind, int64_t N, const double* nodes, int
 int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
                const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
                const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int R,
-               PlanHost& P) {
+               int C, PlanHost& P) {
     // elements outside [elem_lo, elem_hi) take no part (multi-GPU slabs that
     // exchange interface partial sums instead of recomputing the halo)
     auto in_range = [elem_lo, elem_hi](uint32_t e) { return int64_t(e) >= elem_lo && int64_t(e) < elem_hi; };
     const int d = element_dim(kind), k = element_nodes(kind);
     (void)E;
+    // R rows per block, chunks of C halo elements (C threads; R = C x rows per thread)
     if (R != 64 && R != 128 && R != 256) return set_error(TGK_ERR_INPUT, "fused plan: R must be 64, 128 or 256");
+    if (C != 64 && C != 128 && C != 256) return set_error(TGK_ERR_INPUT, "fused plan: chunk size must be 64, 128 or 256");
     P.R = R;
+    P.C = C;
     // --- 1. Morton order of the owned nodes
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (int64_t i = 0; i < N; ++i)
@@ -188,8 +191,8 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
             // (fewer shared-memory bank conflicts; TGK_CHUNK_SORT=0 disables).
             static const bool chunk_sort = !(getenv("TGK_CHUNK_SORT") && atoi(getenv("TGK_CHUNK_SORT")) == 0);
             if (chunk_sort)
-                for (int64_t c0 = 0; c0 < nh; c0 += R) {
-                    const int64_t c1 = std::min<int64_t>(nh, c0 + R);
+                for (int64_t c0 = 0; c0 < nh; c0 += C) {
+                    const int64_t c1 = std::min<int64_t>(nh, c0 + C);
                     std::sort(order.begin() + c0, order.begin() + c1, [&](const auto& x, const auto& y) {
                         const int32_t nx = conn[int64_t(x.second) * k], ny = conn[int64_t(y.second) * k];
                         return nx != ny ? nx < ny : x.second < y.second;
@@ -202,7 +205,7 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
                 where[h] = {order[h].second, static_cast<uint32_t>(h)};
             }
             std::sort(where.begin(), where.end());
-            const int64_t nch = (nh + R - 1) / R;
+            const int64_t nch = (nh + C - 1) / C;
             // records grouped chunk-major, then row, ascending element within a row
             std::vector<std::vector<uint32_t>> per_chunk(nch);
             std::vector<std::vector<uint16_t>> cnt(nch, std::vector<uint16_t>(R, 0));
@@ -217,11 +220,11 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
                     const int a = static_cast<int>(slot % k);
                     const int64_t hpos =
                         std::lower_bound(where.begin(), where.end(), std::make_pair(e, 0u))->second;
-                    const int64_t ch = hpos / R;
+                    const int64_t ch = hpos / C;
                     int pos[4] = {0, 0, 0, 0};
                     for (int bb = 0; bb < k; ++bb)
                         pos[bb] = static_cast<int>(slot_of[static_cast<int64_t>(slot) * k + bb] - rp);
-                    per_chunk[ch].push_back(pack_rec(static_cast<int>(hpos % R), a, pos, k));
+                    per_chunk[ch].push_back(pack_rec(static_cast<int>(hpos % C), a, pos, k));
                     ++cnt[ch][lr];
                 }
             }

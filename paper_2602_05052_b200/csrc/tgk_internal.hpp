@@ -39,12 +39,11 @@ inline int element_nodes(int kind) { return kind == TGK_TRI3 ? 3 : 4; }
 // within a row — so each CSR value is folded in ascending element order, the
 // reference's order (routing.cpp:117-124).
 constexpr int kMaxRowLen = 32;  // CSR row length limit of the packed record (5-bit positions)
-constexpr int kPlanSlots = 3;   // plans cached per routing: R = 64, 128, 256
-
-inline int plan_slot(int R) { return R == 64 ? 2 : (R == 128 ? 0 : 1); }
+constexpr int kPlanSlots = 3;   // plans cached per routing, keyed by (rows per block, chunk size)
 
 struct PlanHost {
-    int R = 256;                         // rows per block = elements per chunk
+    int R = 256;                         // rows per block
+    int C = 256;                         // halo elements per chunk (= threads per block)
     int64_t n_blocks = 0;
     int lmax = 0;                        // max CSR row length
     int max_chunk_recs = 0;              // largest record segment of one chunk (padded)
@@ -64,7 +63,7 @@ struct PlanHost {
 };
 
 struct PlanDev {
-    int R = 0;
+    int R = 0, C = 0;
     int64_t n_blocks = 0;
     int lmax = 0;
     int max_chunk_recs = 0;
@@ -108,7 +107,7 @@ TGK_HD inline uint32_t pack_rec(int hl, int a, const int* pos, int k) {
 int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
                const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
                const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int R,
-               PlanHost& out);
+               int C, PlanHost& out);
 
 }  // namespace tgk
 
@@ -151,5 +150,5 @@ struct tgk_routing {
 
 namespace tgk {
 // Build (once per R) and upload the fused plan of the routing's scalar part.
-int ensure_plan(tgk_routing* r, int R, const PlanDev** out);
+int ensure_plan(tgk_routing* r, int R, const PlanDev** out, int C = 0);  // C = 0: chunk size R
 }
