@@ -12,6 +12,8 @@ namespace tgk {
 int check_bad(unsigned long long* d_bad, cudaStream_t st);
 int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                           double* F, double* M, cudaStream_t st, unsigned long long* d_bad);
+int batched_entries(const tgk_mesh* m, tgk_routing* r, int64_t B, const double* rho, double source, double* K,
+                    double* F, cudaStream_t st, unsigned long long* d_bad);
 int batched_fused(const tgk_mesh* m, tgk_routing* r, int64_t B, const double* rho, double source, double* K,
                   double* F, cudaStream_t st, unsigned long long* d_bad);
 int local_elasticity_nocheck(const tgk_mesh* m, int degree, const double* lam, const double* mu, double* out,
@@ -226,6 +228,11 @@ int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, c
     TGK_TRY(bad.alloc(1));
     CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
     if (B == 0) return TGK_OK;
+    if (!getenv("TGK_BATCHED_LOOP") && !getenv("TGK_BATCHED_CHUNKED")) {
+        const int rc = batched_entries(m, const_cast<tgk_routing*>(r), B, rho, source, K, F, st, bad.p);
+        if (rc == TGK_OK) return check_bad(bad.p, st);
+        if (rc != TGK_ERR_INPUT) return rc;
+    }
     if (!getenv("TGK_BATCHED_LOOP")) {
         const int rc = batched_fused(m, const_cast<tgk_routing*>(r), B, rho, source, K, F, st, bad.p);
         if (rc == TGK_OK) return check_bad(bad.p, st);

@@ -237,6 +237,283 @@ int launch_batched(const BatchedArgs& a, int64_t nb, cudaStream_t st) {
     return TGK_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Entry-owned batched kernel (plan_entries.cpp).  A block owns R rows and its
+// whole halo; thread t owns halo elements t, t+T, ... and CSR entries t, t+T,
+// ...  Prologue: the geometry of its halo elements (det + the k(k+1)/2
+// gradient dot products) into registers, once, and for field 0 the load
+// vector.  Then FPI fields per iteration: each thread writes its halo
+// elements' k(k+1)/2 local stiffness values per field (sc_q = w_q*det*rho_b,
+// K_e[a][b] = sum_q sc_q*(G_a.G_b) in the reference's order,
+// batch.cpp:168-177) to a double-buffered shared array, one barrier, and
+// folds each of its entries' contribution lists in a register from +0.0 in
+// ascending element order (routing.cpp:117-124) and streams the values out.
+// MAXC > 0: the contribution lists (shared-memory offsets) live in registers,
+// padded with the offset of a +0.0 slot (adding +0.0 to a sum that started at
+// +0.0 never changes it: the sum is never -0.0); MAXC = 0: they are read from
+// shared memory.  The next fields' coefficients are prefetched.
+constexpr int kEntryThreads = 256;
+constexpr int kEntryFPI = 2;  // fields per barrier
+
+struct EntryArgs {
+    const double* nodes;
+    const double* rho;  // B x E
+    int64_t E, nnz, B;
+    double source;
+    EntryPlanDev pl;
+    double* K;  // B x nnz
+    double* F;  // N (may be null)
+    int64_t fields_per_block;
+    int streaming_stores;  // st.global.cs (evict-first) for K
+    unsigned long long* bad;
+};
+
+template <int KIND>
+struct ECfg {
+    static constexpr int k = P1<KIND>::k, d = P1<KIND>::d, ND = k * (k + 1) / 2;
+    __host__ __device__ static int fstride(int MH) { return ND * MH + 2; }  // one field's values + the +0.0 slot (even)
+    static size_t smem(const EntryPlanDev& pl, bool lists_in_smem) {
+        auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+        const size_t vals = size_t(2 * kEntryFPI) * fstride(pl.max_halo);
+        size_t o = al(sizeof(double) * std::max(vals, size_t(pl.max_bnodes) * d));  // values | node table
+        if (lists_in_smem) o = al(o + sizeof(uint32_t) * size_t(pl.max_contrib));
+        return o;
+    }
+};
+
+template <int KIND, int DEG, int EPT, int HPT, int MAXC>
+__global__ void __launch_bounds__(kEntryThreads) k_batched_entries(EntryArgs p) {
+    using Rl = Rule<KIND, DEG>;
+    using Cf = ECfg<KIND>;
+    constexpr int k = Cf::k, d = Cf::d, Q = Rl::Q, ND = Cf::ND, T = kEntryThreads, FPI = kEntryFPI;
+    extern __shared__ __align__(16) unsigned char smb[];
+    const EntryPlanDev& pl = p.pl;
+    const int MH = pl.max_halo;
+    const int FS = Cf::fstride(MH);
+    double* kb = reinterpret_cast<double*>(smb);
+    double* nt = kb;  // node table, prologue only
+    uint32_t* cs_s = reinterpret_cast<uint32_t*>(
+        smb + ((sizeof(double) * (size_t(2 * FPI) * FS > size_t(pl.max_bnodes) * d ? size_t(2 * FPI) * FS
+                                                                              : size_t(pl.max_bnodes) * d) +
+               15) &
+              ~size_t(15)));
+
+    const int tid = threadIdx.x;
+    const int64_t blk = blockIdx.x;
+    const int64_t r0 = pl.row_off[blk];
+    const int nr = static_cast<int>(pl.row_off[blk + 1] - r0);
+    const int64_t h0 = pl.halo_off[blk];
+    const int nh = static_cast<int>(pl.halo_off[blk + 1] - h0);
+    const int64_t n0 = pl.bnode_off[blk];
+    const int nbn = static_cast<int>(pl.bnode_off[blk + 1] - n0);
+    const int64_t e0 = pl.ent_off[blk];
+    const int ne = static_cast<int>(pl.ent_off[blk + 1] - e0);
+    const int64_t c0 = pl.contrib_off[blk];
+
+    if (MAXC == 0) {
+        const int ncs = static_cast<int>(pl.contrib_off[blk + 1] - c0);
+        for (int i = tid; i < ncs; i += T) cs_s[i] = __ldg(pl.contrib + c0 + i);
+    }
+    for (int i = tid; i < nbn; i += T) {
+        const int64_t g = pl.bnodes[n0 + i];
+#pragma unroll
+        for (int c = 0; c < d; ++c) nt[i * d + c] = __ldg(p.nodes + g * d + c);
+    }
+    uint32_t eid[HPT];
+#pragma unroll
+    for (int hh = 0; hh < HPT; ++hh) {
+        const int h = tid + hh * T;
+        eid[hh] = h < nh ? __ldg(pl.halo + h0 + h) : 0u;
+    }
+    const int64_t bf0 = int64_t(blockIdx.y) * p.fields_per_block;
+    const int64_t bf1 = bf0 + p.fields_per_block < p.B ? bf0 + p.fields_per_block : p.B;
+    double rn[HPT][FPI];
+#pragma unroll
+    for (int hh = 0; hh < HPT; ++hh)
+#pragma unroll
+        for (int f = 0; f < FPI; ++f)
+            rn[hh][f] = (tid + hh * T < nh && bf0 + f < bf1) ? __ldg(p.rho + (bf0 + f) * p.E + eid[hh]) : 0.0;
+    // my entries: CSR positions and contribution lists
+    const uint32_t zslot = uint32_t(ND * MH);  // +0.0 slot of a field's values
+    int64_t epos[EPT], epos2[EPT];
+    uint32_t cb[EPT], ce[EPT];
+    uint32_t cl[EPT][MAXC > 0 ? MAXC : 1];
+    int wl[EPT];  // warp-uniform longest list
+    {
+        const uint32_t* coff = pl.coff + e0 + blk;
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+            const int e = tid + j * T;
+            epos[j] = e < ne ? __ldg(pl.epos + e0 + e) : 0;
+            epos2[j] = e < ne ? __ldg(pl.epos2 + e0 + e) : -1;
+            cb[j] = e < ne ? __ldg(coff + e) : 0u;
+            ce[j] = e < ne ? __ldg(coff + e + 1) : 0u;
+            wl[j] = static_cast<int>(__reduce_max_sync(0xffffffffu, ce[j] - cb[j]));
+            if (MAXC > 0) {
+#pragma unroll
+                for (int c = 0; c < (MAXC > 0 ? MAXC : 1); ++c)
+                    cl[j][c] = cb[j] + c < ce[j] ? __ldg(pl.contrib + c0 + cb[j] + c) : zslot;
+            }
+        }
+    }
+    __syncthreads();
+    // ---------------- halo geometry, once (batch.cpp:76-154)
+    double gd[HPT][ND], gdet[HPT];
+#pragma unroll
+    for (int hh = 0; hh < HPT; ++hh) {
+        const int h = tid + hh * T;
+        gdet[hh] = 0.0;
+#pragma unroll
+        for (int t = 0; t < ND; ++t) gd[hh][t] = 0.0;
+        if (h < nh) {
+            const uint64_t hc = __ldg(reinterpret_cast<const unsigned long long*>(pl.hconn) + h0 + h);
+            double X[k][d];
+#pragma unroll
+            for (int a = 0; a < k; ++a)
+#pragma unroll
+                for (int c = 0; c < d; ++c) X[a][c] = nt[int((hc >> (16 * a)) & 0xffff) * d + c];
+            double det, G[k][d];
+            if (!simplex_geometry<KIND, false>(X, det, G)) {
+                atomicMin(p.bad, static_cast<unsigned long long>(eid[hh]));
+                det = 0.0;
+#pragma unroll
+                for (int a = 0; a < k; ++a)
+#pragma unroll
+                    for (int c = 0; c < d; ++c) G[a][c] = 0.0;
+            }
+            gdet[hh] = det;
+            int t = 0;
+#pragma unroll
+            for (int a = 0; a < k; ++a)
+#pragma unroll
+                for (int b = a; b < k; ++b) gd[hh][t++] = gdot<KIND>(G, a, b);
+        }
+    }
+    __syncthreads();  // node table (aliasing the value buffers) no longer read
+    for (int i = tid; i < 2 * FPI; i += T) kb[i * FS + zslot] = 0.0;
+    if (bf0 == 0 && p.F != nullptr) {
+        // local_load with a constant source (batch.cpp:280-286) into the second
+        // buffer set (first used by iteration 1), then the ascending-element row fold
+        double* fe = kb + FPI * FS;
+#pragma unroll
+        for (int hh = 0; hh < HPT; ++hh) {
+            const int h = tid + hh * T;
+            if (h < nh) {
+                const double det = gdet[hh];
+#pragma unroll
+                for (int a = 0; a < k; ++a) {
+                    double v = (Rl::w(0) * det * p.source) * basis<KIND, DEG>(0, a);
+#pragma unroll
+                    for (int q = 1; q < Q; ++q) v += (Rl::w(q) * det * p.source) * basis<KIND, DEG>(q, a);
+                    fe[a * MH + h] = v;
+                }
+            }
+        }
+        __syncthreads();
+        const int64_t f0 = pl.fcontrib_off[blk];
+        const uint32_t* fcoff = pl.fcoff + r0 + blk;
+        for (int i = tid; i < nr; i += T) {
+            double v = 0.0;
+            for (uint32_t c = __ldg(fcoff + i); c < __ldg(fcoff + i + 1); ++c) v += fe[__ldg(pl.fcontrib + f0 + c)];
+            p.F[pl.rows[r0 + i]] = v;
+        }
+    }
+    // ---------------- FPI fields per iteration
+    int set = 0;
+    for (int64_t b = bf0; b < bf1; b += FPI, set ^= 1) {
+        double* kv = kb + set * FPI * FS;
+#pragma unroll
+        for (int hh = 0; hh < HPT; ++hh) {
+            const int h = tid + hh * T;
+            if (h < nh) {
+#pragma unroll
+                for (int f = 0; f < FPI; ++f) {
+                    const double rho = rn[hh][f];
+                    if (b + FPI + f < bf1) rn[hh][f] = __ldg(p.rho + (b + FPI + f) * p.E + eid[hh]);
+                    double sc[Q];
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) sc[q] = Rl::w(q) * gdet[hh] * rho;
+#pragma unroll
+                    for (int t = 0; t < ND; ++t) {
+                        const double dot = gd[hh][t];
+                        double v = sc[0] * dot;
+#pragma unroll
+                        for (int q = 1; q < Q; ++q) v += sc[q] * dot;
+                        kv[f * FS + t * MH + h] = v;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const int nf = bf1 - b < FPI ? static_cast<int>(bf1 - b) : FPI;
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+            if (j * T >= ne) break;  // block-uniform
+            double v[FPI];
+#pragma unroll
+            for (int f = 0; f < FPI; ++f) v[f] = 0.0;
+            if (MAXC > 0) {
+#pragma unroll
+                for (int c = 0; c < (MAXC > 0 ? MAXC : 1); ++c) {
+                    if (c < wl[j]) {  // warp-uniform
+#pragma unroll
+                        for (int f = 0; f < FPI; ++f) v[f] += kv[f * FS + cl[j][c]];
+                    }
+                }
+            } else {
+                for (uint32_t c = cb[j]; c < ce[j]; ++c) {
+                    const uint32_t u = cs_s[c];
+#pragma unroll
+                    for (int f = 0; f < FPI; ++f) v[f] += kv[f * FS + u];
+                }
+            }
+            if (tid + j * T < ne) {
+#pragma unroll
+                for (int f = 0; f < FPI; ++f)
+                    if (f < nf) {
+                        double* Kb = p.K + (b + f) * p.nnz;
+                        if (p.streaming_stores) {
+                            __stcs(Kb + epos[j], v[f]);
+                            if (epos2[j] >= 0) __stcs(Kb + epos2[j], v[f]);
+                        } else {
+                            Kb[epos[j]] = v[f];
+                            if (epos2[j] >= 0) Kb[epos2[j]] = v[f];
+                        }
+                    }
+            }
+        }
+    }
+}
+
+template <int KIND, int EPT, int HPT, int MAXC>
+int launch_entries(const EntryArgs& a, int64_t groups, cudaStream_t st) {
+    auto kern = k_batched_entries<KIND, 2, EPT, HPT, MAXC>;
+    const size_t smem = ECfg<KIND>::smem(a.pl, MAXC == 0);
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const dim3 grid(static_cast<unsigned>(a.pl.n_blocks), static_cast<unsigned>(groups));
+    if (a.pl.n_blocks > 0) kern<<<grid, kEntryThreads, smem, st>>>(a);
+    KERNEL_CHECK("batched_entries");
+    return TGK_OK;
+}
+
+template <int KIND, int MAXC>
+int launch_entries_eh(const EntryArgs& a, int ept, int hpt, int64_t groups, cudaStream_t st) {
+    if (hpt == 1) {
+        if (ept == 1) return launch_entries<KIND, 1, 1, MAXC>(a, groups, st);
+        if (ept == 2) return launch_entries<KIND, 2, 1, MAXC>(a, groups, st);
+        return launch_entries<KIND, 4, 1, MAXC>(a, groups, st);
+    }
+    if (ept == 1) return launch_entries<KIND, 1, 2, MAXC>(a, groups, st);
+    if (ept == 2) return launch_entries<KIND, 2, 2, MAXC>(a, groups, st);
+    return launch_entries<KIND, 4, 2, MAXC>(a, groups, st);
+}
+
+int pow2_at_least(int x) {
+    int v = 1;
+    while (v < x) v <<= 1;
+    return v;
+}
+
 }  // namespace
 
 // Returns TGK_ERR_INPUT without launching (and without setting an error
@@ -279,6 +556,61 @@ int batched_fused(const tgk_mesh* m, tgk_routing* r, int64_t B, const double* rh
     if (const char* e = getenv("TGK_BATCHED_FPB")) a.fields_per_block = std::max(1, atoi(e));
     if (m->kind == TGK_TRI3) return launch_batched<TGK_TRI3, 2, R>(a, pl->n_blocks, st);
     return launch_batched<TGK_TET4, 2, R>(a, pl->n_blocks, st);
+}
+
+// Entry-owned batched kernel.  Returns TGK_ERR_INPUT without launching (and
+// without an error message) when it does not apply: element-range slabs, or
+// no rows-per-block choice whose block working set fits.
+int batched_entries(const tgk_mesh* m, tgk_routing* r, int64_t B, const double* rho, double source, double* K,
+                    double* F, cudaStream_t st, unsigned long long* d_bad) {
+    const tgk_routing* s = r->scalar ? r->scalar : r;
+    if (s->elem_hi >= 0) return TGK_ERR_INPUT;
+    int R0 = m->kind == TGK_TRI3 ? 64 : 16;
+    if (const char* e = getenv("TGK_ENTRY_R")) R0 = std::max(1, atoi(e));
+    int maxc_cap = 16;  // register-resident contribution lists up to this length
+    if (const char* e = getenv("TGK_ENTRY_MAXC")) maxc_cap = atoi(e);
+    const EntryPlanDev* pl = nullptr;
+    int ept = 0, hpt = 0, maxc = 0;
+    size_t smem = 0;
+    for (int R = R0; R >= 4; R /= 2) {
+        TGK_TRY(ensure_entry_plan(r, R, &pl));
+        ept = pow2_at_least((pl->max_entries + kEntryThreads - 1) / kEntryThreads);
+        hpt = pow2_at_least((pl->max_halo + kEntryThreads - 1) / kEntryThreads);
+        maxc = pl->max_clen <= 8 && maxc_cap >= 8 ? 8 : pl->max_clen <= 16 && maxc_cap >= 16 ? 16 : 0;
+        smem = m->kind == TGK_TRI3 ? ECfg<TGK_TRI3>::smem(*pl, maxc == 0) : ECfg<TGK_TET4>::smem(*pl, maxc == 0);
+        if (ept <= 4 && hpt <= 2 && smem <= 200 * 1024) break;
+        pl = nullptr;
+    }
+    if (!pl) return TGK_ERR_INPUT;
+    EntryArgs a{};
+    a.nodes = m->nodes;
+    a.rho = rho;
+    a.E = m->E;
+    a.nnz = r->nnz;
+    a.B = B;
+    a.source = source;
+    a.pl = *pl;
+    a.K = K;
+    a.F = F;
+    a.bad = d_bad;
+    a.streaming_stores = 0;
+    if (const char* e = getenv("TGK_ENTRY_STCS")) a.streaming_stores = atoi(e);
+    // fields per block: few enough that the blocks in flight at any time work
+    // on a handful of fields (their coefficient vectors stay in L2 for the
+    // random per-element gathers), enough to amortise the prologue
+    int64_t fpb = 8;
+    if (const char* e = getenv("TGK_ENTRY_FPB")) fpb = std::max(1, atoi(e));
+    a.fields_per_block = std::min<int64_t>(B, fpb);
+    a.fields_per_block += a.fields_per_block % kEntryFPI;  // whole iterations
+    const int64_t groups = (B + a.fields_per_block - 1) / a.fields_per_block;
+    if (m->kind == TGK_TRI3) {
+        if (maxc == 8) return launch_entries_eh<TGK_TRI3, 8>(a, ept, hpt, groups, st);
+        if (maxc == 16) return launch_entries_eh<TGK_TRI3, 16>(a, ept, hpt, groups, st);
+        return launch_entries_eh<TGK_TRI3, 0>(a, ept, hpt, groups, st);
+    }
+    if (maxc == 8) return launch_entries_eh<TGK_TET4, 8>(a, ept, hpt, groups, st);
+    if (maxc == 16) return launch_entries_eh<TGK_TET4, 16>(a, ept, hpt, groups, st);
+    return launch_entries_eh<TGK_TET4, 0>(a, ept, hpt, groups, st);
 }
 
 }  // namespace tgk

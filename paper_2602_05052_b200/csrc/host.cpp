@@ -472,6 +472,7 @@ int tgk_routing_set_owned_rows(tgk_routing* r, int64_t lo, int64_t hi) {
     if (lo < 0 || hi > s->N || lo > hi) return set_error(TGK_ERR_INPUT, "owned row range out of bounds");
     if (s->own_lo == lo && s->own_hi == hi) return TGK_OK;
     for (auto& pl : s->plan) pl.release();
+    s->entry_plan.release();
     s->own_lo = lo;
     s->own_hi = hi;
     return TGK_OK;
@@ -537,6 +538,113 @@ void PlanDev::release() {
     *this = PlanDev{};
 }
 
+// Host copies of the mesh and the scalar routing arrays the plans are built from.
+struct ScalarRoutingHost {
+    std::vector<double> nodes;
+    std::vector<int32_t> conn;
+    std::vector<int64_t> row_ptr;
+    std::vector<uint32_t> vo, vs, slot;
+};
+
+static int fetch_scalar_routing(const tgk_routing* r, ScalarRoutingHost& h) {
+    const tgk_mesh* m = r->mesh;
+    const int k = m->k, d = m->d;
+    h.nodes.resize(m->N * d);
+    h.conn.resize(m->E * k);
+    h.row_ptr.resize(r->N + 1);
+    h.vo.resize(r->N + 1);
+    h.vs.resize(r->E * k);
+    h.slot.resize(r->E * k * k);
+    HCUDA(cudaMemcpy(h.nodes.data(), m->nodes, h.nodes.size() * 8, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(h.conn.data(), m->conn, h.conn.size() * 4, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(h.row_ptr.data(), r->row_ptr, h.row_ptr.size() * 8, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(h.vo.data(), r->vec_offsets, h.vo.size() * 4, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(h.vs.data(), r->vec_slots, h.vs.size() * 4, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(h.slot.data(), r->slot_of, h.slot.size() * 4, cudaMemcpyDeviceToHost));
+    return TGK_OK;
+}
+
+void EntryPlanDev::release() {
+    if (blob) cudaFree(blob);
+    *this = EntryPlanDev{};
+}
+
+// Build (once per R and owned row range) and upload the batched kernel's entry plan.
+int ensure_entry_plan(tgk_routing* rr, int R, const EntryPlanDev** out) {
+    tgk_routing* r = rr->scalar ? rr->scalar : rr;
+    EntryPlanDev& D = r->entry_plan;
+    if (D.blob && D.R == R) {
+        *out = &D;
+        return TGK_OK;
+    }
+    D.release();
+    const tgk_mesh* m = r->mesh;
+    ScalarRoutingHost h;
+    TGK_TRY(fetch_scalar_routing(r, h));
+    EntryPlanHost P;
+    const int64_t lo = r->own_hi < 0 ? 0 : r->own_lo, hi = r->own_hi < 0 ? r->N : r->own_hi;
+    TGK_TRY(build_entry_plan(m->kind, m->N, h.nodes.data(), h.conn.data(), h.row_ptr.data(), h.vo.data(),
+                             h.vs.data(), h.slot.data(), lo, hi, R, P));
+    // one allocation, 16-byte aligned segments
+    size_t total = 0;
+    auto reserve = [&total](const auto& v) {
+        const size_t at = total;
+        total += (v.size() * sizeof(v[0]) + 15) & ~size_t(15);
+        return at;
+    };
+    const size_t o_row_off = reserve(P.row_off), o_halo_off = reserve(P.halo_off), o_bnode_off = reserve(P.bnode_off),
+                 o_ent_off = reserve(P.ent_off), o_contrib_off = reserve(P.contrib_off),
+                 o_fcontrib_off = reserve(P.fcontrib_off), o_epos = reserve(P.epos), o_epos2 = reserve(P.epos2), o_rows = reserve(P.rows),
+                 o_halo = reserve(P.halo), o_bnodes = reserve(P.bnodes), o_contrib = reserve(P.contrib),
+                 o_fcontrib = reserve(P.fcontrib), o_coff = reserve(P.coff), o_fcoff = reserve(P.fcoff),
+                 o_hconn = reserve(P.hconn);
+    std::vector<unsigned char> img(std::max<size_t>(total, 16));
+    auto put = [&img](size_t at, const auto& v) {
+        if (!v.empty()) std::memcpy(img.data() + at, v.data(), v.size() * sizeof(v[0]));
+    };
+    put(o_row_off, P.row_off); put(o_halo_off, P.halo_off); put(o_bnode_off, P.bnode_off);
+    put(o_ent_off, P.ent_off); put(o_contrib_off, P.contrib_off); put(o_fcontrib_off, P.fcontrib_off);
+    put(o_epos, P.epos); put(o_epos2, P.epos2); put(o_rows, P.rows); put(o_halo, P.halo); put(o_bnodes, P.bnodes);
+    put(o_contrib, P.contrib); put(o_fcontrib, P.fcontrib); put(o_coff, P.coff); put(o_fcoff, P.fcoff);
+    put(o_hconn, P.hconn);
+    void* blob = nullptr;
+    HCUDA(cudaMalloc(&blob, img.size()));
+    const cudaError_t ce = cudaMemcpy(blob, img.data(), img.size(), cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+        cudaFree(blob);
+        return set_error(TGK_ERR_CUDA, std::string("entry plan upload: ") + cudaGetErrorString(ce));
+    }
+    auto* base = static_cast<unsigned char*>(blob);
+    D.blob = blob;
+    D.bytes = static_cast<int64_t>(img.size());
+    D.R = R;
+    D.n_blocks = P.n_blocks;
+    D.max_halo = P.max_halo;
+    D.max_bnodes = P.max_bnodes;
+    D.max_contrib = P.max_contrib;
+    D.max_fcontrib = P.max_fcontrib;
+    D.max_entries = P.max_entries;
+    D.max_clen = P.max_clen;
+    D.row_off = reinterpret_cast<const int64_t*>(base + o_row_off);
+    D.halo_off = reinterpret_cast<const int64_t*>(base + o_halo_off);
+    D.bnode_off = reinterpret_cast<const int64_t*>(base + o_bnode_off);
+    D.ent_off = reinterpret_cast<const int64_t*>(base + o_ent_off);
+    D.contrib_off = reinterpret_cast<const int64_t*>(base + o_contrib_off);
+    D.fcontrib_off = reinterpret_cast<const int64_t*>(base + o_fcontrib_off);
+    D.epos = reinterpret_cast<const int64_t*>(base + o_epos);
+    D.epos2 = reinterpret_cast<const int64_t*>(base + o_epos2);
+    D.rows = reinterpret_cast<const uint32_t*>(base + o_rows);
+    D.halo = reinterpret_cast<const uint32_t*>(base + o_halo);
+    D.bnodes = reinterpret_cast<const uint32_t*>(base + o_bnodes);
+    D.contrib = reinterpret_cast<const uint32_t*>(base + o_contrib);
+    D.fcontrib = reinterpret_cast<const uint32_t*>(base + o_fcontrib);
+    D.coff = reinterpret_cast<const uint32_t*>(base + o_coff);
+    D.fcoff = reinterpret_cast<const uint32_t*>(base + o_fcoff);
+    D.hconn = reinterpret_cast<const uint64_t*>(base + o_hconn);
+    *out = &D;
+    return TGK_OK;
+}
+
 // Build (once per R) and upload the fused row-block plan of a scalar routing.
 int ensure_plan(tgk_routing* rr, int R, const PlanDev** out, int C) {
     tgk_routing* r = rr->scalar ? rr->scalar : rr;
@@ -555,17 +663,14 @@ int ensure_plan(tgk_routing* rr, int R, const PlanDev** out, int C) {
     }
     PlanDev& D = *cache;
     const tgk_mesh* m = r->mesh;
-    const int k = m->k, d = m->d;
-    std::vector<double> nodes(m->N * d);
-    std::vector<int32_t> conn(m->E * k);
-    std::vector<int64_t> row_ptr(r->N + 1);
-    std::vector<uint32_t> vo(r->N + 1), vs(r->E * k), slot(r->E * k * k);
-    HCUDA(cudaMemcpy(nodes.data(), m->nodes, nodes.size() * 8, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(conn.data(), m->conn, conn.size() * 4, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(row_ptr.data(), r->row_ptr, row_ptr.size() * 8, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(vo.data(), r->vec_offsets, vo.size() * 4, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(vs.data(), r->vec_slots, vs.size() * 4, cudaMemcpyDeviceToHost));
-    HCUDA(cudaMemcpy(slot.data(), r->slot_of, slot.size() * 4, cudaMemcpyDeviceToHost));
+    ScalarRoutingHost h;
+    TGK_TRY(fetch_scalar_routing(r, h));
+    auto& nodes = h.nodes;
+    auto& conn = h.conn;
+    auto& row_ptr = h.row_ptr;
+    auto& vo = h.vo;
+    auto& vs = h.vs;
+    auto& slot = h.slot;
     PlanHost P;
     const int64_t lo = r->own_hi < 0 ? 0 : r->own_lo, hi = r->own_hi < 0 ? r->N : r->own_hi;
     const int64_t elo = r->elem_hi < 0 ? 0 : r->elem_lo, ehi = r->elem_hi < 0 ? r->E : r->elem_hi;

@@ -366,6 +366,7 @@ tgk_routing::~tgk_routing() {
                     (void*)scratch_F, (void*)scratch_M})
         if (p) cudaFree(p);
     for (auto& pl : plan) pl.release();
+    entry_plan.release();
     for (double* p : scr)
         if (p) cudaFree(p);
     if (scalar && scalar != this) delete scalar;

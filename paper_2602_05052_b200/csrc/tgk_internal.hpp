@@ -109,6 +109,41 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
                const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int R,
                int C, PlanHost& out);
 
+// Entry plan of the batched kernel (plan_entries.cpp, batched.cu): blocks of
+// R owned rows with their whole halo; per owned CSR entry the list of its
+// contributions (halo element | dot-product index << 16, ascending element)
+// so a thread folds the entry in a register.  Per-entry offsets (coff) and
+// per-row load offsets (fcoff) are block-relative and stored n+1 per block
+// (block b's segment starts at ent_off[b] + b, resp. row_off[b] + b).
+struct EntryPlanHost {
+    int R = 64;
+    int64_t n_blocks = 0;
+    int max_halo = 0, max_bnodes = 0, max_contrib = 0, max_fcontrib = 0, max_entries = 0, max_clen = 0;
+    std::vector<int64_t> row_off, halo_off, bnode_off, ent_off, contrib_off, fcontrib_off;
+    std::vector<uint32_t> rows, halo, bnodes, contrib, fcontrib, coff, fcoff;
+    std::vector<uint64_t> hconn;  // 4 x u16 block-local node indices per halo element
+    std::vector<int64_t> epos;    // CSR position of each folded entry
+    std::vector<int64_t> epos2;   // mirrored position (j, i) stored with the same value, or -1
+};
+
+struct EntryPlanDev {
+    int R = 0;
+    int64_t n_blocks = 0;
+    int max_halo = 0, max_bnodes = 0, max_contrib = 0, max_fcontrib = 0, max_entries = 0, max_clen = 0;
+    const int64_t *row_off = nullptr, *halo_off = nullptr, *bnode_off = nullptr, *ent_off = nullptr,
+                  *contrib_off = nullptr, *fcontrib_off = nullptr, *epos = nullptr, *epos2 = nullptr;
+    const uint32_t *rows = nullptr, *halo = nullptr, *bnodes = nullptr, *contrib = nullptr, *fcontrib = nullptr,
+                   *coff = nullptr, *fcoff = nullptr;
+    const uint64_t* hconn = nullptr;
+    void* blob = nullptr;  // one device allocation holding every array
+    int64_t bytes = 0;
+    void release();
+};
+
+int build_entry_plan(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
+                     const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
+                     int64_t row_lo, int64_t row_hi, int R, EntryPlanHost& P);
+
 }  // namespace tgk
 
 // ----------------------------------------------------------------- handles
@@ -138,6 +173,7 @@ struct tgk_routing {
     // scalar (node-level) routing used by vector problems and the fused plan
     tgk_routing* scalar = nullptr;   // == this for components == 1
     tgk::PlanDev plan[tgk::kPlanSlots];
+    tgk::EntryPlanDev entry_plan;    // batched kernel plan (built on first batched call)
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
     int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
     double* scr[6] = {};             // cached device scratch (materialised elasticity path)
@@ -151,4 +187,5 @@ struct tgk_routing {
 namespace tgk {
 // Build (once per R) and upload the fused plan of the routing's scalar part.
 int ensure_plan(tgk_routing* r, int R, const PlanDev** out, int C = 0);  // C = 0: chunk size R
+int ensure_entry_plan(tgk_routing* r, int R, const EntryPlanDev** out);
 }

@@ -104,6 +104,39 @@ def test_batched_tet4_bit_exact(eng):
         assert_bitwise(np_(K[b]), Kr, f"field {b}")
 
 
+@pytest.mark.parametrize("kind,env", [
+    ("tri3", {"TGK_BATCHED_CHUNKED": "1"}),             # row-block chunked kernel
+    ("tri3", {"TGK_ENTRY_R": "8", "TGK_ENTRY_FPB": "3"}),
+    ("tri3", {"TGK_ENTRY_R": "256", "TGK_ENTRY_SORT": "1"}),  # several entries / halo elements per thread
+    ("tri3", {"TGK_ENTRY_SYM": "1", "TGK_ENTRY_MAXC": "0", "TGK_ENTRY_STCS": "1", "TGK_ENTRY_SORT": "2"}),
+    ("tri3", {"TGK_ENTRY_SYM": "1", "TGK_ENTRY_R": "16"}),
+    ("tet4", {"TGK_ENTRY_R": "64"}),
+    ("tet4", {"TGK_ENTRY_R": "4", "TGK_ENTRY_FPB": "1"}),
+])
+def test_batched_paths_bit_exact(eng, monkeypatch, kind, env):
+    """Entry-owned kernel (default), its plan parameters, and the chunked
+    kernel all equal the per-field reference assemble bit for bit."""
+    from paper_2602_05052_b200 import meshgen
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    if kind == "tri3":
+        nodes, elems = meshgen.unstructured_tri(48)
+    else:
+        nodes, elems = port.generate_grid("tet4", [1.0] * 3, [7, 5, 6])
+    m = eng.DeviceMesh(kind, nodes, elems)
+    r = eng.Routing(m, 1)
+    pr = port.Routing(nodes.shape[0], port.dofmap(kind, elems, 1))
+    B = 5
+    rho = meshgen.batch_fields(B, elems.shape[0])
+    K, F = eng.assemble_batched(m, r, rho, source=1.0)
+    torch.cuda.synchronize()
+    for b in range(B):
+        Kr, Fr, _ = port.assemble(kind, nodes, elems, pr, diffusion=("element", rho[b]), sources=[1.0])
+        assert_bitwise(np_(K[b]), Kr, f"field {b}")
+        if b == 0:
+            assert_bitwise(np_(F), Fr, "F")
+
+
 def test_interface_combine_kernel(eng):
     from paper_2602_05052_b200 import dist as D
     rng = np.random.default_rng(9)
