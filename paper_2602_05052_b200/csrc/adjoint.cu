@@ -1,7 +1,9 @@
 // Adjoint pieces (adjoint.cpp:68-82 and the per-element chain rule of
 // acceptance.cpp:357-378 / tg_main.cpp:840-856), batched operator-learning
 // assembly, and the vector (elasticity) assembly path.
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "cuda_util.cuh"
 #include "element.cuh"
@@ -99,6 +101,131 @@ __global__ void __launch_bounds__(128) k_adjoint_gather(const double* nodes, con
     }
 }
 
+// Grouped transpose gather (plan_entries.cpp build_group_plan): a block
+// takes one group of G spatially compact elements (one per thread) and FPB
+// fields.  K0_e stays in registers across the fields; per field the group's
+// lambda_b / U_b node values are gathered once into shared memory (double
+// buffered, the next field's loads in flight while this one is summed), so
+// each node value is read from L2 once per group instead of once per
+// incident element.  Same per-element expression as k_adjoint_gather.
+constexpr int kGroupThreads = 256;
+
+struct GroupArgs {
+    const double* nodes;
+    const int32_t* conn;
+    int64_t E, N, B, fpb;
+    const double* lam;
+    const double* U;
+    double* out;
+    GroupPlanDev pl;
+    unsigned long long* bad;
+};
+
+template <int KIND, int DEG, int NPT>
+__global__ void __launch_bounds__(kGroupThreads) k_adjoint_groups(GroupArgs p) {
+    constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q, T = kGroupThreads;
+    using R = Rule<KIND, DEG>;
+    extern __shared__ __align__(16) double sv[];  // [2 buffers][lambda | U][max_nodes]
+    const int MN = p.pl.max_nodes;
+    const int tid = threadIdx.x;
+    const int64_t g = blockIdx.x;
+    const int64_t q0 = p.pl.grp_off[g];
+    const int ne = static_cast<int>(p.pl.grp_off[g + 1] - q0);
+    const int64_t n0 = p.pl.node_off[g];
+    const int nn = static_cast<int>(p.pl.node_off[g + 1] - n0);
+    const bool has_e = tid < ne;
+    const uint32_t e = has_e ? __ldg(p.pl.elems + q0 + tid) : 0u;
+    const uint64_t lc = has_e ? __ldg(reinterpret_cast<const unsigned long long*>(p.pl.lconn) + q0 + tid) : 0ull;
+    uint32_t gid[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) gid[j] = tid + j * T < nn ? __ldg(p.pl.gnodes + n0 + tid + j * T) : 0u;
+    const int64_t b0 = int64_t(blockIdx.y) * p.fpb;
+    const int64_t b1 = b0 + p.fpb < p.B ? b0 + p.fpb : p.B;
+    double rl[NPT], ru[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        rl[j] = tid + j * T < nn ? __ldg(p.lam + b0 * p.N + gid[j]) : 0.0;
+        ru[j] = tid + j * T < nn ? __ldg(p.U + b0 * p.N + gid[j]) : 0.0;
+    }
+    double K0[k][k];
+    bool ok = false;
+    if (has_e) {
+        double X[k][d];
+#pragma unroll
+        for (int a = 0; a < k; ++a) {
+            const int64_t gn = __ldg(p.conn + int64_t(e) * k + a);
+#pragma unroll
+            for (int c = 0; c < d; ++c) X[a][c] = __ldg(p.nodes + gn * d + c);
+        }
+        double det, G[k][d];
+        ok = simplex_geometry<KIND>(X, det, G);
+        if (!ok) atomicMin(p.bad, static_cast<unsigned long long>(e));
+#pragma unroll
+        for (int a = 0; a < k; ++a)
+#pragma unroll
+            for (int c = a; c < k; ++c) {
+                const double dot = ok ? gdot<KIND>(G, a, c) : 0.0;
+                double v = (R::w(0) * det * 1.0) * dot;
+#pragma unroll
+                for (int q = 1; q < Q; ++q) v += (R::w(q) * det * 1.0) * dot;
+                K0[a][c] = v;
+                K0[c][a] = v;
+            }
+    }
+    int li[k];
+#pragma unroll
+    for (int a = 0; a < k; ++a) li[a] = static_cast<int>((lc >> (16 * a)) & 0xffff);
+    int buf = 0;
+    for (int64_t b = b0; b < b1; ++b, buf ^= 1) {
+        double* sl = sv + size_t(buf) * 2 * MN;
+        double* su = sl + MN;
+#pragma unroll
+        for (int j = 0; j < NPT; ++j)
+            if (tid + j * T < nn) {
+                sl[tid + j * T] = rl[j];
+                su[tid + j * T] = ru[j];
+            }
+        if (b + 1 < b1) {
+#pragma unroll
+            for (int j = 0; j < NPT; ++j)
+                if (tid + j * T < nn) {
+                    rl[j] = __ldg(p.lam + (b + 1) * p.N + gid[j]);
+                    ru[j] = __ldg(p.U + (b + 1) * p.N + gid[j]);
+                }
+        }
+        __syncthreads();
+        if (ok) {
+            double la[k], uc[k];
+#pragma unroll
+            for (int a = 0; a < k; ++a) {
+                la[a] = sl[li[a]];
+                uc[a] = su[li[a]];
+            }
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < k; ++a)
+#pragma unroll
+                for (int c = 0; c < k; ++c) s += la[a] * K0[a][c] * uc[c];
+            p.out[b * p.E + e] = s;
+        }
+    }
+}
+
+template <int KIND, int DEG>
+int launch_adjoint_groups(const GroupArgs& a, int npt, cudaStream_t st) {
+    const size_t smem = sizeof(double) * 4 * size_t(a.pl.max_nodes);
+    const dim3 grid(static_cast<unsigned>(a.pl.n_groups), static_cast<unsigned>((a.B + a.fpb - 1) / a.fpb));
+    auto go = [&](auto kern) -> int {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (a.pl.n_groups > 0) kern<<<grid, kGroupThreads, smem, st>>>(a);
+        KERNEL_CHECK("adjoint_groups");
+        return TGK_OK;
+    };
+    if (npt == 1) return go(k_adjoint_groups<KIND, DEG, 1>);
+    if (npt == 2) return go(k_adjoint_groups<KIND, DEG, 2>);
+    return go(k_adjoint_groups<KIND, DEG, 4>);
+}
+
 // plane-stress lambda (batch.cpp:359-361) in place, and the mu > 0 check
 __global__ void k_plane_stress(double* lam, const double* mu, int64_t n) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -194,19 +321,48 @@ int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, con
     if (r->components != 1) return set_error(TGK_ERR_INPUT, "adjoint_gather: scalar routing required");
     TGK_TRY(ensure_device());
     cudaStream_t st = as_stream(stream);
-    constexpr int FPB = 8;
     DevBuf<unsigned long long> bad;
     TGK_TRY(bad.alloc(1));
     CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    if (m->kind != TGK_TET4 && m->kind != TGK_TRI3) return set_error(TGK_ERR_INPUT, "adjoint_gather: TRI3/TET4 only");
+    if (degree != 1 && degree != 2) return set_error(TGK_ERR_INPUT, "adjoint_gather: degree must be 1 or 2");
+    if (B <= 0) return TGK_OK;
+    if (!getenv("TGK_ADJ_FLAT")) {
+        const GroupPlanDev* pl = nullptr;
+        TGK_TRY(ensure_group_plan(const_cast<tgk_routing*>(r), kGroupThreads, &pl));
+        const int npt = (pl->max_nodes + kGroupThreads - 1) / kGroupThreads;
+        if (npt <= 4) {
+            GroupArgs a{};
+            a.nodes = m->nodes;
+            a.conn = m->conn;
+            a.E = m->E;
+            a.N = m->N;
+            a.B = B;
+            a.fpb = 16;
+            if (const char* e = getenv("TGK_ADJ_FPB")) a.fpb = std::max(1, atoi(e));
+            a.lam = lam;
+            a.U = U;
+            a.out = out;
+            a.pl = *pl;
+            a.bad = bad.p;
+            const int np = npt <= 1 ? 1 : npt <= 2 ? 2 : 4;
+            if (m->kind == TGK_TET4)
+                TGK_TRY((degree == 1 ? launch_adjoint_groups<TGK_TET4, 1>(a, np, st)
+                                     : launch_adjoint_groups<TGK_TET4, 2>(a, np, st)));
+            else
+                TGK_TRY((degree == 1 ? launch_adjoint_groups<TGK_TRI3, 1>(a, np, st)
+                                     : launch_adjoint_groups<TGK_TRI3, 2>(a, np, st)));
+            return check_bad(bad.p, st);
+        }
+    }
+    constexpr int FPB = 8;
     const dim3 grid(grid_for(m->E, 128), static_cast<unsigned>((B + FPB - 1) / FPB));
     if (m->kind == TGK_TET4) {
         if (degree == 1) k_adjoint_gather<TGK_TET4, 1, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
         else k_adjoint_gather<TGK_TET4, 2, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
-    } else if (m->kind == TGK_TRI3) {
+    } else {
         if (degree == 1) k_adjoint_gather<TGK_TRI3, 1, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
         else k_adjoint_gather<TGK_TRI3, 2, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
-    } else {
-        return set_error(TGK_ERR_INPUT, "adjoint_gather: TRI3/TET4 only");
     }
     KERNEL_CHECK("adjoint_gather");
     return check_bad(bad.p, st);

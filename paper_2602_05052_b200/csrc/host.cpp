@@ -645,6 +645,62 @@ int ensure_entry_plan(tgk_routing* rr, int R, const EntryPlanDev** out) {
     return TGK_OK;
 }
 
+void GroupPlanDev::release() {
+    if (blob) cudaFree(blob);
+    *this = GroupPlanDev{};
+}
+
+// Build (once per group size) and upload the adjoint gather's element-group plan.
+int ensure_group_plan(tgk_routing* rr, int G, const GroupPlanDev** out) {
+    tgk_routing* r = rr->scalar ? rr->scalar : rr;
+    GroupPlanDev& D = r->group_plan;
+    if (D.blob && D.G == G) {
+        *out = &D;
+        return TGK_OK;
+    }
+    D.release();
+    const tgk_mesh* m = r->mesh;
+    std::vector<double> nodes(m->N * m->d);
+    std::vector<int32_t> conn(m->E * m->k);
+    HCUDA(cudaMemcpy(nodes.data(), m->nodes, nodes.size() * 8, cudaMemcpyDeviceToHost));
+    HCUDA(cudaMemcpy(conn.data(), m->conn, conn.size() * 4, cudaMemcpyDeviceToHost));
+    GroupPlanHost P;
+    TGK_TRY(build_group_plan(m->kind, m->N, m->E, nodes.data(), conn.data(), G, P));
+    size_t total = 0;
+    auto reserve = [&total](const auto& v) {
+        const size_t at = total;
+        total += (v.size() * sizeof(v[0]) + 15) & ~size_t(15);
+        return at;
+    };
+    const size_t o_grp = reserve(P.grp_off), o_node = reserve(P.node_off), o_el = reserve(P.elems),
+                 o_gn = reserve(P.gnodes), o_lc = reserve(P.lconn);
+    std::vector<unsigned char> img(std::max<size_t>(total, 16));
+    auto put = [&img](size_t at, const auto& v) {
+        if (!v.empty()) std::memcpy(img.data() + at, v.data(), v.size() * sizeof(v[0]));
+    };
+    put(o_grp, P.grp_off); put(o_node, P.node_off); put(o_el, P.elems); put(o_gn, P.gnodes); put(o_lc, P.lconn);
+    void* blob = nullptr;
+    HCUDA(cudaMalloc(&blob, img.size()));
+    const cudaError_t ce = cudaMemcpy(blob, img.data(), img.size(), cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+        cudaFree(blob);
+        return set_error(TGK_ERR_CUDA, std::string("group plan upload: ") + cudaGetErrorString(ce));
+    }
+    auto* base = static_cast<unsigned char*>(blob);
+    D.blob = blob;
+    D.bytes = static_cast<int64_t>(img.size());
+    D.G = G;
+    D.n_groups = P.n_groups;
+    D.max_nodes = P.max_nodes;
+    D.grp_off = reinterpret_cast<const int64_t*>(base + o_grp);
+    D.node_off = reinterpret_cast<const int64_t*>(base + o_node);
+    D.elems = reinterpret_cast<const uint32_t*>(base + o_el);
+    D.gnodes = reinterpret_cast<const uint32_t*>(base + o_gn);
+    D.lconn = reinterpret_cast<const uint64_t*>(base + o_lc);
+    *out = &D;
+    return TGK_OK;
+}
+
 // Build (once per R) and upload the fused row-block plan of a scalar routing.
 int ensure_plan(tgk_routing* rr, int R, const PlanDev** out, int C) {
     tgk_routing* r = rr->scalar ? rr->scalar : rr;

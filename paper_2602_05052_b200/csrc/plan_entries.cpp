@@ -195,4 +195,64 @@ int build_entry_plan(int kind, int64_t N, const double* nodes, const int32_t* co
     return TGK_OK;
 }
 
+int build_group_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn, int G,
+                     GroupPlanHost& P) {
+    const int k = element_nodes(kind), d = element_dim(kind);
+    P = GroupPlanHost{};
+    P.G = G;
+    if (G < 32 || G > 1024) return set_error(TGK_ERR_INPUT, "group plan: group size out of range");
+    std::vector<double> cen(size_t(E) * d, 0.0);
+    for (int64_t e = 0; e < E; ++e)
+        for (int a = 0; a < k; ++a)
+            for (int c = 0; c < d; ++c) cen[e * d + c] += nodes[int64_t(conn[e * k + a]) * d + c];
+    const std::vector<uint32_t> order = morton_order(kind, E, cen.data(), 0, E);
+    const int64_t ng = (E + G - 1) / G;
+    P.n_groups = ng;
+    P.grp_off.resize(ng + 1);
+    P.node_off.assign(ng + 1, 0);
+    P.elems.resize(E);
+    P.lconn.resize(E);
+    std::vector<std::vector<uint32_t>> gn(ng);
+    auto work = [&](int64_t g0, int64_t g1) {
+        for (int64_t g = g0; g < g1; ++g) {
+            const int64_t lo = g * G, hi = std::min<int64_t>(E, lo + G);
+            std::vector<uint32_t> el(order.begin() + lo, order.begin() + hi);
+            std::sort(el.begin(), el.end());  // ascending ids: the output stores of a warp share sectors more often
+            std::vector<uint32_t>& nd = gn[g];
+            for (uint32_t e : el)
+                for (int a = 0; a < k; ++a) nd.push_back(static_cast<uint32_t>(conn[int64_t(e) * k + a]));
+            std::sort(nd.begin(), nd.end());
+            nd.erase(std::unique(nd.begin(), nd.end()), nd.end());
+            for (int64_t i = lo; i < hi; ++i) {
+                const uint32_t e = el[i - lo];
+                P.elems[i] = e;
+                uint64_t lc = 0;
+                for (int a = 0; a < k; ++a) {
+                    const uint32_t n = static_cast<uint32_t>(conn[int64_t(e) * k + a]);
+                    lc |= uint64_t(std::lower_bound(nd.begin(), nd.end(), n) - nd.begin()) << (16 * a);
+                }
+                P.lconn[i] = lc;
+            }
+        }
+    };
+    const int nthreads = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    {
+        std::vector<std::thread> pool;
+        const int64_t per = (ng + nthreads - 1) / nthreads;
+        for (int t = 0; t < nthreads; ++t) {
+            const int64_t g0 = t * per, g1 = std::min(ng, g0 + per);
+            if (g0 < g1) pool.emplace_back(work, g0, g1);
+        }
+        for (auto& th : pool) th.join();
+    }
+    for (int64_t g = 0; g <= ng; ++g) P.grp_off[g] = std::min<int64_t>(E, g * G);
+    for (int64_t g = 0; g < ng; ++g) {
+        P.node_off[g + 1] = P.node_off[g] + static_cast<int64_t>(gn[g].size());
+        P.max_nodes = std::max<int>(P.max_nodes, static_cast<int>(gn[g].size()));
+    }
+    P.gnodes.reserve(P.node_off[ng]);
+    for (const auto& v : gn) P.gnodes.insert(P.gnodes.end(), v.begin(), v.end());
+    return TGK_OK;
+}
+
 }  // namespace tgk

@@ -367,6 +367,7 @@ tgk_routing::~tgk_routing() {
         if (p) cudaFree(p);
     for (auto& pl : plan) pl.release();
     entry_plan.release();
+    group_plan.release();
     for (double* p : scr)
         if (p) cudaFree(p);
     if (scalar && scalar != this) delete scalar;

@@ -140,6 +140,35 @@ struct EntryPlanDev {
     void release();
 };
 
+// Element-group plan of the adjoint transpose gather (plan_entries.cpp,
+// adjoint.cu): elements in Morton order of their centroids, cut into groups
+// of G; per group the element ids, the sorted unique nodes and each element's
+// group-local node indices (4 x u16).  A block stages the group's lambda_b /
+// U_b values once per field instead of gathering them once per element.
+struct GroupPlanHost {
+    int G = 256;
+    int64_t n_groups = 0;
+    int max_nodes = 0;
+    std::vector<int64_t> grp_off, node_off;
+    std::vector<uint32_t> elems, gnodes;
+    std::vector<uint64_t> lconn;
+};
+
+struct GroupPlanDev {
+    int G = 0;
+    int64_t n_groups = 0;
+    int max_nodes = 0;
+    const int64_t *grp_off = nullptr, *node_off = nullptr;
+    const uint32_t *elems = nullptr, *gnodes = nullptr;
+    const uint64_t* lconn = nullptr;
+    void* blob = nullptr;
+    int64_t bytes = 0;
+    void release();
+};
+
+int build_group_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn, int G,
+                     GroupPlanHost& P);
+
 int build_entry_plan(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
                      const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
                      int64_t row_lo, int64_t row_hi, int R, EntryPlanHost& P);
@@ -174,6 +203,7 @@ struct tgk_routing {
     tgk_routing* scalar = nullptr;   // == this for components == 1
     tgk::PlanDev plan[tgk::kPlanSlots];
     tgk::EntryPlanDev entry_plan;    // batched kernel plan (built on first batched call)
+    tgk::GroupPlanDev group_plan;    // adjoint gather plan (built on first adjoint call)
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
     int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
     double* scr[6] = {};             // cached device scratch (materialised elasticity path)
@@ -188,4 +218,5 @@ namespace tgk {
 // Build (once per R) and upload the fused plan of the routing's scalar part.
 int ensure_plan(tgk_routing* r, int R, const PlanDev** out, int C = 0);  // C = 0: chunk size R
 int ensure_entry_plan(tgk_routing* r, int R, const EntryPlanDev** out);
+int ensure_group_plan(tgk_routing* r, int G, const GroupPlanDev** out);
 }

@@ -271,6 +271,37 @@ def test_batched_adjoint_vs_oracle(eng):
         assert_bitwise(got[b], port.adjoint_gather(dm, K0, lam[b], U[b]), f"field {b}")
 
 
+@pytest.mark.parametrize("kind,degree,env", [
+    ("tri3", 2, {}), ("tet4", 1, {}), ("tet4", 2, {"TGK_ADJ_FPB": "3"}),
+    ("tri3", 1, {"TGK_ADJ_FLAT": "1"}), ("tet4", 2, {"TGK_ADJ_FLAT": "1"}),
+    ("unstructured", 1, {"TGK_ADJ_FPB": "1"}),
+])
+def test_adjoint_paths_vs_oracle(eng, monkeypatch, kind, degree, env):
+    """Grouped (default) and flat transpose gathers, bit-exact per field."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    if kind == "unstructured":
+        from paper_2602_05052_b200 import meshgen
+        kind = "tri3"
+        nodes, elems = meshgen.unstructured_tri(40)
+    elif kind == "tri3":
+        nodes, elems = port.generate_grid("tri3", [1.0, 1.0], [33, 29])
+    else:
+        nodes, elems = port.generate_grid("tet4", [1.0] * 3, [7, 6, 8])
+    m = eng.DeviceMesh(kind, nodes, elems)
+    r = eng.Routing(m, 1)
+    Nn, E = nodes.shape[0], elems.shape[0]
+    rng = np.random.default_rng(2100)
+    B = 7
+    lam = rng.random((B, Nn)) - 0.5
+    U = rng.random((B, Nn)) - 0.5
+    got = np_(eng.adjoint_gather(m, r, lam, U, degree=degree))
+    dm = port.dofmap(kind, elems, 1)
+    K0 = port.local(kind, nodes, elems, degree, port.DIFFUSION, np.ones(E * port.tables(kind, degree)["Q"]))
+    for b in range(B):
+        assert_bitwise(got[b], port.adjoint_gather(dm, K0, lam[b], U[b]), f"field {b}")
+
+
 # ------------------------------------------------------------------ errors
 def test_errors(eng):
     from paper_2602_05052_b200 import InputError
