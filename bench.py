@@ -644,7 +644,7 @@ def run_batched(args, ctx, N):
                 roofline={"bound": "hbm", "achieved": ach_b, "peak": peak, "unit": "GB/s",
                           "frac": ach_b / peak, "traffic": ncu_traffic("c4") if ctx.world == 1 else None,
                           "alg_bytes": ab_b, "peak_source": peak_src,
-                          "kernel": "k_batched (one launch per step, all fields)", "kernel_ms": ms_b})
+                          "kernel": "k_batched_entries (one launch per step, all fields)", "kernel_ms": ms_b})
 
 
 def main():
