@@ -115,6 +115,7 @@ class ClockSampler:
         self.index = index
         self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
+        self._ready = threading.Event()  # set once the sampler is initialised (NVML init can take ~100 ms)
         self._t = None
 
     def _run_nvml(self):
@@ -124,6 +125,7 @@ class ClockSampler:
         mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
         names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                  "sw_power_cap": 0x4}
+        self._ready.set()
         while not self._stop.is_set():
             self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
             self.mx.append(mx)
@@ -137,6 +139,7 @@ class ClockSampler:
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        self._ready.set()
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
@@ -160,7 +163,7 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        time.sleep(0.01)
+        self._ready.wait(timeout=10)
         return self
 
     def __exit__(self, *a):

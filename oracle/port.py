@@ -167,9 +167,10 @@ def local(kind, nodes, elems, degree, what, c1, c2=None):
     Q = tables(kind, degree)["Q"]
     c1 = np.ascontiguousarray(c1, dtype=np.float64)
     c2 = None if c2 is None else np.ascontiguousarray(c2, dtype=np.float64)
-    for c in (c1, c2):  # per quadrature point (E x Q); the restatement does not bounds-check
-        if c is not None and c.size != E * Q:
-            raise ValueError(f"local: coefficient has {c.size} values, expected E*Q = {E * Q}")
+    per_point = d if what == LOAD_VECTOR else 1  # vector source: d components per point
+    for c in (c1, c2):  # per quadrature point (E x Q [x d]); the restatement does not bounds-check
+        if c is not None and c.size != E * Q * per_point:
+            raise ValueError(f"local: coefficient has {c.size} values, expected {E * Q * per_point}")
     bad = C.c_int64(-1)
     _check(lib().tgo_local(KINDS[kind], _p(nodes), _p(elems), E, degree, what, _p(c1), _p(c2),
                            _p(out), C.byref(bad)))

@@ -6,7 +6,7 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvidia-smi.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
-timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; grep -E "FAILED|passed|failed" gpurun_out/pytest_gpu.log | tail -5
 for w in ${WORKLOADS:-c2 c2a c1 c3 c4 c5}; do
   timeout 900 python bench.py --workload $w --steps ${STEPS:-20} --warmup 5 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
   python -c "
@@ -21,6 +21,11 @@ for wk in c2:k_fused_scalar c2a:k_fused_scalar c1:k_fused_scalar c3:k_fused_elas
   w=${wk%%:*}; k=${wk##*:}; bw=$w; [ $w = c4adj ] && bw=c4
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
     -o gpurun_out/prof_$w python bench.py --workload $bw --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_full_$w.log 2>&1
+done
+# summaries + traffic.json on the box; keep only the reports named in KEEP (64 MiB merge limit)
+TRAFFIC_OUT=gpurun_out/prof_out python tools/make_traffic.py ${PREFIX:-r01} > /dev/null
+for f in gpurun_out/prof_*.ncu-rep; do
+  case " ${KEEP:-c2} " in *" $(basename $f .ncu-rep | sed s/prof_//) "*) ;; *) rm -f $f ;; esac
 done
 fi
 ls gpurun_out | head -60

@@ -22,7 +22,9 @@ def raw(rep):
 
 def main():
     prefix = sys.argv[1] if len(sys.argv) > 1 else "r01"
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+    outdir = os.environ.get("TRAFFIC_OUT", os.path.join(ROOT, "profiles"))  # on the GPU box: under gpurun_out/
+    os.makedirs(outdir, exist_ok=True)
+    path = os.path.join(outdir, "traffic.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     for w in ["c2", "c2a", "c1", "c3", "c4", "c4adj", "c5"]:
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{w}.ncu-rep")
@@ -35,11 +37,12 @@ def main():
             tot += float(v.replace(",", "")) * UNITS.get(u, 1)
         t, tu = m["gpu__time_duration.sum"]
         data[w] = {"bytes": int(tot), "kernel": m.get("Kernel Name", ("?", ""))[0][:120],
-                   "ncu_time_us": float(t.replace(",", "")) * {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(tu, 1),
+                   "ncu_time_us": float(t.replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1,
+                                                                  "msecond": 1e3, "ms": 1e3}.get(tu, 1),
                    "source": f"ncu --set full --clock-control none, one launch ({prefix})"}
         summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep],
                               capture_output=True, text=True).stdout
-        with open(os.path.join(ROOT, "profiles", f"{prefix}_ncu_{w}.txt"), "w") as f:
+        with open(os.path.join(outdir, f"{prefix}_ncu_{w}.txt"), "w") as f:
             f.write(summ)
     with open(path, "w") as f:
         json.dump(data, f, indent=1, sort_keys=True)
