@@ -84,8 +84,10 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
     const int d = element_dim(kind), k = element_nodes(kind);
     (void)E;
     // R rows per block, chunks of C halo elements (C threads; R = C x rows per thread)
-    if (R != 64 && R != 128 && R != 256) return set_error(TGK_ERR_INPUT, "fused plan: R must be 64, 128 or 256");
-    if (C != 64 && C != 128 && C != 256) return set_error(TGK_ERR_INPUT, "fused plan: chunk size must be 64, 128 or 256");
+    if (R != 16 && R != 32 && R != 64 && R != 128 && R != 256)
+        return set_error(TGK_ERR_INPUT, "fused plan: R must be 16, 32, 64, 128 or 256");
+    if (C != 32 && C != 64 && C != 128 && C != 256)
+        return set_error(TGK_ERR_INPUT, "fused plan: chunk size must be 32, 64, 128 or 256");
     P.R = R;
     P.C = C;
     // --- 1. Morton order of the owned nodes
