@@ -388,9 +388,8 @@ __global__ void __launch_bounds__(R) k_fused_elast(ElastArgs p) {
 //             records' blocks in ascending element order, the diagonal block
 //             entry and F_c (c' = 0) in registers, the others into shared
 //             accumulators [pos][c][c'][row].
-constexpr int kElastR2 = 32;
-template <int D>
-constexpr int elast2_threads() { return 32 * D * D; }
+template <int D, int R>
+constexpr int elast2_threads() { return (R * D * D + 31) / 32 * 32; }
 
 template <int KIND, int DEG>
 struct E2Cfg {
@@ -399,13 +398,13 @@ struct E2Cfg {
     static constexpr int RSP = RS % 2 == 1 ? RS : RS + 1;     // odd stride: spread banks
 };
 
-template <int KIND, int DEG>
-__global__ void __launch_bounds__(elast2_threads<P1<KIND>::d>(), 2) k_fused_elast2(ElastArgs p) {
+template <int KIND, int DEG, int R>
+__global__ void __launch_bounds__(elast2_threads<P1<KIND>::d, R>(), R <= 16 ? 3 : 2) k_fused_elast2(ElastArgs p) {
     using C = ECfg<KIND, DEG>;
     using C2 = E2Cfg<KIND, DEG>;
     using Rl = Rule<KIND, DEG>;
     constexpr int k = C::k, d = C::d, Q = C::Q, ns = d == 2 ? 3 : 6;
-    constexpr int R = kElastR2, T = elast2_threads<d>(), ROS = R + 8, RSP = C2::RSP;
+    constexpr int T = elast2_threads<d, R>(), ROS = R + 8, RSP = C2::RSP;
     const int CH = p.S;  // halo elements per chunk (plan C)
     extern __shared__ __align__(16) unsigned char sme[];
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
@@ -465,9 +464,10 @@ __global__ void __launch_bounds__(elast2_threads<P1<KIND>::d>(), 2) k_fused_elas
 #pragma unroll
     for (int c = 0; c < kRingE - 1; ++c) stage(c);
 
-    // B2 role: warp c*d + c' folds block entry (c, c') of owned row `lane`
-    const bool folder = lane < nr;
-    const int fc = warp / d, fcp = warp % d;
+    // B2 role: thread (block entry (c, c'), owned row) = (tid / R, tid % R)
+    const int fw = tid / R, frow = tid % R;  // block entry (c, c') = fw, owned row
+    const bool folder = fw < d * d && frow < nr;
+    const int fc = folder ? fw / d : 0, fcp = folder ? fw % d : 0;
     double dK = 0.0, dF = 0.0;
     int diag_pos = 0;
 
@@ -614,9 +614,9 @@ __global__ void __launch_bounds__(elast2_threads<P1<KIND>::d>(), 2) k_fused_elas
             }
         }
         __syncthreads();
-        // ---------------- phase B2: fold, warp = block entry (c, c'), lane = owned row
+        // ---------------- phase B2: fold, thread = (block entry (c, c'), owned row)
         if (folder) {
-            for (int j = ro[lane]; j < ro[lane + 1]; ++j) {
+            for (int j = ro[frow]; j < ro[frow + 1]; ++j) {
                 const uint32_t rec = rs[j];
                 const double* src = rb + size_t(j) * RSP + fc * d + fcp;
                 dK += src[0];
@@ -625,11 +625,11 @@ __global__ void __launch_bounds__(elast2_threads<P1<KIND>::d>(), 2) k_fused_elas
 #pragma unroll
                 for (int jj = 0; jj < k - 1; ++jj) {
                     pos[jj] = (rec >> (10 + 5 * jj)) & 31;
-                    old[jj] = acc[((size_t(pos[jj]) * d + fc) * d + fcp) * R + lane];
+                    old[jj] = acc[((size_t(pos[jj]) * d + fc) * d + fcp) * R + frow];
                 }
 #pragma unroll
                 for (int jj = 0; jj < k - 1; ++jj)
-                    acc[((size_t(pos[jj]) * d + fc) * d + fcp) * R + lane] = old[jj] + src[(jj + 1) * d * d];
+                    acc[((size_t(pos[jj]) * d + fc) * d + fcp) * R + frow] = old[jj] + src[(jj + 1) * d * d];
                 if (fcp == 0) dF += rb[size_t(j) * RSP + k * d * d + fc];
                 diag_pos = (rec >> 25) & 31;
             }
@@ -638,8 +638,8 @@ __global__ void __launch_bounds__(elast2_threads<P1<KIND>::d>(), 2) k_fused_elas
     cpa_wait<0>();
     __syncthreads();
     if (folder) {
-        acc[((size_t(diag_pos) * d + fc) * d + fcp) * R + lane] = dK;
-        if (fcp == 0) p.F[int64_t(p.rows[r0 + lane]) * d + fc] = dF;
+        acc[((size_t(diag_pos) * d + fc) * d + fcp) * R + frow] = dK;
+        if (fcp == 0) p.F[int64_t(p.rows[r0 + frow]) * d + fc] = dF;
     }
     __syncthreads();
     // epilogue: node r's d DoF rows = d*d*len contiguous values [d^2 rp, d^2 (rp + len)); a warp per node
@@ -657,10 +657,10 @@ __global__ void __launch_bounds__(elast2_threads<P1<KIND>::d>(), 2) k_fused_elas
     }
 }
 
-template <int KIND, int DEG>
+template <int KIND, int DEG, int R>
 size_t elast2_smem(const ElastArgs& a) {
     using C = ECfg<KIND, DEG>;
-    constexpr int d = C::d, R = kElastR2;
+    constexpr int d = C::d;
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
     size_t o = 0;
     o = al(o + sizeof(double) * size_t(a.S) * C::stride);
@@ -674,15 +674,15 @@ size_t elast2_smem(const ElastArgs& a) {
     return o;
 }
 
-template <int KIND, int DEG>
+template <int KIND, int DEG, int R>
 int launch_elast2(const ElastArgs& a, int64_t nb, cudaStream_t st) {
-    auto kern = k_fused_elast2<KIND, DEG>;
-    const size_t smem = elast2_smem<KIND, DEG>(a);
+    auto kern = k_fused_elast2<KIND, DEG, R>;
+    const size_t smem = elast2_smem<KIND, DEG, R>(a);
     if (smem > 227 * 1024)
         return set_error(TGK_ERR_INPUT, "fused elasticity: block working set exceeds shared memory (" +
                                             std::to_string(smem) + " B)");
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (nb > 0) kern<<<static_cast<unsigned>(nb), elast2_threads<P1<KIND>::d>(), smem, st>>>(a);
+    if (nb > 0) kern<<<static_cast<unsigned>(nb), elast2_threads<P1<KIND>::d, R>(), smem, st>>>(a);
     KERNEL_CHECK("fused_elast2");
     return TGK_OK;
 }
@@ -712,10 +712,11 @@ int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
                               cudaStream_t st) {
     const bool v1 = getenv("TGK_ELAST_V1") != nullptr;
     constexpr int R = 64;
-    int C2 = 128;  // v2 chunk size (measured: 64 -> 9.9 ms, 128 -> 7.2 ms on C3)
+    int C2 = 64, R2 = 16;  // v2 chunk size and rows per block
     if (const char* e = getenv("TGK_ELAST_C")) C2 = atoi(e);
+    if (const char* e = getenv("TGK_ELAST_R")) R2 = atoi(e) == 32 ? 32 : 16;
     const PlanDev* pl = nullptr;
-    TGK_TRY(v1 ? ensure_plan(r, R, &pl) : ensure_plan(r, kElastR2, &pl, C2));
+    TGK_TRY(v1 ? ensure_plan(r, R, &pl) : ensure_plan(r, R2, &pl, C2));
     const bool high = pr->diffusion.type != TGK_FIELD_CONSTANT;  // physics.cpp:18-21
     const int d = m->d;
     ElastArgs a{};
@@ -756,10 +757,16 @@ int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
         } else {
             TGK_TRY((high ? launch_elast<TGK_TRI3, 2, R>(a, pl->n_blocks, st) : launch_elast<TGK_TRI3, 1, R>(a, pl->n_blocks, st)));
         }
-    } else if (m->kind == TGK_TET4) {
-        TGK_TRY((high ? launch_elast2<TGK_TET4, 2>(a, pl->n_blocks, st) : launch_elast2<TGK_TET4, 1>(a, pl->n_blocks, st)));
+    } else if (R2 == 16) {
+        if (m->kind == TGK_TET4)
+            TGK_TRY((high ? launch_elast2<TGK_TET4, 2, 16>(a, pl->n_blocks, st) : launch_elast2<TGK_TET4, 1, 16>(a, pl->n_blocks, st)));
+        else
+            TGK_TRY((high ? launch_elast2<TGK_TRI3, 2, 16>(a, pl->n_blocks, st) : launch_elast2<TGK_TRI3, 1, 16>(a, pl->n_blocks, st)));
     } else {
-        TGK_TRY((high ? launch_elast2<TGK_TRI3, 2>(a, pl->n_blocks, st) : launch_elast2<TGK_TRI3, 1>(a, pl->n_blocks, st)));
+        if (m->kind == TGK_TET4)
+            TGK_TRY((high ? launch_elast2<TGK_TET4, 2, 32>(a, pl->n_blocks, st) : launch_elast2<TGK_TET4, 1, 32>(a, pl->n_blocks, st)));
+        else
+            TGK_TRY((high ? launch_elast2<TGK_TRI3, 2, 32>(a, pl->n_blocks, st) : launch_elast2<TGK_TRI3, 1, 32>(a, pl->n_blocks, st)));
     }
     unsigned long long h[2] = {ULLONG_MAX, ULLONG_MAX};
     CUDA_TRY(cudaMemcpyAsync(h, bad.p, sizeof h, cudaMemcpyDeviceToHost, st));
