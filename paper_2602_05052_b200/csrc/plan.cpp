@@ -74,6 +74,62 @@ std::vector<uint32_t> morton_order(int kind, int64_t N, const double* nodes, int
     return out;
 }
 
+// The halo of a row block (every element incident to one of its rows, inside
+// [elem_lo, elem_hi)) in fold-compatible order.  Level schedule: every owned
+// row's elements must be folded in ascending id, i.e. they form a chain;
+// level(e) = longest chain ending at e.  Ordering the halo by (level, id) keeps
+// each row's elements ascending across and within chunks of C while giving
+// every row at most one element per level -> balanced folds.  Within a chunk
+// the order is free (every consumer folds by element id): each chunk is
+// ordered by the element's first node so the lanes of a warp gather nearby
+// node-table entries (TGK_CHUNK_SORT=0 disables).
+std::vector<uint32_t> order_block_halo(int k, const int32_t* conn, const uint32_t* rows, int64_t nrows,
+                                       const uint32_t* vec_offsets, const uint32_t* vec_slots, int64_t elem_lo,
+                                       int64_t elem_hi, int C) {
+    auto in_range = [elem_lo, elem_hi](uint32_t e) { return int64_t(e) >= elem_lo && int64_t(e) < elem_hi; };
+    std::vector<uint32_t> tmp;
+    for (int64_t i = 0; i < nrows; ++i) {
+        const uint32_t row = rows[i];
+        for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s)
+            if (in_range(vec_slots[s] / k)) tmp.push_back(vec_slots[s] / k);
+    }
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    const int64_t nh = static_cast<int64_t>(tmp.size());
+    std::vector<int> level(nh, 0);
+    {
+        std::vector<std::pair<uint32_t, uint32_t>> edges;  // (next, pred) as halo indices
+        for (int64_t i = 0; i < nrows; ++i) {
+            const uint32_t row = rows[i];
+            int64_t prev = -1;
+            for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s) {
+                const uint32_t e = vec_slots[s] / k;
+                if (!in_range(e)) continue;
+                const int64_t hix = std::lower_bound(tmp.begin(), tmp.end(), e) - tmp.begin();
+                if (prev >= 0) edges.push_back({static_cast<uint32_t>(hix), static_cast<uint32_t>(prev)});
+                prev = hix;
+            }
+        }
+        std::sort(edges.begin(), edges.end());  // by target: a topological order
+        for (const auto& ed : edges) level[ed.first] = std::max(level[ed.first], level[ed.second] + 1);
+    }
+    std::vector<std::pair<int, uint32_t>> order(nh);
+    for (int64_t h = 0; h < nh; ++h) order[h] = {level[h], tmp[h]};
+    std::sort(order.begin(), order.end());
+    static const bool chunk_sort = !(getenv("TGK_CHUNK_SORT") && atoi(getenv("TGK_CHUNK_SORT")) == 0);
+    if (chunk_sort)
+        for (int64_t c0 = 0; c0 < nh; c0 += C) {
+            const int64_t c1 = std::min<int64_t>(nh, c0 + C);
+            std::sort(order.begin() + c0, order.begin() + c1, [&](const auto& x, const auto& y) {
+                const int32_t nx = conn[int64_t(x.second) * k], ny = conn[int64_t(y.second) * k];
+                return nx != ny ? nx < ny : x.second < y.second;
+            });
+        }
+    std::vector<uint32_t> out(nh);
+    for (int64_t h = 0; h < nh; ++h) out[h] = order[h].second;
+    return out;
+}
+
 int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
                const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
                const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int R,
@@ -148,64 +204,13 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
     };
     std::vector<BlockOut> out(nb);
     auto work = [&](int64_t b_begin, int64_t b_end) {
-        std::vector<uint32_t> tmp;
         for (int64_t b = b_begin; b < b_end; ++b) {
             BlockOut& o = out[b];
             const int64_t rs = P.row_off[b], re = P.row_off[b + 1];
-            tmp.clear();
-            for (int64_t i = rs; i < re; ++i) {
-                const uint32_t row = P.rows[i];
-                for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s)
-                    if (in_range(vec_slots[s] / k)) tmp.push_back(vec_slots[s] / k);
-            }
-            std::sort(tmp.begin(), tmp.end());
-            tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-            const int64_t nh = static_cast<int64_t>(tmp.size());
-            // Level schedule: every owned row's elements must be folded in
-            // ascending id, i.e. they form a chain; level(e) = longest chain
-            // ending at e.  Ordering the halo by (level, id) keeps each row's
-            // elements ascending across and within chunks while giving every
-            // row at most one element per level -> balanced phase B.
-            std::vector<int> level(nh, 0);
-            {
-                std::vector<std::pair<uint32_t, uint32_t>> edges;  // (next, pred) as halo indices
-                for (int64_t i = rs; i < re; ++i) {
-                    const uint32_t row = P.rows[i];
-                    int64_t prev = -1;
-                    for (uint32_t s = vec_offsets[row]; s < vec_offsets[row + 1]; ++s) {
-                        const uint32_t e = vec_slots[s] / k;
-                        if (!in_range(e)) continue;
-                        const int64_t hix = std::lower_bound(tmp.begin(), tmp.end(), e) - tmp.begin();
-                        if (prev >= 0) edges.push_back({static_cast<uint32_t>(hix), static_cast<uint32_t>(prev)});
-                        prev = hix;
-                    }
-                }
-                std::sort(edges.begin(), edges.end());  // by target: a topological order
-                for (const auto& ed : edges) level[ed.first] = std::max(level[ed.first], level[ed.second] + 1);
-            }
-            std::vector<std::pair<int, uint32_t>> order(nh);
-            for (int64_t h = 0; h < nh; ++h) order[h] = {level[h], tmp[h]};
-            std::sort(order.begin(), order.end());
-            // Within a chunk the element order is free (records carry the
-            // element's position, and every row folds in ascending element order
-            // whatever the positions): order each chunk by the element's first
-            // node so the lanes of a warp gather nearby node-table entries
-            // (fewer shared-memory bank conflicts; TGK_CHUNK_SORT=0 disables).
-            static const bool chunk_sort = !(getenv("TGK_CHUNK_SORT") && atoi(getenv("TGK_CHUNK_SORT")) == 0);
-            if (chunk_sort)
-                for (int64_t c0 = 0; c0 < nh; c0 += C) {
-                    const int64_t c1 = std::min<int64_t>(nh, c0 + C);
-                    std::sort(order.begin() + c0, order.begin() + c1, [&](const auto& x, const auto& y) {
-                        const int32_t nx = conn[int64_t(x.second) * k], ny = conn[int64_t(y.second) * k];
-                        return nx != ny ? nx < ny : x.second < y.second;
-                    });
-                }
-            o.halo.resize(nh);
+            o.halo = order_block_halo(k, conn, P.rows.data() + rs, re - rs, vec_offsets, vec_slots, elem_lo, elem_hi, C);
+            const int64_t nh = static_cast<int64_t>(o.halo.size());
             std::vector<std::pair<uint32_t, uint32_t>> where(nh);  // (element, position)
-            for (int64_t h = 0; h < nh; ++h) {
-                o.halo[h] = order[h].second;
-                where[h] = {order[h].second, static_cast<uint32_t>(h)};
-            }
+            for (int64_t h = 0; h < nh; ++h) where[h] = {o.halo[h], static_cast<uint32_t>(h)};
             std::sort(where.begin(), where.end());
             const int64_t nch = (nh + C - 1) / C;
             // records grouped chunk-major, then row, ascending element within a row

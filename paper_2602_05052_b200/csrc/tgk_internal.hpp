@@ -101,6 +101,11 @@ TGK_HD inline uint32_t pack_rec(int hl, int a, const int* pos, int k) {
     return r | (uint32_t(pos[a]) << 25);
 }
 
+std::vector<uint32_t> order_block_halo(int k, const int32_t* conn, const uint32_t* rows, int64_t nrows,
+                                       const uint32_t* vec_offsets, const uint32_t* vec_slots, int64_t elem_lo,
+                                       int64_t elem_hi, int C);
+std::vector<uint32_t> morton_order(int kind, int64_t N, const double* nodes, int64_t row_lo, int64_t row_hi);
+
 // Builds the plan on the host from the scalar routing (row_ptr, vec segment
 // map = node->incidence CSR in ascending slot order, slot_of) for the owned
 // row range [row_lo, row_hi) with R rows per block.
@@ -169,6 +174,51 @@ struct GroupPlanDev {
 int build_group_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn, int G,
                      GroupPlanHost& P);
 
+// Scalar entry plan (plan_entries.cpp build_scalar_entry_plan, fused.cu
+// k_fused_entries): blocks of up to T threads; every owned row gets
+// ceil((len + 1) / 8) threads of 8 slots each (slot = one CSR entry of the row
+// or its load F; the diagonal and F take slot 0 of the row's first two
+// threads).  Per chunk of C halo elements one data segment: per thread the 8
+// cumulative item counts (u8), per warp the number of item steps, then the
+// items of each warp [step][lane] — item = h | t << 8 | ab << 12 with h the
+// element's chunk position, t the index of the value in the element's SoA
+// value rows (K_e[a][b] unique (a <= b) rows, then F_e[a] rows) and ab = a k
+// + b the row of M_e[a][b].  Items of a slot are in ascending element id.
+constexpr int kSlotsPerThread = 8;
+struct ScalarEntryPlanHost {
+    int T = 256, C = 256;
+    int64_t n_blocks = 0;
+    int max_bnodes = 0, max_chunk_u16 = 0, max_chunks = 0;
+    int64_t n_halo = 0, data_bytes = 0;
+    std::vector<int64_t> halo_off, bnode_off, chunk_off, chunk_data_off;
+    std::vector<uint32_t> halo, bnodes;
+    std::vector<uint16_t> halo_lconn;  // 4 per halo element
+    std::vector<int64_t> t_rp;         // per block x T: CSR offset of the thread's row (-1: idle)
+    std::vector<uint32_t> t_row;       // per block x T: row (node) id
+    std::vector<uint64_t> t_pos;       // per block x T: 8 slot codes (CSR position, 0xFE load, 0xFF none)
+    std::vector<uint16_t> data;        // chunk segments, 16-byte multiples
+};
+
+struct ScalarEntryPlanDev {
+    int T = 0, C = 0;
+    int64_t n_blocks = 0;
+    int max_bnodes = 0, max_chunk_u16 = 0, max_chunks = 0;
+    int64_t n_halo = 0, bytes = 0;
+    int64_t row_lo = -1, row_hi = -1, elem_lo = -1, elem_hi = -1;  // the ranges it was built for
+    const int64_t *halo_off = nullptr, *bnode_off = nullptr, *chunk_off = nullptr, *chunk_data_off = nullptr,
+                  *t_rp = nullptr;
+    const uint32_t *halo = nullptr, *bnodes = nullptr, *t_row = nullptr;
+    const uint16_t *halo_lconn = nullptr, *data = nullptr;
+    const uint64_t* t_pos = nullptr;
+    void* blob = nullptr;
+    void release();
+};
+
+int build_scalar_entry_plan(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
+                            const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
+                            int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int T, int C,
+                            int R_max, ScalarEntryPlanHost& P);
+
 int build_entry_plan(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
                      const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
                      int64_t row_lo, int64_t row_hi, int R, EntryPlanHost& P);
@@ -204,6 +254,7 @@ struct tgk_routing {
     tgk::PlanDev plan[tgk::kPlanSlots];
     tgk::EntryPlanDev entry_plan;    // batched kernel plan (built on first batched call)
     tgk::GroupPlanDev group_plan;    // adjoint gather plan (built on first adjoint call)
+    tgk::ScalarEntryPlanDev se_plan; // scalar entry-owned fused kernel plan
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
     int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
     double* scr[6] = {};             // cached device scratch (materialised elasticity path)
@@ -219,4 +270,5 @@ namespace tgk {
 int ensure_plan(tgk_routing* r, int R, const PlanDev** out, int C = 0);  // C = 0: chunk size R
 int ensure_entry_plan(tgk_routing* r, int R, const EntryPlanDev** out);
 int ensure_group_plan(tgk_routing* r, int G, const GroupPlanDev** out);
+int ensure_scalar_entry_plan(tgk_routing* r, const ScalarEntryPlanDev** out);
 }
