@@ -225,6 +225,37 @@ REF_SAMPLE = {"c2": (50, 50, 50), "c2a": (50, 50, 50), "c1": (256, 256), "c3": (
               "c5": (64, 64, 64)}
 
 
+def c1_graph_time(ctx, launch, steps):
+    """C1: the same assembly captured `steps` times into one CUDA
+    graph on a side stream and replayed; ms per assembly from CUDA events.  The
+    launch-overhead-free time of a small mesh (reported in config, not as value)."""
+    torch = ctx.torch
+    try:
+        gs = torch.cuda.Stream()
+        sp = C.c_void_p(gs.cuda_stream)
+        with torch.cuda.stream(gs):
+            for _ in range(3):
+                launch(sp)
+        gs.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            for _ in range(steps):
+                launch(sp)
+        g.replay()
+        gs.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        with torch.cuda.stream(gs):
+            e0.record(gs)
+            for _ in range(reps):
+                g.replay()
+            e1.record(gs)
+        gs.synchronize()
+        return {"ms_per_step": e0.elapsed_time(e1) / (reps * steps), "assemblies_per_graph": steps}
+    except Exception as exc:  # capture unsupported here: say why, keep the bench line
+        return {"error": str(exc)[:200]}
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU implementation (compiled from its sources)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -409,6 +440,10 @@ def run_scalar(args, ctx, N):
         torch.cuda.synchronize()
     ms_kernel = ev_k0.elapsed_time(ev_k1) / args.steps
     ms_per_step = ms / args.steps
+    graph = None
+    if args.workload == "c1" and not f32 and world == 1:
+        graph = c1_graph_time(ctx, lambda sp: N.check(L.tgk_assemble_async_d(
+            C.byref(p), mesh._h, routing._h, ptr(K), ptr(F), ptr(M), ptr(bad), sp)), args.steps)
     if kind == "tet4":
         E_own = 6 * s.div[0] * s.div[1] * s.div[2]
         own_rows = (s.own_lo, s.own_hi)
@@ -476,6 +511,8 @@ def run_scalar(args, ctx, N):
                              "recompute_factor": nh.value / max(1, elems.shape[0]), "records": nrec.value,
                              "bytes": pbytes.value},
               "setup_s": setup_s, "kernel_ms": ms_kernel}
+    if graph is not None:
+        config["cuda_graph"] = graph
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
                 gpu_launches=launches, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
