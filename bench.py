@@ -393,7 +393,7 @@ def run_scalar(args, ctx, N):
         if s.mode == "exchange":
             N.check(L.tgk_routing_set_element_range(routing._h, s.elem_lo, s.elem_hi))
     nb, nh, nrec, pbytes = (C.c_int64() for _ in range(4))
-    R_plan = 64 if kw.get("with_mass") else 128  # rows per block of the fused kernel variant (fused.cu)
+    R_plan = 128  # rows per block of the fused kernel (fused.cu fused_rows_per_block)
     N.check(L.tgk_routing_plan_stats(routing._h, R_plan, C.byref(nb), C.byref(nh), C.byref(nrec), C.byref(pbytes)))
     setup_s = time.time() - t0
     with_mass = kw.get("with_mass", False)

@@ -92,10 +92,16 @@ __host__ __device__ constexpr int rot(int a, int b) { return b == a ? 0 : (b < a
 template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, typename T = double>
 struct FusedCfg {
     static constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q;
-    // local tensors in shared memory: rotated rows of 4 values (16-byte aligned)
+    // local tensors in shared memory: rotated rows of 4 values (16-byte aligned).
+    // MDET: the unit mass M_e depends on the element only through det, so
+    // phase A stores det and phase B forms each record's M row from it with
+    // the reference's expression (a smaller block working set: more resident
+    // blocks for C2)
+    static constexpr bool MDET = HAS_M && KTYPE == 0;
+    static constexpr int KIND_ = KIND, DEG_ = DEG;
     static constexpr int offK = 0;
     static constexpr int offM = 4 * k;
-    static constexpr int offF = offM + (HAS_M ? 4 * k : 0);
+    static constexpr int offF = offM + (HAS_M ? (MDET ? 2 : 4 * k) : 0);
     static constexpr int raw = offF + (HAS_F ? 4 : 0);
     // stride = (16-byte vector) x odd: conflict-free 128-bit accesses across lanes
     static constexpr int VEC = 16 / int(sizeof(T));
@@ -138,6 +144,38 @@ __device__ __forceinline__ void load4(const float* src, float (&v)[4]) {
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
 }
 
+// Row a of the unit-coefficient local mass from det, rotated like the record
+// ([M_aa, M_ab for b != a ascending]): local_mass with ones (physics.cpp:70-71,
+// batch.cpp:259-265), M_e[a][b] = sum_q ((w_q det) N_a(q)) N_b(q) in the
+// reference's order — identical to phase A's expression (element_values).
+template <int KIND, int DEG, typename T>
+__device__ __forceinline__ void mass_row(T det, int a, T (&mv)[4]) {
+    using Rl = Rule<KIND, DEG>;
+    constexpr int k = P1<KIND>::k, Q = Rl::Q;
+    T na[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        T v = T(basis<KIND, DEG>(q, 0));
+#pragma unroll
+        for (int c = 1; c < k; ++c) v = a == c ? T(basis<KIND, DEG>(q, c)) : v;
+        na[q] = v;
+    }
+#pragma unroll
+    for (int j = 0; j < k; ++j) {
+        const int b = j == 0 ? a : (j - 1 < a ? j - 1 : j);
+        T v = T(0);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            T nb = T(basis<KIND, DEG>(q, 0));
+#pragma unroll
+            for (int c = 1; c < k; ++c) nb = b == c ? T(basis<KIND, DEG>(q, c)) : nb;
+            const T term = T(Rl::w(q)) * det * na[q] * nb;
+            v = q == 0 ? term : v + term;
+        }
+        mv[j] = v;
+    }
+}
+
 // One record's rotated local tensor row (K, M) and F_e[a] from shared memory.
 template <typename T, bool HAS_M, bool HAS_F>
 struct RowVals {
@@ -151,10 +189,15 @@ struct RowVals {
         const T* src = ke + hl * C::stride + a * 4;
         load4(src + C::offK, kv);
         if constexpr (HAS_M) {
-            T m4[4];
-            load4(src + C::offM, m4);
+            if constexpr (C::MDET) {
+                const T det = ke[hl * C::stride + C::offM];
+                mass_row<C::KIND_, C::DEG_, T>(det, a, mv);
+            } else {
+                T m4[4];
+                load4(src + C::offM, m4);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) mv[i] = m4[i];
+                for (int i = 0; i < 4; ++i) mv[i] = m4[i];
+            }
         }
         if constexpr (HAS_F) f = ke[hl * C::stride + C::offF + a];
     }
@@ -201,7 +244,13 @@ struct RotSink {
         out[C::offK + b * 4 + rot(b, a)] = v;
     }
     __device__ __forceinline__ void K(int a, int b, T v) { out[C::offK + a * 4 + rot(a, b)] = v; }
-    __device__ __forceinline__ void M(int a, int b, T v) { out[C::offM + a * 4 + rot(a, b)] = v; }
+    static constexpr bool kMDet = C::MDET;
+    __device__ __forceinline__ void M(int a, int b, T v) {
+        if constexpr (!C::MDET) out[C::offM + a * 4 + rot(a, b)] = v;
+    }
+    __device__ __forceinline__ void Det(T v) {
+        if constexpr (C::MDET) out[C::offM] = v;
+    }
     __device__ __forceinline__ void F(int a, T v) { out[C::offF + a] = v; }
     __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -274,7 +323,8 @@ __device__ __forceinline__ void element_values(const FieldDev& coef, const Field
                 sink.K(a, b, v);
             }
     }
-    if constexpr (HAS_M) {
+    if constexpr (Sink::kMDet) sink.Det(det);
+    if constexpr (HAS_M && !Sink::kMDet) {
         // with_mass: local_mass with ones (physics.cpp:70-71); w*det*1.0 == w*det
 #pragma unroll
         for (int a = 0; a < k; ++a)
@@ -541,6 +591,8 @@ struct SeSink {
     int h;
     __device__ __forceinline__ void Ksym(int, int, int t, double v) { kv[t * kSeC + h] = v; }
     __device__ __forceinline__ void K(int, int, double) {}  // coefficient mass: not dispatched here
+    static constexpr bool kMDet = false;
+    __device__ __forceinline__ void Det(double) {}
     __device__ __forceinline__ void M(int a, int b, double v) {
         if constexpr (HAS_M) kvm[(a * k + b) * kSeC + h] = v;
     }
@@ -736,10 +788,11 @@ int fused_rows_per_block(const tgk_problem* pr) {
         const int r = atoi(env);
         return r == 64 || r == 128 ? r : TGK_R_BIG;
     }
-    // measured on B200 (profiles/r01_fused_experiments.txt): K+F best at 128
-    // rows per block; with the unit mass the larger per-element working set
-    // fits more resident blocks at 64 rows
-    return pr->with_mass ? 64 : 128;
+    // measured on B200 (profiles/r01_fused_experiments.txt): 128 rows per block
+    // for K+F and, since the unit mass is formed from det in the fold (MDET),
+    // for K+M+F as well
+    (void)pr;
+    return 128;
 }
 
 // Fused scalar assembly core: ktype 0 (diffusion stiffness) / 1 (coefficient
@@ -747,6 +800,7 @@ int fused_rows_per_block(const tgk_problem* pr) {
 static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int degree, bool has_m, bool has_f,
                       FieldDev coef, FieldDev src, void* K, void* F, void* M, cudaStream_t st,
                       unsigned long long* d_bad, bool f32 = false) {
+    if (f32 && R != 64) R = 128;  // the fp32 instances exist for 64 and 128 rows per block
     const PlanDev* pl = nullptr;
     TGK_TRY(ensure_plan(r, R, &pl));
     FusedArgs a{};
