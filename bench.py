@@ -393,7 +393,9 @@ def run_scalar(args, ctx, N):
         if s.mode == "exchange":
             N.check(L.tgk_routing_set_element_range(routing._h, s.elem_lo, s.elem_hi))
     nb, nh, nrec, pbytes = (C.c_int64() for _ in range(4))
-    R_plan = 128  # rows per block of the fused kernel (fused.cu fused_rows_per_block)
+    # rows per block of the fused kernel (fused.cu fused_rows_per_block: 64 below 4 x 128 x #SMs rows)
+    n_rows_own = (s.calc_hi - s.own_lo) if (s is not None and world > 1) else nodes.shape[0]
+    R_plan = 64 if n_rows_own < 128 * 4 * torch.cuda.get_device_properties(ctx.dev).multi_processor_count else 128
     N.check(L.tgk_routing_plan_stats(routing._h, R_plan, C.byref(nb), C.byref(nh), C.byref(nrec), C.byref(pbytes)))
     setup_s = time.time() - t0
     with_mass = kw.get("with_mass", False)

@@ -783,16 +783,20 @@ int dispatch_flags(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, in
 
 }  // namespace
 
-int fused_rows_per_block(const tgk_problem* pr) {
+int fused_rows_per_block(const tgk_problem* pr, int64_t n_rows) {
     if (const char* env = getenv("TGK_FUSED_R")) {
         const int r = atoi(env);
         return r == 64 || r == 128 ? r : TGK_R_BIG;
     }
     // measured on B200 (profiles/r01_fused_experiments.txt): 128 rows per block
     // for K+F and, since the unit mass is formed from det in the fold (MDET),
-    // for K+M+F as well
+    // for K+M+F as well; 64 when 128-row blocks would not fill the GPU once
+    // (C1: 16.0 -> 13.4 us)
     (void)pr;
-    return 128;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return n_rows < int64_t(128) * 4 * sms ? 64 : 128;
 }
 
 // Fused scalar assembly core: ktype 0 (diffusion stiffness) / 1 (coefficient
@@ -909,7 +913,8 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
     const FieldDev coef{pr->diffusion.type, pr->diffusion.value, pr->diffusion.data};
     const FieldDev src = has_f ? FieldDev{pr->source[0].type, pr->source[0].value, pr->source[0].data}
                                : FieldDev{TGK_FIELD_CONSTANT, 0.0, nullptr};
-    return fused_core(m, r, fused_rows_per_block(pr), is_mass ? 1 : 0, degree, pr->with_mass != 0, has_f, coef, src,
+    const int64_t n_rows = r->own_hi < 0 ? r->N : r->own_hi - r->own_lo;
+    return fused_core(m, r, fused_rows_per_block(pr, n_rows), is_mass ? 1 : 0, degree, pr->with_mass != 0, has_f, coef, src,
                       K, F, M, st, d_bad);
 }
 
@@ -924,7 +929,8 @@ int fused_scalar_assemble_f32(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
     const FieldDev coef{pr->diffusion.type, pr->diffusion.value, pr->diffusion.data};
     const FieldDev src = has_f ? FieldDev{pr->source[0].type, pr->source[0].value, pr->source[0].data}
                                : FieldDev{TGK_FIELD_CONSTANT, 0.0, nullptr};
-    return fused_core(m, r, fused_rows_per_block(pr), is_mass ? 1 : 0, high ? 2 : 1, pr->with_mass != 0, has_f,
+    const int64_t n_rows = r->own_hi < 0 ? r->N : r->own_hi - r->own_lo;
+    return fused_core(m, r, fused_rows_per_block(pr, n_rows), is_mass ? 1 : 0, high ? 2 : 1, pr->with_mass != 0, has_f,
                       coef, src, K, F, M, st, d_bad, true);
 }
 
