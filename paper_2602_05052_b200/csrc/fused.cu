@@ -89,7 +89,7 @@ __host__ __device__ constexpr int rot(int a, int b) { return b == a ? 0 : (b < a
 
 // KTYPE 0: diffusion stiffness, 1: coefficient mass (ProblemKind::Mass);
 // T: double (exact mode) or float (fp32 mode)
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, typename T = double>
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, typename T = double, bool FCONST = false>
 struct FusedCfg {
     static constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q;
     // local tensors in shared memory: rotated rows of 4 values (16-byte aligned).
@@ -98,11 +98,14 @@ struct FusedCfg {
     // the reference's expression (a smaller block working set: more resident
     // blocks for C2)
     static constexpr bool MDET = HAS_M && KTYPE == 0;
+    // FDET: with MDET and a constant source the load F_e[a] is formed from det
+    // in the fold as well (same expression as phase A's local_load)
+    static constexpr bool FDET = FCONST && MDET && HAS_F;
     static constexpr int KIND_ = KIND, DEG_ = DEG;
     static constexpr int offK = 0;
     static constexpr int offM = 4 * k;
     static constexpr int offF = offM + (HAS_M ? (MDET ? 2 : 4 * k) : 0);
-    static constexpr int raw = offF + (HAS_F ? 4 : 0);
+    static constexpr int raw = offF + (HAS_F && !FDET ? 4 : 0);
     // stride = (16-byte vector) x odd: conflict-free 128-bit accesses across lanes
     static constexpr int VEC = 16 / int(sizeof(T));
     static constexpr int stride = ((raw + VEC - 1) / VEC) % 2 == 1 ? (raw + VEC - 1) / VEC * VEC
@@ -149,10 +152,9 @@ __device__ __forceinline__ void load4(const float* src, float (&v)[4]) {
 // batch.cpp:259-265), M_e[a][b] = sum_q ((w_q det) N_a(q)) N_b(q) in the
 // reference's order — identical to phase A's expression (element_values).
 template <int KIND, int DEG, typename T>
-__device__ __forceinline__ void mass_row(T det, int a, T (&mv)[4]) {
+__device__ __forceinline__ void mass_row(T det, int a, T (&mv)[4], T (&na)[Rule<KIND, DEG>::Q]) {
     using Rl = Rule<KIND, DEG>;
     constexpr int k = P1<KIND>::k, Q = Rl::Q;
-    T na[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         T v = T(basis<KIND, DEG>(q, 0));
@@ -183,7 +185,7 @@ struct RowVals {
     T mv[HAS_M ? 4 : 1];
     T f;
     template <class C>
-    __device__ __forceinline__ void load(const T* ke, uint32_t rec) {
+    __device__ __forceinline__ void load(const T* ke, uint32_t rec, T fval) {
         const int hl = rec & 0xff;
         const int a = (rec >> 8) & 3;
         const T* src = ke + hl * C::stride + a * 4;
@@ -191,7 +193,18 @@ struct RowVals {
         if constexpr (HAS_M) {
             if constexpr (C::MDET) {
                 const T det = ke[hl * C::stride + C::offM];
-                mass_row<C::KIND_, C::DEG_, T>(det, a, mv);
+                T na[Rule<C::KIND_, C::DEG_>::Q];
+                mass_row<C::KIND_, C::DEG_, T>(det, a, mv, na);
+                if constexpr (C::FDET) {  // local_load with a constant source (batch.cpp:280-286)
+                    using Rl = Rule<C::KIND_, C::DEG_>;
+                    T v = T(0);
+#pragma unroll
+                    for (int q = 0; q < Rl::Q; ++q) {
+                        const T term = (T(Rl::w(q)) * det * fval) * na[q];
+                        v = q == 0 ? term : v + term;
+                    }
+                    f = v;
+                }
             } else {
                 T m4[4];
                 load4(src + C::offM, m4);
@@ -199,7 +212,7 @@ struct RowVals {
                 for (int i = 0; i < 4; ++i) mv[i] = m4[i];
             }
         }
-        if constexpr (HAS_F) f = ke[hl * C::stride + C::offF + a];
+        if constexpr (HAS_F && !C::FDET) f = ke[hl * C::stride + C::offF + a];
     }
 };
 
@@ -251,7 +264,9 @@ struct RotSink {
     __device__ __forceinline__ void Det(T v) {
         if constexpr (C::MDET) out[C::offM] = v;
     }
-    __device__ __forceinline__ void F(int a, T v) { out[C::offF + a] = v; }
+    __device__ __forceinline__ void F(int a, T v) {
+        if constexpr (!C::FDET) out[C::offF + a] = v;
+    }
     __device__ __forceinline__ void zero() {
 #pragma unroll
         for (int i = 0; i < C::raw; ++i) out[i] = T(0);
@@ -352,9 +367,9 @@ __device__ __forceinline__ void element_values(const FieldDev& coef, const Field
     }
 }
 
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV, typename T>
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV, typename T, bool FCONST = false>
 __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
-    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T>;
+    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T, FCONST>;
     constexpr int k = C::k, d = C::d, NV = C::NV;
     constexpr int ROS = R + 8;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -485,11 +500,11 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
             if (j < j1) {
                 uint32_t rec = rs[j];
                 RowVals<T, HAS_M, HAS_F> v;
-                v.template load<C>(ke, rec);
+                v.template load<C>(ke, rec, T(p.src.value));
                 for (; j < j1; ++j) {
                     const uint32_t rec_n = j + 1 < j1 ? rs[j + 1] : rec;
                     RowVals<T, HAS_M, HAS_F> vn;
-                    vn.template load<C>(ke, rec_n);
+                    vn.template load<C>(ke, rec_n, T(p.src.value));
                     // the k-1 positions of one record are distinct columns: load all,
                     // add, store all (no false read-after-write serialisation)
                     int pos[k - 1];
@@ -543,10 +558,10 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
     }
 }
 
-template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV, typename T>
+template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV, typename T, bool FCONST = false>
 int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
-    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T>;
-    auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV, T>;
+    using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T, FCONST>;
+    auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV, T, FCONST>;
     const size_t smem = C::smem_bytes(a.lmax, a.max_recs, a.max_bnodes, a.ntcols);
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (n_blocks > 0) kern<<<static_cast<unsigned>(n_blocks), R, smem, st>>>(a);
@@ -756,7 +771,9 @@ template <int KIND, int DEG, int R, bool FDIV, typename T>
 int dispatch_r(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, cudaStream_t st) {
     if (ktype == 1) return f ? launch_fused<KIND, DEG, 1, false, true, R, FDIV, T>(a, nb, st)
                              : launch_fused<KIND, DEG, 1, false, false, R, FDIV, T>(a, nb, st);
-    if (m && f) return launch_fused<KIND, DEG, 0, true, true, R, FDIV, T>(a, nb, st);
+    if (m && f)
+        return a.src.type == TGK_FIELD_CONSTANT ? launch_fused<KIND, DEG, 0, true, true, R, FDIV, T, true>(a, nb, st)
+                                                : launch_fused<KIND, DEG, 0, true, true, R, FDIV, T>(a, nb, st);
     if (m) return launch_fused<KIND, DEG, 0, true, false, R, FDIV, T>(a, nb, st);
     if (f) return launch_fused<KIND, DEG, 0, false, true, R, FDIV, T>(a, nb, st);
     return launch_fused<KIND, DEG, 0, false, false, R, FDIV, T>(a, nb, st);
