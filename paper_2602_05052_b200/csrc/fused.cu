@@ -100,11 +100,12 @@ struct FusedCfg {
     static constexpr bool MDET = HAS_M && KTYPE == 0;
     // FDET: with MDET and a constant source the load F_e[a] is formed from det
     // in the fold as well (same expression as phase A's local_load)
-    static constexpr bool FDET = FCONST && MDET && HAS_F;
+    static constexpr bool FDET = FCONST && KTYPE == 0 && HAS_F;
+    static constexpr bool DETSLOT = MDET || FDET;  // det stored at offM
     static constexpr int KIND_ = KIND, DEG_ = DEG;
     static constexpr int offK = 0;
     static constexpr int offM = 4 * k;
-    static constexpr int offF = offM + (HAS_M ? (MDET ? 2 : 4 * k) : 0);
+    static constexpr int offF = offM + (DETSLOT ? 2 : (HAS_M ? 4 * k : 0));
     static constexpr int raw = offF + (HAS_F && !FDET ? 4 : 0);
     // stride = (16-byte vector) x odd: conflict-free 128-bit accesses across lanes
     static constexpr int VEC = 16 / int(sizeof(T));
@@ -151,6 +152,19 @@ __device__ __forceinline__ void load4(const float* src, float (&v)[4]) {
 // ([M_aa, M_ab for b != a ascending]): local_mass with ones (physics.cpp:70-71,
 // batch.cpp:259-265), M_e[a][b] = sum_q ((w_q det) N_a(q)) N_b(q) in the
 // reference's order — identical to phase A's expression (element_values).
+// N_a(q) for a runtime local node a (selects, no divergence).
+template <int KIND, int DEG, typename T>
+__device__ __forceinline__ void basis_row(int a, T (&na)[Rule<KIND, DEG>::Q]) {
+    constexpr int k = P1<KIND>::k, Q = Rule<KIND, DEG>::Q;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        T v = T(basis<KIND, DEG>(q, 0));
+#pragma unroll
+        for (int c = 1; c < k; ++c) v = a == c ? T(basis<KIND, DEG>(q, c)) : v;
+        na[q] = v;
+    }
+}
+
 template <int KIND, int DEG, typename T>
 __device__ __forceinline__ void mass_row(T det, int a, T (&mv)[4], T (&na)[Rule<KIND, DEG>::Q]) {
     using Rl = Rule<KIND, DEG>;
@@ -190,27 +204,30 @@ struct RowVals {
         const int a = (rec >> 8) & 3;
         const T* src = ke + hl * C::stride + a * 4;
         load4(src + C::offK, kv);
-        if constexpr (HAS_M) {
+        if constexpr (C::DETSLOT) {
+            using Rl = Rule<C::KIND_, C::DEG_>;
+            const T det = ke[hl * C::stride + C::offM];
+            T na[Rl::Q];
             if constexpr (C::MDET) {
-                const T det = ke[hl * C::stride + C::offM];
-                T na[Rule<C::KIND_, C::DEG_>::Q];
                 mass_row<C::KIND_, C::DEG_, T>(det, a, mv, na);
-                if constexpr (C::FDET) {  // local_load with a constant source (batch.cpp:280-286)
-                    using Rl = Rule<C::KIND_, C::DEG_>;
-                    T v = T(0);
-#pragma unroll
-                    for (int q = 0; q < Rl::Q; ++q) {
-                        const T term = (T(Rl::w(q)) * det * fval) * na[q];
-                        v = q == 0 ? term : v + term;
-                    }
-                    f = v;
-                }
             } else {
-                T m4[4];
-                load4(src + C::offM, m4);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) mv[i] = m4[i];
+                basis_row<C::KIND_, C::DEG_, T>(a, na);
             }
+            if constexpr (C::FDET) {  // local_load with a constant source (batch.cpp:280-286)
+                T v = T(0);
+#pragma unroll
+                for (int q = 0; q < Rl::Q; ++q) {
+                    const T term = (T(Rl::w(q)) * det * fval) * na[q];
+                    v = q == 0 ? term : v + term;
+                }
+                f = v;
+            }
+        }
+        if constexpr (HAS_M && !C::MDET) {
+            T m4[4];
+            load4(src + C::offM, m4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) mv[i] = m4[i];
         }
         if constexpr (HAS_F && !C::FDET) f = ke[hl * C::stride + C::offF + a];
     }
@@ -257,12 +274,13 @@ struct RotSink {
         out[C::offK + b * 4 + rot(b, a)] = v;
     }
     __device__ __forceinline__ void K(int a, int b, T v) { out[C::offK + a * 4 + rot(a, b)] = v; }
-    static constexpr bool kMDet = C::MDET;
+    static constexpr bool kMDet = C::MDET;   // M_e formed from det in the fold: skip it here
+    static constexpr bool kDet = C::DETSLOT;  // store det
     __device__ __forceinline__ void M(int a, int b, T v) {
         if constexpr (!C::MDET) out[C::offM + a * 4 + rot(a, b)] = v;
     }
     __device__ __forceinline__ void Det(T v) {
-        if constexpr (C::MDET) out[C::offM] = v;
+        if constexpr (C::DETSLOT) out[C::offM] = v;
     }
     __device__ __forceinline__ void F(int a, T v) {
         if constexpr (!C::FDET) out[C::offF + a] = v;
@@ -338,7 +356,7 @@ __device__ __forceinline__ void element_values(const FieldDev& coef, const Field
                 sink.K(a, b, v);
             }
     }
-    if constexpr (Sink::kMDet) sink.Det(det);
+    if constexpr (Sink::kDet) sink.Det(det);
     if constexpr (HAS_M && !Sink::kMDet) {
         // with_mass: local_mass with ones (physics.cpp:70-71); w*det*1.0 == w*det
 #pragma unroll
@@ -606,7 +624,7 @@ struct SeSink {
     int h;
     __device__ __forceinline__ void Ksym(int, int, int t, double v) { kv[t * kSeC + h] = v; }
     __device__ __forceinline__ void K(int, int, double) {}  // coefficient mass: not dispatched here
-    static constexpr bool kMDet = false;
+    static constexpr bool kMDet = false, kDet = false;
     __device__ __forceinline__ void Det(double) {}
     __device__ __forceinline__ void M(int a, int b, double v) {
         if constexpr (HAS_M) kvm[(a * k + b) * kSeC + h] = v;
@@ -775,7 +793,9 @@ int dispatch_r(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, cudaSt
         return a.src.type == TGK_FIELD_CONSTANT ? launch_fused<KIND, DEG, 0, true, true, R, FDIV, T, true>(a, nb, st)
                                                 : launch_fused<KIND, DEG, 0, true, true, R, FDIV, T>(a, nb, st);
     if (m) return launch_fused<KIND, DEG, 0, true, false, R, FDIV, T>(a, nb, st);
-    if (f) return launch_fused<KIND, DEG, 0, false, true, R, FDIV, T>(a, nb, st);
+    if (f)
+        return a.src.type == TGK_FIELD_CONSTANT ? launch_fused<KIND, DEG, 0, false, true, R, FDIV, T, true>(a, nb, st)
+                                                : launch_fused<KIND, DEG, 0, false, true, R, FDIV, T>(a, nb, st);
     return launch_fused<KIND, DEG, 0, false, false, R, FDIV, T>(a, nb, st);
 }
 
