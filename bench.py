@@ -645,7 +645,7 @@ def run_elasticity(args, ctx, N):
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                           "frac": achieved / peak, "traffic": ncu_traffic("c3") if ctx.world == 1 else None,
                           "alg_bytes": ab, "compulsory_bytes": comp, "peak_source": peak_src,
-                          "kernel": "k_fused_elast (one launch per step)"})
+                          "kernel": "k_fused_elast2 (one launch per step)"})
 
 
 def run_batched(args, ctx, N):

@@ -142,8 +142,8 @@ int build_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_
     // R rows per block, chunks of C halo elements (C threads; R = C x rows per thread)
     if (R != 16 && R != 32 && R != 64 && R != 128 && R != 256)
         return set_error(TGK_ERR_INPUT, "fused plan: R must be 16, 32, 64, 128 or 256");
-    if (C != 32 && C != 64 && C != 128 && C != 256)
-        return set_error(TGK_ERR_INPUT, "fused plan: chunk size must be 32, 64, 128 or 256");
+    if (C < 16 || C > 256 || C % 16)
+        return set_error(TGK_ERR_INPUT, "fused plan: chunk size must be a multiple of 16 in [16, 256]");
     P.R = R;
     P.C = C;
     // --- 1. Morton order of the owned nodes
