@@ -581,7 +581,13 @@ int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
     using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T, FCONST>;
     auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV, T, FCONST>;
     const size_t smem = C::smem_bytes(a.lmax, a.max_recs, a.max_bnodes, a.ntcols);
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // raise the instance's dynamic shared-memory limit only when it grows (small
+    // meshes are launch-overhead bound; one process drives one device)
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+    }
     if (n_blocks > 0) kern<<<static_cast<unsigned>(n_blocks), R, smem, st>>>(a);
     KERNEL_CHECK("fused_scalar");
     return TGK_OK;
@@ -830,9 +836,12 @@ int fused_rows_per_block(const tgk_problem* pr, int64_t n_rows) {
     // for K+M+F as well; 64 when 128-row blocks would not fill the GPU once
     // (C1: 16.0 -> 13.4 us)
     (void)pr;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static const int sms = [] {
+        int dev = 0, n = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
+    }();
     return n_rows < int64_t(128) * 4 * sms ? 64 : 128;
 }
 
