@@ -321,9 +321,9 @@ int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, con
     if (r->components != 1) return set_error(TGK_ERR_INPUT, "adjoint_gather: scalar routing required");
     TGK_TRY(ensure_device());
     cudaStream_t st = as_stream(stream);
-    DevBuf<unsigned long long> bad;
-    TGK_TRY(bad.alloc(1));
-    CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    unsigned long long* badp = nullptr;  // the routing's persistent status words
+    TGK_TRY(routing_flags(const_cast<tgk_routing*>(r), &badp));
+    CUDA_TRY(cudaMemsetAsync(badp, 0xff, sizeof(unsigned long long), st));
     if (m->kind != TGK_TET4 && m->kind != TGK_TRI3) return set_error(TGK_ERR_INPUT, "adjoint_gather: TRI3/TET4 only");
     if (degree != 1 && degree != 2) return set_error(TGK_ERR_INPUT, "adjoint_gather: degree must be 1 or 2");
     if (B <= 0) return TGK_OK;
@@ -344,7 +344,7 @@ int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, con
             a.U = U;
             a.out = out;
             a.pl = *pl;
-            a.bad = bad.p;
+            a.bad = badp;
             const int np = npt <= 1 ? 1 : npt <= 2 ? 2 : 4;
             if (m->kind == TGK_TET4)
                 TGK_TRY((degree == 1 ? launch_adjoint_groups<TGK_TET4, 1>(a, np, st)
@@ -352,20 +352,20 @@ int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, con
             else
                 TGK_TRY((degree == 1 ? launch_adjoint_groups<TGK_TRI3, 1>(a, np, st)
                                      : launch_adjoint_groups<TGK_TRI3, 2>(a, np, st)));
-            return check_bad(bad.p, st);
+            return check_bad(badp, st);
         }
     }
     constexpr int FPB = 8;
     const dim3 grid(grid_for(m->E, 128), static_cast<unsigned>((B + FPB - 1) / FPB));
     if (m->kind == TGK_TET4) {
-        if (degree == 1) k_adjoint_gather<TGK_TET4, 1, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
-        else k_adjoint_gather<TGK_TET4, 2, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
+        if (degree == 1) k_adjoint_gather<TGK_TET4, 1, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, badp);
+        else k_adjoint_gather<TGK_TET4, 2, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, badp);
     } else {
-        if (degree == 1) k_adjoint_gather<TGK_TRI3, 1, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
-        else k_adjoint_gather<TGK_TRI3, 2, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, bad.p);
+        if (degree == 1) k_adjoint_gather<TGK_TRI3, 1, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, badp);
+        else k_adjoint_gather<TGK_TRI3, 2, FPB><<<grid, 128, 0, st>>>(m->nodes, m->conn, m->E, m->N, B, lam, U, out, badp);
     }
     KERNEL_CHECK("adjoint_gather");
-    return check_bad(bad.p, st);
+    return check_bad(badp, st);
 }
 
 // One batched launch (batched.cu: halo geometry cached per block, all fields
@@ -380,18 +380,18 @@ int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, c
     if (B < 0) return set_error(TGK_ERR_INPUT, "assemble_batched: negative batch");
     TGK_TRY(ensure_device());
     cudaStream_t st = as_stream(stream);
-    DevBuf<unsigned long long> bad;
-    TGK_TRY(bad.alloc(1));
-    CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    unsigned long long* badp = nullptr;  // the routing's persistent status words
+    TGK_TRY(routing_flags(const_cast<tgk_routing*>(r), &badp));
+    CUDA_TRY(cudaMemsetAsync(badp, 0xff, sizeof(unsigned long long), st));
     if (B == 0) return TGK_OK;
     if (!getenv("TGK_BATCHED_LOOP") && !getenv("TGK_BATCHED_CHUNKED")) {
-        const int rc = batched_entries(m, const_cast<tgk_routing*>(r), B, rho, source, K, F, st, bad.p);
-        if (rc == TGK_OK) return check_bad(bad.p, st);
+        const int rc = batched_entries(m, const_cast<tgk_routing*>(r), B, rho, source, K, F, st, badp);
+        if (rc == TGK_OK) return check_bad(badp, st);
         if (rc != TGK_ERR_INPUT) return rc;
     }
     if (!getenv("TGK_BATCHED_LOOP")) {
-        const int rc = batched_fused(m, const_cast<tgk_routing*>(r), B, rho, source, K, F, st, bad.p);
-        if (rc == TGK_OK) return check_bad(bad.p, st);
+        const int rc = batched_fused(m, const_cast<tgk_routing*>(r), B, rho, source, K, F, st, badp);
+        if (rc == TGK_OK) return check_bad(badp, st);
         if (rc != TGK_ERR_INPUT) return rc;
     }
     for (int64_t b = 0; b < B; ++b) {
@@ -401,8 +401,8 @@ int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, c
         p.n_source = (F && b == 0) ? 1 : 0;
         p.source[0] = tgk_field{TGK_FIELD_CONSTANT, source, nullptr, 0};
         TGK_TRY(fused_scalar_assemble(&p, m, const_cast<tgk_routing*>(r), K + b * r->nnz,
-                                      b == 0 ? F : nullptr, nullptr, st, bad.p));
-        if (b + 1 == B || (b & 63) == 63) TGK_TRY(check_bad(bad.p, st));
+                                      b == 0 ? F : nullptr, nullptr, st, badp));
+        if (b + 1 == B || (b & 63) == 63) TGK_TRY(check_bad(badp, st));
     }
     return TGK_OK;
 }

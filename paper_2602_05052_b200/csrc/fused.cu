@@ -884,9 +884,9 @@ static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int d
         TGK_TRY(trace.alloc(pl->n_blocks * 8));
         a.trace = trace.p;
     }
-    DevBuf<unsigned long long> bad;
-    if (!d_bad) TGK_TRY(bad.alloc(1));
-    a.bad = d_bad ? d_bad : bad.p;
+    unsigned long long* own_bad = nullptr;
+    if (!d_bad) TGK_TRY(routing_flags(r, &own_bad));
+    a.bad = d_bad ? d_bad : own_bad;
     CUDA_TRY(cudaMemsetAsync(a.bad, 0xff, sizeof(unsigned long long), st));
     if (!has_f && F) CUDA_TRY(cudaMemsetAsync(F, 0, (f32 ? sizeof(float) : sizeof(double)) * r->N, st));
     bool fdiv = false;
@@ -922,7 +922,7 @@ static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int d
                 rc = degree == 1 ? dispatch_entries<TGK_TRI3, 1>(has_m, has_f, fdiv, e, st)
                                  : dispatch_entries<TGK_TRI3, 2>(has_m, has_f, fdiv, e, st);
             if (rc == TGK_OK) {
-                if (!d_bad) return check_bad(bad.p, st);
+                if (!d_bad) return check_bad(own_bad, st);
                 return TGK_OK;
             }
             if (rc != TGK_ERR_INPUT) return rc;
@@ -944,7 +944,7 @@ static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int d
             fclose(f);
         }
     }
-    if (!d_bad) return check_bad(bad.p, st);
+    if (!d_bad) return check_bad(own_bad, st);
     return TGK_OK;  // asynchronous: the caller inspects *d_bad
 }
 

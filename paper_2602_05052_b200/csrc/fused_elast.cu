@@ -747,10 +747,10 @@ int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
     a.max_chunks = pl->max_block_chunks;
     a.ntcols = d + (a.lam.type == TGK_FIELD_NODAL) + (a.mu.type == TGK_FIELD_NODAL);
     for (int c = 0; c < a.n_src; ++c) a.ntcols += a.src[c].type == TGK_FIELD_NODAL;
-    DevBuf<unsigned long long> bad;
-    TGK_TRY(bad.alloc(2));
-    CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, 2 * sizeof(unsigned long long), st));
-    a.bad = bad.p;
+    unsigned long long* badp = nullptr;  // the routing's persistent status words
+    TGK_TRY(routing_flags(r, &badp));
+    CUDA_TRY(cudaMemsetAsync(badp, 0xff, 2 * sizeof(unsigned long long), st));
+    a.bad = badp;
     if (v1) {
         if (m->kind == TGK_TET4) {
             TGK_TRY((high ? launch_elast<TGK_TET4, 2, R>(a, pl->n_blocks, st) : launch_elast<TGK_TET4, 1, R>(a, pl->n_blocks, st)));
@@ -769,7 +769,7 @@ int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
             TGK_TRY((high ? launch_elast2<TGK_TRI3, 2, 32>(a, pl->n_blocks, st) : launch_elast2<TGK_TRI3, 1, 32>(a, pl->n_blocks, st)));
     }
     unsigned long long h[2] = {ULLONG_MAX, ULLONG_MAX};
-    CUDA_TRY(cudaMemcpyAsync(h, bad.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(h, badp, sizeof h, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     // batch_geometry runs (and throws) before local_stiffness_elasticity checks mu (physics.cpp:11-52)
     if (h[0] != ULLONG_MAX)

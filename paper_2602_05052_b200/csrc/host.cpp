@@ -150,7 +150,7 @@ static double centroid_det(int kind, const double* nodes, const int64_t* conn) {
            J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
 }
 
-int narrow_connectivity(const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
+int narrow_connectivity(tgk_mesh* m, const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
                         cudaStream_t st);
 int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                           double* F, double* M, cudaStream_t st, unsigned long long* d_bad);
@@ -433,7 +433,7 @@ int tgk_mesh_upload(tgk_mesh* m, const double* nodes, const int64_t* elems, void
         if (!m->staging) HCUDA(cudaMalloc(&m->staging, sizeof(int64_t) * std::max<int64_t>(1, n)));
         HCUDA(cudaMemcpyAsync(m->staging, elems, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
         int64_t bad = -1;
-        TGK_TRY(narrow_connectivity(m->staging, n, m->N, m->conn, &bad, st));
+        TGK_TRY(narrow_connectivity(m, m->staging, n, m->N, m->conn, &bad, st));
         if (bad >= 0)
             return set_error(TGK_ERR_INPUT, "element " + std::to_string(bad / m->k) + " references node " +
                                                 std::to_string(elems[bad]) + " outside [0," +
@@ -451,6 +451,8 @@ void tgk_mesh_destroy(tgk_mesh* m) {
         if (m->conn) cudaFree(m->conn);
     }
     if (m->staging) cudaFree(m->staging);
+    if (m->d_flags) cudaFree(m->d_flags);
+    if (m->h_flags) cudaFreeHost(m->h_flags);
     delete m;
 }
 
@@ -775,6 +777,12 @@ int ensure_scalar_entry_plan(tgk_routing* rr, const ScalarEntryPlanDev** out) {
     D.data = reinterpret_cast<const uint16_t*>(base + o_d);
     D.t_pos = reinterpret_cast<const uint64_t*>(base + o_tp);
     *out = &D;
+    return TGK_OK;
+}
+
+int routing_flags(tgk_routing* r, unsigned long long** out) {
+    if (!r->flags) HCUDA(cudaMalloc(&r->flags, 4 * sizeof(unsigned long long)));
+    *out = r->flags;
     return TGK_OK;
 }
 

@@ -368,6 +368,7 @@ tgk_routing::~tgk_routing() {
     for (auto& pl : plan) pl.release();
     entry_plan.release();
     group_plan.release();
+    if (flags) cudaFree(flags);
     se_plan.release();
     for (double* p : scr)
         if (p) cudaFree(p);

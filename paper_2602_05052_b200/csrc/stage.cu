@@ -487,33 +487,39 @@ __global__ void k_coord_range(const double* x, int64_t n, unsigned* bad) {
     if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
 }
 
+// Persistent per-mesh flag words (device + pinned host), allocated on first use.
+int mesh_flags(tgk_mesh* m) {
+    if (!m->d_flags) CUDA_TRY(cudaMalloc(&m->d_flags, 2 * sizeof(unsigned long long)));
+    if (!m->h_flags) CUDA_TRY(cudaMallocHost(&m->h_flags, 2 * sizeof(unsigned long long)));
+    return TGK_OK;
+}
+
 int mesh_division_safe(tgk_mesh* m, cudaStream_t st, bool* safe) {
     if (m->div_safe < 0) {
-        DevBuf<unsigned> flag;
-        TGK_TRY(flag.alloc(1));
-        CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(unsigned), st));
+        TGK_TRY(mesh_flags(m));
+        unsigned* flag = reinterpret_cast<unsigned*>(m->d_flags);
+        CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(unsigned), st));
         const int64_t n = m->N * m->d;
-        k_coord_range<<<std::min<unsigned>(grid_for(n, 256), 148 * 8), 256, 0, st>>>(m->nodes, n, flag.p);
+        k_coord_range<<<std::min<unsigned>(grid_for(n, 256), 148 * 8), 256, 0, st>>>(m->nodes, n, flag);
         KERNEL_CHECK("coord_range");
-        unsigned h = 1;
-        CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(m->h_flags, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
-        m->div_safe = h == 0 ? 1 : 0;
+        m->div_safe = *reinterpret_cast<unsigned*>(m->h_flags) == 0 ? 1 : 0;
     }
     *safe = m->div_safe == 1;
     return TGK_OK;
 }
 
-int narrow_connectivity(const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
+int narrow_connectivity(tgk_mesh* m, const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
                         cudaStream_t st) {
-    DevBuf<unsigned long long> flag;
-    TGK_TRY(flag.alloc(1));
-    CUDA_TRY(cudaMemsetAsync(flag.p, 0xff, sizeof(unsigned long long), st));
-    k_narrow<<<std::min<unsigned>(grid_for(n, 256), 148 * 16), 256, 0, st>>>(src, n, n_nodes, dst, flag.p);
+    TGK_TRY(mesh_flags(m));
+    unsigned long long* flag = m->d_flags + 1;
+    CUDA_TRY(cudaMemsetAsync(flag, 0xff, sizeof(unsigned long long), st));
+    k_narrow<<<std::min<unsigned>(grid_for(n, 256), 148 * 16), 256, 0, st>>>(src, n, n_nodes, dst, flag);
     KERNEL_CHECK("narrow_connectivity");
-    unsigned long long h = ULLONG_MAX;
-    CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(m->h_flags + 1, flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    const unsigned long long h = m->h_flags[1];
     *bad = h == ULLONG_MAX ? -1 : static_cast<int64_t>(h);
     return TGK_OK;
 }

@@ -235,6 +235,10 @@ struct tgk_mesh {
     int64_t* staging = nullptr;  // device int64 connectivity staging for host uploads
     int div_safe = -1;           // coordinates certified for Markstein division (-1 unknown)
     bool owned = false;
+    // persistent validation scratch (no per-call cudaMalloc / cudaFree, which
+    // would serialise the device): 2 device flags, 2 pinned host words
+    unsigned long long* d_flags = nullptr;
+    unsigned long long* h_flags = nullptr;
 };
 
 struct tgk_routing {
@@ -259,6 +263,7 @@ struct tgk_routing {
     int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
     double* scr[6] = {};             // cached device scratch (materialised elasticity path)
     size_t scr_n[6] = {};
+    unsigned long long* flags = nullptr;  // persistent device status words (4), see routing_flags
     double* scratch_K = nullptr;     // device output buffers of the host-buffer entry point
     double* scratch_F = nullptr;
     double* scratch_M = nullptr;
@@ -269,6 +274,10 @@ namespace tgk {
 // Build (once per R) and upload the fused plan of the routing's scalar part.
 int ensure_plan(tgk_routing* r, int R, const PlanDev** out, int C = 0);  // C = 0: chunk size R
 int ensure_entry_plan(tgk_routing* r, int R, const EntryPlanDev** out);
+// The routing's 4 persistent device status words (allocated once: no per-call
+// cudaMalloc / cudaFree, which would serialise the device).  A routing handle
+// is used by one stream at a time.
+int routing_flags(tgk_routing* r, unsigned long long** out);
 int ensure_group_plan(tgk_routing* r, int G, const GroupPlanDev** out);
 int ensure_scalar_entry_plan(tgk_routing* r, const ScalarEntryPlanDev** out);
 }
