@@ -12,7 +12,6 @@ is outside the accelerated path and raises NotImplementedError.
 from __future__ import annotations
 
 import ctypes as C
-import weakref
 
 import numpy as np
 
