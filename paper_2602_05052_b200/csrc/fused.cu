@@ -178,13 +178,13 @@ __device__ __forceinline__ void mass_row(T det, int a, T (&mv)[4], T (&na)[Rule<
     }
 #pragma unroll
     for (int j = 0; j < k; ++j) {
-        const int b = j == 0 ? a : (j - 1 < a ? j - 1 : j);
+        // rotated column: j = 0 is a itself, j >= 1 is local node j-1 (below a) or j
+        const bool lower = j - 1 < a;
         T v = T(0);
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            T nb = T(basis<KIND, DEG>(q, 0));
-#pragma unroll
-            for (int c = 1; c < k; ++c) nb = b == c ? T(basis<KIND, DEG>(q, c)) : nb;
+            const T nb = j == 0 ? na[q]
+                                : (lower ? T(basis<KIND, DEG>(q, j > 0 ? j - 1 : 0)) : T(basis<KIND, DEG>(q, j < k ? j : 0)));
             const T term = T(Rl::w(q)) * det * na[q] * nb;
             v = q == 0 ? term : v + term;
         }
