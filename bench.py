@@ -452,7 +452,8 @@ def run_scalar(args, ctx, N):
     nb, nh, nrec, pbytes = (C.c_int64() for _ in range(4))
     # rows per block of the fused kernel (fused.cu fused_rows_per_block: 64 below 4 x 128 x #SMs rows)
     n_rows_own = (s.calc_hi - s.own_lo) if (s is not None and world > 1) else nodes.shape[0]
-    R_plan = 64 if n_rows_own < 128 * 4 * torch.cuda.get_device_properties(ctx.dev).multi_processor_count else 128
+    R_plan = 64 if (kw.get("with_mass") or
+                    n_rows_own < 128 * 4 * torch.cuda.get_device_properties(ctx.dev).multi_processor_count) else 128
     N.check(L.tgk_routing_plan_stats(routing._h, R_plan, C.byref(nb), C.byref(nh), C.byref(nrec), C.byref(pbytes)))
     setup_s = time.time() - t0
     with_mass = kw.get("with_mass", False)

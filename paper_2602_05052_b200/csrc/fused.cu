@@ -832,10 +832,10 @@ int fused_rows_per_block(const tgk_problem* pr, int64_t n_rows) {
         return r == 64 || r == 128 ? r : TGK_R_BIG;
     }
     // measured on B200 (profiles/r01_fused_experiments.txt): 128 rows per block
-    // for K+F and, since the unit mass is formed from det in the fold (MDET),
-    // for K+M+F as well; 64 when 128-row blocks would not fill the GPU once
-    // (C1: 16.0 -> 13.4 us)
-    (void)pr;
+    // for K+F, 64 for K+M+F (C2: 797 vs 850 us with the mass and load formed
+    // from det in the fold), and 64 when 128-row blocks would not fill the GPU
+    // once (C1: 16.0 -> 13.4 us)
+    if (pr->with_mass) return 64;
     static const int sms = [] {
         int dev = 0, n = 148;
         cudaGetDevice(&dev);
