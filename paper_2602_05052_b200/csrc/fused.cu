@@ -69,6 +69,7 @@ struct FusedArgs {
     int max_recs;
     int max_bnodes;
     int ntcols;  // doubles per node-table entry: 3 coordinates [+ nodal coefficient] [+ nodal source]
+    int max_chunks;  // most halo chunks of one block (dynamic chunk-offset table)
     int debug;  // profiling only (TGK_FUSED_DEBUG): 1 skips phase B, 2 skips phase A math
     long long* trace;  // profiling only (TGK_FUSED_TRACE): per block 8 clock64 stamps
     unsigned long long* bad;
@@ -118,10 +119,11 @@ struct FusedCfg {
     static constexpr int NV = 3;      // TRI3 pads to 3 as well (odd stride)
     // doubles per node in the table: the coordinates, then the nodal
     // coefficient / source columns only when those fields are nodal (FusedArgs::ntcols)
-    static size_t smem_bytes(int lmax, int max_recs, int max_bnodes, int ntcols) {
+    static size_t smem_bytes(int lmax, int max_recs, int max_bnodes, int ntcols, int max_chunks) {
         return sizeof(T) * (size_t(R) * stride + size_t(R) * lmax * nmat + size_t(max_bnodes) * ntcols) +
                kRing * (sizeof(uint32_t) * size_t(max_recs) + sizeof(uint16_t) * size_t(row_off_stride(R)) +
-                        sizeof(uint16_t) * 4 * size_t(R));
+                        sizeof(uint16_t) * 4 * size_t(R)) +
+               sizeof(int64_t) * size_t(max_chunks + 1);
     }
 };
 
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(R, TGK_MINB(R)) k_fused_scalar(FusedArgs p) {
     uint32_t* rec_s = reinterpret_cast<uint32_t*>(nt + p.max_bnodes * p.ntcols);  // kRing x max_recs
     uint16_t* ro_s = reinterpret_cast<uint16_t*>(rec_s + kRing * p.max_recs);  // kRing x ROS
     ushort4* lc_s = reinterpret_cast<ushort4*>(ro_s + kRing * ROS);           // kRing x R
-    __shared__ int64_t cro_s[kMaxChunks + 1];  // this block's chunk record offsets
+    int64_t* cro_s = reinterpret_cast<int64_t*>(lc_s + kRing * R);           // this block's chunk record offsets
 
     const int tid = threadIdx.x;
     const int64_t blk = blockIdx.x;
@@ -580,7 +582,7 @@ template <int KIND, int DEG, int KTYPE, bool HAS_M, bool HAS_F, int R, bool FDIV
 int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
     using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T, FCONST>;
     auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV, T, FCONST>;
-    const size_t smem = C::smem_bytes(a.lmax, a.max_recs, a.max_bnodes, a.ntcols);
+    const size_t smem = C::smem_bytes(a.lmax, a.max_recs, a.max_bnodes, a.ntcols, a.max_chunks);
     // raise the instance's dynamic shared-memory limit only when it grows (small
     // meshes are launch-overhead bound; one process drives one device)
     static size_t smem_set = 0;
@@ -876,6 +878,7 @@ static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int d
     a.lmax = pl->lmax;
     a.max_recs = pl->max_chunk_recs > 0 ? pl->max_chunk_recs : 4;
     a.max_bnodes = (pl->max_bnodes + 3) & ~3;  // node table ends 16-byte aligned for fp32 and fp64
+    a.max_chunks = pl->max_block_chunks;
     a.ntcols = 3 + (nodal_like(a.coef.type) ? 1 : 0) + (has_f && nodal_like(a.src.type) ? 1 : 0);
     if (const char* dbg = getenv("TGK_FUSED_DEBUG")) a.debug = atoi(dbg);
     DevBuf<long long> trace;
