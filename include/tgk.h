@@ -55,10 +55,18 @@ extern "C" {
 #define TGK_FIELD_ELEMENT 1 /* E values                       */
 #define TGK_FIELD_NODAL 2   /* N_node values, interpolated by the basis (batch.cpp:314-333) */
 
-/* arithmetic mode of tgk_problem (fp64 entries): the reference operation order,
- * no FMA contraction, bit-identical CSR values.  The fp32 variant is a separate
- * entry point (tgk_assemble_f32_d) with float outputs. */
+/* arithmetic mode of tgk_problem (fp64 entries).
+ *  TGK_MODE_EXACT: the reference operation order, no FMA contraction, CSR values
+ *    bit-identical to the reference (ascending-element folds, row-block kernel).
+ *  TGK_MODE_FAST: the north star's contract — pattern bit-exact, values within
+ *    |dv| <= 1e-12 |v_ref| + 1e-14 max|v_ref|, bitwise
+ *    deterministic run to run: FMA arithmetic, affine-P1 closed forms of the
+ *    quadrature, a precomputed element-to-CSR-slot list per entry folded in a
+ *    register (fast.cu).  Scalar problems with constant / per-element / nodal
+ *    fields (a nodal mass coefficient, and elasticity, take the exact kernel).
+ * The fp32 variant is a separate entry point (tgk_assemble_f32_d). */
 #define TGK_MODE_EXACT 0
+#define TGK_MODE_FAST 1
 
 typedef struct tgk_mesh tgk_mesh;
 typedef struct tgk_routing tgk_routing;
@@ -79,7 +87,7 @@ typedef struct {
     int n_source;          /* 0, 1 (scalar) or d (elasticity body force) */
     tgk_field source[3];
     int with_mass;         /* also assemble M (scalar problems only; physics.cpp:68-73) */
-    int mode;              /* TGK_MODE_EXACT (the only fp64 mode; other values: status 2) */
+    int mode;              /* TGK_MODE_EXACT or TGK_MODE_FAST (other values: status 2) */
 } tgk_problem;
 
 /* Routing description (RoutingMatrices, routing.hpp:16-32).  All pointers are

@@ -595,204 +595,6 @@ int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
     return TGK_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Entry-owned fused kernel (opt-in, TGK_FUSED_ENTRIES=1; fp64 stiffness
-// [+ unit mass] [+ load]).
-// A block of 256 threads owns the rows of its plan block (plan_entries.cpp
-// build_scalar_entry_plan); every thread owns up to 8 CSR entries (or the
-// row's load F) of one row and keeps their sums in registers.  Per chunk of
-// 256 halo elements: phase A — one thread per element computes the exact
-// K_e (unique a <= b values: bitwise symmetric), M_e and F_e into
-// structure-of-arrays rows in shared memory; phase B — every thread walks its
-// item list for the chunk (items of a slot in ascending element id, chunks in
-// the plan's fold-compatible order) and adds the addressed values to that
-// slot's register sums.  No shared accumulators, no read-modify-write chains,
-// no idle row lanes; each CSR value is the left fold from +0.0 of its
-// contributions in ascending element order (routing.cpp:117-124).
-constexpr int kSeT = 256, kSeC = 256, kSeW = kSeT / 32;
-
-struct SEArgs {
-    const double* nodes;
-    ScalarEntryPlanDev pl;
-    FieldDev coef;
-    FieldDev src;
-    double* K;
-    double* M;
-    double* F;
-    int ntb;     // node-table capacity (multiple of 4)
-    int ntcols;  // 3 coordinates [+ nodal coefficient] [+ nodal source]
-    unsigned long long* bad;
-};
-
-template <int KIND, bool HAS_M>
-struct SeSink {
-    static constexpr int k = P1<KIND>::k, KU = k * (k + 1) / 2;
-    double* kv;   // [KU + k][kSeC]: K unique rows, then F rows
-    double* kvm;  // [k * k][kSeC]
-    int h;
-    __device__ __forceinline__ void Ksym(int, int, int t, double v) { kv[t * kSeC + h] = v; }
-    __device__ __forceinline__ void K(int, int, double) {}  // coefficient mass: not dispatched here
-    static constexpr bool kMDet = false, kDet = false;
-    __device__ __forceinline__ void Det(double) {}
-    __device__ __forceinline__ void M(int a, int b, double v) {
-        if constexpr (HAS_M) kvm[(a * k + b) * kSeC + h] = v;
-    }
-    __device__ __forceinline__ void F(int a, double v) { kv[(KU + a) * kSeC + h] = v; }
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int t = 0; t < KU + k; ++t) kv[t * kSeC + h] = 0.0;
-        if constexpr (HAS_M) {
-#pragma unroll
-            for (int t = 0; t < k * k; ++t) kvm[t * kSeC + h] = 0.0;
-        }
-    }
-};
-
-template <int KIND, bool HAS_M>
-size_t se_smem(const SEArgs& a) {
-    constexpr int k = P1<KIND>::k, KU = k * (k + 1) / 2;
-    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-    size_t o = 0;
-    o = al(o + sizeof(double) * size_t(KU + k) * kSeC);
-    if (HAS_M) o = al(o + sizeof(double) * size_t(k * k) * kSeC);
-    o = al(o + sizeof(double) * size_t(a.ntb) * a.ntcols);
-    o = al(o + sizeof(uint16_t) * 2 * size_t(a.pl.max_chunk_u16));
-    o = al(o + sizeof(ushort4) * 2 * kSeC);
-    return o;
-}
-
-template <int KIND, int DEG, bool HAS_M, bool HAS_F, bool FDIV>
-__global__ void __launch_bounds__(kSeT, 2) k_fused_entries(SEArgs p) {
-    constexpr int k = P1<KIND>::k, d = P1<KIND>::d, KU = k * (k + 1) / 2, NV = 3, S = kSlotsPerThread;
-    constexpr int T = kSeT, C = kSeC;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-    size_t o = 0;
-    double* kv = reinterpret_cast<double*>(smem_raw + o); o = al(o + sizeof(double) * size_t(KU + k) * C);
-    double* kvm = reinterpret_cast<double*>(smem_raw + o);
-    if (HAS_M) o = al(o + sizeof(double) * size_t(k * k) * C);
-    double* nt = reinterpret_cast<double*>(smem_raw + o); o = al(o + sizeof(double) * size_t(p.ntb) * p.ntcols);
-    uint16_t* ring = reinterpret_cast<uint16_t*>(smem_raw + o); o = al(o + sizeof(uint16_t) * 2 * size_t(p.pl.max_chunk_u16));
-    ushort4* lc_s = reinterpret_cast<ushort4*>(smem_raw + o);
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t blk = blockIdx.x;
-    const ScalarEntryPlanDev& pl = p.pl;
-    const int64_t h0 = pl.halo_off[blk];
-    const int64_t nh = pl.halo_off[blk + 1] - h0;
-    const int64_t c0 = pl.chunk_off[blk];
-    const int nch = static_cast<int>(pl.chunk_off[blk + 1] - c0);
-
-    auto stage = [&](int c) {
-        if (c < nch) {
-            const int sl = c & 1;
-            const int64_t db = pl.chunk_data_off[c0 + c];
-            const int n8 = static_cast<int>((pl.chunk_data_off[c0 + c + 1] - db) >> 3);
-            uint16_t* dst = ring + sl * size_t(p.pl.max_chunk_u16);
-            for (int i = tid; i < n8; i += T) cp_async16(dst + 8 * i, pl.data + db + 8 * i);
-            const int64_t hb = h0 + int64_t(c) * C;
-            const int64_t rem = nh - int64_t(c) * C;
-            const int ne = rem < C ? static_cast<int>(rem) : C;
-            if (tid < ne) cp_async8(lc_s + sl * C + tid, pl.halo_lconn + (hb + tid) * 4);
-        }
-        cp_async_commit();
-    };
-    stage(0);
-    // node table (as the row-block kernel): coordinates, nodal coefficient / source columns
-    {
-        const int64_t n0 = pl.bnode_off[blk];
-        const int nbn = static_cast<int>(pl.bnode_off[blk + 1] - n0);
-        for (int i = tid; i < nbn; i += T) {
-            const int64_t g = pl.bnodes[n0 + i];
-#pragma unroll
-            for (int c = 0; c < d; ++c) cp_async8(nt + i * NV + c, p.nodes + g * d + c);
-            if (nodal_like(p.coef.type)) cp_async8(nt + size_t(p.ntb) * NV + i, p.coef.data + g);
-            if (HAS_F && nodal_like(p.src.type))
-                cp_async8(nt + size_t(p.ntb) * (NV + (nodal_like(p.coef.type) ? 1 : 0)) + i, p.src.data + g);
-        }
-        cp_async_commit();
-    }
-    const int64_t my_rp = pl.t_rp[blk * T + tid];
-    const uint64_t my_pos = pl.t_pos[blk * T + tid];
-    double vK[S], vM[HAS_M ? S : 1];
-#pragma unroll
-    for (int u = 0; u < S; ++u) {
-        vK[u] = 0.0;
-        if constexpr (HAS_M) vM[u] = 0.0;
-    }
-    for (int c = 0; c < nch; ++c) {
-        cp_async_wait<0>();  // chunk c (and, first time, the node table) landed
-        __syncthreads();     // visible to all; phase B(c-1) done with the value rows
-        stage(c + 1);        // next chunk's items and connectivity into the other slot
-        const int sl = c & 1;
-        // ---------------- phase A: this thread's element of chunk c
-        const int64_t h = int64_t(c) * C + tid;
-        if (h < nh) {
-            SeSink<KIND, HAS_M> sink{kv, kvm, tid};
-            element_values<KIND, DEG, 0, HAS_M, HAS_F, FDIV, double>(p.coef, p.src, pl.halo, p.bad, p.ntb, nt,
-                                                                    lc_s[sl * C + tid], h0 + h, sink);
-        }
-        __syncthreads();
-        // ---------------- phase B: this thread's slots, items in ascending element
-        const uint16_t* cd = ring + sl * size_t(p.pl.max_chunk_u16);
-        const uint64_t ends = *reinterpret_cast<const uint64_t*>(cd + 4 * tid);
-        const uint16_t* ws = cd + 4 * T;
-        int wb = 0;
-#pragma unroll
-        for (int w = 0; w < kSeW; ++w) wb += w < warp ? int(ws[w]) * 32 : 0;
-        const uint16_t* it = cd + 4 * T + 8 + wb + lane;
-        int s2 = 0;
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-            const int e = static_cast<int>((ends >> (8 * u)) & 0xff);
-            for (; s2 < e; ++s2) {
-                const uint32_t item = it[s2 * 32];
-                vK[u] += kv[item & 0xfff];
-                if constexpr (HAS_M) vM[u] += kvm[((item >> 12) << 8) | (item & 0xff)];
-            }
-        }
-    }
-    // ---------------- epilogue: register sums -> CSR values / load
-    if (my_rp >= 0) {
-        const int64_t row = pl.t_row[blk * T + tid];
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-            const int code = static_cast<int>((my_pos >> (8 * u)) & 0xff);
-            if (code < 32) {
-                p.K[my_rp + code] = vK[u];
-                if constexpr (HAS_M) p.M[my_rp + code] = vM[u];
-            } else if (code == 0xfe) {
-                if (HAS_F) p.F[row] = vK[u];
-            }
-        }
-    }
-}
-
-template <int KIND, int DEG, bool HAS_M, bool HAS_F, bool FDIV>
-int launch_entries_scalar(const SEArgs& a, cudaStream_t st) {
-    auto kern = k_fused_entries<KIND, DEG, HAS_M, HAS_F, FDIV>;
-    const size_t smem = se_smem<KIND, HAS_M>(a);
-    if (smem > 227 * 1024) return TGK_ERR_INPUT;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (a.pl.n_blocks > 0) kern<<<static_cast<unsigned>(a.pl.n_blocks), kSeT, smem, st>>>(a);
-    KERNEL_CHECK("fused_entries");
-    return TGK_OK;
-}
-
-template <int KIND, int DEG>
-int dispatch_entries(bool m, bool f, bool fdiv, const SEArgs& a, cudaStream_t st) {
-    if (fdiv) {
-        if (m && f) return launch_entries_scalar<KIND, DEG, true, true, true>(a, st);
-        if (m) return launch_entries_scalar<KIND, DEG, true, false, true>(a, st);
-        if (f) return launch_entries_scalar<KIND, DEG, false, true, true>(a, st);
-        return launch_entries_scalar<KIND, DEG, false, false, true>(a, st);
-    }
-    if (m && f) return launch_entries_scalar<KIND, DEG, true, true, false>(a, st);
-    if (m) return launch_entries_scalar<KIND, DEG, true, false, false>(a, st);
-    if (f) return launch_entries_scalar<KIND, DEG, false, true, false>(a, st);
-    return launch_entries_scalar<KIND, DEG, false, false, false>(a, st);
-}
-
 template <int KIND, int DEG, int R, bool FDIV, typename T>
 int dispatch_r(int ktype, bool m, bool f, const FusedArgs& a, int64_t nb, cudaStream_t st) {
     if (ktype == 1) return f ? launch_fused<KIND, DEG, 1, false, true, R, FDIV, T>(a, nb, st)
@@ -895,42 +697,6 @@ static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int d
     bool fdiv = false;
     TGK_TRY(mesh_division_safe(const_cast<tgk_mesh*>(m), st, &fdiv));
     if (getenv("TGK_IEEE_DIV")) fdiv = false;
-    if (ktype == 0 && !f32 && !trace_path && !a.debug && getenv("TGK_FUSED_ENTRIES")) {
-        // entry-owned kernel (opt-in: bit-exact, but 1.6x slower than the
-        // row-block kernel on C2a — per-slot item loops diverge across lanes and
-        // the item lists add ~700 MB of plan reads; profiles/r01_fused_experiments.txt);
-        // falls back to the row-block kernel below when its plan does not apply
-        // (rows longer than 31 entries, > 255 items per thread and chunk) or its
-        // working set does not fit
-        const ScalarEntryPlanDev* sp = nullptr;
-        const int prc = ensure_scalar_entry_plan(r, &sp);
-        if (prc != TGK_OK && prc != TGK_ERR_INPUT) return prc;
-        if (prc == TGK_OK) {
-            SEArgs e{};
-            e.nodes = m->nodes;
-            e.pl = *sp;
-            e.coef = a.coef;
-            e.src = a.src;
-            e.K = static_cast<double*>(K);
-            e.M = static_cast<double*>(M);
-            e.F = static_cast<double*>(F);
-            e.ntb = (sp->max_bnodes + 3) & ~3;
-            e.ntcols = a.ntcols;
-            e.bad = a.bad;
-            int rc;
-            if (m->kind == TGK_TET4)
-                rc = degree == 1 ? dispatch_entries<TGK_TET4, 1>(has_m, has_f, fdiv, e, st)
-                                 : dispatch_entries<TGK_TET4, 2>(has_m, has_f, fdiv, e, st);
-            else
-                rc = degree == 1 ? dispatch_entries<TGK_TRI3, 1>(has_m, has_f, fdiv, e, st)
-                                 : dispatch_entries<TGK_TRI3, 2>(has_m, has_f, fdiv, e, st);
-            if (rc == TGK_OK) {
-                if (!d_bad) return check_bad(own_bad, st);
-                return TGK_OK;
-            }
-            if (rc != TGK_ERR_INPUT) return rc;
-        }
-    }
     if (m->kind == TGK_TET4) {
         if (degree == 1) TGK_TRY((dispatch_flags<TGK_TET4, 1>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, f32, st)));
         else TGK_TRY((dispatch_flags<TGK_TET4, 2>(ktype, has_m, has_f, a, pl->n_blocks, R, fdiv, f32, st)));

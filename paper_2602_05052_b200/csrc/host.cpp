@@ -154,6 +154,8 @@ int narrow_connectivity(tgk_mesh* m, const int64_t* src, int64_t n, int64_t n_no
                         cudaStream_t st);
 int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                           double* F, double* M, cudaStream_t st, unsigned long long* d_bad);
+int fast_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F, double* M,
+                         cudaStream_t st, unsigned long long* d_bad);
 int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                         double* F, cudaStream_t st);
 int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
@@ -475,6 +477,7 @@ int tgk_routing_set_owned_rows(tgk_routing* r, int64_t lo, int64_t hi) {
     if (s->own_lo == lo && s->own_hi == hi) return TGK_OK;
     for (auto& pl : s->plan) pl.release();
     s->entry_plan.release();
+    s->fast_plan.release();
     s->own_lo = lo;
     s->own_hi = hi;
     return TGK_OK;
@@ -488,6 +491,7 @@ int tgk_routing_set_element_range(tgk_routing* r, int64_t lo, int64_t hi) {
     if (lo < 0 || hi > s->E || lo > hi) return set_error(TGK_ERR_INPUT, "element range out of bounds");
     if (s->elem_lo == lo && s->elem_hi == hi) return TGK_OK;
     for (auto& pl : s->plan) pl.release();
+    s->fast_plan.release();
     s->elem_lo = lo;
     s->elem_hi = hi;
     return TGK_OK;
@@ -541,14 +545,7 @@ void PlanDev::release() {
 }
 
 // Host copies of the mesh and the scalar routing arrays the plans are built from.
-struct ScalarRoutingHost {
-    std::vector<double> nodes;
-    std::vector<int32_t> conn;
-    std::vector<int64_t> row_ptr;
-    std::vector<uint32_t> vo, vs, slot;
-};
-
-static int fetch_scalar_routing(const tgk_routing* r, ScalarRoutingHost& h) {
+int fetch_scalar_routing(const tgk_routing* r, ScalarRoutingHost& h) {
     const tgk_mesh* m = r->mesh;
     const int k = m->k, d = m->d;
     h.nodes.resize(m->N * d);
@@ -703,83 +700,6 @@ int ensure_group_plan(tgk_routing* rr, int G, const GroupPlanDev** out) {
     return TGK_OK;
 }
 
-void ScalarEntryPlanDev::release() {
-    if (blob) cudaFree(blob);
-    *this = ScalarEntryPlanDev{};
-}
-
-// Build (once per owned-row / element range) and upload the scalar entry plan.
-int ensure_scalar_entry_plan(tgk_routing* rr, const ScalarEntryPlanDev** out) {
-    tgk_routing* r = rr->scalar ? rr->scalar : rr;
-    ScalarEntryPlanDev& D = r->se_plan;
-    const int64_t lo = r->own_hi < 0 ? 0 : r->own_lo, hi = r->own_hi < 0 ? r->N : r->own_hi;
-    const int64_t elo = r->elem_hi < 0 ? 0 : r->elem_lo, ehi = r->elem_hi < 0 ? r->E : r->elem_hi;
-    if (D.blob && D.row_lo == lo && D.row_hi == hi && D.elem_lo == elo && D.elem_hi == ehi) {
-        *out = &D;
-        return TGK_OK;
-    }
-    D.release();
-    const tgk_mesh* m = r->mesh;
-    ScalarRoutingHost h;
-    TGK_TRY(fetch_scalar_routing(r, h));
-    ScalarEntryPlanHost P;
-    int rmax = 128;
-    if (const char* e = getenv("TGK_SE_RMAX")) rmax = std::max(1, atoi(e));
-    TGK_TRY(build_scalar_entry_plan(m->kind, m->N, h.nodes.data(), h.conn.data(), h.row_ptr.data(), h.vo.data(),
-                                    h.vs.data(), h.slot.data(), lo, hi, elo, ehi, 256, 256, rmax, P));
-    size_t total = 0;
-    auto reserve = [&total](const auto& v) {
-        const size_t at = total;
-        total += (v.size() * sizeof(v[0]) + 15) & ~size_t(15);
-        return at;
-    };
-    const size_t o_ho = reserve(P.halo_off), o_bo = reserve(P.bnode_off), o_co = reserve(P.chunk_off),
-                 o_cdo = reserve(P.chunk_data_off), o_trp = reserve(P.t_rp), o_h = reserve(P.halo),
-                 o_bn = reserve(P.bnodes), o_tr = reserve(P.t_row), o_lc = reserve(P.halo_lconn),
-                 o_d = reserve(P.data), o_tp = reserve(P.t_pos);
-    std::vector<unsigned char> img(std::max<size_t>(total, 16));
-    auto put = [&img](size_t at, const auto& v) {
-        if (!v.empty()) std::memcpy(img.data() + at, v.data(), v.size() * sizeof(v[0]));
-    };
-    put(o_ho, P.halo_off); put(o_bo, P.bnode_off); put(o_co, P.chunk_off); put(o_cdo, P.chunk_data_off);
-    put(o_trp, P.t_rp); put(o_h, P.halo); put(o_bn, P.bnodes); put(o_tr, P.t_row); put(o_lc, P.halo_lconn);
-    put(o_d, P.data); put(o_tp, P.t_pos);
-    void* blob = nullptr;
-    HCUDA(cudaMalloc(&blob, img.size()));
-    const cudaError_t ce = cudaMemcpy(blob, img.data(), img.size(), cudaMemcpyHostToDevice);
-    if (ce != cudaSuccess) {
-        cudaFree(blob);
-        return set_error(TGK_ERR_CUDA, std::string("scalar entry plan upload: ") + cudaGetErrorString(ce));
-    }
-    auto* base = static_cast<unsigned char*>(blob);
-    D.blob = blob;
-    D.bytes = static_cast<int64_t>(img.size());
-    D.T = P.T;
-    D.C = P.C;
-    D.n_blocks = P.n_blocks;
-    D.max_bnodes = P.max_bnodes;
-    D.max_chunk_u16 = P.max_chunk_u16;
-    D.max_chunks = P.max_chunks;
-    D.n_halo = P.n_halo;
-    D.row_lo = lo;
-    D.row_hi = hi;
-    D.elem_lo = elo;
-    D.elem_hi = ehi;
-    D.halo_off = reinterpret_cast<const int64_t*>(base + o_ho);
-    D.bnode_off = reinterpret_cast<const int64_t*>(base + o_bo);
-    D.chunk_off = reinterpret_cast<const int64_t*>(base + o_co);
-    D.chunk_data_off = reinterpret_cast<const int64_t*>(base + o_cdo);
-    D.t_rp = reinterpret_cast<const int64_t*>(base + o_trp);
-    D.halo = reinterpret_cast<const uint32_t*>(base + o_h);
-    D.bnodes = reinterpret_cast<const uint32_t*>(base + o_bn);
-    D.t_row = reinterpret_cast<const uint32_t*>(base + o_tr);
-    D.halo_lconn = reinterpret_cast<const uint16_t*>(base + o_lc);
-    D.data = reinterpret_cast<const uint16_t*>(base + o_d);
-    D.t_pos = reinterpret_cast<const uint64_t*>(base + o_tp);
-    *out = &D;
-    return TGK_OK;
-}
-
 int routing_flags(tgk_routing* r, unsigned long long** out) {
     if (!r->flags) HCUDA(cudaMalloc(&r->flags, 4 * sizeof(unsigned long long)));
     *out = r->flags;
@@ -877,7 +797,8 @@ static int check_field(const tgk_field& f, const tgk_mesh* m, const char* what) 
 int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
                  double* M, cudaStream_t st, unsigned long long* d_bad) {
     if (!p || !m || !r) return set_error(TGK_ERR_INPUT, "tgk_assemble: null argument");
-    if (p->mode != TGK_MODE_EXACT) return set_error(TGK_ERR_INPUT, "tgk_assemble: unknown arithmetic mode");
+    if (p->mode != TGK_MODE_EXACT && p->mode != TGK_MODE_FAST)
+        return set_error(TGK_ERR_INPUT, "tgk_assemble: unknown arithmetic mode");
     if (m->kind != TGK_TRI3 && m->kind != TGK_TET4)
         return set_error(TGK_ERR_INPUT, "P1 assembly supports TRI3 and TET4 meshes only");
     const int comps = p->kind == TGK_ELASTICITY ? m->d : 1;
@@ -900,6 +821,10 @@ int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double
         // behind TGK_ELAST_MATERIALISED=1 (needs a routing with segment maps)
         if (getenv("TGK_ELAST_MATERIALISED")) return elasticity_assemble(p, m, r, K, F, st);
         return fused_elasticity_assemble(p, m, r, K, F, st);
+    }
+    if (p->mode == TGK_MODE_FAST) {
+        const int rc = fast_scalar_assemble(p, m, r, K, F, M, st, d_bad);
+        if (rc != kFastNotApplicable) return rc;
     }
     return fused_scalar_assemble(p, m, r, K, F, M, st, d_bad);
 }

@@ -256,217 +256,6 @@ int build_group_plan(int kind, int64_t N, int64_t E, const double* nodes, const 
     return TGK_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Scalar entry plan (see tgk_internal.hpp).  Returns TGK_ERR_INPUT (no message
-// needed by the caller, which falls back to the row-block kernel) when a row
-// is too long for 4 threads of 8 slots or a slot gets more than 255 items in
-// one chunk.
-int build_scalar_entry_plan(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
-                            const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
-                            int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int T, int C,
-                            int R_max, ScalarEntryPlanHost& P) {
-    const int k = element_nodes(kind);
-    const int KU = k * (k + 1) / 2;  // unique K_e values; F_e rows follow
-    constexpr int S = kSlotsPerThread;
-    P = ScalarEntryPlanHost{};
-    P.T = T;
-    P.C = C;
-    if (C > 256 || T % 32 != 0) return set_error(TGK_ERR_INPUT, "scalar entry plan: C <= 256, T multiple of 32");
-    auto in_range = [elem_lo, elem_hi](uint32_t e) { return int64_t(e) >= elem_lo && int64_t(e) < elem_hi; };
-    const std::vector<uint32_t> order = morton_order(kind, N, nodes, row_lo, row_hi);
-    // --- blocks: consecutive Morton rows while their threads fit
-    std::vector<int64_t> bstart{0};
-    {
-        int used = 0, nrow = 0;
-        for (size_t i = 0; i < order.size(); ++i) {
-            const int len = static_cast<int>(row_ptr[order[i] + 1] - row_ptr[order[i]]);
-            const int tpr = (len + 1 + S - 1) / S;
-            if (tpr > 4) return set_error(TGK_ERR_INPUT, "scalar entry plan: row longer than 31 entries");
-            if (used + tpr > T || nrow == R_max) {
-                bstart.push_back(static_cast<int64_t>(i));
-                used = 0;
-                nrow = 0;
-            }
-            used += tpr;
-            ++nrow;
-        }
-        bstart.push_back(static_cast<int64_t>(order.size()));
-        if (order.empty()) bstart = {0};
-    }
-    const int64_t nb = static_cast<int64_t>(bstart.size()) - 1;
-    P.n_blocks = nb;
-    struct BlockOut {
-        std::vector<uint32_t> halo, bnodes;
-        std::vector<uint16_t> lconn;
-        std::vector<int64_t> t_rp;
-        std::vector<uint32_t> t_row;
-        std::vector<uint64_t> t_pos;
-        std::vector<std::vector<uint16_t>> seg;  // per chunk
-        int err = 0;
-    };
-    std::vector<BlockOut> out(nb);
-    const int W = T / 32;
-    auto work = [&](int64_t b0, int64_t b1) {
-        for (int64_t b = b0; b < b1; ++b) {
-            BlockOut& o = out[b];
-            const uint32_t* rows = order.data() + bstart[b];
-            const int nr = static_cast<int>(bstart[b + 1] - bstart[b]);
-            o.halo = order_block_halo(k, conn, rows, nr, vec_offsets, vec_slots, elem_lo, elem_hi, C);
-            const int64_t nh = static_cast<int64_t>(o.halo.size());
-            if (nh > 65535) { o.err = 1; return; }
-            std::vector<std::pair<uint32_t, uint32_t>> where(nh);
-            for (int64_t h = 0; h < nh; ++h) where[h] = {o.halo[h], static_cast<uint32_t>(h)};
-            std::sort(where.begin(), where.end());
-            for (uint32_t e : o.halo)
-                for (int a = 0; a < k; ++a) o.bnodes.push_back(static_cast<uint32_t>(conn[int64_t(e) * k + a]));
-            std::sort(o.bnodes.begin(), o.bnodes.end());
-            o.bnodes.erase(std::unique(o.bnodes.begin(), o.bnodes.end()), o.bnodes.end());
-            if (o.bnodes.size() > 65535) { o.err = 1; return; }
-            o.lconn.assign(nh * 4, 0);
-            for (int64_t h = 0; h < nh; ++h)
-                for (int a = 0; a < k; ++a) {
-                    const uint32_t g = static_cast<uint32_t>(conn[int64_t(o.halo[h]) * k + a]);
-                    o.lconn[h * 4 + a] = static_cast<uint16_t>(std::lower_bound(o.bnodes.begin(), o.bnodes.end(), g) - o.bnodes.begin());
-                }
-            const int64_t nch = (nh + C - 1) / C;
-            // per thread: its slots' item lists per chunk
-            o.t_rp.assign(T, -1);
-            o.t_row.assign(T, 0);
-            o.t_pos.assign(T, ~0ull);
-            std::vector<std::vector<std::vector<uint16_t>>> items(T, std::vector<std::vector<uint16_t>>(nch * S));
-            int t0 = 0;
-            for (int r = 0; r < nr; ++r) {
-                const uint32_t row = rows[r];
-                const int64_t rp = row_ptr[row];
-                const int len = static_cast<int>(row_ptr[row + 1] - rp);
-                const int tpr = (len + 1 + S - 1) / S;
-                // per entry and per chunk item lists (ascending element: vec slots are ascending)
-                std::vector<std::vector<std::vector<uint16_t>>> ent(len + 1, std::vector<std::vector<uint16_t>>(nch));
-                int diag = -1;
-                for (uint32_t s2 = vec_offsets[row]; s2 < vec_offsets[row + 1]; ++s2) {
-                    const uint32_t slot = vec_slots[s2];
-                    const uint32_t e = slot / k;
-                    const int a = static_cast<int>(slot % k);
-                    if (diag < 0) diag = static_cast<int>(slot_of[int64_t(slot) * k + a] - rp);
-                    if (!in_range(e)) continue;
-                    const uint32_t hp = std::lower_bound(where.begin(), where.end(), std::make_pair(e, 0u))->second;
-                    const int64_t ch = hp / C;
-                    const uint16_t h = static_cast<uint16_t>(hp % C);
-                    for (int bb = 0; bb < k; ++bb) {
-                        const int pos = static_cast<int>(slot_of[int64_t(slot) * k + bb] - rp);
-                        ent[pos][ch].push_back(static_cast<uint16_t>(h | (sym_pair(k, a, bb) << 8) | ((a * k + bb) << 12)));
-                    }
-                    ent[len][ch].push_back(static_cast<uint16_t>(h | ((KU + a) << 8)));  // the load F
-                }
-                // slot list: diagonal, F, then the off-diagonal positions ascending
-                std::vector<int> L;
-                if (diag >= 0) L.push_back(diag);
-                L.push_back(len);
-                for (int q = 0; q < len; ++q)
-                    if (q != diag) L.push_back(q);
-                for (int part = 0; part < tpr; ++part) {
-                    const int t = t0 + part;
-                    o.t_rp[t] = rp;
-                    o.t_row[t] = row;
-                    uint64_t codes = ~0ull;
-                    for (int u = 0; u < S; ++u) {
-                        const size_t li = static_cast<size_t>(part + u * tpr);
-                        if (li >= L.size()) break;
-                        const int q = L[li];
-                        const uint64_t code = q == len ? 0xFEull : static_cast<uint64_t>(q);
-                        codes = (codes & ~(0xFFull << (8 * u))) | (code << (8 * u));
-                        for (int64_t ch = 0; ch < nch; ++ch) items[t][ch * S + u] = std::move(ent[q][ch]);
-                    }
-                    o.t_pos[t] = codes;
-                }
-                t0 += tpr;
-            }
-            // chunk segments
-            o.seg.resize(nch);
-            for (int64_t ch = 0; ch < nch; ++ch) {
-                std::vector<uint16_t>& sg = o.seg[ch];
-                std::vector<int> tot(T, 0);
-                sg.assign(size_t(T) * 4 + 8, 0);
-                for (int t = 0; t < T; ++t) {
-                    uint64_t ends = 0;
-                    int acc = 0;
-                    for (int u = 0; u < S; ++u) {
-                        acc += static_cast<int>(items[t][ch * S + u].size());
-                        if (acc > 255) { o.err = 2; return; }
-                        ends |= uint64_t(acc) << (8 * u);
-                    }
-                    tot[t] = acc;
-                    std::memcpy(&sg[size_t(t) * 4], &ends, 8);
-                }
-                for (int w = 0; w < W; ++w) {
-                    int steps = 0;
-                    for (int l = 0; l < 32; ++l) steps = std::max(steps, tot[w * 32 + l]);
-                    sg[size_t(T) * 4 + w] = static_cast<uint16_t>(steps);
-                    const size_t base = sg.size();
-                    sg.resize(base + size_t(steps) * 32, 0);
-                    for (int l = 0; l < 32; ++l) {
-                        int s2 = 0;
-                        for (int u = 0; u < S; ++u)
-                            for (uint16_t it : items[w * 32 + l][ch * S + u]) sg[base + size_t(s2++) * 32 + l] = it;
-                    }
-                }
-                while (sg.size() % 8) sg.push_back(0);
-            }
-        }
-    };
-    const int nthreads = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    {
-        std::vector<std::thread> pool;
-        const int64_t per = (nb + nthreads - 1) / nthreads;
-        for (int t = 0; t < nthreads; ++t) {
-            const int64_t b0 = t * per, b1 = std::min(nb, b0 + per);
-            if (b0 < b1) pool.emplace_back(work, b0, b1);
-        }
-        for (auto& th : pool) th.join();
-    }
-    for (const auto& o : out)
-        if (o.err) return set_error(TGK_ERR_INPUT, o.err == 1 ? "scalar entry plan: block halo too large"
-                                                              : "scalar entry plan: more than 255 items per thread and chunk");
-    P.halo_off.assign(nb + 1, 0);
-    P.bnode_off.assign(nb + 1, 0);
-    P.chunk_off.assign(nb + 1, 0);
-    for (int64_t b = 0; b < nb; ++b) {
-        P.halo_off[b + 1] = P.halo_off[b] + static_cast<int64_t>(out[b].halo.size());
-        P.bnode_off[b + 1] = P.bnode_off[b] + static_cast<int64_t>(out[b].bnodes.size());
-        P.chunk_off[b + 1] = P.chunk_off[b] + static_cast<int64_t>(out[b].seg.size());
-        P.max_bnodes = std::max<int>(P.max_bnodes, static_cast<int>(out[b].bnodes.size()));
-        P.max_chunks = std::max<int>(P.max_chunks, static_cast<int>(out[b].seg.size()));
-    }
-    P.n_halo = P.halo_off[nb];
-    P.chunk_data_off.assign(P.chunk_off[nb] + 1, 0);
-    {
-        int64_t c = 0;
-        for (int64_t b = 0; b < nb; ++b)
-            for (const auto& sg : out[b].seg) {
-                P.chunk_data_off[c + 1] = P.chunk_data_off[c] + static_cast<int64_t>(sg.size());
-                P.max_chunk_u16 = std::max<int>(P.max_chunk_u16, static_cast<int>(sg.size()));
-                ++c;
-            }
-    }
-    P.halo.reserve(P.n_halo);
-    P.halo_lconn.reserve(P.n_halo * 4);
-    P.bnodes.reserve(P.bnode_off[nb]);
-    P.data.reserve(P.chunk_data_off.back());
-    P.t_rp.reserve(nb * T);
-    P.t_row.reserve(nb * T);
-    P.t_pos.reserve(nb * T);
-    for (auto& o : out) {
-        P.halo.insert(P.halo.end(), o.halo.begin(), o.halo.end());
-        P.halo_lconn.insert(P.halo_lconn.end(), o.lconn.begin(), o.lconn.end());
-        P.bnodes.insert(P.bnodes.end(), o.bnodes.begin(), o.bnodes.end());
-        for (const auto& sg : o.seg) P.data.insert(P.data.end(), sg.begin(), sg.end());
-        P.t_rp.insert(P.t_rp.end(), o.t_rp.begin(), o.t_rp.end());
-        P.t_row.insert(P.t_row.end(), o.t_row.begin(), o.t_row.end());
-        P.t_pos.insert(P.t_pos.end(), o.t_pos.begin(), o.t_pos.end());
-    }
-    P.data_bytes = static_cast<int64_t>(P.data.size()) * 2;
-    return TGK_OK;
-}
 
 }  // namespace tgk
 

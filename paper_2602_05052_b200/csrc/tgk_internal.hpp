@@ -174,50 +174,58 @@ struct GroupPlanDev {
 int build_group_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn, int G,
                      GroupPlanHost& P);
 
-// Scalar entry plan (plan_entries.cpp build_scalar_entry_plan, fused.cu
-// k_fused_entries): blocks of up to T threads; every owned row gets
-// ceil((len + 1) / 8) threads of 8 slots each (slot = one CSR entry of the row
-// or its load F; the diagonal and F take slot 0 of the row's first two
-// threads).  Per chunk of C halo elements one data segment: per thread the 8
-// cumulative item counts (u8), per warp the number of item steps, then the
-// items of each warp [step][lane] — item = h | t << 8 | ab << 12 with h the
-// element's chunk position, t the index of the value in the element's SoA
-// value rows (K_e[a][b] unique (a <= b) rows, then F_e[a] rows) and ab = a k
-// + b the row of M_e[a][b].  Items of a slot are in ascending element id.
-constexpr int kSlotsPerThread = 8;
-struct ScalarEntryPlanHost {
-    int T = 256, C = 256;
+// Fast-mode plan (plan_fast.cpp, fast.cu k_fast_scalar): blocks of R owned
+// rows with their whole halo resident in shared memory; per owned CSR entry
+// its element-to-slot list (u16 items = halo index | value index << 12),
+// folded in a register by one lane.  Entry descriptor (u32): bits 0-8 local
+// row, 9-14 position in the row (63: none), 15 diagonal entry (also the row's
+// load), 16-24 / 25-30 local row / position of the mirrored entry (j, i),
+// 31 mirrored.  kFastIdle marks a padding slot.
+constexpr int kFastMaxRows = 511;
+constexpr int kFastMaxRowLen = 62;
+constexpr int kFastNoPos = 63;
+constexpr int kFastMaxHalo = 4095;
+constexpr uint32_t kFastIdle = 0xffffffffu;
+constexpr int kFastNotApplicable = -100;  // fast_scalar_assemble: take the exact kernel
+struct FastPlanHost {
+    int R = 64;
     int64_t n_blocks = 0;
-    int max_bnodes = 0, max_chunk_u16 = 0, max_chunks = 0;
-    int64_t n_halo = 0, data_bytes = 0;
-    std::vector<int64_t> halo_off, bnode_off, chunk_off, chunk_data_off;
-    std::vector<uint32_t> halo, bnodes;
-    std::vector<uint16_t> halo_lconn;  // 4 per halo element
-    std::vector<int64_t> t_rp;         // per block x T: CSR offset of the thread's row (-1: idle)
-    std::vector<uint32_t> t_row;       // per block x T: row (node) id
-    std::vector<uint64_t> t_pos;       // per block x T: 8 slot codes (CSR position, 0xFE load, 0xFF none)
-    std::vector<uint16_t> data;        // chunk segments, 16-byte multiples
+    int max_halo = 0, max_bnodes = 0, max_rows = 0;
+    std::vector<int64_t> row_off, halo_off, bnode_off, ent_off;  // n_blocks+1 each (ent_off: multiples of 32)
+    std::vector<uint32_t> rows, helem, bnodes, desc;
+    std::vector<uint64_t> hconn;    // 4 x u16 block-local node indices per halo element
+    std::vector<int64_t> wg_item;   // per 32 entry slots: first item (u16 units), +1
+    std::vector<uint16_t> items;    // per warp group [step][lane][4]
 };
 
-struct ScalarEntryPlanDev {
-    int T = 0, C = 0;
+// Device form: two byte records per block, each one TMA bulk copy into shared
+// memory (fast.cu).  Record A (prologue + phase A): header {int64 halo base,
+// u32 rows, halo, nodes, tile}, per row int64 CSR offset, u32 row id, u16 tile
+// offset (n+1), u32 node table, u64 block-local connectivity.  Record B
+// (phase B): header {u32 entries, warp groups}, u32 descriptors, u32 warp-group
+// item offsets (n+1), u16 items.  Sections 16-byte aligned.
+struct FastPlanDev {
+    int R = 0;
     int64_t n_blocks = 0;
-    int max_bnodes = 0, max_chunk_u16 = 0, max_chunks = 0;
-    int64_t n_halo = 0, bytes = 0;
+    int max_halo = 0, max_bnodes = 0, max_rows = 0, max_tile = 0;
+    int max_rec_a = 0, max_rec_b = 0;  // bytes
+    int64_t n_halo = 0, n_items = 0, n_entries = 0;
     int64_t row_lo = -1, row_hi = -1, elem_lo = -1, elem_hi = -1;  // the ranges it was built for
-    const int64_t *halo_off = nullptr, *bnode_off = nullptr, *chunk_off = nullptr, *chunk_data_off = nullptr,
-                  *t_rp = nullptr;
-    const uint32_t *halo = nullptr, *bnodes = nullptr, *t_row = nullptr;
-    const uint16_t *halo_lconn = nullptr, *data = nullptr;
-    const uint64_t* t_pos = nullptr;
+    const int64_t *rec_a_off = nullptr, *rec_b_off = nullptr;       // n_blocks+1 byte offsets
+    const unsigned char *rec_a = nullptr, *rec_b = nullptr;
+    const uint32_t* helem = nullptr;  // halo element ids (per-element fields, bad-element report)
     void* blob = nullptr;
+    int64_t bytes = 0;
     void release();
 };
 
-int build_scalar_entry_plan(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
-                            const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
-                            int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi, int T, int C,
-                            int R_max, ScalarEntryPlanHost& P);
+// Returns TGK_ERR_INPUT WITHOUT an error message when the fast layout does not
+// apply (row longer than kFastMaxRowLen, halo larger than kFastMaxHalo):
+// the caller then takes the exact kernel.
+int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
+                    const int64_t* row_ptr, const uint32_t* vec_offsets, const uint32_t* vec_slots,
+                    const uint32_t* slot_of, int64_t row_lo, int64_t row_hi, int64_t elem_lo, int64_t elem_hi,
+                    int R, FastPlanHost& P);
 
 int build_entry_plan(int kind, int64_t N, const double* nodes, const int32_t* conn, const int64_t* row_ptr,
                      const uint32_t* vec_offsets, const uint32_t* vec_slots, const uint32_t* slot_of,
@@ -258,7 +266,7 @@ struct tgk_routing {
     tgk::PlanDev plan[tgk::kPlanSlots];
     tgk::EntryPlanDev entry_plan;    // batched kernel plan (built on first batched call)
     tgk::GroupPlanDev group_plan;    // adjoint gather plan (built on first adjoint call)
-    tgk::ScalarEntryPlanDev se_plan; // scalar entry-owned fused kernel plan
+    tgk::FastPlanDev fast_plan;      // fast-mode plan (TGK_MODE_FAST)
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
     int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
     double* scr[6] = {};             // cached device scratch (materialised elasticity path)
@@ -279,5 +287,14 @@ int ensure_entry_plan(tgk_routing* r, int R, const EntryPlanDev** out);
 // is used by one stream at a time.
 int routing_flags(tgk_routing* r, unsigned long long** out);
 int ensure_group_plan(tgk_routing* r, int G, const GroupPlanDev** out);
-int ensure_scalar_entry_plan(tgk_routing* r, const ScalarEntryPlanDev** out);
+// Fast-mode plan for R rows per block over the routing's owned rows / element
+// range; TGK_ERR_INPUT without a message when the fast layout does not apply.
+int ensure_fast_plan(tgk_routing* r, int R, const FastPlanDev** out);
+struct ScalarRoutingHost {
+    std::vector<double> nodes;
+    std::vector<int32_t> conn;
+    std::vector<int64_t> row_ptr;
+    std::vector<uint32_t> vo, vs, slot;
+};
+int fetch_scalar_routing(const tgk_routing* r, ScalarRoutingHost& h);
 }

@@ -158,8 +158,11 @@ class Routing:
         return self
 
 
+MODES = {"exact": 0, "fast": 1}
+
+
 def make_problem(kind="poisson", diffusion=1.0, lam=1.0, mu=1.0, plane_stress=False, sources=(),
-                 with_mass=False, keep=None):
+                 with_mass=False, keep=None, mode="exact"):
     keep = [] if keep is None else keep
     p = N.Problem()
     p.kind = {"poisson": N.POISSON, "elasticity": N.ELASTICITY, "mass": N.MASS}[kind]
@@ -171,15 +174,21 @@ def make_problem(kind="poisson", diffusion=1.0, lam=1.0, mu=1.0, plane_stress=Fa
     for i, s in enumerate(sources):
         p.source[i] = field(s, keep)
     p.with_mass = int(bool(with_mass))
-    p.mode = N.MODE_EXACT
+    p.mode = MODES[mode]
     return p, keep
 
 
 def assemble(mesh: DeviceMesh, routing: Routing, kind="poisson", diffusion=1.0, lam=1.0, mu=1.0,
-             plane_stress=False, sources=(), with_mass=False, dtype=torch.float64, out=None, stream=None):
+             plane_stress=False, sources=(), with_mass=False, dtype=torch.float64, out=None, stream=None,
+             mode="exact"):
     """tg::assemble (physics.cpp:10-75) on the GPU.  Returns (K values, F, M values | None).
-    dtype=torch.float32 runs the fp32 variant (tgk_assemble_f32_d, scalar problems)."""
-    p, keep = make_problem(kind, diffusion, lam, mu, plane_stress, sources, with_mass)
+    mode="exact": bit-identical to the reference; mode="fast": within the 1e-12
+    scaled tolerance of SURVEY.md 8(c), deterministic (TGK_MODE_FAST).
+    dtype=torch.float32 runs the fp32 variant (tgk_assemble_f32_d, scalar problems).
+    A Mass problem returns no M (physics.cpp:25-31 returns before with_mass)."""
+    if kind == "mass":
+        with_mass = False
+    p, keep = make_problem(kind, diffusion, lam, mu, plane_stress, sources, with_mass, mode=mode)
     if out is None:
         K = torch.empty(routing.nnz, dtype=dtype, device=_DEV)
         F = torch.empty(routing.N, dtype=dtype, device=_DEV)
@@ -196,9 +205,11 @@ def assemble(mesh: DeviceMesh, routing: Routing, kind="poisson", diffusion=1.0, 
 
 
 def assemble_host(mesh: DeviceMesh, routing: Routing, kind="poisson", diffusion=1.0, lam=1.0,
-                  mu=1.0, plane_stress=False, sources=(), with_mass=False, out=None):
+                  mu=1.0, plane_stress=False, sources=(), with_mass=False, out=None, mode="exact"):
     """Same as assemble() through the host-buffer C-ABI entry (copies inside the call)."""
     keep = []
+    if kind == "mass":
+        with_mass = False
 
     def hfield(spec):
         if spec is None or isinstance(spec, (int, float)):
@@ -217,7 +228,7 @@ def assemble_host(mesh: DeviceMesh, routing: Routing, kind="poisson", diffusion=
     for i, s in enumerate(sources):
         p.source[i] = hfield(s)
     p.with_mass = int(bool(with_mass))
-    p.mode = N.MODE_EXACT
+    p.mode = MODES[mode]
     if out is None:
         K = np.empty(routing.nnz)
         F = np.empty(routing.N)

@@ -1,0 +1,184 @@
+"""GPU parity of the fast mode (TGK_MODE_FAST, csrc/fast.cu + csrc/plan_fast.cpp).
+
+The north star's contract: CSR pattern bit-exact (the fast
+mode shares the routing), values within |dv| <= 1e-12 |v_ref| + 1e-14 max|v_ref|
+against the reference (oracle restatement or the unmodified reference library
+oracle/_ref/libtgref.so), and run-to-run bitwise determinism.
+
+Reference semantics: tg::assemble (proj/src/physics.cpp:10-75) with the local
+kernels of proj/src/batch.cpp:156-289 and reduce_matrix/reduce_vector
+(proj/src/routing.cpp:87-132).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import port  # noqa: E402
+from tests._util import assert_bitwise, assert_scaled_close  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def eng():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_05052_b200 import engine
+    return engine
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def permuted(nodes, elems, seed):
+    rng = np.random.default_rng(seed)
+    pn = rng.permutation(nodes.shape[0])
+    inv = np.argsort(pn)
+    return nodes[pn], inv[elems][rng.permutation(elems.shape[0])]
+
+
+def meshes():
+    from paper_2602_05052_b200 import meshgen
+    yield "tri3-grid", "tri3", *port.generate_grid("tri3", [1.0, 1.3], [83, 61])
+    yield "tet4-grid", "tet4", *port.generate_grid("tet4", [1.0, 0.8, 1.1], [19, 14, 17])
+    yield "tri3-unstructured", "tri3", *meshgen.unstructured_tri(64)
+    yield "tet4-permuted", "tet4", *permuted(*port.generate_grid("tet4", [1.0, 1.0, 1.0], [11, 9, 10]), 5)
+
+
+CASES = [
+    ("K+F", dict(sources=[1.0])),
+    ("K", dict()),
+    ("K+M+F", dict(sources=[1.0], with_mass=True)),
+    ("K(2.5)+M", dict(diffusion=2.5, with_mass=True)),
+    ("elem K+F(elem)+M", "elem"),
+    ("nodal K+F(nodal)", "nodal"),
+    ("nodal K+F(const)+M", "nodal-m"),
+    ("mass(const)", dict(problem="mass", diffusion=1.7)),
+    ("mass(elem)", "mass-elem"),
+    ("mass(nodal) -> exact kernel", "mass-nodal"),
+]
+
+
+def _kw(case, E, Nn):
+    rng = np.random.default_rng(7)
+    rho, nod = 0.5 + rng.random(E), 0.5 + rng.random(Nn)
+    if isinstance(case, dict):
+        return dict(case)
+    return {
+        "elem": dict(diffusion=("element", rho), sources=[("element", rho)], with_mass=True),
+        "nodal": dict(diffusion=("nodal", nod), sources=[("nodal", nod)]),
+        "nodal-m": dict(diffusion=("nodal", nod), sources=[2.0], with_mass=True),
+        "mass-elem": dict(problem="mass", diffusion=("element", rho)),
+        "mass-nodal": dict(problem="mass", diffusion=("nodal", nod)),
+    }[case]
+
+
+@pytest.mark.parametrize("name,kind,nodes,elems", list(meshes()), ids=[m[0] for m in meshes()])
+def test_fast_within_tolerance_vs_oracle(eng, name, kind, nodes, elems):
+    E, Nn = elems.shape[0], nodes.shape[0]
+    m = eng.DeviceMesh(kind, nodes, elems)
+    r = eng.Routing(m, 1)
+    pr = port.Routing(Nn, port.dofmap(kind, elems, 1))
+    for label, case in CASES:
+        kw = _kw(case, E, Nn)
+        problem = kw.pop("problem", "poisson")
+        K, F, M = eng.assemble(m, r, kind=problem, mode="fast", **kw)
+        Kr, Fr, Mr = port.assemble(kind, nodes, elems, pr, problem=problem, **kw)
+        assert_scaled_close(np_(K), Kr, what=f"{name} {label} K")
+        assert_scaled_close(np_(F), Fr, what=f"{name} {label} F")
+        if Mr is not None and problem != "mass":
+            assert_scaled_close(np_(M), Mr, what=f"{name} {label} M")
+        # deterministic: a second run is bitwise identical
+        K2, F2, M2 = eng.assemble(m, r, kind=problem, mode="fast", **kw)
+        assert_bitwise(np_(K2), np_(K), f"{name} {label} K rerun")
+        assert_bitwise(np_(F2), np_(F), f"{name} {label} F rerun")
+
+
+@pytest.mark.parametrize("R", ["32", "64", "128", "200"])
+@pytest.mark.parametrize("kind,div", [("tet4", [23, 19, 21]), ("tri3", [150, 131])])
+def test_fast_rows_per_block(eng, monkeypatch, R, kind, div):
+    """Every rows-per-block choice of the fast plan (TGK_FAST_R) meets the tolerance."""
+    monkeypatch.setenv("TGK_FAST_R", R)
+    nodes, elems = port.generate_grid(kind, [1.0, 1.1, 0.9][: len(div)], div)
+    m = eng.DeviceMesh(kind, nodes, elems)
+    r = eng.Routing(m, 1)
+    pr = port.Routing(nodes.shape[0], port.dofmap(kind, elems, 1))
+    for kw in [dict(sources=[1.0]), dict(sources=[1.0], with_mass=True)]:
+        K, F, M = eng.assemble(m, r, mode="fast", **kw)
+        Kr, Fr, Mr = port.assemble(kind, nodes, elems, pr, **kw)
+        assert_scaled_close(np_(K), Kr, what=f"R={R} K")
+        assert_scaled_close(np_(F), Fr, what=f"R={R} F")
+        if Mr is not None:
+            assert_scaled_close(np_(M), Mr, what=f"R={R} M")
+
+
+def test_fast_c1_full_size(eng):
+    nodes, elems = port.generate_grid("tri3", [1.0, 1.0], [256, 256])
+    m = eng.DeviceMesh("tri3", nodes, elems)
+    r = eng.Routing(m, 1)
+    pr = port.Routing(nodes.shape[0], port.dofmap("tri3", elems, 1))
+    K, F, _ = eng.assemble(m, r, mode="fast", sources=[1.0])
+    Kr, Fr, _ = port.assemble("tri3", nodes, elems, pr, sources=[1.0])
+    assert_scaled_close(np_(K), Kr, what="C1 K")
+    assert_scaled_close(np_(F), Fr, what="C1 F")
+
+
+@pytest.mark.slow
+def test_fast_c2_c2a_full_size_vs_reference_library(eng):
+    """C2 (K+M+F) and C2a (K+F) on the 6M-tet Kuhn cube in fast mode against the
+    unmodified reference library's tg::assemble (oracle/_ref/libtgref.so)."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref/libtgref.so not built")
+    ref.set_threads(0)
+    rm = ref.Mesh.grid("tet4", [1.0, 1.0, 1.0], [100, 100, 100])
+    rr = ref.Routing(rm, 1)
+    m = eng.DeviceMesh("tet4", *port.generate_grid("tet4", [1.0] * 3, [100] * 3))
+    r = eng.Routing(m, 1)
+    for kw in [dict(sources=[1.0], with_mass=True), dict(sources=[1.0])]:
+        K, F, M = eng.assemble(m, r, mode="fast", **kw)
+        Kr, Fr, Mr = ref.assemble(rm, rr, **kw)
+        assert_scaled_close(np_(K), Kr, what=f"K {sorted(kw)}")
+        assert_scaled_close(np_(F), Fr, what=f"F {sorted(kw)}")
+        if Mr is not None:
+            assert_scaled_close(np_(M), Mr, what="M")
+        K2, _, _ = eng.assemble(m, r, mode="fast", **kw)
+        assert torch.equal(K.view(torch.int64), K2.view(torch.int64))
+
+
+def test_fast_restricted_rows_and_elements(eng):
+    """Owned-row partitions (halo mode) and element-range slabs (exchange mode)
+    in fast mode: the owned rows agree with the exact kernel within tolerance and
+    the rows outside are left untouched."""
+    from paper_2602_05052_b200 import _native as N
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [12, 10, 14])
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    Nn, E = nodes.shape[0], elems.shape[0]
+    for setter, lo, hi in [("tgk_routing_set_owned_rows", Nn // 3, 2 * Nn // 3),
+                           ("tgk_routing_set_element_range", E // 4, 3 * E // 4)]:
+        r = eng.Routing(m, 1)
+        N.check(getattr(N.lib(), setter)(r._h, lo, hi))
+        out = []
+        for mode in ["exact", "fast"]:
+            K = torch.full((r.nnz,), 7.0, dtype=torch.float64, device="cuda")
+            F = torch.full((r.N,), 7.0, dtype=torch.float64, device="cuda")
+            M = torch.full((r.nnz,), 7.0, dtype=torch.float64, device="cuda")
+            eng.assemble(m, r, sources=[1.0], with_mass=True, mode=mode, out=(K, F, M))
+            out.append((np_(K), np_(F), np_(M)))
+        for a, b, what in zip(out[0], out[1], "KFM"):
+            untouched = a == 7.0
+            assert np.array_equal(untouched, b == 7.0), f"{setter} {what}: written set differs"
+            assert_scaled_close(b[~untouched], a[~untouched], what=f"{setter} {what}")
+
+
+def test_fast_errors(eng):
+    """The smallest inverted element is reported with the reference's message (batch.cpp:124-126)."""
+    from paper_2602_05052_b200 import InputError
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [4, 4, 4])
+    bad = elems.copy()
+    bad[[5, 9]] = bad[[5, 9]][:, [1, 0, 2, 3]]  # inverted elements 5 and 9
+    m = eng.DeviceMesh("tet4", nodes, bad)
+    r = eng.Routing(m, 1)
+    with pytest.raises(InputError, match="element 5 has non-positive Jacobian determinant"):
+        eng.assemble(m, r, sources=[1.0], mode="fast")

@@ -175,36 +175,6 @@ def test_fused_assemble_bit_exact_vs_oracle(eng, kind, div):
     del rng
 
 
-@pytest.mark.parametrize("kind", ["tri3", "tet4", "unstructured"])
-def test_fused_entry_kernel_bit_exact(eng, monkeypatch, kind):
-    """The opt-in entry-owned fused kernel (TGK_FUSED_ENTRIES) against the oracle."""
-    monkeypatch.setenv("TGK_FUSED_ENTRIES", "1")
-    if kind == "unstructured":
-        from paper_2602_05052_b200 import meshgen
-        kind = "tri3"
-        nodes, elems = meshgen.unstructured_tri(50)
-    elif kind == "tri3":
-        nodes, elems = port.generate_grid("tri3", [1.0, 1.2], [61, 47])
-    else:
-        nodes, elems = port.generate_grid("tet4", [1.0, 1.2, 0.9], [17, 13, 15])
-    E, Nn = elems.shape[0], nodes.shape[0]
-    m = eng.DeviceMesh(kind, nodes, elems)
-    r = eng.Routing(m, 1)
-    pr = port.Routing(Nn, port.dofmap(kind, elems, 1))
-    rng = np.random.default_rng(7)
-    rho, nod = 0.5 + rng.random(E), 0.5 + rng.random(Nn)
-    for kw in [dict(sources=[1.0]),
-               dict(diffusion=("element", rho), sources=[1.0], with_mass=True),
-               dict(diffusion=("nodal", nod), sources=[("nodal", nod)]),
-               dict(diffusion=2.5, with_mass=True)]:
-        K, F, M = eng.assemble(m, r, **kw)
-        Kr, Fr, Mr = port.assemble(kind, nodes, elems, pr, **kw)
-        assert_bitwise(np_(K), Kr, f"K {kw.keys()}")
-        assert_bitwise(np_(F), Fr, "F")
-        if Mr is not None:
-            assert_bitwise(np_(M), Mr, "M")
-
-
 def test_assemble_host_entry_matches_device(eng):
     nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [10, 8, 6])
     m = eng.DeviceMesh("tet4", nodes, elems)
