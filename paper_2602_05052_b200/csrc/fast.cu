@@ -51,6 +51,8 @@ struct FastArgs {
     int MB;    // node-table capacity
     int abuf;  // record buffer capacities in bytes (multiples of 16)
     int bbuf;
+    int gl;     // copy-out lanes per row (8, 16 or 32 >= longest row)
+    int debug;  // profiling only (TGK_FAST_DEBUG): 1 skips phase A, 2 phase B, 4 the copy-out
     unsigned long long* bad;
 };
 
@@ -78,19 +80,23 @@ struct FastConst<TGK_TRI3> {
 // KT 0: diffusion stiffness (+ unit mass M if HAS_M), 1: coefficient mass
 // (ProblemKind::Mass).  FT: load none / scalar (f det; constant or
 // per-element source) / per node (nodal source).
+// Value rows in shared memory (row stride MH, plan_fast.cpp formats):
+// K_aa (k rows), K_ab off-diagonal pairs, [S = c det (mass) row], [F rows].
 template <int KIND, int KT, bool HAS_M, int FT>
 struct FastCfg {
     static constexpr int k = P1<KIND>::k, d = P1<KIND>::d;
     static constexpr bool HAS_S = HAS_M || KT == 1;
     static constexpr int NP = KT == 0 ? FastConst<KIND>::np : 0;
+    static constexpr int FMT = KT == 1 ? kFastFmtS16 : (HAS_M ? kFastFmtKS32 : kFastFmtK16);
     static constexpr int SROW = NP;
     static constexpr int FROW = NP + (HAS_S ? 1 : 0);
-    static constexpr int NR = FROW + (FT == 1 ? 1 : FT == 2 ? k : 0);
+    static constexpr int NR = FMT == kFastFmtS16 ? 1 : (FMT == kFastFmtKS32 ? NP + 2 : NP + (FT == 2 ? k : 1));
     static constexpr int NTILE = HAS_M ? 2 : 1;
     __host__ __device__ static int ncol(int ctype) { return d + (ctype == TGK_FIELD_NODAL ? 1 : 0) + (FT == 2 ? 1 : 0); }
     static size_t smem(const FastArgs& a) {
-        return 64 + 2 * size_t(a.abuf) + size_t(a.bbuf) + sizeof(double) * (2 * size_t(ncol(a.ctype)) * a.MB +
-                                                                             size_t(NR) * a.MH + size_t(NTILE) * a.pl.max_tile);
+        return 64 + 2 * size_t(a.abuf) + size_t(a.bbuf) +
+               sizeof(double) * (2 * size_t(ncol(a.ctype)) * a.MB + size_t(NR) * a.MH + size_t(NTILE) * a.pl.max_tile) +
+               sizeof(int64_t) * a.pl.max_rows + sizeof(uint16_t) * (a.pl.max_rows + 1);
     }
 };
 
@@ -165,7 +171,7 @@ struct RecB {
     uint32_t ne, nwg;
     const uint32_t* desc;
     const uint32_t* wgoff;
-    const uint16_t* items;
+    const uint32_t* words;
 };
 __device__ __forceinline__ RecB parse_b(const unsigned char* r) {
     RecB b;
@@ -177,55 +183,290 @@ __device__ __forceinline__ RecB parse_b(const unsigned char* r) {
     o += al16(4 * size_t(b.ne));
     b.wgoff = reinterpret_cast<const uint32_t*>(r + o);
     o += al16(4 * size_t(b.nwg + 1));
-    b.items = reinterpret_cast<const uint16_t*>(r + o);
+    b.words = reinterpret_cast<const uint32_t*>(r + o);
     return b;
 }
 
-// Persistent kernel: CTA c takes row blocks c, c + G, c + 2G, ...  While
-// block b is computed, record A of block b+G (TMA) and then its node table
-// (cp.async gathers) and record B (TMA) stream into the spare buffers, so a
-// block's plan and coordinates are on chip before it starts.
+// ---------------------------------------------------------------- phase A: one element
+// Geometry with FMA and one reciprocal, the unique K_e values from the Gram
+// matrix of the scaled gradients (row a = 0 from the zero row sums of P1
+// stiffness), and the scalars the mass / load are formed from, stored to
+// the value rows of halo slot h.
 template <int KIND, int KT, bool HAS_M, int FT>
-__global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
+__device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, const double* xs, double* kv, int h) {
     using Cf = FastCfg<KIND, KT, HAS_M, FT>;
     using Cn = FastConst<KIND>;
     constexpr int k = Cf::k, d = Cf::d;
+    const int MH = p.MH, MB = p.MB;
+    const double* cn = xs + d * MB;
+    const double* sn = xs + (Cf::ncol(p.ctype) - 1) * MB;
+    const uint64_t hc = A.hconn[h];
+    int l[k];
+#pragma unroll
+    for (int a = 0; a < k; ++a) l[a] = static_cast<int>((hc >> (16 * a)) & 0xffff);
+    double det;
+    double kp[Cn::np];
+    auto coef_w = [&](double wsum_) -> double {
+        if (p.ctype == TGK_FIELD_CONSTANT) return p.cval * wsum_;
+        if (p.ctype == TGK_FIELD_ELEMENT) return __ldg(p.cdata + __ldg(p.pl.helem + A.hbase + h)) * wsum_;
+        double sacc = cn[l[0]];
+#pragma unroll
+        for (int a = 1; a < k; ++a) sacc += cn[l[a]];
+        return sacc * Cn::wa;
+    };
+    if constexpr (KIND == TGK_TET4) {
+        const double x0 = xs[l[0]], y0 = xs[MB + l[0]], z0 = xs[2 * MB + l[0]];
+        const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0, e1z = xs[2 * MB + l[1]] - z0;
+        const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0, e2z = xs[2 * MB + l[2]] - z0;
+        const double e3x = xs[l[3]] - x0, e3y = xs[MB + l[3]] - y0, e3z = xs[2 * MB + l[3]] - z0;
+        // rows of J^{-1} times det: grad N_b = c_b / det (b = 1..3)
+        const double c1x = __fma_rn(e2y, e3z, -(e2z * e3y)), c1y = __fma_rn(e2z, e3x, -(e2x * e3z)),
+                     c1z = __fma_rn(e2x, e3y, -(e2y * e3x));
+        const double c2x = __fma_rn(e3y, e1z, -(e3z * e1y)), c2y = __fma_rn(e3z, e1x, -(e3x * e1z)),
+                     c2z = __fma_rn(e3x, e1y, -(e3y * e1x));
+        const double c3x = __fma_rn(e1y, e2z, -(e1z * e2y)), c3y = __fma_rn(e1z, e2x, -(e1x * e2z)),
+                     c3z = __fma_rn(e1x, e2y, -(e1y * e2x));
+        det = dot3(e1x, e1y, e1z, c1x, c1y, c1z);
+        if constexpr (KT == 0) {
+            const double s = coef_w(Cn::wsum) * __drcp_rn(det);
+            const double k11 = s * dot3(c1x, c1y, c1z, c1x, c1y, c1z);
+            const double k12 = s * dot3(c1x, c1y, c1z, c2x, c2y, c2z);
+            const double k13 = s * dot3(c1x, c1y, c1z, c3x, c3y, c3z);
+            const double k22 = s * dot3(c2x, c2y, c2z, c2x, c2y, c2z);
+            const double k23 = s * dot3(c2x, c2y, c2z, c3x, c3y, c3z);
+            const double k33 = s * dot3(c3x, c3y, c3z, c3x, c3y, c3z);
+            const double k01 = -((k11 + k12) + k13), k02 = -((k12 + k22) + k23), k03 = -((k13 + k23) + k33);
+            kp[0] = -((k01 + k02) + k03);  // rows: K_aa, then 01 02 03 12 13 23
+            kp[1] = k11; kp[2] = k22; kp[3] = k33;
+            kp[4] = k01; kp[5] = k02; kp[6] = k03;
+            kp[7] = k12; kp[8] = k13; kp[9] = k23;
+        }
+    } else {
+        const double x0 = xs[l[0]], y0 = xs[MB + l[0]];
+        const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0;
+        const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0;
+        det = __fma_rn(e1x, e2y, -(e1y * e2x));
+        if constexpr (KT == 0) {
+            const double s = coef_w(Cn::wsum) * __drcp_rn(det);
+            // grad N_1 = (e2y, -e2x) / det, grad N_2 = (-e1y, e1x) / det
+            const double k11 = s * __fma_rn(e2y, e2y, e2x * e2x);
+            const double k12 = -(s * __fma_rn(e2y, e1y, e2x * e1x));
+            const double k22 = s * __fma_rn(e1y, e1y, e1x * e1x);
+            const double k01 = -(k11 + k12), k02 = -(k12 + k22);
+            kp[0] = -(k01 + k02);  // rows: K_aa, then 01 02 12
+            kp[1] = k11; kp[2] = k22;
+            kp[3] = k01; kp[4] = k02; kp[5] = k12;
+        }
+    }
+    double sv = 0.0;
+    if constexpr (KT == 1) {
+        const double c = p.ctype == TGK_FIELD_CONSTANT ? p.cval : __ldg(p.cdata + __ldg(p.pl.helem + A.hbase + h));
+        sv = c * det;
+    } else if constexpr (HAS_M) {
+        sv = det;
+    }
+    double fv[k];
+    if constexpr (FT == 1) {
+        const double f = p.stype == TGK_FIELD_CONSTANT ? p.sval : __ldg(p.sdata + __ldg(p.pl.helem + A.hbase + h));
+        fv[0] = f * det;
+    } else if constexpr (FT == 2) {
+        double fs = sn[l[0]];
+#pragma unroll
+        for (int a = 1; a < k; ++a) fs += sn[l[a]];
+        const double dm = det * Cn::moff;
+#pragma unroll
+        for (int a = 0; a < k; ++a) fv[a] = dm * (fs + sn[l[a]]);
+    }
+    if (det <= 0.0) {  // batch.cpp:98-101 (a NaN det passes, as in the reference)
+        atomicMin(p.bad, static_cast<unsigned long long>(__ldg(p.pl.helem + A.hbase + h)));
+#pragma unroll
+        for (int t = 0; t < Cn::np; ++t) kp[t] = 0.0;
+        sv = 0.0;
+#pragma unroll
+        for (int a = 0; a < k; ++a) fv[a] = 0.0;
+    }
+    if constexpr (KT == 0) {
+#pragma unroll
+        for (int t = 0; t < Cn::np; ++t) kv[t * MH + h] = kp[t];
+    }
+    if constexpr (Cf::HAS_S) kv[Cf::SROW * MH + h] = sv;
+    if constexpr (FT == 1) kv[Cf::FROW * MH + h] = fv[0];
+    if constexpr (FT == 2) {
+#pragma unroll
+        for (int a = 0; a < k; ++a) kv[(Cf::FROW + a) * MH + h] = fv[a];
+    }
+}
+
+// ---------------------------------------------------------------- phase B: one warp group of entries
+// Lane `lane` of warp group w folds its entry's items (direct value indices,
+// plan_fast.cpp formats) from the value rows into the output tile.  Two
+// steps per iteration with the next two steps' words already in flight,
+// four partial sums per value: independent loads, short add chains.
+template <int KIND, int KT, bool HAS_M, int FT>
+__device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, const RecB& Bq, const double* kv,
+                                           double* tk, double* tm, int w, int lane) {
+    using Cf = FastCfg<KIND, KT, HAS_M, FT>;
+    using Cn = FastConst<KIND>;
+    constexpr int k = Cf::k;
+    const int MH = p.MH;
+    const uint32_t desc = Bq.desc[w * 32 + lane];
+    const uint32_t i0 = Bq.wgoff[w];
+    const int steps = static_cast<int>((Bq.wgoff[w + 1] - i0) >> 6);  // 64 words per step
+    const uint2* ip = reinterpret_cast<const uint2*>(Bq.words + i0) + lane;
+    const bool diag = (__shfl_sync(0xffffffffu, desc, 0) >> 15) & 1u;  // warp-uniform class
+    double k0 = 0.0, k1 = 0.0, k2 = 0.0, k3 = 0.0, s0 = 0.0, s1 = 0.0, f0 = 0.0, f1 = 0.0;
+    constexpr bool WIDE_OFF = Cf::FMT == kFastFmtKS32;
+    const bool wide = WIDE_OFF || (Cf::FMT == kFastFmtK16 && diag);
+    const uint32_t zw = uint32_t(MH - 1) | (uint32_t(MH - 1) << 16);
+    const uint2 padw = make_uint2(zw, zw);
+    uint2 wa = steps > 0 ? ip[0] : padw;
+    uint2 wb = steps > 1 ? ip[32] : padw;
+    if (wide) {  // u32 items: low = K (or S) index, high = S / F index
+        auto eat = [&](uint32_t it, double& kk, double& ss, double& ff) {
+            const int lo = static_cast<int>(it & 0xffffu), hi = static_cast<int>(it >> 16);
+            kk += kv[lo];
+            if constexpr (Cf::FMT == kFastFmtKS32) {
+                ss += kv[hi];
+                if constexpr (FT == 1) {
+                    if (diag) ff += kv[hi + MH];
+                }
+            } else if constexpr (FT > 0) {
+                ff += kv[hi];
+            }
+        };
+        for (int st = 0; st < steps; st += 2) {
+            const uint2 wc = st + 2 < steps ? ip[(st + 2) * 32] : padw;
+            const uint2 wd = st + 3 < steps ? ip[(st + 3) * 32] : padw;
+            eat(wa.x, k0, s0, f0);
+            eat(wa.y, k1, s1, f1);
+            eat(wb.x, k2, s0, f0);
+            eat(wb.y, k3, s1, f1);
+            wa = wc;
+            wb = wd;
+        }
+    } else {  // u16 items: K (or S) index
+        for (int st = 0; st < steps; st += 2) {
+            const uint2 wc = st + 2 < steps ? ip[(st + 2) * 32] : padw;
+            const uint2 wd = st + 3 < steps ? ip[(st + 3) * 32] : padw;
+            const double v0 = kv[wa.x & 0xffffu], v1 = kv[wa.x >> 16], v2 = kv[wa.y & 0xffffu], v3 = kv[wa.y >> 16];
+            const double v4 = kv[wb.x & 0xffffu], v5 = kv[wb.x >> 16], v6 = kv[wb.y & 0xffffu], v7 = kv[wb.y >> 16];
+            k0 += v0;
+            k1 += v1;
+            k2 += v2;
+            k3 += v3;
+            k0 += v4;
+            k1 += v5;
+            k2 += v6;
+            k3 += v7;
+            wa = wc;
+            wb = wd;
+        }
+    }
+    k0 += k2;
+    k1 += k3;
+    if (diag) {  // split diagonal lists: partial sums of kFastDiagSplit lanes
+        constexpr int DS = kFastDiagSplit(k);
+#pragma unroll
+        for (int o = 1; o < DS; o <<= 1) {
+            k0 += __shfl_xor_sync(0xffffffffu, k0, o);
+            k1 += __shfl_xor_sync(0xffffffffu, k1, o);
+            if constexpr (Cf::HAS_S) {
+                s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            }
+            if constexpr (FT > 0) {
+                f0 += __shfl_xor_sync(0xffffffffu, f0, o);
+                f1 += __shfl_xor_sync(0xffffffffu, f1, o);
+            }
+        }
+    }
+    if constexpr (KT == 1) {  // S16: the K folds summed S
+        s0 = k0;
+        s1 = k1;
+    }
+    if (desc >= kFastPart) return;  // idle or a split diagonal's partial lane
+    const double kacc = k0 + k1, sacc = s0 + s1, facc = f0 + f1;
+    const int lr = static_cast<int>(desc & 0x1ffu), pos = static_cast<int>((desc >> 9) & 63u);
+    const double mh = diag ? Cn::mdiag : Cn::moff;
+    const double kval = KT == 0 ? kacc : sacc * mh;
+    if (pos != kFastNoPos) {
+        const int at = A.toff[lr] + pos;
+        tk[at] = kval;
+        if constexpr (HAS_M) tm[at] = sacc * mh;
+    }
+    if constexpr (FT > 0) {
+        if (diag) p.F[A.srow[lr]] = FT == 1 ? facc * Cn::wa : facc;
+    }
+    if (desc >> 31) {
+        const int lr2 = static_cast<int>((desc >> 16) & 0x1ffu), pos2 = static_cast<int>((desc >> 25) & 63u);
+        const int at = A.toff[lr2] + pos2;
+        tk[at] = kval;
+        if constexpr (HAS_M) tm[at] = sacc * mh;
+    }
+}
+
+// Persistent kernel: CTA c takes row blocks c, c + G, c + 2G, ... (iteration
+// it = block c + it G).  Per iteration:
+//   top       the warps write block it-1's output tile to HBM (coalesced row
+//             segments; overlaps phase A);
+//   phase A   block it's element values into the value rows;        | barrier
+//   phase B   block it+1's node table starts streaming in (cp.async
+//             gathers), then block it's CSR entries are folded into the
+//             output tile;                                          | barrier
+//   refill    TMA bulk copies of record A(it+2) and record B(it+1) into the
+//             slots just consumed.
+// A block's plan and coordinates are on chip before it starts, so no HBM
+// latency sits on a CTA's critical path.  (A warp-specialised variant —
+// producer warps running phase A of block it+1 while consumer warps fold
+// block it from a second value buffer — measured slower: 474-715 vs 370 us
+// on C2a, profiles/r02_fast_experiments.txt.)
+template <int KIND, int KT, bool HAS_M, int FT>
+__global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
+    using Cf = FastCfg<KIND, KT, HAS_M, FT>;
+    constexpr int d = Cf::d;
     extern __shared__ __align__(128) unsigned char smb[];
     const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = T >> 5;
     const int MH = p.MH, MB = p.MB;
     const FastPlanDev& pl = p.pl;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smb);  // record A slot 0 / 1, record B
-    unsigned char* const ra0 = smb + 64;
-    unsigned char* const ra1 = smb + 64 + p.abuf;
-    unsigned char* rb = smb + 64 + 2 * p.abuf;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smb);  // record A slots 0-1, record B
+    unsigned char* const ra_base = smb + 64;
+    unsigned char* const rb = ra_base + 2 * size_t(p.abuf);
     const bool cnodal = p.ctype == TGK_FIELD_NODAL;
     const int ncol = Cf::ncol(p.ctype);
-    double* const xs0 = reinterpret_cast<double*>(rb + p.bbuf);
-    double* const xs1 = xs0 + size_t(ncol) * MB;
-    double* kv = xs1 + size_t(ncol) * MB;  // NR x MH value rows
-    double* tk = kv + size_t(Cf::NR) * MH;    // output tile (K), then M
-    double* tm = tk + pl.max_tile;
+    double* const xs_base = reinterpret_cast<double*>(rb + size_t(p.bbuf));
+    double* const kv = xs_base + 2 * size_t(ncol) * MB;  // NR x MH value rows
+    double* const tk = kv + size_t(Cf::NR) * MH;          // output tile (K), then M
+    double* const tm = tk + pl.max_tile;
+    int64_t* const trp = reinterpret_cast<int64_t*>(tm + (HAS_M ? pl.max_tile : 0));  // tile rows' CSR offsets
+    uint16_t* const ttoff = reinterpret_cast<uint16_t*>(trp + pl.max_rows);           // tile row offsets (n+1)
+    auto ra = [&](int64_t it) { return ra_base + size_t(it & 1) * p.abuf; };
+    auto xsp = [&](int64_t it) { return xs_base + size_t(it & 1) * ncol * MB; };
 
-    const int64_t nb = pl.n_blocks, G = gridDim.x;
-    int64_t b = blockIdx.x;
-    if (b >= nb) return;
+    const int64_t nb = pl.n_blocks, G = gridDim.x, b0 = blockIdx.x;
+    if (b0 >= nb) return;
+    const int64_t n_it = (nb - b0 + G - 1) / G;
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        mbar_init(&bars[2], 1);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     if (tid < Cf::NR) kv[tid * MH + MH - 1] = 0.0;  // the zero slot padding items point at
     __syncthreads();
-    auto load_a = [&](int64_t blk, int slot) {
+    auto load_a = [&](int64_t it) {
+        const int64_t blk = b0 + it * G;
         const int64_t o = pl.rec_a_off[blk];
-        bulk_load(slot ? ra1 : ra0, pl.rec_a + o, static_cast<uint32_t>(pl.rec_a_off[blk + 1] - o), &bars[slot]);
+        bulk_load(ra(it), pl.rec_a + o, static_cast<uint32_t>(pl.rec_a_off[blk + 1] - o), &bars[it & 1]);
     };
-    auto load_b = [&](int64_t blk) {
+    auto load_b = [&](int64_t it) {
+        const int64_t blk = b0 + it * G;
         const int64_t o = pl.rec_b_off[blk];
         bulk_load(rb, pl.rec_b + o, static_cast<uint32_t>(pl.rec_b_off[blk + 1] - o), &bars[2]);
     };
-    auto gather = [&](const RecA& A, double* xs) {
+    auto wait_a = [&](int64_t it) { mbar_wait(&bars[it & 1], static_cast<uint32_t>((it >> 1) & 1)); };
+    auto wait_b = [&](int64_t it) { mbar_wait(&bars[2], static_cast<uint32_t>(it & 1)); };
+    auto gather = [&](int64_t it) {
+        const RecA A = parse_a(ra(it));
+        double* xs = xsp(it);
         for (int i = tid; i < int(A.nbn); i += T) {
             const int64_t g = A.bnodes[i];
 #pragma unroll
@@ -235,210 +476,59 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
         }
         cp_async_commit();
     };
-    if (tid == 0) {
-        load_a(b, 0);
-        load_b(b);
-    }
-    mbar_wait(&bars[0], 0);
-    uint32_t phs = 0b01u, phb = 0;  // bit s: parity record-A slot s completes with next
-    gather(parse_a(ra0), xs0);
-    cp_async_wait_all();
-    __syncthreads();
-    int slot = 0;
-    for (;;) {
-        const int64_t bn = b + G;
-        const RecA A = parse_a(slot ? ra1 : ra0);
-        const double* xs = slot ? xs1 : xs0;
-        const double* cn = xs + d * MB;
-        const double* sn = xs + (ncol - 1) * MB;
-        if (tid == 0 && bn < nb) {
-            fence_proxy_async();
-            load_a(bn, slot ^ 1);
-        }
-        // ---------------- phase A: element values
-        for (int h = tid; h < int(A.nh); h += T) {
-            const uint64_t hc = A.hconn[h];
-            int l[k];
-#pragma unroll
-            for (int a = 0; a < k; ++a) l[a] = static_cast<int>((hc >> (16 * a)) & 0xffff);
-            double det;
-            double kp[Cn::np];
-            auto coef_w = [&](double wsum_) -> double {
-                if (p.ctype == TGK_FIELD_CONSTANT) return p.cval * wsum_;
-                if (p.ctype == TGK_FIELD_ELEMENT) return __ldg(p.cdata + __ldg(pl.helem + A.hbase + h)) * wsum_;
-                double sacc = cn[l[0]];
-#pragma unroll
-                for (int a = 1; a < k; ++a) sacc += cn[l[a]];
-                return sacc * Cn::wa;
-            };
-            if constexpr (KIND == TGK_TET4) {
-                const double x0 = xs[l[0]], y0 = xs[MB + l[0]], z0 = xs[2 * MB + l[0]];
-                const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0, e1z = xs[2 * MB + l[1]] - z0;
-                const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0, e2z = xs[2 * MB + l[2]] - z0;
-                const double e3x = xs[l[3]] - x0, e3y = xs[MB + l[3]] - y0, e3z = xs[2 * MB + l[3]] - z0;
-                // rows of J^{-1} times det: grad N_b = c_b / det (b = 1..3)
-                const double c1x = __fma_rn(e2y, e3z, -(e2z * e3y)), c1y = __fma_rn(e2z, e3x, -(e2x * e3z)),
-                             c1z = __fma_rn(e2x, e3y, -(e2y * e3x));
-                const double c2x = __fma_rn(e3y, e1z, -(e3z * e1y)), c2y = __fma_rn(e3z, e1x, -(e3x * e1z)),
-                             c2z = __fma_rn(e3x, e1y, -(e3y * e1x));
-                const double c3x = __fma_rn(e1y, e2z, -(e1z * e2y)), c3y = __fma_rn(e1z, e2x, -(e1x * e2z)),
-                             c3z = __fma_rn(e1x, e2y, -(e1y * e2x));
-                det = dot3(e1x, e1y, e1z, c1x, c1y, c1z);
-                if constexpr (KT == 0) {
-                    const double s = coef_w(Cn::wsum) * __drcp_rn(det);
-                    const double k11 = s * dot3(c1x, c1y, c1z, c1x, c1y, c1z);
-                    const double k12 = s * dot3(c1x, c1y, c1z, c2x, c2y, c2z);
-                    const double k13 = s * dot3(c1x, c1y, c1z, c3x, c3y, c3z);
-                    const double k22 = s * dot3(c2x, c2y, c2z, c2x, c2y, c2z);
-                    const double k23 = s * dot3(c2x, c2y, c2z, c3x, c3y, c3z);
-                    const double k33 = s * dot3(c3x, c3y, c3z, c3x, c3y, c3z);
-                    // row a = 0 from the zero row sums of P1 stiffness (grad N_0 = -sum_b grad N_b)
-                    const double k01 = -((k11 + k12) + k13), k02 = -((k12 + k22) + k23), k03 = -((k13 + k23) + k33);
-                    kp[0] = -((k01 + k02) + k03);
-                    kp[1] = k01; kp[2] = k02; kp[3] = k03;
-                    kp[4] = k11; kp[5] = k12; kp[6] = k13;
-                    kp[7] = k22; kp[8] = k23; kp[9] = k33;
-                }
-            } else {
-                const double x0 = xs[l[0]], y0 = xs[MB + l[0]];
-                const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0;
-                const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0;
-                det = __fma_rn(e1x, e2y, -(e1y * e2x));
-                if constexpr (KT == 0) {
-                    const double s = coef_w(Cn::wsum) * __drcp_rn(det);
-                    // grad N_1 = (e2y, -e2x) / det, grad N_2 = (-e1y, e1x) / det
-                    const double k11 = s * __fma_rn(e2y, e2y, e2x * e2x);
-                    const double k12 = -(s * __fma_rn(e2y, e1y, e2x * e1x));
-                    const double k22 = s * __fma_rn(e1y, e1y, e1x * e1x);
-                    const double k01 = -(k11 + k12), k02 = -(k12 + k22);
-                    kp[0] = -(k01 + k02);
-                    kp[1] = k01; kp[2] = k02;
-                    kp[3] = k11; kp[4] = k12; kp[5] = k22;
-                }
-            }
-            double sv = 0.0;
-            if constexpr (KT == 1) {
-                const double c =
-                    p.ctype == TGK_FIELD_CONSTANT ? p.cval : __ldg(p.cdata + __ldg(pl.helem + A.hbase + h));
-                sv = c * det;
-            } else if constexpr (HAS_M) {
-                sv = det;
-            }
-            double fv[k];
-            if constexpr (FT == 1) {
-                const double f =
-                    p.stype == TGK_FIELD_CONSTANT ? p.sval : __ldg(p.sdata + __ldg(pl.helem + A.hbase + h));
-                fv[0] = f * det;
-            } else if constexpr (FT == 2) {
-                double fs = sn[l[0]];
-#pragma unroll
-                for (int a = 1; a < k; ++a) fs += sn[l[a]];
-                const double dm = det * Cn::moff;
-#pragma unroll
-                for (int a = 0; a < k; ++a) fv[a] = dm * (fs + sn[l[a]]);
-            }
-            if (det <= 0.0) {  // batch.cpp:98-101 (a NaN det passes, as in the reference)
-                atomicMin(p.bad, static_cast<unsigned long long>(__ldg(pl.helem + A.hbase + h)));
-#pragma unroll
-                for (int t = 0; t < Cn::np; ++t) kp[t] = 0.0;
-                sv = 0.0;
-#pragma unroll
-                for (int a = 0; a < k; ++a) fv[a] = 0.0;
-            }
-            if constexpr (KT == 0) {
-#pragma unroll
-                for (int t = 0; t < Cn::np; ++t) kv[t * MH + h] = kp[t];
-            }
-            if constexpr (Cf::HAS_S) kv[Cf::SROW * MH + h] = sv;
-            if constexpr (FT == 1) kv[Cf::FROW * MH + h] = fv[0];
-            if constexpr (FT == 2) {
-#pragma unroll
-                for (int a = 0; a < k; ++a) kv[(Cf::FROW + a) * MH + h] = fv[a];
-            }
-        }
-        __syncthreads();
-        // next block's node table streams in during phase B
-        if (bn < nb) {
-            mbar_wait(&bars[slot ^ 1], (phs >> (slot ^ 1)) & 1u);
-            phs ^= 1u << (slot ^ 1);
-            gather(parse_a(slot ? ra0 : ra1), slot ? xs0 : xs1);
-        }
-        mbar_wait(&bars[2], phb);
-        phb ^= 1;
-        const RecB Bq = parse_b(rb);
-        // ---------------- phase B: one lane per CSR entry, register folds into the output tile
-        for (int s = tid; s < int(Bq.ne); s += T) {
-            const uint32_t desc = Bq.desc[s];
-            const int w = s >> 5;
-            const uint32_t i0 = Bq.wgoff[w];
-            const int steps = static_cast<int>((Bq.wgoff[w + 1] - i0) >> 7);
-            const uint2* ip = reinterpret_cast<const uint2*>(Bq.items + i0) + lane;
-            const bool diag = (__shfl_sync(0xffffffffu, desc, 0) >> 15) & 1u;  // warp-uniform class
-            double kacc = 0.0, sacc = 0.0, facc = 0.0;
-            if (diag) {
-                for (int st = 0; st < steps; ++st) {
-                    const uint2 wv = ip[st * 32];
-                    const uint32_t its[4] = {wv.x & 0xffffu, wv.x >> 16, wv.y & 0xffffu, wv.y >> 16};
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int h = static_cast<int>(its[j] & 0xfffu), a = static_cast<int>(its[j] >> 12);
-                        if constexpr (KT == 0) kacc += kv[(a * k - ((a * (a - 1)) >> 1)) * MH + h];
-                        if constexpr (Cf::HAS_S) sacc += kv[Cf::SROW * MH + h];
-                        if constexpr (FT == 1) facc += kv[Cf::FROW * MH + h];
-                        if constexpr (FT == 2) facc += kv[(Cf::FROW + a) * MH + h];
-                    }
-                }
-            } else {
-                for (int st = 0; st < steps; ++st) {
-                    const uint2 wv = ip[st * 32];
-                    const uint32_t its[4] = {wv.x & 0xffffu, wv.x >> 16, wv.y & 0xffffu, wv.y >> 16};
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int h = static_cast<int>(its[j] & 0xfffu), q = static_cast<int>(its[j] >> 12);
-                        if constexpr (KT == 0) kacc += kv[q * MH + h];
-                        if constexpr (Cf::HAS_S) sacc += kv[Cf::SROW * MH + h];
-                    }
-                }
-            }
-            if (desc == kFastIdle) continue;
-            const int lr = static_cast<int>(desc & 0x1ffu), pos = static_cast<int>((desc >> 9) & 63u);
-            const double mh = diag ? Cn::mdiag : Cn::moff;
-            const double kval = KT == 0 ? kacc : sacc * mh;
-            if (pos != kFastNoPos) {
-                const int at = A.toff[lr] + pos;
-                tk[at] = kval;
-                if constexpr (HAS_M) tm[at] = sacc * mh;
-            }
-            if constexpr (FT > 0) {
-                if (diag) p.F[A.srow[lr]] = FT == 1 ? facc * Cn::wa : facc;
-            }
-            if (desc >> 31) {
-                const int lr2 = static_cast<int>((desc >> 16) & 0x1ffu), pos2 = static_cast<int>((desc >> 25) & 63u);
-                const int at = A.toff[lr2] + pos2;
-                tk[at] = kval;
-                if constexpr (HAS_M) tm[at] = sacc * mh;
-            }
-        }
-        __syncthreads();
-        if (tid == 0 && bn < nb) {
-            fence_proxy_async();
-            load_b(bn);
-        }
-        // ---------------- coalesced copy-out: one warp per owned row
-        for (int lr = warp; lr < int(A.nr); lr += nwarp) {
-            const int64_t rp = A.rp[lr];
-            const int t0 = A.toff[lr], len = A.toff[lr + 1] - t0;
-            for (int q = lane; q < len; q += 32) {
+    // the previous block's tile to HBM: groups of GL lanes per row
+    int tile_rows = 0;
+    auto copy_out = [&]() {
+        if (p.debug & 4) return;
+        const int GL = p.gl, gpw = 32 / GL;
+        const int gi = lane / GL, gl = lane % GL;
+#pragma unroll 4
+        for (int lr = warp * gpw + gi; lr < tile_rows; lr += nwarp * gpw) {
+            const int64_t rp = trp[lr];
+            const int t0 = ttoff[lr], len = ttoff[lr + 1] - t0;
+            for (int q = gl; q < len; q += GL) {
                 p.K[rp + q] = tk[t0 + q];
                 if constexpr (HAS_M) p.M[rp + q] = tm[t0 + q];
             }
         }
-        if (bn >= nb) break;
+    };
+    if (tid == 0) {
+        load_a(0);
+        if (n_it > 1) load_a(1);
+        load_b(0);
+    }
+    wait_a(0);
+    gather(0);
+    cp_async_wait_all();
+    __syncthreads();
+    for (int64_t it = 0; it < n_it; ++it) {
+        const RecA A = parse_a(ra(it));
+        copy_out();  // block it-1 (tile_rows = 0 on the first iteration)
+        const int nh_run = (p.debug & 1) ? 0 : int(A.nh);
+        for (int h = tid; h < nh_run; h += T) fast_element<KIND, KT, HAS_M, FT>(p, A, xsp(it), kv, h);
+        __syncthreads();
+        if (it + 1 < n_it) {  // block it+1's node table streams in during phase B
+            wait_a(it + 1);
+            gather(it + 1);
+        }
+        wait_b(it);
+        const RecB Bq = parse_b(rb);
+        for (int i = tid; i <= int(A.nr); i += T) {  // the tile's row map for the copy-out
+            if (i < int(A.nr)) trp[i] = A.rp[i];
+            ttoff[i] = A.toff[i];
+        }
+        tile_rows = int(A.nr);
+        const int nwg = (p.debug & 2) ? 0 : int(Bq.nwg);
+        for (int w = warp; w < nwg; w += nwarp) fast_group<KIND, KT, HAS_M, FT>(p, A, Bq, kv, tk, tm, w, lane);
         cp_async_wait_all();
         __syncthreads();
-        b = bn;
-        slot ^= 1;
+        if (tid == 0) {  // records A(it) and B(it) are consumed: refill their slots
+            fence_proxy_async();
+            if (it + 2 < n_it) load_a(it + 2);
+            if (it + 1 < n_it) load_b(it + 1);
+        }
     }
+    copy_out();  // the last block
 }
 
 template <int KIND, int KT, bool HAS_M, int FT>
@@ -465,6 +555,16 @@ int launch_fast(const FastArgs& a, int threads, cudaStream_t st) {
     if (per_sm < 1) return kFastNotApplicable;
     if (const char* e = getenv("TGK_FAST_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
     const int64_t grid = std::min<int64_t>(a.pl.n_blocks, int64_t(per_sm) * nsm);
+    if (getenv("TGK_FAST_VERBOSE")) {
+        static int printed = 0;
+        if (printed++ < 4)
+            fprintf(stderr,
+                    "[fast] R=%d blocks=%lld halo=%lld (max %d, MH=%d) rows/value NR=%d entries=%lld words=%lld "
+                    "recA max %d recB max %d plan %.1f MB smem %zu B, %d CTA/SM x %d threads, grid %lld\n",
+                    a.pl.R, (long long)a.pl.n_blocks, (long long)a.pl.n_halo, a.pl.max_halo, a.MH,
+                    FastCfg<KIND, KT, HAS_M, FT>::NR, (long long)a.pl.n_entries, (long long)a.pl.n_words,
+                    a.pl.max_rec_a, a.pl.max_rec_b, a.pl.bytes / 1e6, smem, per_sm, threads, (long long)grid);
+    }
     if (grid > 0) kern<<<static_cast<unsigned>(grid), threads, smem, st>>>(a);
     KERNEL_CHECK("fast_scalar");
     return TGK_OK;
@@ -487,9 +587,18 @@ int dispatch_fast(int kt, bool m, int ft, const FastArgs& a, int T, cudaStream_t
 
 int check_bad(unsigned long long* d_bad, cudaStream_t st);
 
-int fast_rows_per_block(int kind) {
-    if (const char* e = getenv("TGK_FAST_R")) return std::max(1, std::min(kFastMaxRows, atoi(e)));
-    return kind == TGK_TET4 ? 64 : 128;
+// Rows per block and threads per CTA (B200 sweeps, profiles/r02_fast_experiments.txt):
+// TET4 stiffness [+ load] 32 rows x 256 threads (3 CTAs/SM); with the unit
+// mass (two value rows more, two output tiles) 96 rows x 512 threads;
+// TRI3 128 rows x 256 threads.
+struct FastShape {
+    int R, T;
+};
+FastShape fast_shape(int kind, int fmt) {
+    FastShape s{kind == TGK_TET4 ? (fmt == kFastFmtKS32 ? 96 : 32) : 128, kind == TGK_TET4 && fmt == kFastFmtKS32 ? 512 : 256};
+    if (const char* e = getenv("TGK_FAST_R")) s.R = std::max(1, std::min(kFastMaxRows, atoi(e)));
+    if (const char* e = getenv("TGK_FAST_T")) s.T = std::max(32, std::min(kFastMaxThreads, atoi(e) / 32 * 32));
+    return s;
 }
 
 // Fast-mode scalar assembly.  Returns kFastNotApplicable when the fast layout
@@ -505,8 +614,14 @@ int fast_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* 
         if (f->type != TGK_FIELD_CONSTANT && f->type != TGK_FIELD_ELEMENT && f->type != TGK_FIELD_NODAL)
             return kFastNotApplicable;
     const FastPlanDev* pl = nullptr;
+    const int ft = !has_f ? 0 : pr->source[0].type == TGK_FIELD_NODAL ? 2 : 1;
+    const int kt = is_mass ? 1 : 0;
+    const bool hm = !is_mass && pr->with_mass && M;
+    if (hm && ft == 2) return kFastNotApplicable;  // nodal load with the unit mass: exact kernel
+    const int fmt = kt == 1 ? kFastFmtS16 : (hm ? kFastFmtKS32 : kFastFmtK16);
+    const FastShape shape = fast_shape(m->kind, fmt);
     {
-        const int prc = ensure_fast_plan(r, fast_rows_per_block(m->kind), &pl);
+        const int prc = ensure_fast_plan(r, shape.R, fmt, ft == 2, &pl);
         if (prc == TGK_ERR_INPUT) return kFastNotApplicable;
         if (prc != TGK_OK) return prc;
     }
@@ -522,20 +637,18 @@ int fast_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* 
     a.K = K;
     a.M = M;
     a.F = F;
-    a.MH = pl->max_halo + 1;
+    a.MH = pl->MH;
     a.MB = (pl->max_bnodes + 1) & ~1;
     a.abuf = (pl->max_rec_a + 15) & ~15;
     a.bbuf = (pl->max_rec_b + 15) & ~15;
-    int T = 256;
-    if (const char* e = getenv("TGK_FAST_T")) T = std::max(32, std::min(kFastMaxThreads, atoi(e) / 32 * 32));
+    if (const char* e = getenv("TGK_FAST_DEBUG")) a.debug = atoi(e);
+    a.gl = pl->max_len <= 8 ? 8 : pl->max_len <= 16 ? 16 : 32;
+    const int T = shape.T;
     unsigned long long* own_bad = nullptr;
     if (!d_bad) TGK_TRY(routing_flags(r, &own_bad));
     a.bad = d_bad ? d_bad : own_bad;
     CUDA_TRY(cudaMemsetAsync(a.bad, 0xff, sizeof(unsigned long long), st));
     if (!has_f && F) CUDA_TRY(cudaMemsetAsync(F, 0, sizeof(double) * r->N, st));
-    const int ft = !has_f ? 0 : a.stype == TGK_FIELD_NODAL ? 2 : 1;
-    const int kt = is_mass ? 1 : 0;
-    const bool hm = !is_mass && pr->with_mass && M;
     const int rc = m->kind == TGK_TET4 ? dispatch_fast<TGK_TET4>(kt, hm, ft, a, T, st)
                                        : dispatch_fast<TGK_TRI3>(kt, hm, ft, a, T, st);
     if (rc != TGK_OK) return rc;

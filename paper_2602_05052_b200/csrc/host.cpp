@@ -477,7 +477,7 @@ int tgk_routing_set_owned_rows(tgk_routing* r, int64_t lo, int64_t hi) {
     if (s->own_lo == lo && s->own_hi == hi) return TGK_OK;
     for (auto& pl : s->plan) pl.release();
     s->entry_plan.release();
-    s->fast_plan.release();
+    for (auto& fp : s->fast_plan) fp.release();
     s->own_lo = lo;
     s->own_hi = hi;
     return TGK_OK;
@@ -491,7 +491,7 @@ int tgk_routing_set_element_range(tgk_routing* r, int64_t lo, int64_t hi) {
     if (lo < 0 || hi > s->E || lo > hi) return set_error(TGK_ERR_INPUT, "element range out of bounds");
     if (s->elem_lo == lo && s->elem_hi == hi) return TGK_OK;
     for (auto& pl : s->plan) pl.release();
-    s->fast_plan.release();
+    for (auto& fp : s->fast_plan) fp.release();
     s->elem_lo = lo;
     s->elem_hi = hi;
     return TGK_OK;

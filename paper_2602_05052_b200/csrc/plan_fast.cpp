@@ -3,8 +3,8 @@
 // The plan is the north star's "precomputed element-to-CSR-slot permutation":
 // for every CSR entry a CUDA block owns, the list of (halo element, local
 // pair) whose local value lands on it — exactly the segments of the
-// reference's mat_offsets/mat_slots (routing.cpp:64-84), re-expressed against
-// the block's shared-memory element values.  Layout:
+// reference's mat_offsets/mat_slots (routing.cpp:64-84), re-expressed as
+// shared-memory addresses of the block's element values.  Layout:
 //
 //  - owned rows in Morton order of their coordinates, cut into blocks of R
 //    rows (compact in space => small halos);
@@ -16,13 +16,16 @@
 //    stored to (i, j) and (j, i) (K, M symmetric: both folds would run over
 //    the same elements with K_e[a][b] == K_e[b][a]).  Entries are sorted by
 //    list length (warps of uniform work), each class padded to whole warps;
-//  - per warp of 32 entries the items, u16 = halo index | value index << 12,
-//    interleaved [step][lane][4] so every step is one coalesced 8-byte load
-//    per lane.  Short lists are padded with the block's zero slot.
+//  - per warp of 32 entries the items, interleaved [step][lane][8 bytes] so
+//    every step is one coalesced 8-byte load per lane.  Items are direct
+//    indices of the values in the block's shared-memory value rows (format
+//    below); short lists are padded with the zero slot.
 #include <algorithm>
 #include <cstring>
 #include <numeric>
 #include <thread>
+
+#include <cuda_runtime.h>
 
 #include "tgk_internal.hpp"
 
@@ -34,6 +37,17 @@ constexpr int kSymTet[4][4] = {{0, 1, 2, 3}, {1, 4, 5, 6}, {2, 5, 7, 8}, {3, 6, 
 constexpr int kSymTri[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
 
 inline int sym_pair_k(int k, int a, int b) { return k == 4 ? kSymTet[a][b] : kSymTri[a][b]; }
+
+// value row of a packed pair (sym index): K_aa rows 0..k-1, then the
+// off-diagonal pairs in sym order (tet: 01 02 03 12 13 23; tri: 01 02 12)
+inline int pair_row(int k, int q) {
+    if (k == 4) {
+        static const int r[10] = {0, 4, 5, 6, 1, 7, 8, 2, 9, 3};
+        return r[q];
+    }
+    static const int r[6] = {0, 3, 4, 1, 5, 2};
+    return r[q];
+}
 
 }  // namespace
 
@@ -56,8 +70,8 @@ int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const i
     struct BlockOut {
         std::vector<uint32_t> rows, helem, bnodes, desc;
         std::vector<uint64_t> hconn;
-        std::vector<uint16_t> items;
-        std::vector<int64_t> wg_items;  // items per warp group (u16 units)
+        std::vector<uint32_t> list_off;  // per entry, n+1 (block-relative)
+        std::vector<uint16_t> items;     // generic items: halo index | (pair or a) << 12
         bool fail = false;
     };
     std::vector<BlockOut> out(nb);
@@ -96,9 +110,8 @@ int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const i
             auto halo_index = [&o](uint32_t e) {
                 return static_cast<uint16_t>(std::lower_bound(o.helem.begin(), o.helem.end(), e) - o.helem.begin());
             };
-            // entries: (class, steps, lr, p) sort key + desc + list
             struct Ent {
-                int cls, steps, lr, p;
+                int cls, len, lr, p;
                 uint32_t desc;
                 int list;
             };
@@ -108,8 +121,8 @@ int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const i
                 const uint32_t row = o.rows[lr];
                 const int64_t rp = row_ptr[row];
                 const int len = static_cast<int>(row_ptr[row + 1] - rp);
-                std::vector<int> col(len, -1);         // owned local row of the column, or -1
-                std::vector<int> pos2(len, -1);        // position of `row` within that row
+                std::vector<int> col(len, -1);   // owned local row of the column, or -1
+                std::vector<int> pos2(len, -1);  // position of `row` within that row
                 std::vector<std::vector<uint16_t>> ent(len);
                 std::vector<uint16_t> diag;
                 int pdiag = kFastNoPos;
@@ -150,35 +163,36 @@ int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const i
                     ents.push_back({1, 0, lr, p, d, static_cast<int>(lists.size()) - 1});
                 }
             }
-            for (auto& en : ents) en.steps = (static_cast<int>(lists[en.list].size()) + 3) / 4;
+            for (auto& en : ents) en.len = static_cast<int>(lists[en.list].size());
             std::stable_sort(ents.begin(), ents.end(), [](const Ent& x, const Ent& y) {
                 if (x.cls != y.cls) return x.cls < y.cls;
-                if (x.steps != y.steps) return x.steps > y.steps;
+                if (x.len != y.len) return x.len > y.len;
                 if (x.lr != y.lr) return x.lr < y.lr;
                 return x.p < y.p;
             });
-            const uint16_t zero_item = static_cast<uint16_t>(kFastMaxHalo);  // the zero slot, value index 0
+            o.list_off.push_back(0);
+            const int dsplit = kFastDiagSplit(k);
             for (int cls = 0; cls < 2; ++cls) {
-                std::vector<const Ent*> c;
-                for (const auto& en : ents)
-                    if (en.cls == cls) c.push_back(&en);
-                for (size_t w0 = 0; w0 < c.size(); w0 += 32) {
-                    int steps = 0;
-                    for (size_t l = w0; l < std::min(c.size(), w0 + 32); ++l) steps = std::max(steps, c[l]->steps);
-                    const size_t base = o.items.size();
-                    o.items.resize(base + size_t(steps) * 32 * 4, zero_item);
-                    for (int lane = 0; lane < 32; ++lane) {
-                        const size_t l = w0 + lane;
-                        if (l >= c.size()) {
-                            o.desc.push_back(kFastIdle);
-                            continue;
-                        }
-                        o.desc.push_back(c[l]->desc);
-                        const auto& li = lists[c[l]->list];
-                        for (size_t t = 0; t < li.size(); ++t)
-                            o.items[base + (t / 4) * 128 + lane * 4 + (t % 4)] = li[t];
+                size_t n = 0;
+                for (const auto& en : ents) {
+                    if (en.cls != cls) continue;
+                    const auto& li = lists[en.list];
+                    // a diagonal entry's list (the row's incident elements, ~24 in 3D)
+                    // is split over dsplit consecutive lanes, summed by shuffles:
+                    // balanced warps instead of a few long folds
+                    const int parts = cls == 0 ? dsplit : 1;
+                    const size_t chunk = (li.size() + parts - 1) / parts;
+                    for (int q = 0; q < parts; ++q) {
+                        o.desc.push_back(q == 0 ? en.desc : kFastPart);
+                        const size_t t0 = std::min(li.size(), q * chunk), t1 = std::min(li.size(), t0 + chunk);
+                        o.items.insert(o.items.end(), li.begin() + t0, li.begin() + t1);
+                        o.list_off.push_back(static_cast<uint32_t>(o.items.size()));
+                        ++n;
                     }
-                    o.wg_items.push_back(int64_t(steps) * 128);
+                }
+                for (; n % 32; ++n) {  // whole warps per class
+                    o.desc.push_back(kFastIdle);
+                    o.list_off.push_back(static_cast<uint32_t>(o.items.size()));
                 }
             }
         }
@@ -216,89 +230,159 @@ int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const i
     cat(&BlockOut::hconn, nullptr, P.hconn);
     cat(&BlockOut::bnodes, &P.bnode_off, P.bnodes);
     cat(&BlockOut::desc, &P.ent_off, P.desc);
-    cat(&BlockOut::items, nullptr, P.items);
-    // warp-group item offsets (u16 units), one per 32 entry slots, +1
-    P.wg_item.assign(P.desc.size() / 32 + 1, 0);
-    {
-        size_t g = 0;
-        int64_t acc = 0;
-        for (int64_t b = 0; b < nb; ++b)
-            for (int64_t n : out[b].wg_items) {
-                P.wg_item[g++] = acc;
-                acc += n;
-            }
-        P.wg_item[g] = acc;
-    }
-    for (int64_t b = 0; b < nb; ++b) {
+    cat(&BlockOut::items, &P.item_off, P.items);
+    P.list_off.clear();
+    for (int64_t b = 0; b < nb; ++b) {  // block-relative, n+1 per block
+        P.list_off.insert(P.list_off.end(), out[b].list_off.begin(), out[b].list_off.end());
         P.max_halo = std::max<int>(P.max_halo, static_cast<int>(out[b].helem.size()));
         P.max_bnodes = std::max<int>(P.max_bnodes, static_cast<int>(out[b].bnodes.size()));
         P.max_rows = std::max<int>(P.max_rows, static_cast<int>(out[b].rows.size()));
     }
-    // padding items point at the zero slot, halo index max_halo of every value row
-    for (uint16_t& it : P.items)
-        if ((it & 0xfff) == kFastMaxHalo) it = static_cast<uint16_t>((it & 0xf000) | P.max_halo);
     return TGK_OK;
 }
 
-}  // namespace tgk
-
 // ---------------------------------------------------------------------------
-// Upload (one device allocation, 16-byte aligned segments), cached on the
-// scalar routing per (R, owned rows, element range).
-#include <cuda_runtime.h>
-
-namespace tgk {
-
+// Upload: two byte records per block (layout in tgk_internal.hpp FastPlanDev)
+// with the items resolved for the value-row format (fast.cu FastCfg):
+//   kFastFmtK16  stiffness [+ load]: rows K_aa (k), K_ab (off-diagonal pairs),
+//                F (load scalar f det, or k rows F_e[a] with a nodal source);
+//                off-diagonal items u16 = K row * MH + h; diagonal items
+//                u32 = K index | F index << 16;
+//   kFastFmtKS32 stiffness + unit mass [+ scalar load]: rows K_aa, K_ab, S
+//                (det), F; all items u32 = K index | S index << 16 (F index =
+//                S index + MH);
+//   kFastFmtS16  coefficient mass (ProblemKind::Mass): row S (c det); items
+//                u16 = h.
+// MH = max halo + 1: index MH - 1 of every row is the +0.0 padding slot.
 void FastPlanDev::release() {
     if (blob) cudaFree(blob);
     *this = FastPlanDev{};
 }
 
-int ensure_fast_plan(tgk_routing* rr, int R, const FastPlanDev** out) {
+int fast_value_rows(int k, int fmt, bool fnodal) {
+    const int np = k * (k + 1) / 2;
+    if (fmt == kFastFmtS16) return 1;
+    if (fmt == kFastFmtKS32) return np + 2;
+    return np + (fnodal ? k : 1);
+}
+
+int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPlanDev** out) {
     tgk_routing* r = rr->scalar ? rr->scalar : rr;
-    FastPlanDev& D = r->fast_plan;
     const int64_t lo = r->own_hi < 0 ? 0 : r->own_lo, hi = r->own_hi < 0 ? r->N : r->own_hi;
     const int64_t elo = r->elem_hi < 0 ? 0 : r->elem_lo, ehi = r->elem_hi < 0 ? r->E : r->elem_hi;
-    if (D.blob && D.R == R && D.row_lo == lo && D.row_hi == hi && D.elem_lo == elo && D.elem_hi == ehi) {
-        *out = &D;
-        return TGK_OK;
-    }
-    D.release();
+    for (auto& D : r->fast_plan)
+        if (D.blob && D.R == R && D.fmt == fmt && D.fnodal == fnodal && D.row_lo == lo && D.row_hi == hi &&
+            D.elem_lo == elo && D.elem_hi == ehi) {
+            *out = &D;
+            return TGK_OK;
+        }
+    FastPlanDev* slot = nullptr;
+    for (auto& D : r->fast_plan)
+        if (!D.blob) {
+            slot = &D;
+            break;
+        }
+    if (!slot) slot = &r->fast_plan[r->fast_plan_next++ % kFastPlanSlots];  // evict round-robin
+    slot->release();
+    FastPlanDev& D = *slot;
     const tgk_mesh* m = r->mesh;
+    const int k = m->k;
     ScalarRoutingHost h;
     TGK_TRY(fetch_scalar_routing(r, h));
     FastPlanHost P;
     const int rc = build_fast_plan(m->kind, m->N, m->E, h.nodes.data(), h.conn.data(), h.row_ptr.data(), h.vo.data(),
                                    h.vs.data(), h.slot.data(), lo, hi, elo, ehi, R, P);
     if (rc != TGK_OK) return rc;
-    // ---- per-block records (layout: tgk_internal.hpp FastPlanDev; fast.cu FastRecA/B)
+    const int MH = P.max_halo + 1;
+    const int NP = k * (k + 1) / 2;
+    const int nrows = fast_value_rows(k, fmt, fnodal);
+    if (int64_t(nrows) * MH > 65536) return TGK_ERR_INPUT;  // items are u16 indices: not applicable
+    const uint32_t zero = uint32_t(MH - 1);
+    // generic item -> resolved index / word
+    auto off_item = [&](uint16_t g) -> uint32_t {  // off-diagonal
+        const uint32_t hh = g & 0xfffu, q = g >> 12;
+        if (fmt == kFastFmtS16) return hh;
+        const uint32_t kidx = uint32_t(pair_row(k, int(q))) * MH + hh;
+        if (fmt == kFastFmtK16) return kidx;
+        return kidx | ((uint32_t(NP) * MH + hh) << 16);
+    };
+    auto diag_item = [&](uint16_t g) -> uint32_t {
+        const uint32_t hh = g & 0xfffu, a = g >> 12;
+        if (fmt == kFastFmtS16) return hh;
+        const uint32_t kidx = a * MH + hh;
+        if (fmt == kFastFmtKS32) return kidx | ((uint32_t(NP) * MH + hh) << 16);
+        return kidx | ((uint32_t(NP + (fnodal ? a : 0)) * MH + hh) << 16);
+    };
     auto al16 = [](size_t x) { return (x + 15) & ~size_t(15); };
     const int64_t nb = P.n_blocks;
     std::vector<int64_t> a_off(nb + 1, 0), b_off(nb + 1, 0);
-    int max_a = 0, max_b = 0, max_tile = 0;
+    std::vector<std::vector<unsigned char>> recb(nb);
+    int max_a = 0, max_b = 0, max_tile = 0, max_len = 0;
+    int64_t n_words = 0;
     for (int64_t b = 0; b < nb; ++b) {
         const size_t nr = size_t(P.row_off[b + 1] - P.row_off[b]), nh = size_t(P.halo_off[b + 1] - P.halo_off[b]),
-                     nbn = size_t(P.bnode_off[b + 1] - P.bnode_off[b]), ne = size_t(P.ent_off[b + 1] - P.ent_off[b]);
-        const size_t nwg = ne / 32;
-        const int64_t g0 = P.ent_off[b] / 32;
-        const size_t ni = size_t(P.wg_item[g0 + nwg] - P.wg_item[g0]);
+                     nbn = size_t(P.bnode_off[b + 1] - P.bnode_off[b]);
         const size_t sa = 32 + al16(8 * nr) + al16(4 * nr) + al16(2 * (nr + 1)) + al16(4 * nbn) + al16(8 * nh);
-        const size_t sb = 16 + al16(4 * ne) + al16(4 * (nwg + 1)) + al16(2 * ni);
         a_off[b + 1] = a_off[b] + int64_t(sa);
-        b_off[b + 1] = b_off[b] + int64_t(sb);
         max_a = std::max<int>(max_a, int(sa));
+        // record B: header, descriptors, warp-group word offsets, words
+        const int64_t e0 = P.ent_off[b];
+        const uint32_t ne = uint32_t(P.ent_off[b + 1] - e0), nwg = ne / 32;
+        const uint32_t* loff = P.list_off.data() + e0 + b;  // block-relative, n+1
+        const uint16_t* gi = P.items.data() + P.item_off[b];
+        std::vector<uint32_t> wgoff(nwg + 1, 0), words;
+        for (uint32_t w = 0; w < nwg; ++w) {
+            const bool diag = (P.desc[e0 + w * 32] >> 15) & 1u;  // lane 0 is never idle
+            const bool wide = fmt == kFastFmtKS32 || (fmt == kFastFmtK16 && diag);
+            const int per_step = wide ? 2 : 4;
+            int steps = 0;
+            for (int l = 0; l < 32; ++l) {
+                const int n = int(loff[w * 32 + l + 1] - loff[w * 32 + l]);
+                steps = std::max(steps, (n + per_step - 1) / per_step);
+            }
+            const size_t base = words.size();
+            words.resize(base + size_t(steps) * 64, zero | (zero << 16));
+            for (int l = 0; l < 32; ++l) {
+                const uint32_t i0 = loff[w * 32 + l], i1 = loff[w * 32 + l + 1];
+                for (uint32_t t = 0; t < i1 - i0; ++t) {
+                    const uint32_t v = diag ? diag_item(gi[i0 + t]) : off_item(gi[i0 + t]);
+                    const size_t at = base + size_t(t / per_step) * 64 + size_t(l) * 2;
+                    if (wide) {
+                        words[at + (t % 2)] = v;
+                    } else {
+                        uint32_t& wd = words[at + (t % 4) / 2];
+                        wd = (t % 2) ? ((wd & 0xffffu) | (v << 16)) : ((wd & 0xffff0000u) | v);
+                    }
+                }
+            }
+            wgoff[w + 1] = uint32_t(words.size());
+        }
+        const size_t sb = 16 + al16(4 * size_t(ne)) + al16(4 * size_t(nwg + 1)) + al16(4 * words.size());
+        auto& rbv = recb[b];
+        rbv.assign(sb, 0);
+        const uint32_t hb[2] = {ne, nwg};
+        std::memcpy(rbv.data(), hb, 8);
+        size_t o = 16;
+        std::memcpy(rbv.data() + o, P.desc.data() + e0, 4 * size_t(ne));
+        o += al16(4 * size_t(ne));
+        std::memcpy(rbv.data() + o, wgoff.data(), 4 * size_t(nwg + 1));
+        o += al16(4 * size_t(nwg + 1));
+        if (!words.empty()) std::memcpy(rbv.data() + o, words.data(), 4 * words.size());
+        n_words += int64_t(words.size());
+        b_off[b + 1] = b_off[b] + int64_t(sb);
         max_b = std::max<int>(max_b, int(sb));
     }
     std::vector<unsigned char> ra(size_t(a_off[nb])), rb(size_t(b_off[nb]));
     for (int64_t b = 0; b < nb; ++b) {
-        const int64_t r0 = P.row_off[b], h0 = P.halo_off[b], n0 = P.bnode_off[b], e0 = P.ent_off[b];
+        const int64_t r0 = P.row_off[b], h0 = P.halo_off[b], n0 = P.bnode_off[b];
         const uint32_t nr = uint32_t(P.row_off[b + 1] - r0), nh = uint32_t(P.halo_off[b + 1] - h0),
-                       nbn = uint32_t(P.bnode_off[b + 1] - n0), ne = uint32_t(P.ent_off[b + 1] - e0);
+                       nbn = uint32_t(P.bnode_off[b + 1] - n0);
         unsigned char* pa = ra.data() + a_off[b];
         std::vector<uint16_t> toff(nr + 1, 0);
         for (uint32_t i = 0; i < nr; ++i) {
             const uint32_t row = P.rows[r0 + i];
             toff[i + 1] = uint16_t(toff[i] + (h.row_ptr[row + 1] - h.row_ptr[row]));
+            max_len = std::max<int>(max_len, int(h.row_ptr[row + 1] - h.row_ptr[row]));
         }
         max_tile = std::max<int>(max_tile, toff[nr]);
         const uint32_t hdr[4] = {nr, nh, nbn, toff[nr]};
@@ -317,21 +401,9 @@ int ensure_fast_plan(tgk_routing* rr, int R, const FastPlanDev** out) {
         std::memcpy(pa + o, P.bnodes.data() + n0, 4 * size_t(nbn));
         o += al16(4 * size_t(nbn));
         std::memcpy(pa + o, P.hconn.data() + h0, 8 * size_t(nh));
-        unsigned char* pb = rb.data() + b_off[b];
-        const uint32_t nwg = ne / 32;
-        const int64_t g0 = e0 / 32;
-        const uint32_t hb[2] = {ne, nwg};
-        std::memcpy(pb, hb, 8);
-        o = 16;
-        std::memcpy(pb + o, P.desc.data() + e0, 4 * size_t(ne));
-        o += al16(4 * size_t(ne));
-        for (uint32_t w = 0; w <= nwg; ++w) {
-            const uint32_t rel = uint32_t(P.wg_item[g0 + w] - P.wg_item[g0]);
-            std::memcpy(pb + o + 4 * w, &rel, 4);
-        }
-        o += al16(4 * size_t(nwg + 1));
-        std::memcpy(pb + o, P.items.data() + P.wg_item[g0], 2 * size_t(P.wg_item[g0 + nwg] - P.wg_item[g0]));
+        std::memcpy(rb.data() + b_off[b], recb[b].data(), recb[b].size());
     }
+    recb.clear();
     size_t total = 0;
     auto reserve = [&total](size_t bytes) {
         const size_t at = total;
@@ -358,15 +430,20 @@ int ensure_fast_plan(tgk_routing* rr, int R, const FastPlanDev** out) {
     D.blob = blob;
     D.bytes = static_cast<int64_t>(img.size());
     D.R = R;
+    D.fmt = fmt;
+    D.fnodal = fnodal;
+    D.MH = MH;
     D.n_blocks = P.n_blocks;
     D.max_halo = P.max_halo;
     D.max_bnodes = P.max_bnodes;
     D.max_rows = P.max_rows;
     D.max_tile = max_tile;
+    D.max_len = max_len;
     D.max_rec_a = max_a;
     D.max_rec_b = max_b;
     D.n_halo = static_cast<int64_t>(P.helem.size());
     D.n_items = static_cast<int64_t>(P.items.size());
+    D.n_words = n_words;
     D.n_entries = static_cast<int64_t>(P.desc.size());
     D.row_lo = lo;
     D.row_hi = hi;

@@ -369,7 +369,7 @@ tgk_routing::~tgk_routing() {
     entry_plan.release();
     group_plan.release();
     if (flags) cudaFree(flags);
-    fast_plan.release();
+    for (auto& fp : fast_plan) fp.release();
     for (double* p : scr)
         if (p) cudaFree(p);
     if (scalar && scalar != this) delete scalar;

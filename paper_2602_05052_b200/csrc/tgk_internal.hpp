@@ -186,30 +186,39 @@ constexpr int kFastMaxRowLen = 62;
 constexpr int kFastNoPos = 63;
 constexpr int kFastMaxHalo = 4095;
 constexpr uint32_t kFastIdle = 0xffffffffu;
+constexpr uint32_t kFastPart = 0xfffffffeu;  // lanes 1.. of a split diagonal entry
+TGK_HD constexpr int kFastDiagSplit(int k) { return k == 4 ? 4 : 2; }
 constexpr int kFastNotApplicable = -100;  // fast_scalar_assemble: take the exact kernel
 struct FastPlanHost {
     int R = 64;
     int64_t n_blocks = 0;
     int max_halo = 0, max_bnodes = 0, max_rows = 0;
-    std::vector<int64_t> row_off, halo_off, bnode_off, ent_off;  // n_blocks+1 each (ent_off: multiples of 32)
+    std::vector<int64_t> row_off, halo_off, bnode_off, ent_off, item_off;  // n_blocks+1 each (ent_off: multiples of 32)
     std::vector<uint32_t> rows, helem, bnodes, desc;
-    std::vector<uint64_t> hconn;    // 4 x u16 block-local node indices per halo element
-    std::vector<int64_t> wg_item;   // per 32 entry slots: first item (u16 units), +1
-    std::vector<uint16_t> items;    // per warp group [step][lane][4]
+    std::vector<uint64_t> hconn;     // 4 x u16 block-local node indices per halo element
+    std::vector<uint32_t> list_off;  // per block, per entry: item offsets (block-relative), n+1 per block
+    std::vector<uint16_t> items;     // generic items: halo index | (pair, or a for diagonals) << 12
 };
+
+// value-row formats of the fast kernel (plan_fast.cpp ensure_fast_plan)
+constexpr int kFastFmtK16 = 0;   // stiffness [+ load]
+constexpr int kFastFmtKS32 = 1;  // stiffness + unit mass [+ scalar load]
+constexpr int kFastFmtS16 = 2;   // coefficient mass
+constexpr int kFastPlanSlots = 3;
 
 // Device form: two byte records per block, each one TMA bulk copy into shared
 // memory (fast.cu).  Record A (prologue + phase A): header {int64 halo base,
 // u32 rows, halo, nodes, tile}, per row int64 CSR offset, u32 row id, u16 tile
 // offset (n+1), u32 node table, u64 block-local connectivity.  Record B
 // (phase B): header {u32 entries, warp groups}, u32 descriptors, u32 warp-group
-// item offsets (n+1), u16 items.  Sections 16-byte aligned.
+// word offsets (n+1), the item words.  Sections 16-byte aligned.
 struct FastPlanDev {
-    int R = 0;
+    int R = 0, fmt = -1, MH = 0;
+    bool fnodal = false;
     int64_t n_blocks = 0;
-    int max_halo = 0, max_bnodes = 0, max_rows = 0, max_tile = 0;
+    int max_halo = 0, max_bnodes = 0, max_rows = 0, max_tile = 0, max_len = 0;
     int max_rec_a = 0, max_rec_b = 0;  // bytes
-    int64_t n_halo = 0, n_items = 0, n_entries = 0;
+    int64_t n_halo = 0, n_items = 0, n_words = 0, n_entries = 0;
     int64_t row_lo = -1, row_hi = -1, elem_lo = -1, elem_hi = -1;  // the ranges it was built for
     const int64_t *rec_a_off = nullptr, *rec_b_off = nullptr;       // n_blocks+1 byte offsets
     const unsigned char *rec_a = nullptr, *rec_b = nullptr;
@@ -218,6 +227,7 @@ struct FastPlanDev {
     int64_t bytes = 0;
     void release();
 };
+int fast_value_rows(int k, int fmt, bool fnodal);
 
 // Returns TGK_ERR_INPUT WITHOUT an error message when the fast layout does not
 // apply (row longer than kFastMaxRowLen, halo larger than kFastMaxHalo):
@@ -266,7 +276,8 @@ struct tgk_routing {
     tgk::PlanDev plan[tgk::kPlanSlots];
     tgk::EntryPlanDev entry_plan;    // batched kernel plan (built on first batched call)
     tgk::GroupPlanDev group_plan;    // adjoint gather plan (built on first adjoint call)
-    tgk::FastPlanDev fast_plan;      // fast-mode plan (TGK_MODE_FAST)
+    tgk::FastPlanDev fast_plan[tgk::kFastPlanSlots];  // fast-mode plans (TGK_MODE_FAST), per R / format / ranges
+    int fast_plan_next = 0;
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
     int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
     double* scr[6] = {};             // cached device scratch (materialised elasticity path)
@@ -289,7 +300,7 @@ int routing_flags(tgk_routing* r, unsigned long long** out);
 int ensure_group_plan(tgk_routing* r, int G, const GroupPlanDev** out);
 // Fast-mode plan for R rows per block over the routing's owned rows / element
 // range; TGK_ERR_INPUT without a message when the fast layout does not apply.
-int ensure_fast_plan(tgk_routing* r, int R, const FastPlanDev** out);
+int ensure_fast_plan(tgk_routing* r, int R, int fmt, bool fnodal, const FastPlanDev** out);
 struct ScalarRoutingHost {
     std::vector<double> nodes;
     std::vector<int32_t> conn;

@@ -1,5 +1,5 @@
 #!/bin/bash
-# fast-mode tests + ncu capture of k_fast_scalar on C2a
-timeout 900 python -m pytest tests/test_gpu_fast.py -x -q -m gpu --durations=10 2>&1 | tail -15
-timeout 600 ncu --set full --import-source on -k regex:k_fast_scalar -c 1 -o gpurun_out/fast_c2a -f python tools/fast_bench.py c2a --reps 1 --modes fast > gpurun_out/ncu_fast.log 2>&1
-tail -3 gpurun_out/ncu_fast.log
+# ncu capture of k_fast_scalar on C2a (args: R T [tag])
+R=${1:-32}; T=${2:-256}; TAG=${3:-}
+TGK_FAST_VERBOSE=1 TGK_FAST_R=$R TGK_FAST_T=$T timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fast_scalar -c 1 -o gpurun_out/fast_c2a_R${R}_T${T}${TAG} -f python tools/fast_bench.py c2a --reps 1 --modes fast > gpurun_out/ncu_fast_R${R}.log 2>&1
+grep "\[fast\]" gpurun_out/ncu_fast_R${R}.log | head -2; tail -2 gpurun_out/ncu_fast_R${R}.log
