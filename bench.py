@@ -221,7 +221,12 @@ def ref_problem_kw(workload):
     return dict(kw or {})
 
 
-REF_SAMPLE = {"c2": (50, 50, 50), "c2a": (50, 50, 50), "c1": (256, 256), "c3": (30, 30, 30),
+# Reference-arm / cpu_baseline meshes: the workload's own configuration for
+# C1, C2 and C2a (same-config ratio; ~4 s per CPU step at 100^3 on 16
+# cores), bounded samples for C3 (the reference routing of the 3-DoF 100^3
+# mesh takes minutes single-threaded) and C5 (100.7M tets need > 100 GB of
+# host RAM in the reference's materialised Stage I).
+REF_SAMPLE = {"c2": (100, 100, 100), "c2a": (100, 100, 100), "c1": (256, 256), "c3": (30, 30, 30),
               "c5": (64, 64, 64)}
 
 
@@ -358,8 +363,7 @@ def cpu_baseline_line(workload):
             sample = f"tg::assemble per field on the C4 mesh, 4 fields ({E} element-fields), best of 2"
         else:
             kind = WORKLOADS[workload][0]
-            smp = {"c2": (40, 40, 40), "c2a": (40, 40, 40), "c3": (25, 25, 25), "c5": (40, 40, 40)}.get(
-                workload, REF_SAMPLE.get(workload))
+            smp = REF_SAMPLE.get(workload)
             E, times = cpu_reference_time(kind, smp, ref_problem_kw(workload), 3, 1)
             sample = (f"tg::assemble (oracle/_ref, reference sources) on {kind} Kuhn {'x'.join(map(str, smp))} "
                       f"= {E} elements, best of 3")
@@ -458,7 +462,7 @@ def run_scalar(args, ctx, N):
     setup_s = time.time() - t0
     with_mass = kw.get("with_mass", False)
     has_f = bool(kw.get("sources"))
-    p, keep = engine.make_problem("poisson", **kw)
+    p, keep = engine.make_problem("poisson", mode=args.mode, **kw)
     f32 = args.precision == "f32"
     vdt = torch.float32 if f32 else torch.float64
     K = torch.zeros(routing.nnz, dtype=vdt, device=ctx.dev)
@@ -500,6 +504,25 @@ def run_scalar(args, ctx, N):
         torch.cuda.synchronize()
     ms_kernel = ev_k0.elapsed_time(ev_k1) / args.steps
     ms_per_step = ms / args.steps
+    other = None  # the other fp64 mode's kernel time on the same inputs (both modes reported)
+    if not f32:
+        q, keep_q = engine.make_problem("poisson", mode="exact" if args.mode == "fast" else "fast", **kw)
+        qK, qF = torch.empty_like(K), torch.empty_like(F)
+        qM = torch.empty_like(M) if M is not None else None
+
+        def kernel_other():
+            N.check(L.tgk_assemble_async_d(C.byref(q), mesh._h, routing._h, ptr(qK), ptr(qF), ptr(qM), ptr(bad),
+                                           ctx.sp))
+        for _ in range(2):
+            kernel_other()
+        ctx.barrier()
+        ev_k0.record(ctx.stream)
+        for _ in range(args.steps):
+            kernel_other()
+        ev_k1.record(ctx.stream)
+        torch.cuda.synchronize()
+        other = ev_k0.elapsed_time(ev_k1) / args.steps
+        del qK, qF, qM
     graph = None
     if args.workload == "c1" and not f32 and world == 1:
         graph = c1_graph_time(ctx, lambda sp: N.check(L.tgk_assemble_async_d(
@@ -573,14 +596,30 @@ def run_scalar(args, ctx, N):
     peak, peak_src = peaks()
     achieved = ab / (ms_kernel * 1e-3) / 1e9
     launches = args.steps * (1 + (2 * (2 if with_mass else 1) if exchange and s.receives_down else 0))
-    config = {"workload": desc, "elements_per_gpu": E_own, "nnz_per_gpu": nnz_own, "mode": "exact (bit-identical)",
+    fast = args.mode == "fast" and not f32
+    mode_desc = ("fast (TGK_MODE_FAST: CSR pattern bit-exact, values within |dv| <= 1e-12|v_ref| + 1e-14 max|v_ref| "
+                 "of the reference, bitwise deterministic; tests/test_gpu_fast.py)" if fast else
+                 "exact (bit-identical to the reference)" if not f32 else "fp32 (|dv| <= 1e-5|v| + 1e-7 max|v|)")
+    fplan = None
+    if fast:
+        fr, fb, fh, fe, fw, fby = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        if L.tgk_routing_fast_plan_info(routing._h, C.byref(fr), C.byref(fb), C.byref(fh), C.byref(fe), C.byref(fw),
+                                        C.byref(fby)) == 0:
+            fplan = {"rows_per_block": fr.value, "blocks": fb.value, "halo_elements": fh.value,
+                     "recompute_factor": fh.value / max(1, E_own), "entries": fe.value, "item_words": fw.value,
+                     "bytes": fby.value}
+    config = {"workload": desc, "elements_per_gpu": E_own, "nnz_per_gpu": nnz_own, "mode": mode_desc,
               "parallelism": parallelism,
               "l2": "inputs larger than L2 (working set > 126 MB L2)" if ab > 2e8 else
                     "working set below L2 size (C1 parity config; no flush between steps)",
-              "fused_plan": {"rows_per_block": R_plan, "blocks": nb.value, "halo_elements": nh.value,
+              "exact_plan": {"rows_per_block": R_plan, "blocks": nb.value, "halo_elements": nh.value,
                              "recompute_factor": nh.value / max(1, elems.shape[0]), "records": nrec.value,
                              "bytes": pbytes.value},
               "setup_s": setup_s, "kernel_ms": ms_kernel}
+    if fplan is not None:
+        config["fast_plan"] = fplan
+    if other is not None:
+        config["other_mode_kernel_ms"] = {("exact" if fast else "fast"): other}
     if graph is not None:
         config["cuda_graph"] = graph
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
@@ -588,7 +627,8 @@ def run_scalar(args, ctx, N):
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                           "frac": achieved / peak, "traffic": ncu_traffic(args.workload) if world == 1 else None,
                           "alg_bytes": ab, "compulsory_bytes": comp,
-                          "peak_source": peak_src, "kernel": "k_fused_scalar (one launch per step)",
+                          "peak_source": peak_src,
+                          "kernel": ("k_fast_scalar" if fast else "k_fused_scalar") + " (one launch per step)",
                           "kernel_ms": ms_kernel})
 
 
@@ -825,6 +865,8 @@ def main():
     ap.add_argument("--dist-mode", default="exchange", choices=["exchange", "halo"])
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
                     help="f32: the fp32 variant of the fused scalar kernel (tgk_assemble_f32_d)")
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact"],
+                    help="fp64 arithmetic mode of the scalar workloads (TGK_MODE_FAST / TGK_MODE_EXACT)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample", type=int, nargs="*", default=None)

@@ -180,6 +180,12 @@ int tgk_interface_combine_d(const double* d_lower, double* d_values, int64_t n, 
  * factor), packed records, device bytes. */
 int tgk_routing_plan_stats(tgk_routing* r, int rows_per_block, int64_t* n_blocks, int64_t* n_halo,
                            int64_t* n_records, int64_t* bytes);
+/* Fast-mode plan of the latest TGK_MODE_FAST assembly on this routing
+ * (plan_fast.cpp): rows per block, blocks, halo elements (halo / E = recompute
+ * factor), CSR entries folded (after the symmetric dedup, padded), item words,
+ * device bytes.  Status 2 before the first fast-mode assembly. */
+int tgk_routing_fast_plan_info(const tgk_routing* r, int* rows_per_block, int64_t* n_blocks, int64_t* n_halo,
+                               int64_t* n_entries, int64_t* n_words, int64_t* bytes);
 /* Routing cache file in the reference layout ("tg-rout2", save_routing routing.cpp:194-209). */
 int tgk_routing_save(const tgk_routing* r, uint64_t mesh_hash, const char* path);
 /* load_routing (routing.cpp:211-234): *hit = 0 (status 0) on a missing file or a

@@ -16,6 +16,7 @@ TRI3, QUAD4, TET4 = 0, 1, 2
 POISSON, ELASTICITY, MASS = 0, 1, 2
 FIELD_CONSTANT, FIELD_ELEMENT, FIELD_NODAL = 0, 1, 2
 MODE_EXACT = 0
+MODE_FAST = 1
 ROUTING_SEGMENTS = 1
 KINDS = {"tri3": TRI3, "quad4": QUAD4, "tet4": TET4}
 KIND_NAMES = {v: k.upper() for k, v in KINDS.items()}
@@ -94,6 +95,7 @@ _SIGS = {
     "tgk_bicgstab_d": (_I, [_I64, _P, _P, _P, _P, _P, _D, _D, _I64, _P, _P, _P, _P]),
     "tgk_copy_d2d": (_I, [_P, _P, _I64, _P]),
     "tgk_routing_plan_stats": (_I, [_P, _I, _P, _P, _P, _P]),
+    "tgk_routing_fast_plan_info": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "tgk_routing_save": (_I, [_P, C.c_uint64, C.c_char_p]),
     "tgk_geometry_d": (_I, [_P, _I, _P, _P, _P, _P, _P, _P]),
     "tgk_local_stiffness_diffusion_d": (_I, [_P, _I, _P, _P, _P]),

@@ -478,6 +478,7 @@ int tgk_routing_set_owned_rows(tgk_routing* r, int64_t lo, int64_t hi) {
     for (auto& pl : s->plan) pl.release();
     s->entry_plan.release();
     for (auto& fp : s->fast_plan) fp.release();
+    s->fast_plan_used = nullptr;
     s->own_lo = lo;
     s->own_hi = hi;
     return TGK_OK;
@@ -492,6 +493,7 @@ int tgk_routing_set_element_range(tgk_routing* r, int64_t lo, int64_t hi) {
     if (s->elem_lo == lo && s->elem_hi == hi) return TGK_OK;
     for (auto& pl : s->plan) pl.release();
     for (auto& fp : s->fast_plan) fp.release();
+    s->fast_plan_used = nullptr;
     s->elem_lo = lo;
     s->elem_hi = hi;
     return TGK_OK;

@@ -273,7 +273,7 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
     for (auto& D : r->fast_plan)
         if (D.blob && D.R == R && D.fmt == fmt && D.fnodal == fnodal && D.row_lo == lo && D.row_hi == hi &&
             D.elem_lo == elo && D.elem_hi == ehi) {
-            *out = &D;
+            *out = r->fast_plan_used = &D;
             return TGK_OK;
         }
     FastPlanDev* slot = nullptr;
@@ -454,8 +454,27 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
     D.rec_a = base + o_ra;
     D.rec_b = base + o_rb;
     D.helem = reinterpret_cast<const uint32_t*>(base + o_he);
-    *out = &D;
+    *out = r->fast_plan_used = &D;
     return TGK_OK;
 }
+
+}  // namespace tgk
+
+extern "C" int tgk_routing_fast_plan_info(const tgk_routing* rr, int* rows_per_block, int64_t* n_blocks, int64_t* n_halo,
+                                          int64_t* n_entries, int64_t* n_words, int64_t* bytes) {
+    if (!rr) return tgk::set_error(TGK_ERR_INPUT, "null routing");
+    const tgk_routing* r = rr->scalar ? rr->scalar : rr;
+    const tgk::FastPlanDev* D = r->fast_plan_used;
+    if (!D || !D->blob) return tgk::set_error(TGK_ERR_INPUT, "no fast-mode assembly on this routing yet");
+    if (rows_per_block) *rows_per_block = D->R;
+    if (n_blocks) *n_blocks = D->n_blocks;
+    if (n_halo) *n_halo = D->n_halo;
+    if (n_entries) *n_entries = D->n_entries;
+    if (n_words) *n_words = D->n_words;
+    if (bytes) *bytes = D->bytes;
+    return TGK_OK;
+}
+
+namespace tgk {
 
 }  // namespace tgk

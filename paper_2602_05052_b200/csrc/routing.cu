@@ -370,6 +370,7 @@ tgk_routing::~tgk_routing() {
     group_plan.release();
     if (flags) cudaFree(flags);
     for (auto& fp : fast_plan) fp.release();
+    fast_plan_used = nullptr;
     for (double* p : scr)
         if (p) cudaFree(p);
     if (scalar && scalar != this) delete scalar;

@@ -278,6 +278,7 @@ struct tgk_routing {
     tgk::GroupPlanDev group_plan;    // adjoint gather plan (built on first adjoint call)
     tgk::FastPlanDev fast_plan[tgk::kFastPlanSlots];  // fast-mode plans (TGK_MODE_FAST), per R / format / ranges
     int fast_plan_next = 0;
+    const tgk::FastPlanDev* fast_plan_used = nullptr;  // the plan of the latest fast-mode assembly
     int64_t own_lo = 0, own_hi = -1;  // owned scalar row range (-1: all rows)
     int64_t elem_lo = 0, elem_hi = -1;  // elements taking part in the fused assembly (-1: all)
     double* scr[6] = {};             // cached device scratch (materialised elasticity path)
