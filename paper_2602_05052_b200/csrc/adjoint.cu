@@ -298,6 +298,56 @@ int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r
     return TGK_OK;
 }
 
+int ensure_scalar_segments(tgk_routing* r, cudaStream_t st);
+
+// Scalar assembly (physics.cpp:10-75) through the materialised Stage I + II
+// drop-ins: evaluate -> local_stiffness_diffusion / local_mass -> reduce_matrix,
+// local_load -> reduce_vector.  Bit-identical to the reference for any mesh
+// connectivity: the fallback of the fused kernels when a mesh exceeds their
+// plan layouts (rows longer than 32 entries, halos beyond the block tables;
+// fused.cu), so nothing the reference assembles is rejected.  Builds the
+// routing's segment maps on first use; partitioned routings are not supported
+// on this path.
+int materialised_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
+                                 double* M, cudaStream_t st, unsigned long long* d_bad) {
+    if (r->own_hi >= 0 || r->elem_hi >= 0)
+        return set_error(TGK_ERR_INPUT, "assemble: this mesh exceeds the fused plan layout and the materialised "
+                                        "fallback does not support row / element partitions");
+    const bool is_mass = pr->kind == TGK_MASS;
+    const bool high = pr->diffusion.type != TGK_FIELD_CONSTANT || is_mass || pr->with_mass;
+    const int degree = high ? 2 : 1;  // default_mass_degree / default_stiffness_degree (physics.cpp:18-21)
+    const bool has_f = !is_mass && pr->n_source > 0;
+    TGK_TRY(ensure_scalar_segments(r, st));
+    int Q = 0;
+    TGK_TRY(tgk_tables(m->kind, degree, &Q, nullptr, nullptr, nullptr, nullptr));
+    const int64_t nq = m->E * Q;
+    double *coef, *local;
+    TGK_TRY(routing_scratch(r, 0, nq, &coef));
+    TGK_TRY(routing_scratch(r, 2, size_t(m->E) * m->k * m->k, &local));
+    if (d_bad) CUDA_TRY(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), st));
+    TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->diffusion, coef, st));
+    if (is_mass) TGK_TRY(tgk_local_mass_d(m, degree, coef, local, st));
+    else TGK_TRY(tgk_local_stiffness_diffusion_d(m, degree, coef, local, st));
+    TGK_TRY(tgk_reduce_matrix_d(r, local, K, st));
+    if (pr->with_mass && !is_mass && M) {
+        const tgk_field ones{TGK_FIELD_CONSTANT, 1.0, nullptr, 0};
+        TGK_TRY(tgk_evaluate_field_d(m, degree, &ones, coef, st));
+        TGK_TRY(tgk_local_mass_d(m, degree, coef, local, st));
+        TGK_TRY(tgk_reduce_matrix_d(r, local, M, st));
+    }
+    if (F) {
+        if (has_f) {
+            TGK_TRY(tgk_evaluate_field_d(m, degree, &pr->source[0], coef, st));
+            TGK_TRY(tgk_local_load_d(m, degree, coef, local, st));
+            TGK_TRY(tgk_reduce_vector_d(r, local, F, st));
+        } else {
+            CUDA_TRY(cudaMemsetAsync(F, 0, sizeof(double) * r->N, st));
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return TGK_OK;
+}
+
 }  // namespace tgk
 
 extern "C" {

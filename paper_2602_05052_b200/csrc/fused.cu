@@ -719,6 +719,9 @@ static int fused_core(const tgk_mesh* m, tgk_routing* r, int R, int ktype, int d
 
 // Scalar fused assembly on device buffers.  With d_bad == nullptr it checks
 // the bad-element flag (synchronising); otherwise it is fully asynchronous.
+int materialised_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
+                                 double* M, cudaStream_t st, unsigned long long* d_bad);
+
 int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                           double* F, double* M, cudaStream_t st, unsigned long long* d_bad) {
     const bool is_mass = pr->kind == TGK_MASS;
@@ -729,8 +732,17 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
     const FieldDev src = has_f ? FieldDev{pr->source[0].type, pr->source[0].value, pr->source[0].data}
                                : FieldDev{TGK_FIELD_CONSTANT, 0.0, nullptr};
     const int64_t n_rows = r->own_hi < 0 ? r->N : r->own_hi - r->own_lo;
-    return fused_core(m, r, fused_rows_per_block(pr, n_rows), is_mass ? 1 : 0, degree, pr->with_mass != 0, has_f, coef, src,
-                      K, F, M, st, d_bad);
+    const int R = fused_rows_per_block(pr, n_rows);
+    {
+        // the row-block plan's layout limits (rows of <= 32 entries, <= 255 halo
+        // chunks and <= 65535 nodes per block): any other mesh takes the
+        // materialised Stage I + II path, bit-identical as well
+        const PlanDev* pl = nullptr;
+        const int prc = r->lmax > kMaxRowLen ? TGK_ERR_INPUT : ensure_plan(r, R, &pl);
+        if (prc == TGK_ERR_INPUT) return materialised_scalar_assemble(pr, m, r, K, F, M, st, d_bad);
+        if (prc != TGK_OK) return prc;
+    }
+    return fused_core(m, r, R, is_mass ? 1 : 0, degree, pr->with_mass != 0, has_f, coef, src, K, F, M, st, d_bad);
 }
 
 // fp32 mode (tgk_assemble_f32_d): the same fused kernel in single precision,

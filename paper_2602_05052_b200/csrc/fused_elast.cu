@@ -708,6 +708,9 @@ int launch_elast(const ElastArgs& a, int64_t nb, cudaStream_t st) {
 }  // namespace
 
 // Fused elasticity on device buffers (r: the vector routing; its scalar part carries the plan).
+int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
+                        cudaStream_t st);
+
 int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
                               cudaStream_t st) {
     const bool v1 = getenv("TGK_ELAST_V1") != nullptr;
@@ -716,7 +719,14 @@ int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
     if (const char* e = getenv("TGK_ELAST_C")) C2 = atoi(e);
     if (const char* e = getenv("TGK_ELAST_R")) R2 = atoi(e) == 32 ? 32 : 16;
     const PlanDev* pl = nullptr;
-    TGK_TRY(v1 ? ensure_plan(r, R, &pl) : ensure_plan(r, R2, &pl, C2));
+    {
+        // the row-block plan's layout limits (fused.cu): other meshes take the
+        // materialised Stage I + II path (elasticity_assemble), bit-identical too
+        const tgk_routing* s = r->scalar ? r->scalar : r;
+        const int prc = s->lmax > kMaxRowLen ? TGK_ERR_INPUT : (v1 ? ensure_plan(r, R, &pl) : ensure_plan(r, R2, &pl, C2));
+        if (prc == TGK_ERR_INPUT) return elasticity_assemble(pr, m, r, K, F, st);
+        if (prc != TGK_OK) return prc;
+    }
     const bool high = pr->diffusion.type != TGK_FIELD_CONSTANT;  // physics.cpp:18-21
     const int d = m->d;
     ElastArgs a{};

@@ -65,8 +65,11 @@ __global__ void k_row_pattern(const int32_t* conn, int k, int64_t N, const uint3
         const int64_t e = vec_slots[s] / k;
         for (int b = 0; b < k; ++b) {
             len = insert_unique(list, len, conn[e * k + b]);
-            if (len >= kMaxRow) {
-                atomicExch(overflow, 1);
+            if (len >= kMaxRow) {  // long row: built by k_row_long (global scratch list)
+                if (!FILL) {
+                    row_len[i] = -1;
+                    atomicExch(overflow, 1);
+                }
                 return;
             }
         }
@@ -77,6 +80,40 @@ __global__ void k_row_pattern(const int32_t* conn, int k, int64_t N, const uint3
         int64_t* out = cols + row_ptr[i];
         for (int p = 0; p < len; ++p) out[p] = list[p];
     }
+}
+
+// Rows with kMaxRow or more neighbours (fans, high-valence nodes of
+// unstructured meshes): one thread per such row builds the sorted unique list
+// in a global scratch segment bounded by its incidences x k.
+__global__ void k_row_long(const int32_t* conn, int k, const uint32_t* vec_off, const uint32_t* vec_slots,
+                           const int64_t* rows, const int64_t* scr_off, int64_t n_long, int32_t* scr,
+                           int64_t* row_len) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_long) return;
+    const int64_t i = rows[t];
+    int32_t* list = scr + scr_off[t];
+    int64_t len = 0;
+    for (uint32_t s = vec_off[i]; s < vec_off[i + 1]; ++s) {
+        const int64_t e = vec_slots[s] / k;
+        for (int b = 0; b < k; ++b) {
+            const int32_t v = conn[e * k + b];
+            int64_t p = len;
+            while (p > 0 && list[p - 1] > v) --p;
+            if (p > 0 && list[p - 1] == v) continue;
+            for (int64_t q = len; q > p; --q) list[q] = list[q - 1];
+            list[p] = v;
+            ++len;
+        }
+    }
+    row_len[i] = len;
+}
+
+__global__ void k_row_long_fill(const int64_t* rows, const int64_t* scr_off, int64_t n_long, const int32_t* scr,
+                                const int64_t* row_ptr, int64_t* cols) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_long) return;
+    const int64_t i = rows[t];
+    for (int64_t p = 0; p < row_ptr[i + 1] - row_ptr[i]; ++p) cols[row_ptr[i] + p] = scr[scr_off[t] + p];
 }
 
 __device__ __forceinline__ int64_t find_col(const int64_t* cols, int64_t lo, int64_t hi, int64_t j) {
@@ -110,14 +147,16 @@ __global__ void k_mat_count(int k, int64_t N, const uint32_t* vec_off, const uin
 }
 
 // mat_slots fill (routing.cpp:72-83): ascending slot within each nonzero
+// (rows longer than kMaxRow keep their cursors in the global scratch gcur, nnz entries)
 __global__ void k_mat_fill(int k, int64_t N, const uint32_t* vec_off, const uint32_t* vec_slots,
                            const int64_t* row_ptr, const uint32_t* slot_of,
-                           const uint32_t* mat_off, uint32_t* mat_slots) {
+                           const uint32_t* mat_off, uint32_t* mat_slots, uint32_t* gcur) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int64_t rp = row_ptr[i];
     const int len = static_cast<int>(row_ptr[i + 1] - rp);
-    uint32_t cur[kMaxRow];
+    uint32_t lcur[kMaxRow];
+    uint32_t* cur = len > kMaxRow ? gcur + rp : lcur;
     for (int p = 0; p < len; ++p) cur[p] = mat_off[rp + p];
     for (uint32_t s = vec_off[i]; s < vec_off[i + 1]; ++s) {
         const uint64_t slot = vec_slots[s];
@@ -172,12 +211,13 @@ __global__ void k_vec_mat_count(int c, int64_t nnz_s, const int64_t* rp_s, int64
 __global__ void k_vec_mat_fill(int c, int k, int64_t N, const uint32_t* vo_s, const uint32_t* vs_s,
                                const int64_t* rp_s, const uint32_t* slot_of_s,
                                const int64_t* rp_v, const uint32_t* mat_off_v,
-                               uint32_t* mat_slots_v) {
+                               uint32_t* mat_slots_v, uint32_t* gcur) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= N * c) return;
     const int64_t i = r / c, ci = r % c;
     const int64_t len = rp_s[i + 1] - rp_s[i];
-    uint32_t cur[kMaxRow * 3];
+    uint32_t lcur[kMaxRow * 3];
+    uint32_t* cur = len * c > kMaxRow * 3 ? gcur + rp_v[r] : lcur;
     for (int64_t q = 0; q < len * c; ++q) cur[q] = mat_off_v[rp_v[r] + q];
     const uint32_t kv = k * c;
     for (uint32_t s_ix = vo_s[i]; s_ix < vo_s[i + 1]; ++s_ix) {
@@ -254,11 +294,33 @@ int build_scalar(const tgk_mesh* m, int flags, cudaStream_t st, tgk_routing* r) 
     int ovf = 0;
     CUDA_TRY(cudaMemcpyAsync(&ovf, overflow.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    if (ovf) return set_error(TGK_ERR_INPUT, "build_routing: a mesh node has more than 63 neighbours");
+    DevBuf<int64_t> long_rows, long_off;
+    DevBuf<int32_t> long_scr;
+    int64_t n_long = 0;
     {
-        // row length max (for the fused plan) and row_ptr
         std::vector<int64_t> h_len(N);
         CUDA_TRY(cudaMemcpy(h_len.data(), row_len.p, N * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        if (ovf) {  // rows of kMaxRow+ neighbours: global-scratch builder
+            std::vector<uint32_t> h_vo(N + 1);
+            CUDA_TRY(cudaMemcpy(h_vo.data(), vo.p, (N + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            std::vector<int64_t> lr, lo{0};
+            for (int64_t i = 0; i < N; ++i)
+                if (h_len[i] < 0) {
+                    lr.push_back(i);
+                    lo.push_back(lo.back() + int64_t(h_vo[i + 1] - h_vo[i]) * k);
+                }
+            n_long = static_cast<int64_t>(lr.size());
+            TGK_TRY(long_rows.alloc(n_long));
+            TGK_TRY(long_off.alloc(n_long + 1));
+            TGK_TRY(long_scr.alloc(std::max<int64_t>(1, lo.back())));
+            CUDA_TRY(cudaMemcpy(long_rows.p, lr.data(), n_long * sizeof(int64_t), cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(long_off.p, lo.data(), (n_long + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+            k_row_long<<<grid_for(n_long, 64), 64, 0, st>>>(m->conn, k, vo.p, vs.p, long_rows.p, long_off.p, n_long,
+                                                            long_scr.p, row_len.p);
+            KERNEL_CHECK("row_long");
+            CUDA_TRY(cudaMemcpy(h_len.data(), row_len.p, N * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        }
+        // row length max (for the fused plans) and row_ptr
         int64_t lmax = 0;
         for (auto v : h_len) lmax = v > lmax ? v : lmax;
         r->lmax = static_cast<int>(lmax);
@@ -272,6 +334,10 @@ int build_scalar(const tgk_mesh* m, int flags, cudaStream_t st, tgk_routing* r) 
     k_row_pattern<true><<<grid_for(N, 128), 128, 0, st>>>(m->conn, k, N, vo.p, vs.p, nullptr, rp.p,
                                                          cols.p, overflow.p);
     KERNEL_CHECK("row_pattern_fill");
+    if (n_long > 0) {
+        k_row_long_fill<<<grid_for(n_long, 64), 64, 0, st>>>(long_rows.p, long_off.p, n_long, long_scr.p, rp.p, cols.p);
+        KERNEL_CHECK("row_long_fill");
+    }
     // 4: element-to-slot map
     DevBuf<uint32_t> slot;
     TGK_TRY(slot.alloc(Ek * k));
@@ -289,8 +355,11 @@ int build_scalar(const tgk_mesh* m, int flags, cudaStream_t st, tgk_routing* r) 
         k_mat_count<<<grid_for(N, 128), 128, 0, st>>>(k, N, vo.p, vs.p, rp.p, slot.p, mcount.p);
         KERNEL_CHECK("mat_count");
         TGK_TRY(exclusive_scan<uint32_t>(mcount.p, mo.p, nnz + 1, st));
-        k_mat_fill<<<grid_for(N, 128), 128, 0, st>>>(k, N, vo.p, vs.p, rp.p, slot.p, mo.p, ms.p);
+        DevBuf<uint32_t> gcur;
+        if (r->lmax > kMaxRow) TGK_TRY(gcur.alloc(nnz));
+        k_mat_fill<<<grid_for(N, 128), 128, 0, st>>>(k, N, vo.p, vs.p, rp.p, slot.p, mo.p, ms.p, gcur.p);
         KERNEL_CHECK("mat_fill");
+        CUDA_TRY(cudaStreamSynchronize(st));
         r->mat_offsets = mo.release();
         r->mat_slots = ms.release();
     }
@@ -341,10 +410,13 @@ int build_vector(const tgk_mesh* m, int c, int flags, cudaStream_t st, tgk_routi
         TGK_TRY(mo.alloc(r->nnz + 1));
         TGK_TRY(exclusive_scan<uint32_t>(mcount.p, mo.p, r->nnz + 1, st));
         TGK_TRY(ms.alloc(E * static_cast<int64_t>(r->k) * r->k));
+        DevBuf<uint32_t> gcur;
+        if (s->lmax * c > kMaxRow * 3) TGK_TRY(gcur.alloc(r->nnz));
         k_vec_mat_fill<<<grid_for(N * c, 128), 128, 0, st>>>(c, k, N, s->vec_offsets, s->vec_slots,
                                                             s->row_ptr, s->slot_of, rp.p, mo.p,
-                                                            ms.p);
+                                                            ms.p, gcur.p);
         KERNEL_CHECK("vec_mat_fill");
+        CUDA_TRY(cudaStreamSynchronize(st));
         r->vec_offsets = vo.release();
         r->vec_slots = vs.release();
         r->mat_offsets = mo.release();
@@ -358,6 +430,36 @@ int build_vector(const tgk_mesh* m, int c, int flags, cudaStream_t st, tgk_routi
 }
 
 }  // namespace
+
+// The reference segment maps (mat_offsets / mat_slots, routing.cpp:64-83) of a
+// scalar routing built without TGK_ROUTING_SEGMENTS, on demand (the
+// materialised Stage II fallback of the fused kernels needs them).
+int ensure_scalar_segments(tgk_routing* r, cudaStream_t st) {
+    if (r->mat_offsets) return TGK_OK;
+    if (r->components != 1) return set_error(TGK_ERR_INPUT, "segment maps: scalar routing expected");
+    const int k = r->k;
+    const int64_t N = r->N, E = r->E, nnz = r->nnz;
+    if (E * k * static_cast<int64_t>(k) > static_cast<int64_t>(UINT32_MAX))
+        return set_error(TGK_ERR_INPUT, "build_routing: mesh exceeds 2^32-1 local matrix slots");
+    DevBuf<uint32_t> mcount, mo, ms, gcur;
+    TGK_TRY(mcount.alloc(nnz + 1));
+    TGK_TRY(mo.alloc(nnz + 1));
+    TGK_TRY(ms.alloc(E * k * k));
+    CUDA_TRY(cudaMemsetAsync(mcount.p, 0, (nnz + 1) * sizeof(uint32_t), st));
+    k_mat_count<<<grid_for(N, 128), 128, 0, st>>>(k, N, r->vec_offsets, r->vec_slots, r->row_ptr, r->slot_of,
+                                                 mcount.p);
+    KERNEL_CHECK("mat_count");
+    TGK_TRY(exclusive_scan<uint32_t>(mcount.p, mo.p, nnz + 1, st));
+    if (r->lmax > kMaxRow) TGK_TRY(gcur.alloc(nnz));
+    k_mat_fill<<<grid_for(N, 128), 128, 0, st>>>(k, N, r->vec_offsets, r->vec_slots, r->row_ptr, r->slot_of, mo.p,
+                                                ms.p, gcur.p);
+    KERNEL_CHECK("mat_fill");
+    CUDA_TRY(cudaStreamSynchronize(st));
+    r->mat_offsets = mo.release();
+    r->mat_slots = ms.release();
+    return TGK_OK;
+}
+
 }  // namespace tgk
 
 tgk_routing::~tgk_routing() {
