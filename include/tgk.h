@@ -49,11 +49,16 @@ extern "C" {
 #define TGK_MASS 2
 
 /* coefficient field types — tg::CoefficientField variants (coefficient.hpp:17-50).
- * Analytic (a host std::function) has no device form: evaluate it on the host
- * and pass an element or quadrature table instead. */
+ * Analytic (a host std::function) has no device form: the caller evaluates it
+ * (CoefficientField::evaluate, coefficient.cpp:34-55) and passes the quadrature
+ * table (TGK_FIELD_QUAD). */
 #define TGK_FIELD_CONSTANT 0
 #define TGK_FIELD_ELEMENT 1 /* E values                       */
 #define TGK_FIELD_NODAL 2   /* N_node values, interpolated by the basis (batch.cpp:314-333) */
+#define TGK_FIELD_QUAD 3    /* E x Q values at the quadrature points of the degree assemble()
+                               selects (physics.cpp:18-21): any CoefficientField, Analytic
+                               included, evaluated by the caller; assembled through the
+                               materialised Stage I + II kernels (bit-identical) */
 
 /* arithmetic mode of tgk_problem (fp64 entries).
  *  TGK_MODE_EXACT: the reference operation order, no FMA contraction, CSR values
@@ -163,6 +168,14 @@ int tgk_routing_get_view(const tgk_routing* r, tgk_routing_view* out);
 int tgk_routing_copy(const tgk_routing* r, int64_t* row_ptr, int64_t* col_idx, uint32_t* slot_of,
                      uint32_t* vec_offsets, uint32_t* vec_slots, uint32_t* mat_offsets,
                      uint32_t* mat_slots);
+/* Device routing from a caller's RoutingMatrices host arrays (routing.hpp:16-32:
+ * pattern offsets / cols, vec_ and mat_ segment maps) — the drop-in keeps the
+ * caller's routing instead of rebuilding it.  Sizes must match the mesh
+ * (N = N_node * components, k = k_geom * components). */
+int tgk_routing_create_host(const tgk_mesh* m, int components, int64_t N, int64_t E, int k, int64_t nnz,
+                            const int64_t* row_ptr, const int64_t* col_idx, const uint32_t* vec_offsets,
+                            const uint32_t* vec_slots, const uint32_t* mat_offsets, const uint32_t* mat_slots,
+                            void* stream, tgk_routing** out);
 /* Row-owning partitions: restrict the fused assembly to the scalar (node)
  * rows [row_lo, row_hi) of this routing; elements incident to them are
  * recomputed as halo.  Other output rows are left untouched.  Resets the plan. */
@@ -310,6 +323,12 @@ int tgk_expand_d(const tgk_condensed* c, const double* d_u_free, double* d_u, vo
 void tgk_condensed_destroy(tgk_condensed* c);
 /* Device-to-device copy on a stream (plumbing for the Python layer). */
 int tgk_copy_d2d(void* dst, const void* src, int64_t nbytes, void* stream);
+/* Device memory plumbing for host-language callers without the CUDA runtime
+ * headers (adapter/physics_gpu.cpp, ctypes): cudaMalloc / cudaFree / blocking copies. */
+int tgk_alloc_d(void** p, int64_t nbytes);
+int tgk_free_d(void* p);
+int tgk_copy_d2h(void* dst, const void* src, int64_t nbytes);
+int tgk_copy_h2d(void* dst, const void* src, int64_t nbytes);
 /* bicgstab (solver.cpp:105-227): Jacobi-preconditioned BiCGSTAB with up to 8
  * restarts, divergence rollback and best-iterate fallback, on device CSR.
  * d_x holds the initial guess and receives the solution.  Dot products are

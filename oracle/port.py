@@ -26,12 +26,18 @@ class Field(C.Structure):
 
 
 def field(spec):
-    """spec: float (constant) | ('element', array) | ('nodal', array)."""
+    """spec: float (constant) | ('element', array) | ('nodal', array);
+    reference library only: ('checkerboard', frequency) | ('multisine', (K, r)) —
+    the reference's Analytic fields checkerboard_source / multi_sine_field."""
     if spec is None:
         return None, None
     if isinstance(spec, (int, float)):
         return Field(0, float(spec), None, 0), None
     kind, arr = spec
+    if kind == "checkerboard":
+        return Field(3, float(arr), None, 0), None
+    if kind == "multisine":
+        return Field(4, float(arr[1]), None, int(arr[0])), None
     arr = np.ascontiguousarray(arr, dtype=np.float64)
     t = {"element": 1, "nodal": 2}[kind]
     return Field(t, 0.0, arr.ctypes.data, arr.size), arr

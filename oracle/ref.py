@@ -15,7 +15,8 @@ import numpy as np
 from .port import Field, field, KINDS, PROBLEMS, element_dim, element_nodes
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_ref", "libtgref.so")
+# oracle/ref_gpu.py loads this module a second time with the GPU drop-in library
+LIB_PATH = os.environ.get("_TGREF_LIB_OVERRIDE") or os.path.join(_HERE, "_ref", "libtgref.so")
 
 _lib = None
 
@@ -64,6 +65,7 @@ def lib():
         L.tgr_reduce_vector.argtypes = [P, P, P]
         L.tgr_scatter_add.argtypes = [P] * 8
         L.tgr_assemble.argtypes = [P, P, C.c_int, P, P, P, C.c_int, C.c_int, P, C.c_int, P, P, P, P]
+        L.tgr_last_pattern_shared.restype = C.c_int
         L.tgr_gradient_products.argtypes = [P] * 5
         L.tgr_simp_sensitivity.argtypes = [P, P, P, C.c_double, C.c_double, C.c_double, P, P, P]
         L.tgr_allen_cahn.argtypes = [P, P, P, C.c_double, P, P]
@@ -81,6 +83,11 @@ def _p(a):
 def _check(rc):
     if rc != 0:
         raise RefError(rc, lib().tgr_last_error().decode())
+
+
+def last_pattern_shared():
+    """1 if the last assemble() returned K (and M) on the routing's own pattern pointer."""
+    return lib().tgr_last_pattern_shared()
 
 
 def set_threads(n):

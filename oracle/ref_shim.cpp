@@ -379,10 +379,18 @@ CoefficientField field_of(const tgr_field& f) {
         case 0: return CoefficientField::constant(f.value);
         case 1: return CoefficientField::per_element(std::vector<double>(f.data, f.data + f.n));
         case 2: return CoefficientField::nodal(std::vector<double>(f.data, f.data + f.n));
+        // the reference's own Analytic fields (physics.cpp:77-107)
+        case 3: return checkerboard_source(static_cast<int>(f.value));
+        case 4: return multi_sine_field(static_cast<int>(f.n), f.value, 7);
     }
     throw InputError("unknown field type");
 }
+thread_local int g_pattern_shared = -1;
 }  // namespace
+
+// 1 if the last tgr_assemble returned K (and M) on the routing's own pattern
+// pointer (routing.cpp:114; checked by timestep.cpp:140, adjoint.cpp:73), else 0.
+int tgr_last_pattern_shared() { return g_pattern_shared; }
 
 // assemble (physics.cpp:10-75).  problem: 0 Poisson, 1 elasticity, 2 mass.
 // seconds: steady_clock duration of the assemble() call alone.
@@ -406,6 +414,9 @@ int tgr_assemble(void* mp, void* rp, int problem, const tgr_field* diffusion,
         const auto sys = assemble(ps, m, rr.dofmap, rr.routing, with_mass != 0);
         const auto t1 = std::chrono::steady_clock::now();
         if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        g_pattern_shared = sys.K.pattern.get() == rr.routing.pattern.get() &&
+                           (!sys.M || sys.M->pattern.get() == rr.routing.pattern.get()) && sys.K.symmetric &&
+                           (!sys.M || sys.M->symmetric);
         if (K) std::memcpy(K, sys.K.values.data(), sys.K.values.size() * 8);
         if (F) std::memcpy(F, sys.F.data(), sys.F.size() * 8);
         if (M && sys.M) std::memcpy(M, sys.M->values.data(), sys.M->values.size() * 8);

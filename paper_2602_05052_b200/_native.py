@@ -94,6 +94,11 @@ _SIGS = {
     "tgk_condensed_destroy": (None, [_P]),
     "tgk_bicgstab_d": (_I, [_I64, _P, _P, _P, _P, _P, _D, _D, _I64, _P, _P, _P, _P]),
     "tgk_copy_d2d": (_I, [_P, _P, _I64, _P]),
+    "tgk_alloc_d": (_I, [_P, _I64]),
+    "tgk_free_d": (_I, [_P]),
+    "tgk_copy_d2h": (_I, [_P, _P, _I64]),
+    "tgk_copy_h2d": (_I, [_P, _P, _I64]),
+    "tgk_routing_create_host": (_I, [_P, _I, _I64, _I64, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tgk_routing_plan_stats": (_I, [_P, _I, _P, _P, _P, _P]),
     "tgk_routing_fast_plan_info": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "tgk_routing_save": (_I, [_P, C.c_uint64, C.c_char_p]),

@@ -156,6 +156,8 @@ int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing*
                           double* F, double* M, cudaStream_t st, unsigned long long* d_bad);
 int fast_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F, double* M,
                          cudaStream_t st, unsigned long long* d_bad);
+int materialised_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
+                                 double* M, cudaStream_t st, unsigned long long* d_bad);
 int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                         double* F, cudaStream_t st);
 int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
@@ -778,8 +780,16 @@ int ensure_plan(tgk_routing* rr, int R, const PlanDev** out, int C) {
     return TGK_OK;
 }
 
-static int check_field(const tgk_field& f, const tgk_mesh* m, const char* what) {
+static int check_field(const tgk_field& f, const tgk_mesh* m, const char* what, int degree = 0) {
     if (f.type == TGK_FIELD_CONSTANT) return TGK_OK;
+    if (f.type == TGK_FIELD_QUAD) {
+        int Q = 0;
+        TGK_TRY(tgk_tables(m->kind, degree, &Q, nullptr, nullptr, nullptr, nullptr));
+        if (f.n != m->E * Q)
+            return set_error(TGK_ERR_INPUT, std::string(what) + ": quadrature table: expected E x Q = " +
+                                                std::to_string(m->E * Q) + " values, got " + std::to_string(f.n));
+        return TGK_OK;
+    }
     if (f.type == TGK_FIELD_ELEMENT) {
         if (f.n != m->E)
             return set_error(TGK_ERR_INPUT, std::string(what) + ": per-element coefficient: expected " +
@@ -806,14 +816,20 @@ int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double
     const int comps = p->kind == TGK_ELASTICITY ? m->d : 1;
     if (r->components != comps)
         return set_error(TGK_ERR_INPUT, "assemble: dofmap component count does not match problem kind");
-    TGK_TRY(check_field(p->diffusion, m, "diffusion"));
+    // quadrature degree of physics.cpp:18-21 (the QUAD tables must be at it)
+    const bool high = p->diffusion.type != TGK_FIELD_CONSTANT || p->kind == TGK_MASS || p->with_mass;
+    const int degree = high ? 2 : 1;
+    TGK_TRY(check_field(p->diffusion, m, "diffusion", degree));
     if (p->kind == TGK_ELASTICITY) {
-        TGK_TRY(check_field(p->lambda, m, "lambda"));
-        TGK_TRY(check_field(p->mu, m, "mu"));
+        TGK_TRY(check_field(p->lambda, m, "lambda", degree));
+        TGK_TRY(check_field(p->mu, m, "mu", degree));
         if (p->n_source > 0 && p->n_source != m->d)
             return set_error(TGK_ERR_INPUT, "elasticity body force needs one component per dimension");
     }
-    for (int s = 0; s < std::min(p->n_source, 3); ++s) TGK_TRY(check_field(p->source[s], m, "source"));
+    for (int s = 0; s < std::min(p->n_source, 3); ++s) TGK_TRY(check_field(p->source[s], m, "source", degree));
+    bool quad = p->diffusion.type == TGK_FIELD_QUAD;
+    for (int s = 0; s < std::min(p->n_source, 3); ++s) quad = quad || p->source[s].type == TGK_FIELD_QUAD;
+    if (p->kind == TGK_ELASTICITY) quad = quad || p->lambda.type == TGK_FIELD_QUAD || p->mu.type == TGK_FIELD_QUAD;
     if (p->with_mass && comps != 1)
         return set_error(TGK_ERR_INPUT, "mass matrix assembly only supported for scalar fields");
     TGK_TRY(host_ensure_device());
@@ -821,9 +837,10 @@ int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double
         // fused row-block kernel (fused_elast.cu); the materialised Stage I + II
         // path (evaluate -> local_stiffness_elasticity -> reduce_matrix) remains
         // behind TGK_ELAST_MATERIALISED=1 (needs a routing with segment maps)
-        if (getenv("TGK_ELAST_MATERIALISED")) return elasticity_assemble(p, m, r, K, F, st);
+        if (quad || getenv("TGK_ELAST_MATERIALISED")) return elasticity_assemble(p, m, r, K, F, st);
         return fused_elasticity_assemble(p, m, r, K, F, st);
     }
+    if (quad) return materialised_scalar_assemble(p, m, r, K, F, M, st, d_bad);
     if (p->mode == TGK_MODE_FAST) {
         const int rc = fast_scalar_assemble(p, m, r, K, F, M, st, d_bad);
         if (rc != kFastNotApplicable) return rc;
@@ -848,6 +865,8 @@ int tgk_assemble_f32_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routin
         return set_error(TGK_ERR_INPUT, "P1 assembly supports TRI3 and TET4 meshes only");
     if (p->kind == TGK_ELASTICITY || r->components != 1)
         return set_error(TGK_ERR_INPUT, "tgk_assemble_f32_d: scalar problems only");
+    if (p->diffusion.type == TGK_FIELD_QUAD || (p->n_source > 0 && p->source[0].type == TGK_FIELD_QUAD))
+        return set_error(TGK_ERR_INPUT, "tgk_assemble_f32_d: quadrature-table fields are fp64-only");
     TGK_TRY(check_field(p->diffusion, m, "diffusion"));
     for (int s = 0; s < std::min(p->n_source, 3); ++s) TGK_TRY(check_field(p->source[s], m, "source"));
     TGK_TRY(host_ensure_device());

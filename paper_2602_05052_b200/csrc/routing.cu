@@ -479,6 +479,67 @@ tgk_routing::~tgk_routing() {
 }
 
 
+namespace tgk {
+
+// Device routing from host arrays in the reference layout (the cache loader
+// and tgk_routing_create_host): pattern + segment maps uploaded, the
+// element-to-slot map inverted from mat_slots, the scalar routing of vector
+// problems rebuilt on the GPU.
+int routing_from_arrays(const tgk_mesh* m, int components, int64_t N, int64_t E, int k, int64_t nnz,
+                        const int64_t* off, const int64_t* cols, const uint32_t* vo, const uint32_t* vs,
+                        const uint32_t* mo, const uint32_t* ms, cudaStream_t st, int* hit, tgk_routing** out) {
+    TGK_TRY(ensure_device());
+    const size_t Ek = static_cast<size_t>(E) * k;
+    auto* r = new tgk_routing();
+    r->mesh = m;
+    r->N = N;
+    r->E = E;
+    r->k = k;
+    r->nnz = nnz;
+    r->components = components;
+    int64_t lmax = 0;
+    for (int64_t i = 0; i < N; ++i) lmax = std::max<int64_t>(lmax, off[i + 1] - off[i]);
+    r->lmax = static_cast<int>(components == 1 ? lmax : lmax / components);
+    auto up = [](auto*& dst, const auto* src, size_t n) -> int {
+        using T = typename std::remove_const<typename std::remove_pointer<decltype(src)>::type>::type;
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&dst), std::max<size_t>(1, n) * sizeof(T)));
+        if (n) CUDA_TRY(cudaMemcpy(dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+        return TGK_OK;
+    };
+    int rc = TGK_OK;
+    if (!rc) rc = up(r->row_ptr, off, size_t(N + 1));
+    if (!rc) rc = up(r->col_idx, cols, size_t(nnz));
+    if (!rc) rc = up(r->vec_offsets, vo, size_t(N + 1));
+    if (!rc) rc = up(r->vec_slots, vs, Ek);
+    if (!rc) rc = up(r->mat_offsets, mo, size_t(nnz + 1));
+    if (!rc) rc = up(r->mat_slots, ms, Ek * k);
+    if (!rc && components == 1) {
+        // element-to-slot map = inverse of the segment map (slot_of[mat_slots[u]] = t)
+        std::vector<uint32_t> slot(Ek * k);
+        for (int64_t t = 0; t < nnz; ++t)
+            for (uint32_t u = mo[t]; u < mo[t + 1]; ++u) slot[ms[u]] = static_cast<uint32_t>(t);
+        rc = up(r->slot_of, slot.data(), slot.size());
+        r->scalar = r;
+    } else if (!rc) {
+        // the fused kernels run on the node-level (scalar) routing: rebuild it on the GPU
+        auto* s = new tgk_routing();
+        s->mesh = m;
+        rc = build_scalar(m, 0, st, s);
+        if (rc) delete s;
+        else r->scalar = s;
+    }
+    if (rc) {
+        if (r->scalar == r) r->scalar = nullptr;
+        delete r;
+        return rc;
+    }
+    *hit = 1;
+    *out = r;
+    return TGK_OK;
+}
+
+}  // namespace tgk
+
 extern "C" {
 
 int tgk_routing_build(const tgk_mesh* m, int components, int flags, void* stream,
@@ -564,54 +625,28 @@ int tgk_routing_load(const tgk_mesh* m, int components, uint64_t mesh_hash, cons
                     rd(vs.data(), vs.size() * 4) && rd(mo.data(), mo.size() * 4) && rd(ms.data(), ms.size() * 4);
     std::fclose(f);
     if (!ok) return TGK_OK;
-    TGK_TRY(ensure_device());
-    cudaStream_t st = as_stream(stream);
-    auto* r = new tgk_routing();
-    r->mesh = m;
-    r->N = N;
-    r->E = E;
-    r->k = k;
-    r->nnz = nnz;
-    r->components = components;
-    int64_t lmax = 0;
-    for (int64_t i = 0; i < N; ++i) lmax = std::max<int64_t>(lmax, off[i + 1] - off[i]);
-    r->lmax = static_cast<int>(lmax);
-    auto up = [](auto*& dst, const auto& v) -> int {
-        using T = typename std::remove_reference<decltype(v)>::type::value_type;
-        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&dst), std::max<size_t>(1, v.size()) * sizeof(T)));
-        if (!v.empty()) CUDA_TRY(cudaMemcpy(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-        return TGK_OK;
-    };
-    int rc = TGK_OK;
-    if (!rc) rc = up(r->row_ptr, off);
-    if (!rc) rc = up(r->col_idx, cols);
-    if (!rc) rc = up(r->vec_offsets, vo);
-    if (!rc) rc = up(r->vec_slots, vs);
-    if (!rc) rc = up(r->mat_offsets, mo);
-    if (!rc) rc = up(r->mat_slots, ms);
-    if (!rc && components == 1) {
-        // element-to-slot map = inverse of the segment map (slot_of[mat_slots[u]] = t)
-        std::vector<uint32_t> slot(Ek * k);
-        for (int64_t t = 0; t < nnz; ++t)
-            for (uint32_t u = mo[t]; u < mo[t + 1]; ++u) slot[ms[u]] = static_cast<uint32_t>(t);
-        rc = up(r->slot_of, slot);
-        r->scalar = r;
-    } else if (!rc) {
-        // the fused kernels run on the node-level (scalar) routing: rebuild it on the GPU
-        auto* s = new tgk_routing();
-        s->mesh = m;
-        rc = build_scalar(m, 0, st, s);
-        if (rc) delete s;
-        else r->scalar = s;
-    }
-    if (rc) {
-        if (r->scalar == r) r->scalar = nullptr;
-        delete r;
-        return rc;
-    }
-    *hit = 1;
-    *out = r;
-    return TGK_OK;
+    return tgk::routing_from_arrays(m, components, N, E, k, nnz, off.data(), cols.data(), vo.data(), vs.data(),
+                                    mo.data(), ms.data(), as_stream(stream), hit, out);
+}
+
+// Device routing from a caller's RoutingMatrices host arrays (routing.hpp:16-32):
+// the caller's pattern and segment maps are uploaded as given, no rebuild.
+int tgk_routing_create_host(const tgk_mesh* m, int components, int64_t N, int64_t E, int k, int64_t nnz,
+                            const int64_t* row_ptr, const int64_t* col_idx, const uint32_t* vec_offsets,
+                            const uint32_t* vec_slots, const uint32_t* mat_offsets, const uint32_t* mat_slots,
+                            void* stream, tgk_routing** out) {
+    using namespace tgk;
+    if (!m || !out || !row_ptr || !col_idx || !vec_offsets || !vec_slots || !mat_offsets || !mat_slots)
+        return set_error(TGK_ERR_INPUT, "tgk_routing_create_host: null argument");
+    if (components != 1 && components != m->d)
+        return set_error(TGK_ERR_INPUT, "components per node must be 1 or the mesh dimension");
+    if (N != m->N * components || E != m->E || k != m->k * components)
+        return set_error(TGK_ERR_INPUT, "tgk_routing_create_host: routing sizes do not match the mesh");
+    if (row_ptr[N] != nnz || int64_t(vec_offsets[N]) != E * k || int64_t(mat_offsets[nnz]) != E * k * k)
+        return set_error(TGK_ERR_INPUT, "tgk_routing_create_host: inconsistent routing arrays");
+    int hit = 0;
+    return routing_from_arrays(m, components, N, E, k, nnz, row_ptr, col_idx, vec_offsets, vec_slots, mat_offsets,
+                               mat_slots, as_stream(stream), &hit, out);
 }
 
 int tgk_routing_copy(const tgk_routing* r, int64_t* row_ptr, int64_t* col_idx, uint32_t* slot_of,

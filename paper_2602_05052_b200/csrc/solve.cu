@@ -542,4 +542,34 @@ int tgk_copy_d2d(void* dst, const void* src, int64_t nbytes, void* stream) {
 
 void tgk_condensed_destroy(tgk_condensed* c) { delete c; }
 
+// Device memory plumbing for host-language callers without the CUDA runtime
+// headers (the C++ adapter, ctypes).
+int tgk_alloc_d(void** p, int64_t nbytes) {
+    using namespace tgk;
+    if (!p || nbytes < 0) return set_error(TGK_ERR_INPUT, "alloc_d: bad arguments");
+    TGK_TRY(ensure_device());
+    *p = nullptr;
+    CUDA_TRY(cudaMalloc(p, nbytes > 0 ? size_t(nbytes) : 1));
+    return TGK_OK;
+}
+
+int tgk_free_d(void* p) {
+    if (p) cudaFree(p);
+    return TGK_OK;
+}
+
+int tgk_copy_d2h(void* dst, const void* src, int64_t nbytes) {
+    using namespace tgk;
+    if (nbytes < 0 || (nbytes > 0 && (!dst || !src))) return set_error(TGK_ERR_INPUT, "copy_d2h: bad arguments");
+    if (nbytes) CUDA_TRY(cudaMemcpy(dst, src, nbytes, cudaMemcpyDeviceToHost));
+    return TGK_OK;
+}
+
+int tgk_copy_h2d(void* dst, const void* src, int64_t nbytes) {
+    using namespace tgk;
+    if (nbytes < 0 || (nbytes > 0 && (!dst || !src))) return set_error(TGK_ERR_INPUT, "copy_h2d: bad arguments");
+    if (nbytes) CUDA_TRY(cudaMemcpy(dst, src, nbytes, cudaMemcpyHostToDevice));
+    return TGK_OK;
+}
+
 }  // extern "C"

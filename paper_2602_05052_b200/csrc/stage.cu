@@ -589,6 +589,15 @@ int tgk_evaluate_field_d(const tgk_mesh* m, int degree, const tgk_field* f, doub
         return set_error(TGK_ERR_INPUT, "nodal field: expected " + std::to_string(m->N) +
                                             " values, got " + std::to_string(f->n));
     cudaStream_t st = as_stream(stream);
+    if (f->type == TGK_FIELD_QUAD) {  // already at the quadrature points: E x Q copy
+        int Q = 0;
+        TGK_TRY(tgk_tables(m->kind, degree, &Q, nullptr, nullptr, nullptr, nullptr));
+        if (f->n != m->E * Q)
+            return set_error(TGK_ERR_INPUT, "quadrature table: expected E x Q = " + std::to_string(m->E * Q) +
+                                                " values, got " + std::to_string(f->n));
+        CUDA_TRY(cudaMemcpyAsync(out, f->data, sizeof(double) * f->n, cudaMemcpyDeviceToDevice, st));
+        return TGK_OK;
+    }
     if (m->kind == TGK_TET4)
         TGK_TRY((dispatch_degree<TGK_TET4, EvalLaunch>(degree, m, f, out, st)));
     else
