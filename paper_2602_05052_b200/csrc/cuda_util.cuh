@@ -75,6 +75,32 @@ inline unsigned grid_for(int64_t n, int block) {
     return static_cast<unsigned>(g);
 }
 
+// Per-device caches (a process may drive several GPUs): the SM count, and a
+// kernel instance's raised dynamic shared-memory limit (`done` is the call
+// site's static array of kMaxDevices sizes).
+constexpr int kMaxDevices = 64;
+inline int sm_count() {
+    static int n[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (dev >= kMaxDevices) {
+        int v = 148;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }
+    if (n[dev] == 0) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+    return n[dev] > 0 ? n[dev] : 148;
+}
+template <class Kern>
+int raise_smem_limit(Kern kern, size_t smem, size_t* done) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < kMaxDevices && done[dev] >= smem) return TGK_OK;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (dev < kMaxDevices) done[dev] = smem;
+    return TGK_OK;
+}
+
 // Device-side first-bad-element reporter (smallest index wins: deterministic).
 struct BadElem {
     unsigned long long* flag;  // init to ~0ull

@@ -536,20 +536,9 @@ int launch_fast(const FastArgs& a, int threads, cudaStream_t st) {
     auto kern = k_fast_scalar<KIND, KT, HAS_M, FT>;
     const size_t smem = FastCfg<KIND, KT, HAS_M, FT>::smem(a);
     if (smem > 227 * 1024) return kFastNotApplicable;  // the caller takes the exact kernel
-    // opt-in size per kernel instance and device (a process may drive several GPUs)
-    static size_t done[64] = {};
-    static int sms[64] = {};
-    int dev = 0;
-    CUDA_TRY(cudaGetDevice(&dev));
-    if (dev >= 64 || done[dev] < smem) {
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        if (dev < 64) done[dev] = smem;
-    }
-    int nsm = dev < 64 ? sms[dev] : 0;
-    if (nsm == 0) {
-        CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        if (dev < 64) sms[dev] = nsm;
-    }
+    static size_t done[kMaxDevices] = {};  // opt-in size per kernel instance and device
+    TGK_TRY(raise_smem_limit(kern, smem, done));
+    const int nsm = sm_count();
     int per_sm = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
     if (per_sm < 1) return kFastNotApplicable;

@@ -583,13 +583,10 @@ int launch_fused(const FusedArgs& a, int64_t n_blocks, cudaStream_t st) {
     using C = FusedCfg<KIND, DEG, KTYPE, HAS_M, HAS_F, R, T, FCONST>;
     auto kern = k_fused_scalar<KIND, DEG, KTYPE, HAS_M, HAS_F, R, FDIV, T, FCONST>;
     const size_t smem = C::smem_bytes(a.lmax, a.max_recs, a.max_bnodes, a.ntcols, a.max_chunks);
-    // raise the instance's dynamic shared-memory limit only when it grows (small
-    // meshes are launch-overhead bound; one process drives one device)
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set = smem;
-    }
+    // raise the instance's dynamic shared-memory limit only when it grows, per
+    // device (small meshes are launch-overhead bound)
+    static size_t smem_set[kMaxDevices] = {};
+    TGK_TRY(raise_smem_limit(kern, smem, smem_set));
     if (n_blocks > 0) kern<<<static_cast<unsigned>(n_blocks), R, smem, st>>>(a);
     KERNEL_CHECK("fused_scalar");
     return TGK_OK;
@@ -640,12 +637,7 @@ int fused_rows_per_block(const tgk_problem* pr, int64_t n_rows) {
     // from det in the fold), and 64 when 128-row blocks would not fill the GPU
     // once (C1: 16.0 -> 13.4 us)
     if (pr->with_mass) return 64;
-    static const int sms = [] {
-        int dev = 0, n = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n;
-    }();
+    const int sms = sm_count();
     return n_rows < int64_t(128) * 4 * sms ? 64 : 128;
 }
 
