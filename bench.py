@@ -69,6 +69,10 @@ WORKLOADS = {
            "strong"),
     "c5": ("tet4", (256, 256, 256), dict(sources=[1.0]),
            "C5: 3D Poisson P1 tet K+F, Kuhn 256^3 (100.7M tets) partitioned into z-slabs, fp64, Q=1", "strong"),
+    "rm": ("tri3", (1000, 500), None,
+           "RM: the reduce_matrix drop-in (routing.cpp:109-132) on the reference's published reduction workload, "
+           "TRI3 1000x500 over [1, 0.5] (E = 1e6; acceptance.cpp:677-689, 12.25 ms in proj/test_output.txt:24), fp64",
+           "weak"),
 }
 C4_FIELDS = 256
 LAME = (0.3 / (1.3 * 0.4), 1.0 / (2 * 1.3))  # lame_from_young(1, 0.3) (batch.cpp:353-357)
@@ -192,6 +196,23 @@ def cpu_reference_time(kind, divs, problem_kw, steps, warmup, threads=0):
     return m.E, times
 
 
+def cpu_reference_rm(steps, warmup, threads=0):
+    """reduce_matrix of the reference (routing.cpp:109-132) on the RM workload, the unit-coefficient
+    local stiffness of the reference's own Stage I as input (acceptance.cpp:677-689)."""
+    from oracle import ref
+    ref.set_threads(threads)
+    m = ref.Mesh.grid("tri3", [1.0, 0.5], [1000, 500])
+    r = ref.Routing(m, 1)
+    K_local = ref.local(m, 1, 0, np.ones(m.E))
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        r.reduce_matrix(K_local)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    return m.E, times
+
+
 def cpu_reference_c4(steps, warmup, fields=4, threads=0):
     """B x (per-element evaluate + local_stiffness_diffusion + reduce_matrix) (+F) of the reference on
     the C4 mesh, `fields` fields per step (a bounded sample of the 256-field batch)."""
@@ -227,7 +248,7 @@ def ref_problem_kw(workload):
 # mesh takes minutes single-threaded) and C5 (100.7M tets need > 100 GB of
 # host RAM in the reference's materialised Stage I).
 REF_SAMPLE = {"c2": (100, 100, 100), "c2a": (100, 100, 100), "c1": (256, 256), "c3": (30, 30, 30),
-              "c5": (64, 64, 64)}
+              "c5": (64, 64, 64), "rm": (1000, 500)}
 
 
 def e2e_pipelined(ctx, N, L, engine, kind, nodes, elems, p, with_mass, h_nodes, h_elems, fK, fF, fM, steps,
@@ -331,6 +352,9 @@ def run_reference(args):
     if args.workload == "c4":
         E, times = cpu_reference_c4(args.steps, args.warmup)
         sample = f"C4 mesh, 4 of the 256 coefficient fields per step ({E} element-fields)"
+    elif args.workload == "rm":
+        E, times = cpu_reference_rm(args.steps, args.warmup)
+        sample = f"reduce_matrix on tri3 1000x500 ({E} elements) per step (the workload itself)"
     else:
         smp = tuple(args.ref_sample) if args.ref_sample else REF_SAMPLE[args.workload]
         E, times = cpu_reference_time(kind, smp, ref_problem_kw(args.workload), args.steps, args.warmup)
@@ -361,6 +385,9 @@ def cpu_baseline_line(workload):
         if workload == "c4":
             E, times = cpu_reference_c4(2, 1)
             sample = f"tg::assemble per field on the C4 mesh, 4 fields ({E} element-fields), best of 2"
+        elif workload == "rm":
+            E, times = cpu_reference_rm(5, 1)
+            sample = f"reduce_matrix (oracle/_ref) on tri3 1000x500 = {E} elements, best of 5"
         else:
             kind = WORKLOADS[workload][0]
             smp = REF_SAMPLE.get(workload)
@@ -706,6 +733,66 @@ def run_elasticity(args, ctx, N):
                           "kernel": "k_fused_elast2 (one launch per step)"})
 
 
+def run_reduce(args, ctx, N):
+    """rm: the materialised Stage II drop-in tgk_reduce_matrix_d (k_segment_reduce) on the reference's
+    published reduction workload; input = the unit-coefficient local stiffness (E x 3 x 3) in HBM."""
+    torch = ctx.torch
+    from paper_2602_05052_b200 import engine, tgfem
+    kind, div, _, desc, scaling = WORKLOADS["rm"]
+    t0 = time.time()
+    m = tgfem.generate_grid(kind, [1.0, 0.5], list(div))
+    mesh = engine.DeviceMesh(kind, m.nodes, m.elements)
+    routing = engine.Routing(mesh, 1, segments=True)
+    E, Nn = m.element_count(), m.node_count()
+    local = engine.local_stiffness_diffusion(mesh, 1, torch.ones(E, dtype=torch.float64, device=ctx.dev))
+    vals = torch.empty(routing.nnz, dtype=torch.float64, device=ctx.dev)
+    setup_s = time.time() - t0
+    L = N.lib()
+
+    def step():
+        N.check(L.tgk_reduce_matrix_d(routing._h, ptr(local), ptr(vals), ctx.sp))
+
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(ctx.local_rank) as clocks:
+        ms = ctx.timed(step, args.steps)
+    ms_per_step = ms / args.steps
+    value = E * ctx.world / (ms_per_step * 1e-3)
+    nnz = routing.nnz
+    # algorithmic bytes: segment offsets + slots + the gathered local values + the CSR values written
+    ab = (nnz + 1) * 4 + E * 9 * 4 + E * 9 * 8 + nnz * 8
+    peak, peak_src = peaks()
+    achieved = ab / (ms_per_step * 1e-3) / 1e9
+    e2e = None
+    if args.e2e_steps > 0:
+        h_local = torch.empty(local.shape, dtype=torch.float64).pin_memory()
+        h_local.copy_(local)
+        h_vals = torch.empty(nnz, dtype=torch.float64).pin_memory()
+
+        def e2e_step():  # host K_local in, host CSR values out (the reference's calling pattern)
+            local.copy_(h_local, non_blocking=True)
+            step()
+            h_vals.copy_(vals, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_step()
+        w0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e2e_s = ctx.max_over_ranks((time.perf_counter() - w0) / args.e2e_steps)
+        e2e = {"value": E * ctx.world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h_local.numel() * 8),
+               "d2h_bytes_per_step": int(nnz * 8), "ms_per_step": e2e_s * 1e3,
+               "path": "pinned H2D of K_local (E x 9) + tgk_reduce_matrix_d + D2H of the CSR values"}
+    config = {"workload": desc, "elements": E, "nnz": nnz, "mode": "exact (bit-identical)",
+              "parallelism": "single GPU" if ctx.world == 1 else f"{ctx.world} independent replicas",
+              "l2": "inputs larger than L2 (72 MB K_local + 13 MB segments + 28 MB values ~ L2 size; not flushed)",
+              "reference_published_ms": 12.25, "setup_s": setup_s}
+    return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
+                gpu_launches=args.steps, clocks=clocks.summary(),
+                roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                          "frac": achieved / peak, "traffic": None, "alg_bytes": ab, "peak_source": peak_src,
+                          "kernel": "k_segment_reduce (one launch per step)", "kernel_ms": ms_per_step})
+
+
 def run_batched(args, ctx, N):
     """c4: batched per-element coefficient fields + adjoint gather; fields sharded across ranks."""
     torch = ctx.torch
@@ -880,6 +967,8 @@ def main():
         r = run_elasticity(args, ctx, N)
     elif args.workload == "c4":
         r = run_batched(args, ctx, N)
+    elif args.workload == "rm":
+        r = run_reduce(args, ctx, N)
     else:
         r = run_scalar(args, ctx, N)
     cpu = None

@@ -147,11 +147,19 @@ int tgk_tables(int kind, int degree, int* Q, double* points, double* weights, do
 /* Upload a tg::Mesh (host arrays, int64 connectivity) to the device. */
 int tgk_mesh_create(int kind, const double* nodes, int64_t n_nodes, const int64_t* elems,
                     int64_t n_elems, tgk_mesh** out);
-/* Wrap device arrays (node-major fp64 coordinates, int32 connectivity); not owned. */
+/* Wrap device arrays (node-major fp64 coordinates, int32 connectivity); not owned.
+ * The caller must not change the connectivity of a wrapped mesh that has
+ * routings, and must call tgk_mesh_coordinates_changed() after changing its
+ * coordinates in place (the fused kernels certify coordinates once). */
 int tgk_mesh_create_d(int kind, const double* d_nodes, int64_t n_nodes, const int32_t* d_elems,
                       int64_t n_elems, tgk_mesh** out);
-/* Re-upload host arrays into an existing mesh of the same sizes (timed e2e path). */
+/* Re-upload host arrays (either may be NULL) into an existing mesh of the same
+ * sizes (timed e2e path).  New coordinates are re-certified on the next call;
+ * connectivity that DIFFERS from the current one marks every routing built
+ * from this mesh stale: they then fail with status 2 until rebuilt. */
 int tgk_mesh_upload(tgk_mesh* m, const double* nodes, const int64_t* elems, void* stream);
+/* Coordinates of a wrapped (tgk_mesh_create_d) mesh were changed in place. */
+int tgk_mesh_coordinates_changed(tgk_mesh* m);
 void tgk_mesh_destroy(tgk_mesh* m);
 int tgk_mesh_info(const tgk_mesh* m, int* kind, int64_t* n_nodes, int64_t* n_elems,
                   const double** d_nodes, const int32_t** d_elems);

@@ -369,6 +369,7 @@ int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, con
     using namespace tgk;
     if (!m || !r) return set_error(TGK_ERR_INPUT, "adjoint_gather: null argument");
     if (r->components != 1) return set_error(TGK_ERR_INPUT, "adjoint_gather: scalar routing required");
+    TGK_TRY(check_routing_fresh(m, r));
     TGK_TRY(ensure_device());
     cudaStream_t st = as_stream(stream);
     unsigned long long* badp = nullptr;  // the routing's persistent status words
@@ -427,6 +428,7 @@ int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, c
     if (!m || !r) return set_error(TGK_ERR_INPUT, "assemble_batched: null argument");
     if (mode != TGK_MODE_EXACT) return set_error(TGK_ERR_INPUT, "assemble_batched: unknown arithmetic mode");
     if (r->components != 1) return set_error(TGK_ERR_INPUT, "assemble_batched: scalar routing required");
+    TGK_TRY(check_routing_fresh(m, r));
     if (B < 0) return set_error(TGK_ERR_INPUT, "assemble_batched: negative batch");
     TGK_TRY(ensure_device());
     cudaStream_t st = as_stream(stream);

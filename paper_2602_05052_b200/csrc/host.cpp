@@ -448,6 +448,12 @@ int tgk_mesh_upload(tgk_mesh* m, const double* nodes, const int64_t* elems, void
     return TGK_OK;
 }
 
+int tgk_mesh_coordinates_changed(tgk_mesh* m) {
+    if (!m) return set_error(TGK_ERR_INPUT, "null mesh");
+    m->div_safe = -1;  // re-certified for the Markstein division on the next fused call
+    return TGK_OK;
+}
+
 void tgk_mesh_destroy(tgk_mesh* m) {
     if (!m) return;
     if (m->owned) {
@@ -816,6 +822,7 @@ int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double
     const int comps = p->kind == TGK_ELASTICITY ? m->d : 1;
     if (r->components != comps)
         return set_error(TGK_ERR_INPUT, "assemble: dofmap component count does not match problem kind");
+    TGK_TRY(check_routing_fresh(m, r));
     // quadrature degree of physics.cpp:18-21 (the QUAD tables must be at it)
     const bool high = p->diffusion.type != TGK_FIELD_CONSTANT || p->kind == TGK_MASS || p->with_mass;
     const int degree = high ? 2 : 1;
@@ -865,6 +872,7 @@ int tgk_assemble_f32_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routin
         return set_error(TGK_ERR_INPUT, "P1 assembly supports TRI3 and TET4 meshes only");
     if (p->kind == TGK_ELASTICITY || r->components != 1)
         return set_error(TGK_ERR_INPUT, "tgk_assemble_f32_d: scalar problems only");
+    TGK_TRY(tgk::check_routing_fresh(m, r));
     if (p->diffusion.type == TGK_FIELD_QUAD || (p->n_source > 0 && p->source[0].type == TGK_FIELD_QUAD))
         return set_error(TGK_ERR_INPUT, "tgk_assemble_f32_d: quadrature-table fields are fp64-only");
     TGK_TRY(check_field(p->diffusion, m, "diffusion"));
@@ -880,6 +888,7 @@ int tgk_allen_cahn_d(const tgk_mesh* m, const tgk_routing* r, const double* d_u,
     if (m->kind != TGK_TRI3 && m->kind != TGK_TET4)
         return set_error(TGK_ERR_INPUT, "P1 assembly supports TRI3 and TET4 meshes only");
     if (r->components != 1) return set_error(TGK_ERR_INPUT, "AllenCahnStepper: scalar fields only");  // timestep.cpp:137
+    TGK_TRY(tgk::check_routing_fresh(m, r));
     TGK_TRY(host_ensure_device());
     return tgk::fused_allen_cahn(m, const_cast<tgk_routing*>(r), d_u, eps, d_T, d_F, static_cast<cudaStream_t>(stream));
 }

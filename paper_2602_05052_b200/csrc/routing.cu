@@ -434,6 +434,13 @@ int build_vector(const tgk_mesh* m, int c, int flags, cudaStream_t st, tgk_routi
 // The reference segment maps (mat_offsets / mat_slots, routing.cpp:64-83) of a
 // scalar routing built without TGK_ROUTING_SEGMENTS, on demand (the
 // materialised Stage II fallback of the fused kernels needs them).
+int check_routing_fresh(const tgk_mesh* m, const tgk_routing* r) {
+    if (r->mesh == m && r->mesh_version != m->conn_version)
+        return set_error(TGK_ERR_INPUT, "routing was built for an earlier connectivity of this mesh "
+                                        "(tgk_mesh_upload changed it): destroy and rebuild the routing");
+    return TGK_OK;
+}
+
 int ensure_scalar_segments(tgk_routing* r, cudaStream_t st) {
     if (r->mat_offsets) return TGK_OK;
     if (r->components != 1) return set_error(TGK_ERR_INPUT, "segment maps: scalar routing expected");
@@ -492,6 +499,7 @@ int routing_from_arrays(const tgk_mesh* m, int components, int64_t N, int64_t E,
     const size_t Ek = static_cast<size_t>(E) * k;
     auto* r = new tgk_routing();
     r->mesh = m;
+    r->mesh_version = m->conn_version;
     r->N = N;
     r->E = E;
     r->k = k;
@@ -524,6 +532,7 @@ int routing_from_arrays(const tgk_mesh* m, int components, int64_t N, int64_t E,
         // the fused kernels run on the node-level (scalar) routing: rebuild it on the GPU
         auto* s = new tgk_routing();
         s->mesh = m;
+        s->mesh_version = m->conn_version;
         rc = build_scalar(m, 0, st, s);
         if (rc) delete s;
         else r->scalar = s;
@@ -554,6 +563,7 @@ int tgk_routing_build(const tgk_mesh* m, int components, int flags, void* stream
     cudaStream_t st = as_stream(stream);
     auto* s = new tgk_routing();
     s->mesh = m;
+    s->mesh_version = m->conn_version;
     int rc = build_scalar(m, components == 1 ? flags : 0, st, s);
     if (rc != TGK_OK) {
         delete s;
@@ -565,6 +575,7 @@ int tgk_routing_build(const tgk_mesh* m, int components, int flags, void* stream
     }
     auto* v = new tgk_routing();
     v->mesh = m;
+    v->mesh_version = m->conn_version;
     rc = build_vector(m, components, flags | TGK_ROUTING_SEGMENTS, st, s, v);
     if (rc != TGK_OK) {
         v->scalar = s;

@@ -443,14 +443,19 @@ int run_local(const tgk_mesh* m, int degree, const double* c1, const double* c2,
     return check_bad(bad.p, st);
 }
 
+// int64 -> int32 connectivity with the range check of mesh.cpp:61-64; also
+// records whether any entry differs from the previous contents (`changed`).
 __global__ void k_narrow(const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst,
-                         unsigned long long* bad) {
+                         unsigned long long* bad, unsigned long long* changed) {
+    bool diff = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = src[i];
         if (v < 0 || v >= n_nodes) atomicMin(bad, static_cast<unsigned long long>(i));
+        diff = diff || dst[i] != static_cast<int32_t>(v);
         dst[i] = static_cast<int32_t>(v);
     }
+    if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) atomicOr(changed, 1ull);
 }
 
 }  // namespace
@@ -489,8 +494,8 @@ __global__ void k_coord_range(const double* x, int64_t n, unsigned* bad) {
 
 // Persistent per-mesh flag words (device + pinned host), allocated on first use.
 int mesh_flags(tgk_mesh* m) {
-    if (!m->d_flags) CUDA_TRY(cudaMalloc(&m->d_flags, 2 * sizeof(unsigned long long)));
-    if (!m->h_flags) CUDA_TRY(cudaMallocHost(&m->h_flags, 2 * sizeof(unsigned long long)));
+    if (!m->d_flags) CUDA_TRY(cudaMalloc(&m->d_flags, 3 * sizeof(unsigned long long)));
+    if (!m->h_flags) CUDA_TRY(cudaMallocHost(&m->h_flags, 3 * sizeof(unsigned long long)));
     return TGK_OK;
 }
 
@@ -513,14 +518,16 @@ int mesh_division_safe(tgk_mesh* m, cudaStream_t st, bool* safe) {
 int narrow_connectivity(tgk_mesh* m, const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
                         cudaStream_t st) {
     TGK_TRY(mesh_flags(m));
-    unsigned long long* flag = m->d_flags + 1;
+    unsigned long long* flag = m->d_flags + 1;  // [1] first bad entry, [2] changed
     CUDA_TRY(cudaMemsetAsync(flag, 0xff, sizeof(unsigned long long), st));
-    k_narrow<<<std::min<unsigned>(grid_for(n, 256), 148 * 16), 256, 0, st>>>(src, n, n_nodes, dst, flag);
+    CUDA_TRY(cudaMemsetAsync(flag + 1, 0, sizeof(unsigned long long), st));
+    k_narrow<<<std::min<unsigned>(grid_for(n, 256), 148 * 16), 256, 0, st>>>(src, n, n_nodes, dst, flag, flag + 1);
     KERNEL_CHECK("narrow_connectivity");
-    CUDA_TRY(cudaMemcpyAsync(m->h_flags + 1, flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(m->h_flags + 1, flag, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     const unsigned long long h = m->h_flags[1];
     *bad = h == ULLONG_MAX ? -1 : static_cast<int64_t>(h);
+    if (m->h_flags[2]) ++m->conn_version;  // routings built before refuse to assemble (check_routing_fresh)
     return TGK_OK;
 }
 

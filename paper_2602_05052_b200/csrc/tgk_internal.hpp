@@ -252,6 +252,7 @@ struct tgk_mesh {
     int32_t* conn = nullptr;     // device, E x k
     int64_t* staging = nullptr;  // device int64 connectivity staging for host uploads
     int div_safe = -1;           // coordinates certified for Markstein division (-1 unknown)
+    uint64_t conn_version = 0;   // bumped whenever an upload changes the connectivity
     bool owned = false;
     // persistent validation scratch (no per-call cudaMalloc / cudaFree, which
     // would serialise the device): 2 device flags, 2 pinned host words
@@ -264,6 +265,7 @@ struct tgk_routing {
     int k = 0, components = 1;
     int lmax = 0;                    // max scalar row length
     const tgk_mesh* mesh = nullptr;
+    uint64_t mesh_version = 0;       // the mesh's conn_version the routing was built for
     int64_t* row_ptr = nullptr;
     int64_t* col_idx = nullptr;
     uint32_t* slot_of = nullptr;     // scalar routing only
@@ -302,6 +304,9 @@ int ensure_group_plan(tgk_routing* r, int G, const GroupPlanDev** out);
 // Fast-mode plan for R rows per block over the routing's owned rows / element
 // range; TGK_ERR_INPUT without a message when the fast layout does not apply.
 int ensure_fast_plan(tgk_routing* r, int R, int fmt, bool fnodal, const FastPlanDev** out);
+// status 2 when the mesh's connectivity changed (tgk_mesh_upload) after the
+// routing was built from it: its pattern, slot map and plans are stale
+int check_routing_fresh(const tgk_mesh* m, const tgk_routing* r);
 struct ScalarRoutingHost {
     std::vector<double> nodes;
     std::vector<int32_t> conn;

@@ -37,8 +37,12 @@ class Mesh:
         self._kind = _kind_code(kind.lower())
         self.dim = 3 if self._kind == N.TET4 else 2
         k = 3 if self._kind == N.TRI3 else 4
-        self._nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, self.dim)
-        self._elements = np.ascontiguousarray(elements, dtype=np.int64).reshape(-1, k)
+        # private copies, exposed read-only: the device mesh / routing cached in
+        # _dev stay consistent with them (the reference returns copies, module.cpp:63-75)
+        self._nodes = np.array(nodes, dtype=np.float64).reshape(-1, self.dim)
+        self._elements = np.array(elements, dtype=np.int64).reshape(-1, k)
+        self._nodes.setflags(write=False)
+        self._elements.setflags(write=False)
         self._boundary = None if boundary_nodes is None else np.asarray(boundary_nodes, np.int64)
         self.boundary_tags = {}  # gmsh entity tag -> sorted node ids (mesh.hpp boundary_tags)
         self._dev = {}

@@ -128,3 +128,28 @@ def test_high_valence_elasticity_and_batched(eng):
         assert_bitwise(np_(Kb[b]), Kr, f"batched field {b}")
         if b == 0:
             assert_bitwise(np_(Fb), Fr, "batched F")
+
+
+def test_connectivity_change_marks_routings_stale(eng):
+    """tgk_mesh_upload with DIFFERENT connectivity invalidates routings built
+    before; identical connectivity (the e2e path) does not."""
+    from paper_2602_05052_b200 import InputError
+    from paper_2602_05052_b200 import _native as N
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [3, 3, 3])
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    r = eng.Routing(m, 1)
+    L = N.lib()
+    n64 = np.ascontiguousarray(nodes)
+    e64 = np.ascontiguousarray(elems, dtype=np.int64)
+    N.check(L.tgk_mesh_upload(m._h, n64.ctypes.data, e64.ctypes.data, None))
+    K1, _, _ = eng.assemble(m, r, sources=[1.0])  # same connectivity: still valid
+    e2 = e64.copy()
+    e2[[0, 1]] = e2[[1, 0]]
+    N.check(L.tgk_mesh_upload(m._h, None, e2.ctypes.data, None))
+    with pytest.raises(InputError, match="earlier connectivity"):
+        eng.assemble(m, r, sources=[1.0])
+    r2 = eng.Routing(m, 1)
+    K2, _, _ = eng.assemble(m, r2, sources=[1.0])
+    pr = port.Routing(nodes.shape[0], port.dofmap("tet4", e2, 1))
+    Kr, _, _ = port.assemble("tet4", nodes, e2, pr, sources=[1.0])
+    assert_bitwise(np_(K2), Kr, "rebuilt routing")
