@@ -669,7 +669,7 @@ def run_elasticity(args, ctx, N):
     mesh = engine.DeviceMesh(kind, m.nodes, m.elements)
     routing = engine.Routing(mesh, 3)
     setup_s = time.time() - t0
-    p, keep = engine.make_problem("elasticity", lam=LAME[0], mu=LAME[1], sources=[1.0, 1.0, 1.0])
+    p, keep = engine.make_problem("elasticity", lam=LAME[0], mu=LAME[1], sources=[1.0, 1.0, 1.0], mode=args.mode)
     K = torch.empty(routing.nnz, dtype=torch.float64, device=ctx.dev)
     F = torch.empty(routing.N, dtype=torch.float64, device=ctx.dev)
     L = N.lib()
@@ -682,6 +682,16 @@ def run_elasticity(args, ctx, N):
     with ClockSampler(ctx.local_rank) as clocks:
         ms = ctx.timed(step, args.steps)
     ms_per_step = ms / args.steps
+    # the other fp64 mode on the same inputs (both modes reported)
+    q, keep_q = engine.make_problem("elasticity", lam=LAME[0], mu=LAME[1], sources=[1.0, 1.0, 1.0],
+                                    mode="exact" if args.mode == "fast" else "fast")
+    qK, qF = torch.empty_like(K), torch.empty_like(F)
+
+    def step_other():
+        N.check(L.tgk_assemble_d(C.byref(q), mesh._h, routing._h, ptr(qK), ptr(qF), None, ctx.sp))
+    step_other()
+    other_ms = ctx.timed(step_other, max(3, args.steps // 4)) / max(3, args.steps // 4)
+    del qK, qF
     E = m.element_count()
     value = E * ctx.world / (ms_per_step * 1e-3)
     ab, comp = alg_bytes(kind, E, m.node_count(), routing.nnz, False, True, comps=3)
@@ -721,16 +731,21 @@ def run_elasticity(args, ctx, N):
                                 "tgk_assemble_d -> D2H of K, F into pinned host buffers; two device buffer sets on "
                                 "three streams so step i's D2H overlaps step i+1's H2D and compute (sync_drop_in: "
                                 "the blocking tgk_assemble into pageable buffers)")
+    fast = args.mode == "fast"
     config = {"workload": desc, "elements_per_gpu": E, "nnz_per_gpu": routing.nnz,
+              "mode": ("fast (TGK_MODE_FAST: within |dv| <= 1e-12|v_ref| + 1e-14 max|v_ref|, deterministic; "
+                       "tests/test_gpu_fast.py)" if fast else "exact (bit-identical to the reference)"),
               "parallelism": "single GPU" if ctx.world == 1 else f"{ctx.world} independent replicas",
-              "path": "fused row-block elasticity kernel (fused_elast.cu): one launch per step",
-              "l2": "inputs larger than L2", "setup_s": setup_s}
+              "path": ("fast elasticity kernel (fast.cu k_fast_elast)" if fast else
+                       "fused row-block elasticity kernel (fused_elast.cu)") + ": one launch per step",
+              "l2": "inputs larger than L2", "setup_s": setup_s,
+              "other_mode_kernel_ms": {("exact" if fast else "fast"): other_ms}}
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
                 gpu_launches=args.steps, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                           "frac": achieved / peak, "traffic": ncu_traffic("c3") if ctx.world == 1 else None,
                           "alg_bytes": ab, "compulsory_bytes": comp, "peak_source": peak_src,
-                          "kernel": "k_fused_elast2 (one launch per step)"})
+                          "kernel": ("k_fast_elast" if fast else "k_fused_elast2") + " (one launch per step)"})
 
 
 def run_reduce(args, ctx, N):

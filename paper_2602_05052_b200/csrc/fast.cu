@@ -646,3 +646,356 @@ int fast_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* 
 }
 
 }  // namespace tgk
+
+// ===========================================================================
+// Fast-mode vector elasticity (TGK_MODE_FAST; physics.cpp:45-66 with constant
+// Lamé parameters and a constant body force).  The plan is the scalar fast
+// plan (plan_fast.cpp, format kFastFmtE16): every scalar CSR entry (i, j) is a
+// d x d block of the vector CSR (dofmap.cpp:18-19 node-major interleave).
+// Phase A stores per halo element its physical basis gradients g_a and
+// c = |T^| det; phase B folds per scalar entry the isotropic block
+//   K_e[a r][b s] = c (lambda g_a,r g_b,s + mu g_a,s g_b,r + mu delta_rs g_a.g_b)
+// — local_stiffness_elasticity's B^T D B (batch.cpp:198-246) in closed form —
+// over the entry's elements, and the load F_i,r = f_r sum_e c_e / k
+// (local_load_vector, batch.cpp:291-312, constant source).  The mirrored entry
+// (j, i) receives the transposed block.
+namespace tgk {
+namespace {
+
+struct FastElastArgs {
+    const double* nodes;
+    FastPlanDev pl;
+    double lam, mu;  // plane-stress lambda already applied (physics.cpp:50-53)
+    double f[3];     // constant body force (n_source == d), else 0
+    double* K;
+    double* F;
+    int MH, MB, abuf, bbuf, gl, debug;
+    unsigned long long* bad;
+};
+
+template <int KIND, bool HAS_F>
+struct FastElastCfg {
+    static constexpr int k = P1<KIND>::k, d = P1<KIND>::d;
+    static constexpr int CROW = k * d;  // rows 0..kd-1: g_a,r (row a d + r); row kd: c = |T^| det
+    static constexpr int NR = k * d + 1;
+    static size_t smem(const FastElastArgs& a) {
+        return 64 + 2 * size_t(a.abuf) + size_t(a.bbuf) +
+               sizeof(double) * (2 * size_t(d) * a.MB + size_t(NR) * a.MH + size_t(d) * d * a.pl.max_tile) +
+               sizeof(int64_t) * a.pl.max_rows + sizeof(uint16_t) * (a.pl.max_rows + 1);
+    }
+};
+
+template <int KIND, bool HAS_F>
+__device__ __forceinline__ void elast_element(const FastElastArgs& p, const RecA& A, const double* xs, double* kv,
+                                              int h) {
+    using Cf = FastElastCfg<KIND, HAS_F>;
+    constexpr int k = Cf::k, d = Cf::d;
+    const int MH = p.MH, MB = p.MB;
+    const uint64_t hc = A.hconn[h];
+    int l[k];
+#pragma unroll
+    for (int a = 0; a < k; ++a) l[a] = static_cast<int>((hc >> (16 * a)) & 0xffff);
+    double g[k][d], det;
+    if constexpr (KIND == TGK_TET4) {
+        const double x0 = xs[l[0]], y0 = xs[MB + l[0]], z0 = xs[2 * MB + l[0]];
+        const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0, e1z = xs[2 * MB + l[1]] - z0;
+        const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0, e2z = xs[2 * MB + l[2]] - z0;
+        const double e3x = xs[l[3]] - x0, e3y = xs[MB + l[3]] - y0, e3z = xs[2 * MB + l[3]] - z0;
+        const double c1x = __fma_rn(e2y, e3z, -(e2z * e3y)), c1y = __fma_rn(e2z, e3x, -(e2x * e3z)),
+                     c1z = __fma_rn(e2x, e3y, -(e2y * e3x));
+        const double c2x = __fma_rn(e3y, e1z, -(e3z * e1y)), c2y = __fma_rn(e3z, e1x, -(e3x * e1z)),
+                     c2z = __fma_rn(e3x, e1y, -(e3y * e1x));
+        const double c3x = __fma_rn(e1y, e2z, -(e1z * e2y)), c3y = __fma_rn(e1z, e2x, -(e1x * e2z)),
+                     c3z = __fma_rn(e1x, e2y, -(e1y * e2x));
+        det = dot3(e1x, e1y, e1z, c1x, c1y, c1z);
+        const double rd = __drcp_rn(det);
+        g[1][0] = c1x * rd; g[1][1] = c1y * rd; g[1][2] = c1z * rd;
+        g[2][0] = c2x * rd; g[2][1] = c2y * rd; g[2][2] = c2z * rd;
+        g[3][0] = c3x * rd; g[3][1] = c3y * rd; g[3][2] = c3z * rd;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) g[0][r] = -((g[1][r] + g[2][r]) + g[3][r]);
+    } else {
+        const double x0 = xs[l[0]], y0 = xs[MB + l[0]];
+        const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0;
+        const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0;
+        det = __fma_rn(e1x, e2y, -(e1y * e2x));
+        const double rd = __drcp_rn(det);
+        g[1][0] = e2y * rd; g[1][1] = -(e2x * rd);
+        g[2][0] = -(e1y * rd); g[2][1] = e1x * rd;
+        g[0][0] = -(g[1][0] + g[2][0]); g[0][1] = -(g[1][1] + g[2][1]);
+    }
+    double c = det * FastConst<KIND>::wsum;
+    if (det <= 0.0) {  // batch.cpp:98-101
+        atomicMin(p.bad, static_cast<unsigned long long>(__ldg(p.pl.helem + A.hbase + h)));
+        c = 0.0;
+#pragma unroll
+        for (int a = 0; a < k; ++a)
+#pragma unroll
+            for (int r = 0; r < d; ++r) g[a][r] = 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < k; ++a)
+#pragma unroll
+        for (int r = 0; r < d; ++r) kv[(a * d + r) * MH + h] = g[a][r];
+    kv[Cf::CROW * MH + h] = c;
+}
+
+// Lane `lane` of warp group w: one scalar entry's d x d block (and, for a
+// diagonal entry, the row's d load values) folded over its elements.
+template <int KIND, bool HAS_F>
+__device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& A, const RecB& Bq, const double* kv,
+                                            double* tk, int w, int lane) {
+    using Cf = FastElastCfg<KIND, HAS_F>;
+    constexpr int k = Cf::k, d = Cf::d;
+    const int MH = p.MH;
+    const uint32_t desc = Bq.desc[w * 32 + lane];
+    const uint32_t i0 = Bq.wgoff[w];
+    const int steps = static_cast<int>((Bq.wgoff[w + 1] - i0) >> 6);
+    const uint2* ip = reinterpret_cast<const uint2*>(Bq.words + i0) + lane;
+    const bool diag = (__shfl_sync(0xffffffffu, desc, 0) >> 15) & 1u;
+    double acc[d][d], fac = 0.0;
+#pragma unroll
+    for (int r = 0; r < d; ++r)
+#pragma unroll
+        for (int s = 0; s < d; ++s) acc[r][s] = 0.0;
+    const double lam = p.lam, mu = p.mu;
+    auto eat = [&](uint32_t it) {
+        const int h = static_cast<int>(it & 0xfffu), a = static_cast<int>((it >> 14) & 3u),
+                  b = static_cast<int>((it >> 12) & 3u);
+        const double c = kv[Cf::CROW * MH + h];
+        double ga[d], gb[d];
+#pragma unroll
+        for (int r = 0; r < d; ++r) {
+            ga[r] = kv[(a * d + r) * MH + h];
+            gb[r] = kv[(b * d + r) * MH + h];
+        }
+        const double lc = lam * c, mc = mu * c;
+        double dt = ga[0] * gb[0];
+#pragma unroll
+        for (int r = 1; r < d; ++r) dt = __fma_rn(ga[r], gb[r], dt);
+        double u[d], v[d];
+#pragma unroll
+        for (int r = 0; r < d; ++r) {
+            u[r] = lc * ga[r];
+            v[r] = mc * ga[r];
+        }
+#pragma unroll
+        for (int r = 0; r < d; ++r)
+#pragma unroll
+            for (int s = 0; s < d; ++s) acc[r][s] = __fma_rn(u[r], gb[s], __fma_rn(v[s], gb[r], acc[r][s]));
+#pragma unroll
+        for (int r = 0; r < d; ++r) acc[r][r] = __fma_rn(mc, dt, acc[r][r]);
+        if constexpr (HAS_F) fac += c;
+    };
+    const uint32_t zw = (uint32_t(MH - 1) | (uint32_t(MH - 1) << 16));  // (h = zero slot, a = b = 0)
+    // the zero slot is h = max_halo; its values are +0.0 in every row (padding items)
+    for (int st = 0; st < steps; ++st) {
+        const uint2 wv = ip[st * 32];
+        eat(wv.x & 0xffffu);
+        eat(wv.x >> 16);
+        eat(wv.y & 0xffffu);
+        eat(wv.y >> 16);
+    }
+    (void)zw;
+    if (diag) {  // split diagonal lists: partial sums of kFastDiagSplit lanes
+        constexpr int DS = kFastDiagSplit(k);
+#pragma unroll
+        for (int o = 1; o < DS; o <<= 1) {
+#pragma unroll
+            for (int r = 0; r < d; ++r)
+#pragma unroll
+                for (int s = 0; s < d; ++s) acc[r][s] += __shfl_xor_sync(0xffffffffu, acc[r][s], o);
+            if constexpr (HAS_F) fac += __shfl_xor_sync(0xffffffffu, fac, o);
+        }
+    }
+    if (desc >= kFastPart) return;
+    const int lr = static_cast<int>(desc & 0x1ffu), pos = static_cast<int>((desc >> 9) & 63u);
+    if (pos != kFastNoPos) {
+        const int L = A.toff[lr + 1] - A.toff[lr];
+        double* t = tk + d * d * A.toff[lr] + d * pos;
+#pragma unroll
+        for (int r = 0; r < d; ++r)
+#pragma unroll
+            for (int s = 0; s < d; ++s) t[r * d * L + s] = acc[r][s];
+    }
+    if constexpr (HAS_F) {
+        if (diag) {
+            const int64_t row = A.srow[lr];
+#pragma unroll
+            for (int r = 0; r < d; ++r) p.F[row * d + r] = p.f[r] * fac * (1.0 / k);
+        }
+    }
+    if (desc >> 31) {  // the mirrored entry (j, i) holds the transposed block
+        const int lr2 = static_cast<int>((desc >> 16) & 0x1ffu), pos2 = static_cast<int>((desc >> 25) & 63u);
+        const int L2 = A.toff[lr2 + 1] - A.toff[lr2];
+        double* t = tk + d * d * A.toff[lr2] + d * pos2;
+#pragma unroll
+        for (int r = 0; r < d; ++r)
+#pragma unroll
+            for (int s = 0; s < d; ++s) t[s * d * L2 + r] = acc[r][s];
+    }
+}
+
+// Persistent kernel, the same pipeline as k_fast_scalar (TMA-fed records,
+// cp.async node tables, tile copy-out overlapping phase A).
+template <int KIND, bool HAS_F>
+__global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p) {
+    using Cf = FastElastCfg<KIND, HAS_F>;
+    constexpr int d = Cf::d;
+    extern __shared__ __align__(128) unsigned char smb[];
+    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = T >> 5;
+    const int MH = p.MH, MB = p.MB;
+    const FastPlanDev& pl = p.pl;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smb);
+    unsigned char* const ra_base = smb + 64;
+    unsigned char* const rb = ra_base + 2 * size_t(p.abuf);
+    double* const xs_base = reinterpret_cast<double*>(rb + size_t(p.bbuf));
+    double* const kv = xs_base + 2 * size_t(d) * MB;
+    double* const tk = kv + size_t(Cf::NR) * MH;
+    int64_t* const trp = reinterpret_cast<int64_t*>(tk + size_t(d) * d * pl.max_tile);
+    uint16_t* const ttoff = reinterpret_cast<uint16_t*>(trp + pl.max_rows);
+    auto ra = [&](int64_t it) { return ra_base + size_t(it & 1) * p.abuf; };
+    auto xsp = [&](int64_t it) { return xs_base + size_t(it & 1) * d * MB; };
+    const int64_t nb = pl.n_blocks, G = gridDim.x, b0 = blockIdx.x;
+    if (b0 >= nb) return;
+    const int64_t n_it = (nb - b0 + G - 1) / G;
+    if (tid == 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    if (tid < Cf::NR) kv[tid * MH + MH - 1] = 0.0;
+    __syncthreads();
+    auto load_a = [&](int64_t it) {
+        const int64_t blk = b0 + it * G, o = pl.rec_a_off[blk];
+        bulk_load(ra(it), pl.rec_a + o, static_cast<uint32_t>(pl.rec_a_off[blk + 1] - o), &bars[it & 1]);
+    };
+    auto load_b = [&](int64_t it) {
+        const int64_t blk = b0 + it * G, o = pl.rec_b_off[blk];
+        bulk_load(rb, pl.rec_b + o, static_cast<uint32_t>(pl.rec_b_off[blk + 1] - o), &bars[2]);
+    };
+    auto wait_a = [&](int64_t it) { mbar_wait(&bars[it & 1], static_cast<uint32_t>((it >> 1) & 1)); };
+    auto wait_b = [&](int64_t it) { mbar_wait(&bars[2], static_cast<uint32_t>(it & 1)); };
+    auto gather = [&](int64_t it) {
+        const RecA A = parse_a(ra(it));
+        double* xs = xsp(it);
+        for (int i = tid; i < int(A.nbn); i += T) {
+            const int64_t g = A.bnodes[i];
+#pragma unroll
+            for (int c = 0; c < d; ++c) cp_async8(xs + c * MB + i, p.nodes + g * d + c);
+        }
+        cp_async_commit();
+    };
+    int tile_rows = 0;
+    auto copy_out = [&]() {  // scalar row i's d rows are one contiguous d^2 L run of the vector CSR
+        if (p.debug & 4) return;
+        for (int lr = warp; lr < tile_rows; lr += nwarp) {
+            const int64_t rp = trp[lr] * (d * d);
+            const int t0 = ttoff[lr] * (d * d), len = (ttoff[lr + 1] - ttoff[lr]) * (d * d);
+            for (int q = lane; q < len; q += 32) p.K[rp + q] = tk[t0 + q];
+        }
+    };
+    if (tid == 0) {
+        load_a(0);
+        if (n_it > 1) load_a(1);
+        load_b(0);
+    }
+    wait_a(0);
+    gather(0);
+    cp_async_wait_all();
+    __syncthreads();
+    for (int64_t it = 0; it < n_it; ++it) {
+        const RecA A = parse_a(ra(it));
+        copy_out();
+        const int nh_run = (p.debug & 1) ? 0 : int(A.nh);
+        for (int h = tid; h < nh_run; h += T) elast_element<KIND, HAS_F>(p, A, xsp(it), kv, h);
+        __syncthreads();
+        if (it + 1 < n_it) {
+            wait_a(it + 1);
+            gather(it + 1);
+        }
+        wait_b(it);
+        const RecB Bq = parse_b(rb);
+        for (int i = tid; i <= int(A.nr); i += T) {
+            if (i < int(A.nr)) trp[i] = A.rp[i];
+            ttoff[i] = A.toff[i];
+        }
+        tile_rows = int(A.nr);
+        const int nwg = (p.debug & 2) ? 0 : int(Bq.nwg);
+        for (int w = warp; w < nwg; w += nwarp) elast_group<KIND, HAS_F>(p, A, Bq, kv, tk, w, lane);
+        cp_async_wait_all();
+        __syncthreads();
+        if (tid == 0) {
+            fence_proxy_async();
+            if (it + 2 < n_it) load_a(it + 2);
+            if (it + 1 < n_it) load_b(it + 1);
+        }
+    }
+    copy_out();
+}
+
+template <int KIND, bool HAS_F>
+int launch_fast_elast(const FastElastArgs& a, int threads, cudaStream_t st) {
+    auto kern = k_fast_elast<KIND, HAS_F>;
+    const size_t smem = FastElastCfg<KIND, HAS_F>::smem(a);
+    if (smem > 227 * 1024) return kFastNotApplicable;
+    static size_t done[kMaxDevices] = {};
+    TGK_TRY(raise_smem_limit(kern, smem, done));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    if (per_sm < 1) return kFastNotApplicable;
+    if (const char* e = getenv("TGK_FAST_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
+    const int64_t grid = std::min<int64_t>(a.pl.n_blocks, int64_t(per_sm) * sm_count());
+    if (grid > 0) kern<<<static_cast<unsigned>(grid), threads, smem, st>>>(a);
+    KERNEL_CHECK("fast_elast");
+    return TGK_OK;
+}
+
+}  // namespace
+
+// Fast-mode elasticity; kFastNotApplicable unless lambda, mu (and the body
+// force) are constants — the exact kernels take every other case.
+int fast_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
+                             cudaStream_t st) {
+    const int d = m->d;
+    if (pr->lambda.type != TGK_FIELD_CONSTANT || pr->mu.type != TGK_FIELD_CONSTANT) return kFastNotApplicable;
+    for (int c = 0; c < pr->n_source; ++c)
+        if (pr->source[c].type != TGK_FIELD_CONSTANT) return kFastNotApplicable;
+    if (!(pr->mu.value > 0.0)) return set_error(TGK_ERR_INPUT, "elasticity requires mu > 0");  // batch.cpp:194-195
+    const bool has_f = pr->n_source > 0;
+    int R = m->kind == TGK_TET4 ? 32 : 64, T = 256;  // B200 sweep: C3 0.95 (R=16) -> 0.89 ms (R=32)
+    if (const char* e = getenv("TGK_FAST_ER")) R = std::max(1, std::min(kFastMaxRows, atoi(e)));
+    if (const char* e = getenv("TGK_FAST_ET")) T = std::max(32, std::min(kFastMaxThreads, atoi(e) / 32 * 32));
+    const FastPlanDev* pl = nullptr;
+    {
+        const int prc = ensure_fast_plan(r, R, kFastFmtE16, false, &pl);
+        if (prc == TGK_ERR_INPUT) return kFastNotApplicable;
+        if (prc != TGK_OK) return prc;
+    }
+    FastElastArgs a{};
+    a.nodes = m->nodes;
+    a.pl = *pl;
+    a.lam = pr->lambda.value;
+    a.mu = pr->mu.value;
+    if (d == 2 && pr->plane_stress) a.lam = 2.0 * a.lam * a.mu / (a.lam + 2.0 * a.mu);  // plane_stress_lambda
+    for (int c = 0; c < d; ++c) a.f[c] = has_f ? pr->source[c].value : 0.0;
+    a.K = K;
+    a.F = F;
+    a.MH = pl->MH;
+    a.MB = (pl->max_bnodes + 1) & ~1;
+    a.abuf = (pl->max_rec_a + 15) & ~15;
+    a.bbuf = (pl->max_rec_b + 15) & ~15;
+    if (const char* e = getenv("TGK_FAST_DEBUG")) a.debug = atoi(e);
+    unsigned long long* bad = nullptr;
+    TGK_TRY(routing_flags(r, &bad));
+    a.bad = bad;
+    CUDA_TRY(cudaMemsetAsync(a.bad, 0xff, sizeof(unsigned long long), st));
+    if (!has_f && F) CUDA_TRY(cudaMemsetAsync(F, 0, sizeof(double) * r->N, st));
+    int rc;
+    if (m->kind == TGK_TET4) rc = has_f ? launch_fast_elast<TGK_TET4, true>(a, T, st) : launch_fast_elast<TGK_TET4, false>(a, T, st);
+    else rc = has_f ? launch_fast_elast<TGK_TRI3, true>(a, T, st) : launch_fast_elast<TGK_TRI3, false>(a, T, st);
+    if (rc != TGK_OK) return rc;
+    return check_bad(bad, st);
+}
+
+}  // namespace tgk

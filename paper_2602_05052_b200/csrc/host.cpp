@@ -158,6 +158,8 @@ int fast_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* 
                          cudaStream_t st, unsigned long long* d_bad);
 int materialised_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
                                  double* M, cudaStream_t st, unsigned long long* d_bad);
+int fast_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
+                             cudaStream_t st);
 int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
                         double* F, cudaStream_t st);
 int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
@@ -845,6 +847,10 @@ int assemble_dev(const tgk_problem* p, const tgk_mesh* m, tgk_routing* r, double
         // path (evaluate -> local_stiffness_elasticity -> reduce_matrix) remains
         // behind TGK_ELAST_MATERIALISED=1 (needs a routing with segment maps)
         if (quad || getenv("TGK_ELAST_MATERIALISED")) return elasticity_assemble(p, m, r, K, F, st);
+        if (p->mode == TGK_MODE_FAST) {
+            const int rc = fast_elasticity_assemble(p, m, r, K, F, st);
+            if (rc != kFastNotApplicable) return rc;
+        }
         return fused_elasticity_assemble(p, m, r, K, F, st);
     }
     if (quad) return materialised_scalar_assemble(p, m, r, K, F, M, st, d_bad);

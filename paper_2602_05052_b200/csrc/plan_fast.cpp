@@ -71,7 +71,7 @@ int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const i
         std::vector<uint32_t> rows, helem, bnodes, desc;
         std::vector<uint64_t> hconn;
         std::vector<uint32_t> list_off;  // per entry, n+1 (block-relative)
-        std::vector<uint16_t> items;     // generic items: halo index | (pair or a) << 12
+        std::vector<uint16_t> items;     // generic items: halo index | (a * 4 + b) << 12 (row node a, column node b)
         bool fail = false;
     };
     std::vector<BlockOut> out(nb);
@@ -144,9 +144,9 @@ int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const i
                             col[p] = lj;
                             pos2[p] = static_cast<int>(int64_t(slot_of[(int64_t(e) * k + bb) * k + a]) - row_ptr[j]);
                         }
-                        if (use) ent[p].push_back(static_cast<uint16_t>(h | (sym_pair_k(k, a, bb) << 12)));
+                        if (use) ent[p].push_back(static_cast<uint16_t>(h | ((a * 4 + bb) << 12)));
                     }
-                    if (use) diag.push_back(static_cast<uint16_t>(h | (a << 12)));
+                    if (use) diag.push_back(static_cast<uint16_t>(h | ((a * 4 + a) << 12)));
                 }
                 // the row's diagonal entry (also its load value)
                 lists.push_back(std::move(diag));
@@ -252,7 +252,10 @@ int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const i
 //                (det), F; all items u32 = K index | S index << 16 (F index =
 //                S index + MH);
 //   kFastFmtS16  coefficient mass (ProblemKind::Mass): row S (c det); items
-//                u16 = h.
+//                u16 = h;
+//   kFastFmtE16  vector elasticity (fast.cu k_fast_elast): items u16 = the
+//                generic h | (a * 4 + b) << 12, the kernel reads the scaled
+//                gradients of nodes a, b of halo element h.
 // MH = max halo + 1: index MH - 1 of every row is the +0.0 padding slot.
 void FastPlanDev::release() {
     if (blob) cudaFree(blob);
@@ -262,6 +265,7 @@ void FastPlanDev::release() {
 int fast_value_rows(int k, int fmt, bool fnodal) {
     const int np = k * (k + 1) / 2;
     if (fmt == kFastFmtS16) return 1;
+    if (fmt == kFastFmtE16) return 1;  // items carry (h, a, b), not value indices
     if (fmt == kFastFmtKS32) return np + 2;
     return np + (fnodal ? k : 1);
 }
@@ -300,15 +304,17 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
     const uint32_t zero = uint32_t(MH - 1);
     // generic item -> resolved index / word
     auto off_item = [&](uint16_t g) -> uint32_t {  // off-diagonal
-        const uint32_t hh = g & 0xfffu, q = g >> 12;
+        const uint32_t hh = g & 0xfffu, a = (g >> 12) >> 2, b = (g >> 12) & 3u;
         if (fmt == kFastFmtS16) return hh;
-        const uint32_t kidx = uint32_t(pair_row(k, int(q))) * MH + hh;
+        if (fmt == kFastFmtE16) return g;  // elasticity: the kernel reads g_a, g_b of element h
+        const uint32_t kidx = uint32_t(pair_row(k, sym_pair_k(k, int(a), int(b)))) * MH + hh;
         if (fmt == kFastFmtK16) return kidx;
         return kidx | ((uint32_t(NP) * MH + hh) << 16);
     };
     auto diag_item = [&](uint16_t g) -> uint32_t {
-        const uint32_t hh = g & 0xfffu, a = g >> 12;
+        const uint32_t hh = g & 0xfffu, a = (g >> 12) >> 2;
         if (fmt == kFastFmtS16) return hh;
+        if (fmt == kFastFmtE16) return g;
         const uint32_t kidx = a * MH + hh;
         if (fmt == kFastFmtKS32) return kidx | ((uint32_t(NP) * MH + hh) << 16);
         return kidx | ((uint32_t(NP + (fnodal ? a : 0)) * MH + hh) << 16);
@@ -333,7 +339,7 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
         std::vector<uint32_t> wgoff(nwg + 1, 0), words;
         for (uint32_t w = 0; w < nwg; ++w) {
             const bool diag = (P.desc[e0 + w * 32] >> 15) & 1u;  // lane 0 is never idle
-            const bool wide = fmt == kFastFmtKS32 || (fmt == kFastFmtK16 && diag);
+            const bool wide = fmt == kFastFmtKS32 || (fmt == kFastFmtK16 && diag);  // E16 / S16: u16 items
             const int per_step = wide ? 2 : 4;
             int steps = 0;
             for (int l = 0; l < 32; ++l) {

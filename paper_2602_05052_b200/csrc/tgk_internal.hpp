@@ -197,13 +197,14 @@ struct FastPlanHost {
     std::vector<uint32_t> rows, helem, bnodes, desc;
     std::vector<uint64_t> hconn;     // 4 x u16 block-local node indices per halo element
     std::vector<uint32_t> list_off;  // per block, per entry: item offsets (block-relative), n+1 per block
-    std::vector<uint16_t> items;     // generic items: halo index | (pair, or a for diagonals) << 12
+    std::vector<uint16_t> items;     // generic items: halo index | (a * 4 + b) << 12 (row node a, column node b)
 };
 
 // value-row formats of the fast kernel (plan_fast.cpp ensure_fast_plan)
 constexpr int kFastFmtK16 = 0;   // stiffness [+ load]
 constexpr int kFastFmtKS32 = 1;  // stiffness + unit mass [+ scalar load]
 constexpr int kFastFmtS16 = 2;   // coefficient mass
+constexpr int kFastFmtE16 = 3;   // vector elasticity (3 x 3 / 2 x 2 blocks per scalar entry)
 constexpr int kFastPlanSlots = 3;
 
 // Device form: two byte records per block, each one TMA bulk copy into shared

@@ -182,3 +182,49 @@ def test_fast_errors(eng):
     r = eng.Routing(m, 1)
     with pytest.raises(InputError, match="element 5 has non-positive Jacobian determinant"):
         eng.assemble(m, r, sources=[1.0], mode="fast")
+
+
+@pytest.mark.parametrize("kind,mesh,kw", [
+    ("tet4", "grid", dict(sources=[1.0, 1.0, 1.0])),
+    ("tet4", "permuted", dict(sources=[0.5, -1.0, 2.0])),
+    ("tet4", "grid", dict()),
+    ("tri3", "grid", dict(sources=[1.0, -0.5])),
+    ("tri3", "unstructured", dict(plane_stress=True, sources=[1.0, 1.0])),
+], ids=["tet-grid-f", "tet-permuted-f", "tet-grid-nof", "tri-grid-f", "tri-unstructured-planestress"])
+def test_fast_elasticity_vs_oracle(eng, kind, mesh, kw):
+    """Fast-mode vector elasticity (k_fast_elast): 3x3 / 2x2 blocks on the
+    scalar fast plan, within the scaled tolerance of local_stiffness_elasticity
+    + reduce_matrix (batch.cpp:183-248, routing.cpp:109-132)."""
+    from paper_2602_05052_b200 import meshgen
+    if mesh == "unstructured":
+        nodes, elems = meshgen.unstructured_tri(40)
+    elif mesh == "permuted":
+        nodes, elems = permuted(*port.generate_grid("tet4", [1.0, 1.2, 0.8], [8, 7, 9]), 3)
+    else:
+        nodes, elems = port.generate_grid(kind, [1.0, 1.1, 0.9][: 3 if kind == "tet4" else 2],
+                                          [9, 8, 7] if kind == "tet4" else [31, 27])
+    d = 3 if kind == "tet4" else 2
+    m = eng.DeviceMesh(kind, nodes, elems)
+    rv = eng.Routing(m, d)
+    prv = port.Routing(nodes.shape[0] * d, port.dofmap(kind, elems, d))
+    lam, mu = 0.5769230769230769, 0.38461538461538464
+    K, F, _ = eng.assemble(m, rv, kind="elasticity", lam=lam, mu=mu, mode="fast", **kw)
+    Kr, Fr, _ = port.assemble(kind, nodes, elems, prv, problem="elasticity", lam=lam, mu=mu, **kw)
+    assert_scaled_close(np_(K), Kr, what="elasticity K")
+    assert_scaled_close(np_(F), Fr, what="elasticity F")
+    K2, F2, _ = eng.assemble(m, rv, kind="elasticity", lam=lam, mu=mu, mode="fast", **kw)
+    assert_bitwise(np_(K2), np_(K), "elasticity rerun")
+
+
+def test_fast_elasticity_c3_30(eng):
+    """C3's fast kernel on a 30^3 Kuhn cube (162k tets, 3 DoF/node)."""
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [30, 30, 30])
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    rv = eng.Routing(m, 3)
+    pr = port.Routing(nodes.shape[0] * 3, port.dofmap("tet4", elems, 3))
+    lam, mu = 0.5769230769230769, 0.38461538461538464
+    K, F, _ = eng.assemble(m, rv, kind="elasticity", lam=lam, mu=mu, sources=[1.0, 1.0, 1.0], mode="fast")
+    Kr, Fr, _ = port.assemble("tet4", nodes, elems, pr, problem="elasticity", lam=lam, mu=mu,
+                              sources=[1.0, 1.0, 1.0])
+    assert_scaled_close(np_(K), Kr, what="C3 K")
+    assert_scaled_close(np_(F), Fr, what="C3 F")
