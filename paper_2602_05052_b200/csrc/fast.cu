@@ -315,52 +315,41 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
     const uint2* ip = reinterpret_cast<const uint2*>(Bq.words + i0) + lane;
     const bool diag = (__shfl_sync(0xffffffffu, desc, 0) >> 15) & 1u;  // warp-uniform class
     double k0 = 0.0, k1 = 0.0, k2 = 0.0, k3 = 0.0, s0 = 0.0, s1 = 0.0, f0 = 0.0, f1 = 0.0;
-    constexpr bool WIDE_OFF = Cf::FMT == kFastFmtKS32;
-    const bool wide = WIDE_OFF || (Cf::FMT == kFastFmtK16 && diag);
+    // u16 items h | q << 12: K_ab at row q, S at SROW, F at FROW (+ a = q for a
+    // nodal load on a diagonal); padding items address the +0.0 slot
     const uint32_t zw = uint32_t(MH - 1) | (uint32_t(MH - 1) << 16);
     const uint2 padw = make_uint2(zw, zw);
     uint2 wa = steps > 0 ? ip[0] : padw;
     uint2 wb = steps > 1 ? ip[32] : padw;
-    if (wide) {  // u32 items: low = K (or S) index, high = S / F index
-        auto eat = [&](uint32_t it, double& kk, double& ss, double& ff) {
-            const int lo = static_cast<int>(it & 0xffffu), hi = static_cast<int>(it >> 16);
-            kk += kv[lo];
-            if constexpr (Cf::FMT == kFastFmtKS32) {
-                ss += kv[hi];
-                if constexpr (FT == 1) {
-                    if (diag) ff += kv[hi + MH];
-                }
-            } else if constexpr (FT > 0) {
-                ff += kv[hi];
-            }
-        };
-        for (int st = 0; st < steps; st += 2) {
-            const uint2 wc = st + 2 < steps ? ip[(st + 2) * 32] : padw;
-            const uint2 wd = st + 3 < steps ? ip[(st + 3) * 32] : padw;
-            eat(wa.x, k0, s0, f0);
-            eat(wa.y, k1, s1, f1);
-            eat(wb.x, k2, s0, f0);
-            eat(wb.y, k3, s1, f1);
-            wa = wc;
-            wb = wd;
+    auto eat = [&](uint32_t it, double& kk, double& ss, double& ff) {
+        const int h = static_cast<int>(it & 0xfffu), q = static_cast<int>(it >> 12);
+        if constexpr (KT == 0) kk += kv[q * MH + h];
+        if constexpr (Cf::HAS_S) ss += kv[Cf::SROW * MH + h];
+        if constexpr (FT == 1) {
+            if (diag) ff += kv[Cf::FROW * MH + h];
         }
-    } else {  // u16 items: K (or S) index
-        for (int st = 0; st < steps; st += 2) {
-            const uint2 wc = st + 2 < steps ? ip[(st + 2) * 32] : padw;
-            const uint2 wd = st + 3 < steps ? ip[(st + 3) * 32] : padw;
-            const double v0 = kv[wa.x & 0xffffu], v1 = kv[wa.x >> 16], v2 = kv[wa.y & 0xffffu], v3 = kv[wa.y >> 16];
-            const double v4 = kv[wb.x & 0xffffu], v5 = kv[wb.x >> 16], v6 = kv[wb.y & 0xffffu], v7 = kv[wb.y >> 16];
-            k0 += v0;
-            k1 += v1;
-            k2 += v2;
-            k3 += v3;
-            k0 += v4;
-            k1 += v5;
-            k2 += v6;
-            k3 += v7;
-            wa = wc;
-            wb = wd;
+        if constexpr (FT == 2) {
+            if (diag) ff += kv[(Cf::FROW + q) * MH + h];
         }
+    };
+    for (int st = 0; st < steps; st += 2) {
+        const uint2 wc = st + 2 < steps ? ip[(st + 2) * 32] : padw;
+        const uint2 wd = st + 3 < steps ? ip[(st + 3) * 32] : padw;
+        eat(wa.x & 0xffffu, k0, s0, f0);
+        eat(wa.x >> 16, k1, s1, f1);
+        eat(wa.y & 0xffffu, k2, s0, f0);
+        eat(wa.y >> 16, k3, s1, f1);
+        eat(wb.x & 0xffffu, k0, s0, f0);
+        eat(wb.x >> 16, k1, s1, f1);
+        eat(wb.y & 0xffffu, k2, s0, f0);
+        eat(wb.y >> 16, k3, s1, f1);
+        wa = wc;
+        wb = wd;
+    }
+    if constexpr (KT == 1) {  // coefficient mass: the folds summed S
+        k0 = s0;
+        k1 = s1;
+        k2 = k3 = 0.0;
     }
     k0 += k2;
     k1 += k3;
@@ -380,7 +369,7 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
             }
         }
     }
-    if constexpr (KT == 1) {  // S16: the K folds summed S
+    if constexpr (KT == 1) {  // the value below is S-based
         s0 = k0;
         s1 = k1;
     }
@@ -578,13 +567,13 @@ int check_bad(unsigned long long* d_bad, cudaStream_t st);
 
 // Rows per block and threads per CTA (B200 sweeps, profiles/r02_fast_experiments.txt):
 // TET4 stiffness [+ load] 32 rows x 256 threads (3 CTAs/SM); with the unit
-// mass (two value rows more, two output tiles) 96 rows x 512 threads;
+// mass (two value rows more, two output tiles) 48 rows x 384 threads;
 // TRI3 128 rows x 256 threads.
 struct FastShape {
     int R, T;
 };
 FastShape fast_shape(int kind, int fmt) {
-    FastShape s{kind == TGK_TET4 ? (fmt == kFastFmtKS32 ? 96 : 32) : 128, kind == TGK_TET4 && fmt == kFastFmtKS32 ? 512 : 256};
+    FastShape s{kind == TGK_TET4 ? (fmt == kFastFmtKS32 ? 48 : 32) : 128, kind == TGK_TET4 && fmt == kFastFmtKS32 ? 384 : 256};
     if (const char* e = getenv("TGK_FAST_R")) s.R = std::max(1, std::min(kFastMaxRows, atoi(e)));
     if (const char* e = getenv("TGK_FAST_T")) s.T = std::max(32, std::min(kFastMaxThreads, atoi(e) / 32 * 32));
     return s;
@@ -610,7 +599,7 @@ int fast_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* 
     const int fmt = kt == 1 ? kFastFmtS16 : (hm ? kFastFmtKS32 : kFastFmtK16);
     const FastShape shape = fast_shape(m->kind, fmt);
     {
-        const int prc = ensure_fast_plan(r, shape.R, fmt, ft == 2, &pl);
+        const int prc = ensure_fast_plan(r, shape.R, kFastFmtK16, false, &pl);  // one item layout for every scalar format
         if (prc == TGK_ERR_INPUT) return kFastNotApplicable;
         if (prc != TGK_OK) return prc;
     }

@@ -299,25 +299,21 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
     if (rc != TGK_OK) return rc;
     const int MH = P.max_halo + 1;
     const int NP = k * (k + 1) / 2;
-    const int nrows = fast_value_rows(k, fmt, fnodal);
-    if (int64_t(nrows) * MH > 65536) return TGK_ERR_INPUT;  // items are u16 indices: not applicable
-    const uint32_t zero = uint32_t(MH - 1);
+    const uint32_t zero = uint32_t(MH - 1);  // padding item: halo slot max_halo (+0.0), row 0
     // generic item -> resolved index / word
-    auto off_item = [&](uint16_t g) -> uint32_t {  // off-diagonal
-        const uint32_t hh = g & 0xfffu, a = (g >> 12) >> 2, b = (g >> 12) & 3u;
-        if (fmt == kFastFmtS16) return hh;
+    // scalar formats: u16 = h | (value row of K_ab) << 12 — off-diagonal pairs
+    // their row (k..NP-1), diagonals a (row a = K_aa); the kernel forms the
+    // S / F indices from h (and a) itself.  Elasticity: the generic item.
+    (void)NP;
+    (void)zero;
+    auto off_item = [&](uint16_t g) -> uint32_t {
         if (fmt == kFastFmtE16) return g;  // elasticity: the kernel reads g_a, g_b of element h
-        const uint32_t kidx = uint32_t(pair_row(k, sym_pair_k(k, int(a), int(b)))) * MH + hh;
-        if (fmt == kFastFmtK16) return kidx;
-        return kidx | ((uint32_t(NP) * MH + hh) << 16);
+        const uint32_t hh = g & 0xfffu, a = (g >> 12) >> 2, b = (g >> 12) & 3u;
+        return hh | (uint32_t(pair_row(k, sym_pair_k(k, int(a), int(b)))) << 12);
     };
     auto diag_item = [&](uint16_t g) -> uint32_t {
-        const uint32_t hh = g & 0xfffu, a = (g >> 12) >> 2;
-        if (fmt == kFastFmtS16) return hh;
         if (fmt == kFastFmtE16) return g;
-        const uint32_t kidx = a * MH + hh;
-        if (fmt == kFastFmtKS32) return kidx | ((uint32_t(NP) * MH + hh) << 16);
-        return kidx | ((uint32_t(NP + (fnodal ? a : 0)) * MH + hh) << 16);
+        return (g & 0xfffu) | (uint32_t((g >> 12) >> 2) << 12);
     };
     auto al16 = [](size_t x) { return (x + 15) & ~size_t(15); };
     const int64_t nb = P.n_blocks;
@@ -339,7 +335,7 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
         std::vector<uint32_t> wgoff(nwg + 1, 0), words;
         for (uint32_t w = 0; w < nwg; ++w) {
             const bool diag = (P.desc[e0 + w * 32] >> 15) & 1u;  // lane 0 is never idle
-            const bool wide = fmt == kFastFmtKS32 || (fmt == kFastFmtK16 && diag);  // E16 / S16: u16 items
+            const bool wide = false;  // u16 items, 4 per 8-byte step
             const int per_step = wide ? 2 : 4;
             int steps = 0;
             for (int l = 0; l < 32; ++l) {
