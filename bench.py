@@ -101,12 +101,16 @@ def alg_bytes(kind, E, Nn, nnz, with_mass, has_f, comps=1, vbytes=8):
     return b, b - E * k * k * 4
 
 
-def ncu_traffic(workload):
+def ncu_traffic(workload, kernel=None):
     """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel per launch, from the
-    committed ncu --set full capture of this workload (profiles/traffic.json), or None."""
+    committed ncu --set full capture of this workload (profiles/traffic.json) when it captured
+    `kernel` (the one this run times), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(workload, {}).get("bytes")
+            e = json.load(f).get(workload, {})
+        if kernel and kernel not in e.get("kernel", ""):
+            return None
+        return e.get("bytes")
     except Exception:
         return None
 
@@ -652,7 +656,7 @@ def run_scalar(args, ctx, N):
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
                 gpu_launches=launches, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                          "frac": achieved / peak, "traffic": ncu_traffic(args.workload) if world == 1 else None,
+                          "frac": achieved / peak, "traffic": ncu_traffic(args.workload, "k_fast_scalar" if fast else "k_fused_scalar") if world == 1 else None,
                           "alg_bytes": ab, "compulsory_bytes": comp,
                           "peak_source": peak_src,
                           "kernel": ("k_fast_scalar" if fast else "k_fused_scalar") + " (one launch per step)",
@@ -743,7 +747,7 @@ def run_elasticity(args, ctx, N):
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
                 gpu_launches=args.steps, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                          "frac": achieved / peak, "traffic": ncu_traffic("c3") if ctx.world == 1 else None,
+                          "frac": achieved / peak, "traffic": ncu_traffic("c3", "k_fast_elast" if fast else "k_fused_elast") if ctx.world == 1 else None,
                           "alg_bytes": ab, "compulsory_bytes": comp, "peak_source": peak_src,
                           "kernel": ("k_fast_elast" if fast else "k_fused_elast2") + " (one launch per step)"})
 
@@ -804,8 +808,9 @@ def run_reduce(args, ctx, N):
     return dict(value=value, ms_per_step=ms_per_step, scaling=scaling, config=config, e2e=e2e,
                 gpu_launches=args.steps, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                          "frac": achieved / peak, "traffic": None, "alg_bytes": ab, "peak_source": peak_src,
-                          "kernel": "k_segment_reduce (one launch per step)", "kernel_ms": ms_per_step})
+                          "frac": achieved / peak, "traffic": ncu_traffic("rm", "k_segment_reduce") if ctx.world == 1 else None, "alg_bytes": ab,
+                          "peak_source": peak_src, "kernel": "k_segment_reduce (one launch per step)",
+                          "kernel_ms": ms_per_step})
 
 
 def run_batched(args, ctx, N):

@@ -21,12 +21,12 @@ def raw(rep):
 
 
 def main():
-    prefix = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    prefix = sys.argv[1] if len(sys.argv) > 1 else "r02"
     outdir = os.environ.get("TRAFFIC_OUT", os.path.join(ROOT, "profiles"))  # on the GPU box: under gpurun_out/
     os.makedirs(outdir, exist_ok=True)
     path = os.path.join(outdir, "traffic.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
-    for w in ["c2", "c2a", "c1", "c3", "c4", "c4adj", "c5"]:
+    for w in ["c2", "c2a", "c1", "c3", "c4", "c4adj", "c5", "rm"]:
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{w}.ncu-rep")
         if not os.path.exists(rep):
             continue
