@@ -247,6 +247,15 @@ int tgk_reduce_matrix_d(const tgk_routing* r, const double* d_local, double* d_v
                         void* stream);
 int tgk_reduce_vector_d(const tgk_routing* r, const double* d_local, double* d_F, void* stream);
 
+/* scatter_add_oracle (routing.cpp:134-175): the reference's independent
+ * correctness baseline — its own pattern and a per-element scatter in element
+ * order — by a different GPU algorithm than tgk_routing_build (one stable
+ * radix sort of all (row, col) contribution keys).  HOST buffers: call with
+ * offsets = cols = values = NULL to get *nnz, then with N+1 / nnz / nnz
+ * arrays; local_vectors (E x k) and F (N) may be NULL.  Bit-identical. */
+int tgk_scatter_add(const tgk_mesh* m, const double* local_matrices, const double* local_vectors, int64_t* nnz,
+                    int64_t* offsets, int64_t* cols, double* values, double* F);
+
 /* ------------------------------------------------------------------ fused assembly */
 /* tg::assemble (physics.cpp:10-75): Map fused with Reduce — local tensors
  * never touch HBM.  Writes K values (nnz), F (N) and, with with_mass, M values.

@@ -95,6 +95,7 @@ _SIGS = {
     "tgk_bicgstab_d": (_I, [_I64, _P, _P, _P, _P, _P, _D, _D, _I64, _P, _P, _P, _P]),
     "tgk_copy_d2d": (_I, [_P, _P, _I64, _P]),
     "tgk_alloc_d": (_I, [_P, _I64]),
+    "tgk_scatter_add": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "tgk_mesh_coordinates_changed": (_I, [_P]),
     "tgk_free_d": (_I, [_P]),
     "tgk_copy_d2h": (_I, [_P, _P, _I64]),

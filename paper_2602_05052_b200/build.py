@@ -27,7 +27,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler",
 CXXFLAGS = ["-O3", "-fPIC", "-std=c++17", "-Wall", "-Wno-unused-function",
             f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}", f"-I{os.path.join(CUDA, 'include')}"]
 
-CU = ["routing.cu", "stage.cu", "fused.cu", "fast.cu", "batched.cu", "fused_elast.cu", "adjoint.cu", "solve.cu"]
+CU = ["routing.cu", "stage.cu", "fused.cu", "fast.cu", "batched.cu", "fused_elast.cu", "adjoint.cu", "solve.cu", "scatter.cu"]
 CPP = ["host.cpp", "plan.cpp", "plan_entries.cpp", "plan_fast.cpp"]
 HEADERS = ["tgk_internal.hpp", "element.cuh", "cuda_util.cuh"]
 

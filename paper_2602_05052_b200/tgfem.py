@@ -158,10 +158,24 @@ def reduce_matrix(mesh: Mesh, local_matrices):
 
 
 def scatter_add_oracle(mesh: Mesh, local_matrices):
-    """Classic scatter-add result (module.cpp:122-132).  On the GPU the per-element
-    scatter in ascending element order is realised as the equivalent ordered
-    gather, so the values are identical by construction (routing.cpp:163-174)."""
-    return reduce_matrix(mesh, local_matrices)
+    """Classic scatter-add result (module.cpp:122-132): its own pattern and a
+    per-element scatter in element order (routing.cpp:134-175), computed on the
+    GPU by an algorithm independent of the routing build (tgk_scatter_add: one
+    stable radix sort of all (row, col) contribution keys, run sums in slot order)."""
+    loc = np.ascontiguousarray(local_matrices, dtype=np.float64)
+    k = mesh.elements.shape[1]
+    if loc.size != mesh.element_count() * k * k:
+        raise InputError("scatter_add_oracle: local tensor shape mismatch")
+    dm = mesh._device()
+    nnz = C.c_int64()
+    check(lib().tgk_scatter_add(dm._h, loc.ctypes.data, None, C.byref(nnz), None, None, None, None))
+    n = mesh.node_count()
+    offsets = np.zeros(n + 1, np.int64)
+    cols = np.zeros(nnz.value, np.int64)
+    values = np.zeros(nnz.value)
+    check(lib().tgk_scatter_add(dm._h, loc.ctypes.data, None, C.byref(nnz), offsets.ctypes.data, cols.ctypes.data,
+                                values.ctypes.data, None))
+    return {"rows": n, "offsets": offsets, "cols": cols, "values": values}
 
 
 def compliance(F, U):

@@ -153,3 +153,39 @@ def test_connectivity_change_marks_routings_stale(eng):
     pr = port.Routing(nodes.shape[0], port.dofmap("tet4", e2, 1))
     Kr, _, _ = port.assemble("tet4", nodes, e2, pr, sources=[1.0])
     assert_bitwise(np_(K2), Kr, "rebuilt routing")
+
+
+@pytest.mark.parametrize("kind,mesh", [("tri3", "unstructured"), ("tet4", "bicone")], ids=["tri-unstructured", "tet-bicone"])
+def test_scatter_add_oracle_independent_vs_reference(eng, kind, mesh):
+    """tgk_scatter_add (the reference's scatter_add_oracle, routing.cpp:134-175,
+    by a global key sort independent of the routing build) against the
+    reference library: pattern and values bit-identical, with and without F."""
+    from oracle import ref
+    from paper_2602_05052_b200 import _native as N
+    from paper_2602_05052_b200 import meshgen, tgfem
+    import ctypes as C
+    if not ref.available():
+        pytest.skip("reference library not built")
+    nodes, elems = meshgen.unstructured_tri(24) if mesh == "unstructured" else bicone_tet(70)
+    k = elems.shape[1]
+    rng = np.random.default_rng(3)
+    lk = rng.standard_normal((elems.shape[0], k, k))
+    lf = rng.standard_normal((elems.shape[0], k))
+    rm = ref.Mesh.from_arrays(kind, nodes, elems)
+    rr = ref.Routing(rm, 1)
+    offs, cols, vals, F = rr.scatter_add(lk, lf)
+    m = eng.DeviceMesh(kind, nodes, elems)
+    nnz = C.c_int64()
+    L = N.lib()
+    N.check(L.tgk_scatter_add(m._h, lk.ctypes.data, None, C.byref(nnz), None, None, None, None))
+    assert nnz.value == cols.size
+    o2, c2, v2, F2 = (np.zeros(offs.size, np.int64), np.zeros(cols.size, np.int64), np.zeros(cols.size),
+                      np.zeros(F.size))
+    N.check(L.tgk_scatter_add(m._h, lk.ctypes.data, lf.ctypes.data, C.byref(nnz), o2.ctypes.data,
+                              c2.ctypes.data, v2.ctypes.data, F2.ctypes.data))
+    assert np.array_equal(o2, offs) and np.array_equal(c2, cols)
+    assert_bitwise(v2, vals, "scatter K")
+    assert_bitwise(F2, F, "scatter F")
+    tm = tgfem.Mesh(kind, nodes, elems)
+    d = tgfem.scatter_add_oracle(tm, lk)
+    assert_bitwise(d["values"], vals, "tgfem.scatter_add_oracle")
