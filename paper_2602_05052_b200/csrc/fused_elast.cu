@@ -111,273 +111,11 @@ __device__ __forceinline__ double fieldE_q(const FieldE& f, const double* nod, i
     return f.type == TGK_FIELD_ELEMENT ? __ldg(f.data + e) : f.value;
 }
 
-template <int KIND, int DEG, int R>
-__global__ void __launch_bounds__(R) k_fused_elast(ElastArgs p) {
-    using C = ECfg<KIND, DEG>;
-    using Rl = Rule<KIND, DEG>;
-    constexpr int k = C::k, d = C::d, Q = C::Q, ns = d == 2 ? 3 : 6, ROS = R + 8;
-    extern __shared__ __align__(16) unsigned char sme[];
-    double* ke = reinterpret_cast<double*>(sme);                       // R x stride
-    double* acc = ke + R * C::stride;                                    // lmax*d*d x S
-    double* nt = acc + ((size_t(p.lmax) * d * d * p.S + 1) & ~size_t(1));  // max_bnodes x ntcols (16 B aligned)
-    uint32_t* rec_s = reinterpret_cast<uint32_t*>(nt + size_t(p.max_bnodes) * p.ntcols);
-    uint16_t* ro_s = reinterpret_cast<uint16_t*>(rec_s + kRingE * p.max_recs);
-    ushort4* lc_s = reinterpret_cast<ushort4*>(ro_s + kRingE * ROS);
-    int64_t* cro = reinterpret_cast<int64_t*>(lc_s + kRingE * R);
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t blk = blockIdx.x;
-    const int64_t r0 = p.row_off[blk];
-    const int nr = static_cast<int>(p.row_off[blk + 1] - r0);
-    const int64_t h0 = p.halo_off[blk];
-    const int64_t nh = p.halo_off[blk + 1] - h0;
-    const int64_t c0 = p.chunk_off[blk];
-    const int nch = static_cast<int>(p.chunk_off[blk + 1] - c0);
-    const int64_t n0 = p.bnode_off[blk];
-    const int nbn = static_cast<int>(p.bnode_off[blk + 1] - n0);
-
-    for (int i = tid; i <= nch; i += R) cro[i] = p.chunk_rec_off[c0 + i];
-    // node table: coordinates, then nodal field columns (lambda, mu, sources) when present
-    for (int i = tid; i < nbn; i += R) {
-        const int64_t g = p.bnodes[n0 + i];
-#pragma unroll
-        for (int c = 0; c < d; ++c) cpa8(nt + i * p.ntcols + c, p.nodes + g * d + c);
-        int col = d;
-        if (p.lam.type == TGK_FIELD_NODAL) cpa8(nt + i * p.ntcols + col++, p.lam.data + g);
-        if (p.mu.type == TGK_FIELD_NODAL) cpa8(nt + i * p.ntcols + col++, p.mu.data + g);
-        for (int c = 0; c < p.n_src; ++c)
-            if (p.src[c].type == TGK_FIELD_NODAL) cpa8(nt + i * p.ntcols + col++, p.src[c].data + g);
-    }
-    cpa_commit();
-    for (int i = tid; i < p.lmax * d * d * p.S; i += R) acc[i] = 0.0;
-    __syncthreads();
-
-    auto stage = [&](int c) {
-        if (c < nch) {
-            const int sl = c % kRingE;
-            const int64_t cg = c0 + c;
-            const int64_t rb = cro[c];
-            const int nrec4 = static_cast<int>((cro[c + 1] - rb) >> 2);
-            uint32_t* rdst = rec_s + sl * p.max_recs;
-            for (int i = tid; i < nrec4; i += R) cpa16(rdst + 4 * i, p.recs + rb + 4 * i);
-            uint16_t* odst = ro_s + sl * ROS;
-            for (int i = tid; i < ROS / 8; i += R) cpa16(odst + 8 * i, p.chunk_row_off + cg * ROS + 8 * i);
-            const int64_t hb = h0 + int64_t(c) * R;
-            const int64_t rem = nh - int64_t(c) * R;
-            const int ne = rem < R ? static_cast<int>(rem) : R;
-            if (tid < ne) cpa8(lc_s + sl * R + tid, p.halo_lconn + (hb + tid) * 4);
-        }
-        cpa_commit();
-    };
-#pragma unroll
-    for (int c = 0; c < kRingE - 1; ++c) stage(c);
-
-    double dK[d][d], dF[d];
-#pragma unroll
-    for (int c = 0; c < d; ++c) {
-        dF[c] = 0.0;
-#pragma unroll
-        for (int cp = 0; cp < d; ++cp) dK[c][cp] = 0.0;
-    }
-    int diag_pos = 0;
-
-    for (int c = 0; c < nch; ++c) {
-        cpa_wait<kRingE - 2>();
-        __syncthreads();
-        stage(c + kRingE - 1);
-        const int sl = c % kRingE;
-        // ---------------- phase A: geometry and quadrature values of this thread's element
-        const int64_t h = int64_t(c) * R + tid;
-        if (h < nh) {
-            const ushort4 ln = lc_s[sl * R + tid];
-            const int ids[4] = {ln.x, ln.y, ln.z, ln.w};
-            double X[k][d];
-#pragma unroll
-            for (int a = 0; a < k; ++a)
-#pragma unroll
-                for (int cc = 0; cc < d; ++cc) X[a][cc] = nt[ids[a] * p.ntcols + cc];
-            double* out = ke + tid * C::stride;
-            double det, G[k][d];
-            const int64_t e = p.halo[h0 + h];
-            if (!simplex_geometry<KIND, false>(X, det, G)) {
-                atomicMin(p.bad, static_cast<unsigned long long>(e));
-                det = 0.0;
-#pragma unroll
-                for (int a = 0; a < k; ++a)
-#pragma unroll
-                    for (int cc = 0; cc < d; ++cc) G[a][cc] = 0.0;
-            }
-#pragma unroll
-            for (int a = 0; a < k; ++a)
-#pragma unroll
-                for (int cc = 0; cc < d; ++cc) out[C::offG + a * d + cc] = G[a][cc];
-            out[C::offDet] = det;
-            int col = d;
-            double nl[k], nm[k];
-            if (p.lam.type == TGK_FIELD_NODAL) {
-#pragma unroll
-                for (int a = 0; a < k; ++a) nl[a] = nt[ids[a] * p.ntcols + col];
-                ++col;
-            }
-            if (p.mu.type == TGK_FIELD_NODAL) {
-#pragma unroll
-                for (int a = 0; a < k; ++a) nm[a] = nt[ids[a] * p.ntcols + col];
-                ++col;
-            }
-#pragma unroll
-            for (int q = 0; q < Q; ++q) {
-                double lam = fieldE_q<KIND, DEG>(p.lam, nl, e, q);
-                const double mu = fieldE_q<KIND, DEG>(p.mu, nm, e, q);
-                if (mu <= 0.0) atomicMin(p.bad + 1, 0ull);  // batch.cpp:194-195
-                if (d == 2 && p.plane_stress) lam = 2.0 * lam * mu / (lam + 2.0 * mu);  // batch.cpp:359-361
-                out[C::offLam + q] = lam;
-                out[C::offMu + q] = mu;
-            }
-            for (int cc = 0; cc < d; ++cc) {
-                double ns_[k];
-                const bool nodal = cc < p.n_src && p.src[cc].type == TGK_FIELD_NODAL;
-                if (nodal) {
-#pragma unroll
-                    for (int a = 0; a < k; ++a) ns_[a] = nt[ids[a] * p.ntcols + col];
-                    ++col;
-                }
-#pragma unroll
-                for (int q = 0; q < Q; ++q)
-                    out[C::offF + q * d + cc] = cc < p.n_src ? fieldE_q<KIND, DEG>(p.src[cc], ns_, e, q) : 0.0;
-            }
-        }
-        __syncthreads();
-        // ---------------- phase B: owned node row tid folds its records of chunk c
-        if (tid < nr) {
-            const uint16_t* ro = ro_s + sl * ROS;
-            const uint32_t* rs = rec_s + sl * p.max_recs;
-            for (int j = ro[tid]; j < ro[tid + 1]; ++j) {
-                const uint32_t rec = rs[j];
-                const int hl = rec & 0xff;
-                const int a = (rec >> 8) & 3;
-                const double* el = ke + hl * C::stride;
-                double G[k][d];
-#pragma unroll
-                for (int b = 0; b < k; ++b)
-#pragma unroll
-                    for (int cc = 0; cc < d; ++cc) G[b][cc] = el[C::offG + b * d + cc];
-                double Ga[d];
-#pragma unroll
-                for (int cc = 0; cc < d; ++cc) Ga[cc] = a == 0 ? G[0][cc] : a == 1 ? G[1][cc] : a == 2 ? G[2][cc] : G[k - 1][cc];
-                const double det = el[C::offDet];
-                // block row a of K_e: Kb[b][c][c'] = K_e[a*d+c][b*d+c'] (batch.cpp:229-243)
-                double Kb[k][d][d];
-#pragma unroll
-                for (int b = 0; b < k; ++b)
-#pragma unroll
-                    for (int cc = 0; cc < d; ++cc)
-#pragma unroll
-                        for (int cp = 0; cp < d; ++cp) Kb[b][cc][cp] = 0.0;
-                double Fa[d];
-#pragma unroll
-                for (int cc = 0; cc < d; ++cc) Fa[cc] = 0.0;
-#pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const double lam = el[C::offLam + q], mu = el[C::offMu + q];
-                    const double two_mu = 2.0 * mu;
-                    const double scale = Rl::w(q) * det;
-#pragma unroll
-                    for (int b = 0; b < k; ++b)
-#pragma unroll
-                        for (int cp = 0; cp < d; ++cp) {
-                            const double g = G[b][cp];
-                            const double tr = 0.0 + g;  // batch.cpp:231-232
-#pragma unroll
-                            for (int cc = 0; cc < d; ++cc) {
-                                double s = 0.0;
-#pragma unroll
-                                for (int i = 0; i < ns; ++i) {
-                                    const int ga = vcomp<d>(i, cc);
-                                    if (ga < 0) continue;
-                                    double DB;
-                                    if (i < d) {
-                                        DB = i == cp ? lam * tr + two_mu * g : lam * tr + two_mu * 0.0;
-                                    } else {
-                                        const int gb = vcomp<d>(i, cp);
-                                        if (gb < 0) continue;
-                                        DB = mu * G[b][gb];
-                                    }
-                                    s += Ga[ga] * DB;
-                                }
-                                Kb[b][cc][cp] += scale * s;
-                            }
-                        }
-                    // local_load_vector (batch.cpp:303-308): Fe[a*d+c] += scale * B[a] * f[c]
-                    const double sB = scale * (a == 0 ? basis<KIND, DEG>(q, 0) : a == 1 ? basis<KIND, DEG>(q, 1)
-                                                : a == 2 ? basis<KIND, DEG>(q, 2) : basis<KIND, DEG>(q, k - 1));
-#pragma unroll
-                    for (int cc = 0; cc < d; ++cc) Fa[cc] += sB * el[C::offF + q * d + cc];
-                }
-                // fold: the diagonal block (b == a) and F in registers, others into shared memory
-                int jj = 0;
-#pragma unroll
-                for (int b = 0; b < k; ++b) {
-                    if (b == a) {
-#pragma unroll
-                        for (int cc = 0; cc < d; ++cc)
-#pragma unroll
-                            for (int cp = 0; cp < d; ++cp) dK[cc][cp] += Kb[b][cc][cp];
-                        continue;
-                    }
-                    const int pos = (rec >> (10 + 5 * jj)) & 31;
-                    ++jj;
-                    double* ab = acc + size_t(pos) * d * d * p.S + tid;
-                    double old[d * d];
-#pragma unroll
-                    for (int t = 0; t < d * d; ++t) old[t] = ab[t * p.S];
-#pragma unroll
-                    for (int cc = 0; cc < d; ++cc)
-#pragma unroll
-                        for (int cp = 0; cp < d; ++cp) ab[(cc * d + cp) * p.S] = old[cc * d + cp] + Kb[b][cc][cp];
-                }
-#pragma unroll
-                for (int cc = 0; cc < d; ++cc) dF[cc] += Fa[cc];
-                diag_pos = (rec >> 25) & 31;
-            }
-        }
-    }
-    cpa_wait<0>();
-    __syncthreads();
-    if (tid < nr) {
-        double* ab = acc + size_t(diag_pos) * d * d * p.S + tid;
-#pragma unroll
-        for (int cc = 0; cc < d; ++cc)
-#pragma unroll
-            for (int cp = 0; cp < d; ++cp) ab[(cc * d + cp) * p.S] = dK[cc][cp];
-        const int64_t row = p.rows[r0 + tid];
-#pragma unroll
-        for (int cc = 0; cc < d; ++cc) p.F[row * d + cc] = dF[cc];
-    }
-    __syncthreads();
-    // epilogue: node r's d DoF rows = d*d*len contiguous values [d^2 rp, d^2 (rp + len))
-    constexpr int W = R / 32;
-    for (int rb = warp * 32; rb < nr; rb += W * 32) {
-        const int64_t my = rb + lane < nr ? p.rows_rp[r0 + rb + lane] : 0;
-        const int nn = nr - rb < 32 ? nr - rb : 32;
-        for (int i = 0; i < nn; ++i) {
-            const long long pk = __shfl_sync(0xffffffffu, static_cast<long long>(my), i);
-            const int64_t rp = pk & ((int64_t(1) << 56) - 1);
-            const int len = static_cast<int>(pk >> 56);
-            double* dst = p.K + rp * d * d;
-            for (int v = lane; v < d * d * len; v += 32) {
-                const int cc = v / (d * len), rem = v % (d * len);
-                const int pos = rem / d, cp = rem % d;
-                dst[v] = acc[(size_t(pos) * d * d + cc * d + cp) * p.S + rb + i];
-            }
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
-// v2 (default): the block rows of K_e are computed by one thread per RECORD
-// (all lanes busy) instead of by the owned row's thread, then folded.
+// Exact fused elasticity: the block rows of K_e are computed by one thread per
+// RECORD (all lanes busy), then folded.
 // Per chunk of C halo elements:
-//   phase A   one thread per element: geometry + quadrature values (as v1);
+//   phase A   one thread per element: geometry + quadrature values;
 //   phase B1  one thread per record (element e, owned node a): block row a of
 //             local_stiffness_elasticity (batch.cpp:198-246, structural
 //             nonzeros only, per-value quadrature fold in the reference order)
@@ -687,24 +425,6 @@ int launch_elast2(const ElastArgs& a, int64_t nb, cudaStream_t st) {
     return TGK_OK;
 }
 
-template <int KIND, int DEG, int R>
-int launch_elast(const ElastArgs& a, int64_t nb, cudaStream_t st) {
-    using C = ECfg<KIND, DEG>;
-    constexpr int d = C::d;
-    auto kern = k_fused_elast<KIND, DEG, R>;
-    const size_t smem = sizeof(double) * (size_t(R) * C::stride + ((size_t(a.lmax) * d * d * a.S + 1) & ~size_t(1)) +
-                                          size_t(a.max_bnodes) * a.ntcols) +
-                        kRingE * (sizeof(uint32_t) * a.max_recs + sizeof(uint16_t) * (R + 8) + 8 * R) +
-                        sizeof(int64_t) * (a.max_chunks + 2) + 64;
-    if (smem > 227 * 1024)
-        return set_error(TGK_ERR_INPUT, "fused elasticity: block working set exceeds shared memory (" +
-                                            std::to_string(smem) + " B)");
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (nb > 0) kern<<<static_cast<unsigned>(nb), R, smem, st>>>(a);
-    KERNEL_CHECK("fused_elast");
-    return TGK_OK;
-}
-
 }  // namespace
 
 // Fused elasticity on device buffers (r: the vector routing; its scalar part carries the plan).
@@ -713,8 +433,6 @@ int elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r
 
 int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
                               cudaStream_t st) {
-    const bool v1 = getenv("TGK_ELAST_V1") != nullptr;
-    constexpr int R = 64;
     int C2 = 48, R2 = 16;  // v2 chunk size and rows per block (measured: C3 6.65 ms at 64, 5.65 ms at 48)
     if (const char* e = getenv("TGK_ELAST_C")) C2 = atoi(e);
     if (const char* e = getenv("TGK_ELAST_R")) R2 = atoi(e) == 32 ? 32 : 16;
@@ -723,7 +441,7 @@ int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
         // the row-block plan's layout limits (fused.cu): other meshes take the
         // materialised Stage I + II path (elasticity_assemble), bit-identical too
         const tgk_routing* s = r->scalar ? r->scalar : r;
-        const int prc = s->lmax > kMaxRowLen ? TGK_ERR_INPUT : (v1 ? ensure_plan(r, R, &pl) : ensure_plan(r, R2, &pl, C2));
+        const int prc = s->lmax > kMaxRowLen ? TGK_ERR_INPUT : ensure_plan(r, R2, &pl, C2);
         if (prc == TGK_ERR_INPUT) return elasticity_assemble(pr, m, r, K, F, st);
         if (prc != TGK_OK) return prc;
     }
@@ -751,7 +469,7 @@ int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
     a.K = K;
     a.F = F;
     a.lmax = pl->lmax > 0 ? pl->lmax : 1;
-    a.S = v1 ? R + 1 : C2;  // v1: accumulator row stride; v2: chunk size
+    a.S = C2;  // chunk size
     a.max_recs = pl->max_chunk_recs > 0 ? pl->max_chunk_recs : 4;
     a.max_bnodes = pl->max_bnodes + (pl->max_bnodes & 1);
     a.max_chunks = pl->max_block_chunks;
@@ -761,13 +479,7 @@ int fused_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_rout
     TGK_TRY(routing_flags(r, &badp));
     CUDA_TRY(cudaMemsetAsync(badp, 0xff, 2 * sizeof(unsigned long long), st));
     a.bad = badp;
-    if (v1) {
-        if (m->kind == TGK_TET4) {
-            TGK_TRY((high ? launch_elast<TGK_TET4, 2, R>(a, pl->n_blocks, st) : launch_elast<TGK_TET4, 1, R>(a, pl->n_blocks, st)));
-        } else {
-            TGK_TRY((high ? launch_elast<TGK_TRI3, 2, R>(a, pl->n_blocks, st) : launch_elast<TGK_TRI3, 1, R>(a, pl->n_blocks, st)));
-        }
-    } else if (R2 == 16) {
+    if (R2 == 16) {
         if (m->kind == TGK_TET4)
             TGK_TRY((high ? launch_elast2<TGK_TET4, 2, 16>(a, pl->n_blocks, st) : launch_elast2<TGK_TET4, 1, 16>(a, pl->n_blocks, st)));
         else
