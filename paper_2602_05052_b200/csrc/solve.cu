@@ -155,6 +155,31 @@ __global__ void k_dot_partial(const double* a, const double* b, int64_t n, doubl
     }
     if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
 }
+// two dot products in one pass (a.b, c.d), each with k_dot_partial's exact
+// partition and tree order (bitwise equal to two separate calls)
+__global__ void k_dot2_partial(const double* a, const double* b, const double* c, const double* d, int64_t n,
+                               double* part) {
+    __shared__ double sh[2][kDotThreads];
+    double s0 = 0.0, s1 = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)kDotThreads + threadIdx.x; i < n; i += (int64_t)kDotBlocks * kDotThreads) {
+        s0 += a[i] * b[i];
+        s1 += c[i] * d[i];
+    }
+    sh[0][threadIdx.x] = s0;
+    sh[1][threadIdx.x] = s1;
+    __syncthreads();
+    for (int w = kDotThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sh[0][threadIdx.x] += sh[0][threadIdx.x + w];
+            sh[1][threadIdx.x] += sh[1][threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = sh[0][0];
+        part[kDotBlocks + blockIdx.x] = sh[1][0];
+    }
+}
 __global__ void k_dot_final(const double* part, double* out) {
     __shared__ double sh[512];
     sh[threadIdx.x] = threadIdx.x < kDotBlocks ? part[threadIdx.x] : 0.0;
@@ -419,8 +444,8 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
     DevBuf<double> r, p, v, phat, shat, s, t, rt, inv, best_x, part, scal;
     DevBuf<int> flag;
     for (DevBuf<double>* b : {&r, &p, &v, &phat, &shat, &s, &t, &rt, &inv, &best_x}) TGK_TRY(b->alloc(n));
-    TGK_TRY(part.alloc(kDotBlocks));
-    TGK_TRY(scal.alloc(1));
+    TGK_TRY(part.alloc(2 * kDotBlocks));
+    TGK_TRY(scal.alloc(2));
     TGK_TRY(flag.alloc(1));
     const unsigned G = grid_n(n);
     auto dot = [&](const double* a, const double* b, double* out) -> int {
@@ -428,6 +453,19 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
         k_dot_final<<<1, 512, 0, st>>>(part.p, scal.p);
         CUDA_TRY(cudaMemcpyAsync(out, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
+        return TGK_OK;
+    };
+    // (a.b, c.d) with one host synchronisation
+    auto dot2 = [&](const double* a, const double* b, const double* c, const double* d, double* o0,
+                    double* o1) -> int {
+        k_dot2_partial<<<kDotBlocks, kDotThreads, 0, st>>>(a, b, c, d, n, part.p);
+        k_dot_final<<<1, 512, 0, st>>>(part.p, scal.p);
+        k_dot_final<<<1, 512, 0, st>>>(part.p + kDotBlocks, scal.p + 1);
+        double h[2];
+        CUDA_TRY(cudaMemcpyAsync(h, scal.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        *o0 = h[0];
+        *o1 = h[1];
         return TGK_OK;
     };
     auto nrm = [&](const double* a, double* out) -> int {
@@ -480,9 +518,12 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
         CUDA_TRY(cudaMemsetAsync(p.p, 0, sizeof(double) * n, st));
         CUDA_TRY(cudaMemsetAsync(v.p, 0, sizeof(double) * n, st));
         double rho = 1.0, alpha = 1.0, omega = 1.0;
+        double rho_next = 0.0;  // rt . r of the current r, when already known
+        bool have_rho = false;
         while (res > tol && iters < max_iter) {
-            double rho_new = 0.0;
-            TGK_TRY(dot(rt.p, r.p, &rho_new));
+            double rho_new = rho_next;
+            if (!have_rho) TGK_TRY(dot(rt.p, r.p, &rho_new));
+            have_rho = false;
             if (!std::isfinite(rho_new) || std::abs(rho_new) < eps_bd * norm_b * norm_b) break;
             const double beta = (rho_new / rho) * (alpha / omega);
             rho = rho_new;
@@ -504,15 +545,18 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
             k_scale<<<G, 256, 0, st>>>(n, inv.p, s.p, shat.p);
             k_spmv<<<G, 256, 0, st>>>(n, d_offsets, d_cols, d_values, shat.p, t.p);
             double tt = 0.0, ts = 0.0;
-            TGK_TRY(dot(t.p, t.p, &tt));
-            TGK_TRY(dot(t.p, s.p, &ts));
+            TGK_TRY(dot2(t.p, t.p, t.p, s.p, &tt, &ts));
             omega = ts / tt;
             if (!std::isfinite(omega) || tt < eps_bd) {
                 k_bicg_x<<<G, 256, 0, st>>>(n, alpha, phat.p, 0.0, nullptr, nullptr, nullptr, d_x, nullptr, 0);
                 break;
             }
             k_bicg_x<<<G, 256, 0, st>>>(n, alpha, phat.p, omega, shat.p, s.p, t.p, d_x, r.p, 1);
-            TGK_TRY(nrm(r.p, &res));
+            // ||r|| and the next iteration's rho = rt . r in one pass (4 host syncs per iteration)
+            double rr = 0.0;
+            TGK_TRY(dot2(r.p, r.p, rt.p, r.p, &rr, &rho_next));
+            res = std::sqrt(rr);
+            have_rho = true;
             if (!std::isfinite(res)) break;
         }
         KERNEL_CHECK("bicgstab");
