@@ -52,7 +52,7 @@ struct FastArgs {
     int abuf;  // record buffer capacities in bytes (multiples of 16)
     int bbuf;
     int gl;     // copy-out lanes per row (8, 16 or 32 >= longest row)
-    int debug;  // profiling only (TGK_FAST_DEBUG): 1 skips phase A, 2 phase B, 4 the copy-out
+    int debug;  // profiling only (TGK_FAST_DEBUG): 1 skips phase A, 2 phase B, 4 the copy-out, 8 the node gathers, 16 record B
     unsigned long long* bad;
 };
 
@@ -456,7 +456,8 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
     auto gather = [&](int64_t it) {
         const RecA A = parse_a(ra(it));
         double* xs = xsp(it);
-        for (int i = tid; i < int(A.nbn); i += T) {
+        const int nbn_run = (p.debug & 8) ? 0 : int(A.nbn);
+        for (int i = tid; i < nbn_run; i += T) {
             const int64_t g = A.bnodes[i];
 #pragma unroll
             for (int c = 0; c < d; ++c) cp_async8(xs + c * MB + i, p.nodes + g * d + c);
@@ -500,7 +501,7 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
             wait_a(it + 1);
             gather(it + 1);
         }
-        wait_b(it);
+        if (!(p.debug & 16)) wait_b(it);
         const RecB Bq = parse_b(rb);
         for (int i = tid; i <= int(A.nr); i += T) {  // the tile's row map for the copy-out
             if (i < int(A.nr)) trp[i] = A.rp[i];
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
         if (tid == 0) {  // records A(it) and B(it) are consumed: refill their slots
             fence_proxy_async();
             if (it + 2 < n_it) load_a(it + 2);
-            if (it + 1 < n_it) load_b(it + 1);
+            if (it + 1 < n_it && !(p.debug & 16)) load_b(it + 1);
         }
     }
     copy_out();  // the last block
