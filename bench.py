@@ -839,10 +839,9 @@ def run_batched(args, ctx, N):
     E, Nn = elems.shape[0], nodes.shape[0]
     mesh = engine.DeviceMesh("tri3", nodes, elems)
     routing = engine.Routing(mesh, 1)
-    if C4_FIELDS % ctx.world:
-        raise SystemExit("c4: 256 fields do not split evenly")
-    Bl = C4_FIELDS // ctx.world
-    b0 = ctx.rank * Bl
+    from paper_2602_05052_b200 import dist as D
+    b0, b1 = D.field_shard(C4_FIELDS, ctx.rank, ctx.world)
+    Bl = b1 - b0
     rho_h = np.stack([0.5 + np.random.default_rng(1000 + b).random(E) for b in range(b0, b0 + Bl)])
     lam_h = np.stack([np.random.default_rng(2000 + b).random(Nn) - 0.5 for b in range(b0, b0 + Bl)])
     U_h = np.stack([np.random.default_rng(3000 + b).random(Nn) - 0.5 for b in range(b0, b0 + Bl)])

@@ -132,6 +132,15 @@ def exchange_interface(K, F, row_ptr, s: Slab, combine, dist, group=None):
     return (0 if send is None else send.numel() * 8) + (0 if recv is None else recv.numel() * 8)
 
 
+def field_shard(B, rank, world):
+    """Batched coefficient fields (C4) shard trivially: rank r
+    assembles fields [b0, b1) — contiguous, balanced to within one field, no
+    collective (every field's K_b, adjoint row drho_b is independent)."""
+    if B < 0 or world < 1 or not 0 <= rank < world:
+        raise ValueError("field_shard: bad arguments")
+    return rank * B // world, (rank + 1) * B // world
+
+
 def gpu_combine(lower, values):
     """values = lower + values on the GPU (libtgk tgk_interface_combine_d)."""
     import ctypes as C

@@ -129,3 +129,52 @@ def test_slab_partition_covers_grid():
             elems += s.elem_hi - s.elem_lo
         assert rows == (div[0] + 1) * (div[1] + 1) * (div[2] * world + 1)
         assert elems == 6 * div[0] * div[1] * div[2] * world
+
+
+def _field_worker(rank, world, port_, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_05052_b200 import meshgen
+        nodes, elems = meshgen.unstructured_tri(16)
+        B = 7
+        b0, b1 = D.field_shard(B, rank, world)
+        rho = meshgen.batch_fields(B, elems.shape[0])[b0:b1]
+        r = port.Routing(nodes.shape[0], port.dofmap("tri3", elems, 1))
+        K = np.stack([port.assemble("tri3", nodes, elems, r, diffusion=("element", rho[i]))[0]
+                      for i in range(b1 - b0)]) if b1 > b0 else np.zeros((0, r.nnz))
+        # gather the shards (the bench needs no collective; this only checks the union)
+        sizes = [None] * world
+        dist.all_gather_object(sizes, (b0, b1))
+        out = [None] * world
+        dist.all_gather_object(out, K)
+        if rank == 0:
+            q.put((sizes, np.concatenate(out)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_c4_field_sharding_covers_every_field_once(world):
+    """C4 field sharding (dist.field_shard, bench.py c4): contiguous disjoint
+    shards covering all fields; the gathered per-field assemblies equal the
+    single-process batch bit for bit."""
+    from paper_2602_05052_b200 import meshgen
+    nodes, elems = meshgen.unstructured_tri(16)
+    B = 7
+    rho = meshgen.batch_fields(B, elems.shape[0])
+    r = port.Routing(nodes.shape[0], port.dofmap("tri3", elems, 1))
+    want = np.stack([port.assemble("tri3", nodes, elems, r, diffusion=("element", rho[b]))[0] for b in range(B)])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_field_worker, args=(rk, world, port_, q)) for rk in range(world)]
+    for p in procs:
+        p.start()
+    sizes, got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sizes[0][0] == 0 and sizes[-1][1] == B
+    assert all(sizes[i][1] == sizes[i + 1][0] for i in range(world - 1))
+    assert_bitwise(got, want, "sharded fields")
