@@ -289,6 +289,25 @@ int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B,
                            const double* d_rho, double source, double* d_K, double* d_F,
                            int mode, void* stream);
 
+/* Batched assembly over coefficient fields, any problem kind (Poisson, mass,
+ * elasticity) and mode: batch member b is *p with each listed slot replaced by
+ * the per-element field (device) fb[i].data + b * fb[i].stride (stride 0: E).
+ * Outputs are stacked member-major: d_K B x nnz, d_F B x N (may be NULL),
+ * d_M B x nnz (p->with_mass; may be NULL).  Each member's arithmetic is that
+ * of tgk_assemble_d on the same problem (exact: bit-identical to tg::assemble). */
+#define TGK_SLOT_DIFFUSION 0
+#define TGK_SLOT_LAMBDA 1
+#define TGK_SLOT_MU 2
+#define TGK_SLOT_SOURCE0 3 /* +c: body-force component c (c < n_source) */
+typedef struct {
+    int slot;           /* TGK_SLOT_* */
+    const double* data; /* device, per-element values of member 0 */
+    int64_t stride;     /* values between consecutive members (0: E) */
+} tgk_field_batch;
+int tgk_assemble_fields_batched_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, int64_t B,
+                                  const tgk_field_batch* fb, int n_fb, double* d_K, double* d_F, double* d_M,
+                                  void* stream);
+
 /* Allen-Cahn Newton re-assembly (AllenCahnStepper::step, timestep.cpp:144-178;
  * SURVEY.md 8(f) rank 1), fused in one pass at the mass degree for the nodal
  * state u (N values, device):

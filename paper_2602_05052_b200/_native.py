@@ -44,6 +44,13 @@ class Problem(C.Structure):
                 ("with_mass", C.c_int), ("mode", C.c_int)]
 
 
+class FieldBatch(C.Structure):
+    _fields_ = [("slot", C.c_int), ("data", C.c_void_p), ("stride", C.c_int64)]
+
+
+SLOTS = {"diffusion": 0, "lam": 1, "mu": 2, "source0": 3, "source1": 4, "source2": 5}
+
+
 class RoutingView(C.Structure):
     _fields_ = [("N", C.c_int64), ("E", C.c_int64), ("nnz", C.c_int64), ("k", C.c_int),
                 ("components", C.c_int), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p),
@@ -117,6 +124,7 @@ _SIGS = {
     "tgk_assemble_async_d": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "tgk_assemble": (_I, [_P, _P, _P, _P, _P, _P]),
     "tgk_assemble_batched_d": (_I, [_P, _P, _I64, _P, _D, _P, _P, _I, _P]),
+    "tgk_assemble_fields_batched_d": (_I, [_P, _P, _P, _I64, _P, _I, _P, _P, _P, _P]),
     "tgk_gradient_products_d": (_I, [_P, _I64, _P, _P, _P, _P, _P]),
     "tgk_adjoint_gather_d": (_I, [_P, _P, _I64, _P, _P, _P, _I, _P]),
 }

@@ -655,19 +655,28 @@ namespace {
 struct FastElastArgs {
     const double* nodes;
     FastPlanDev pl;
-    double lam, mu;  // plane-stress lambda already applied (physics.cpp:50-53)
-    double f[3];     // constant body force (n_source == d), else 0
+    double lam, mu;                  // constant Lame parameters (plane-stress lambda applied, physics.cpp:50-53)
+    const double* lam_d;             // per-element lambda / mu (LT == 1; nullptr: the constant)
+    const double* mu_d;
+    int plane_stress;                // 2D: lambda' = 2 lambda mu / (lambda + 2 mu) per element (LT == 1)
+    double f[3];                     // constant body force (FT == 1)
+    const double* fd[3];             // per-element body force components (FT == 2; nullptr: f[c])
     double* K;
     double* F;
     int MH, MB, abuf, bbuf, gl, debug;
-    unsigned long long* bad;
+    unsigned long long* bad;         // [0] smallest element with det <= 0, [1] mu <= 0 seen
 };
 
-template <int KIND, bool HAS_F>
+// LT: Lame parameters constant (0) or per element (1); FT: body force none /
+// constant / per element.  Value rows: g_a,r (row a d + r), c = |T^| det,
+// [lambda c, mu c], [f_r c].
+template <int KIND, int LT, int FT>
 struct FastElastCfg {
     static constexpr int k = P1<KIND>::k, d = P1<KIND>::d;
-    static constexpr int CROW = k * d;  // rows 0..kd-1: g_a,r (row a d + r); row kd: c = |T^| det
-    static constexpr int NR = k * d + 1;
+    static constexpr int CROW = k * d;
+    static constexpr int LROW = k * d + 1, MROW = k * d + 2;
+    static constexpr int FROW = k * d + 1 + (LT ? 2 : 0);
+    static constexpr int NR = FROW + (FT == 2 ? d : 0);
     static size_t smem(const FastElastArgs& a) {
         return 64 + 2 * size_t(a.abuf) + size_t(a.bbuf) +
                sizeof(double) * (2 * size_t(d) * a.MB + size_t(NR) * a.MH + size_t(d) * d * a.pl.max_tile) +
@@ -675,10 +684,10 @@ struct FastElastCfg {
     }
 };
 
-template <int KIND, bool HAS_F>
+template <int KIND, int LT, int FT>
 __device__ __forceinline__ void elast_element(const FastElastArgs& p, const RecA& A, const double* xs, double* kv,
                                               int h) {
-    using Cf = FastElastCfg<KIND, HAS_F>;
+    using Cf = FastElastCfg<KIND, LT, FT>;
     constexpr int k = Cf::k, d = Cf::d;
     const int MH = p.MH, MB = p.MB;
     const uint64_t hc = A.hconn[h];
@@ -715,51 +724,88 @@ __device__ __forceinline__ void elast_element(const FastElastArgs& p, const RecA
         g[0][0] = -(g[1][0] + g[2][0]); g[0][1] = -(g[1][1] + g[2][1]);
     }
     double c = det * FastConst<KIND>::wsum;
+    double lc = 0.0, mc = 0.0, fc[d];
+    if constexpr (LT == 1 || FT == 2) {
+        const int64_t e = __ldg(p.pl.helem + A.hbase + h);
+        if constexpr (LT == 1) {
+            double lam = p.lam_d ? __ldg(p.lam_d + e) : p.lam;
+            const double mu = p.mu_d ? __ldg(p.mu_d + e) : p.mu;
+            if (!(mu > 0.0)) atomicOr(p.bad + 1, 1ull);  // batch.cpp:194-195
+            if (p.plane_stress) lam = 2.0 * lam * mu / (lam + 2.0 * mu);  // plane_stress_lambda, batch.cpp:359-361
+            lc = lam * c;
+            mc = mu * c;
+        }
+        if constexpr (FT == 2) {
+#pragma unroll
+            for (int r = 0; r < d; ++r) fc[r] = (p.fd[r] ? __ldg(p.fd[r] + e) : p.f[r]) * c;
+        }
+    }
     if (det <= 0.0) {  // batch.cpp:98-101
         atomicMin(p.bad, static_cast<unsigned long long>(__ldg(p.pl.helem + A.hbase + h)));
-        c = 0.0;
+        c = lc = mc = 0.0;
 #pragma unroll
         for (int a = 0; a < k; ++a)
 #pragma unroll
             for (int r = 0; r < d; ++r) g[a][r] = 0.0;
+        if constexpr (FT == 2) {
+#pragma unroll
+            for (int r = 0; r < d; ++r) fc[r] = 0.0;
+        }
     }
 #pragma unroll
     for (int a = 0; a < k; ++a)
 #pragma unroll
         for (int r = 0; r < d; ++r) kv[(a * d + r) * MH + h] = g[a][r];
     kv[Cf::CROW * MH + h] = c;
+    if constexpr (LT == 1) {
+        kv[Cf::LROW * MH + h] = lc;
+        kv[Cf::MROW * MH + h] = mc;
+    }
+    if constexpr (FT == 2) {
+#pragma unroll
+        for (int r = 0; r < d; ++r) kv[(Cf::FROW + r) * MH + h] = fc[r];
+    }
 }
 
 // Lane `lane` of warp group w: one scalar entry's d x d block (and, for a
 // diagonal entry, the row's d load values) folded over its elements.
-template <int KIND, bool HAS_F>
+template <int KIND, int LT, int FT>
 __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& A, const RecB& Bq, const double* kv,
                                             double* tk, int w, int lane) {
-    using Cf = FastElastCfg<KIND, HAS_F>;
-    constexpr int k = Cf::k, d = Cf::d;
+    using Cf = FastElastCfg<KIND, LT, FT>;
+    constexpr int k = Cf::k, d = Cf::d, NF = FT == 2 ? Cf::d : 1;
     const int MH = p.MH;
     const uint32_t desc = Bq.desc[w * 32 + lane];
     const uint32_t i0 = Bq.wgoff[w];
     const int steps = static_cast<int>((Bq.wgoff[w + 1] - i0) >> 6);
     const uint2* ip = reinterpret_cast<const uint2*>(Bq.words + i0) + lane;
     const bool diag = (__shfl_sync(0xffffffffu, desc, 0) >> 15) & 1u;
-    double acc[d][d], fac = 0.0;
+    double acc[d][d], fac[NF];
 #pragma unroll
     for (int r = 0; r < d; ++r)
 #pragma unroll
         for (int s = 0; s < d; ++s) acc[r][s] = 0.0;
+#pragma unroll
+    for (int r = 0; r < NF; ++r) fac[r] = 0.0;
     const double lam = p.lam, mu = p.mu;
     auto eat = [&](uint32_t it) {
         const int h = static_cast<int>(it & 0xfffu), a = static_cast<int>((it >> 14) & 3u),
                   b = static_cast<int>((it >> 12) & 3u);
-        const double c = kv[Cf::CROW * MH + h];
+        double lc, mc, c = 0.0;
+        if constexpr (LT == 1) {
+            lc = kv[Cf::LROW * MH + h];
+            mc = kv[Cf::MROW * MH + h];
+        } else {
+            c = kv[Cf::CROW * MH + h];
+            lc = lam * c;
+            mc = mu * c;
+        }
         double ga[d], gb[d];
 #pragma unroll
         for (int r = 0; r < d; ++r) {
             ga[r] = kv[(a * d + r) * MH + h];
             gb[r] = kv[(b * d + r) * MH + h];
         }
-        const double lc = lam * c, mc = mu * c;
         double dt = ga[0] * gb[0];
 #pragma unroll
         for (int r = 1; r < d; ++r) dt = __fma_rn(ga[r], gb[r], dt);
@@ -775,10 +821,13 @@ __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& 
             for (int s = 0; s < d; ++s) acc[r][s] = __fma_rn(u[r], gb[s], __fma_rn(v[s], gb[r], acc[r][s]));
 #pragma unroll
         for (int r = 0; r < d; ++r) acc[r][r] = __fma_rn(mc, dt, acc[r][r]);
-        if constexpr (HAS_F) fac += c;
+        if constexpr (FT == 1) fac[0] += LT == 1 ? kv[Cf::CROW * MH + h] : c;
+        if constexpr (FT == 2) {
+#pragma unroll
+            for (int r = 0; r < d; ++r) fac[r] += kv[(Cf::FROW + r) * MH + h];
+        }
     };
-    const uint32_t zw = (uint32_t(MH - 1) | (uint32_t(MH - 1) << 16));  // (h = zero slot, a = b = 0)
-    // the zero slot is h = max_halo; its values are +0.0 in every row (padding items)
+    // padding items address the +0.0 slot (h = max_halo, a = b = 0)
     for (int st = 0; st < steps; ++st) {
         const uint2 wv = ip[st * 32];
         eat(wv.x & 0xffffu);
@@ -786,7 +835,6 @@ __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& 
         eat(wv.y & 0xffffu);
         eat(wv.y >> 16);
     }
-    (void)zw;
     if (diag) {  // split diagonal lists: partial sums of kFastDiagSplit lanes
         constexpr int DS = kFastDiagSplit(k);
 #pragma unroll
@@ -795,7 +843,10 @@ __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& 
             for (int r = 0; r < d; ++r)
 #pragma unroll
                 for (int s = 0; s < d; ++s) acc[r][s] += __shfl_xor_sync(0xffffffffu, acc[r][s], o);
-            if constexpr (HAS_F) fac += __shfl_xor_sync(0xffffffffu, fac, o);
+            if constexpr (FT > 0) {
+#pragma unroll
+                for (int r = 0; r < NF; ++r) fac[r] += __shfl_xor_sync(0xffffffffu, fac[r], o);
+            }
         }
     }
     if (desc >= kFastPart) return;
@@ -808,11 +859,12 @@ __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& 
 #pragma unroll
             for (int s = 0; s < d; ++s) t[r * d * L + s] = acc[r][s];
     }
-    if constexpr (HAS_F) {
+    if constexpr (FT > 0) {
         if (diag) {
             const int64_t row = A.srow[lr];
 #pragma unroll
-            for (int r = 0; r < d; ++r) p.F[row * d + r] = p.f[r] * fac * (1.0 / k);
+            for (int r = 0; r < d; ++r)
+                p.F[row * d + r] = (FT == 1 ? p.f[r] * fac[0] : fac[r]) * (1.0 / k);
         }
     }
     if (desc >> 31) {  // the mirrored entry (j, i) holds the transposed block
@@ -828,9 +880,9 @@ __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& 
 
 // Persistent kernel, the same pipeline as k_fast_scalar (TMA-fed records,
 // cp.async node tables, tile copy-out overlapping phase A).
-template <int KIND, bool HAS_F>
+template <int KIND, int LT, int FT>
 __global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p) {
-    using Cf = FastElastCfg<KIND, HAS_F>;
+    using Cf = FastElastCfg<KIND, LT, FT>;
     constexpr int d = Cf::d;
     extern __shared__ __align__(128) unsigned char smb[];
     const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = T >> 5;
@@ -898,7 +950,7 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p)
         const RecA A = parse_a(ra(it));
         copy_out();
         const int nh_run = (p.debug & 1) ? 0 : int(A.nh);
-        for (int h = tid; h < nh_run; h += T) elast_element<KIND, HAS_F>(p, A, xsp(it), kv, h);
+        for (int h = tid; h < nh_run; h += T) elast_element<KIND, LT, FT>(p, A, xsp(it), kv, h);
         __syncthreads();
         if (it + 1 < n_it) {
             wait_a(it + 1);
@@ -912,7 +964,7 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p)
         }
         tile_rows = int(A.nr);
         const int nwg = (p.debug & 2) ? 0 : int(Bq.nwg);
-        for (int w = warp; w < nwg; w += nwarp) elast_group<KIND, HAS_F>(p, A, Bq, kv, tk, w, lane);
+        for (int w = warp; w < nwg; w += nwarp) elast_group<KIND, LT, FT>(p, A, Bq, kv, tk, w, lane);
         cp_async_wait_all();
         __syncthreads();
         if (tid == 0) {
@@ -924,10 +976,10 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p)
     copy_out();
 }
 
-template <int KIND, bool HAS_F>
+template <int KIND, int LT, int FT>
 int launch_fast_elast(const FastElastArgs& a, int threads, cudaStream_t st) {
-    auto kern = k_fast_elast<KIND, HAS_F>;
-    const size_t smem = FastElastCfg<KIND, HAS_F>::smem(a);
+    auto kern = k_fast_elast<KIND, LT, FT>;
+    const size_t smem = FastElastCfg<KIND, LT, FT>::smem(a);
     if (smem > 227 * 1024) return kFastNotApplicable;
     static size_t done[kMaxDevices] = {};
     TGK_TRY(raise_smem_limit(kern, smem, done));
@@ -943,16 +995,30 @@ int launch_fast_elast(const FastElastArgs& a, int threads, cudaStream_t st) {
 
 }  // namespace
 
-// Fast-mode elasticity; kFastNotApplicable unless lambda, mu (and the body
-// force) are constants — the exact kernels take every other case.
+template <int KIND>
+int dispatch_fast_elast(int lt, int ft, const FastElastArgs& a, int T, cudaStream_t st) {
+    if (lt == 0) return ft == 0 ? launch_fast_elast<KIND, 0, 0>(a, T, st)
+                      : ft == 1 ? launch_fast_elast<KIND, 0, 1>(a, T, st) : launch_fast_elast<KIND, 0, 2>(a, T, st);
+    return ft == 0 ? launch_fast_elast<KIND, 1, 0>(a, T, st)
+         : ft == 1 ? launch_fast_elast<KIND, 1, 1>(a, T, st) : launch_fast_elast<KIND, 1, 2>(a, T, st);
+}
+
+// Fast-mode elasticity (constant or per-element Lame parameters and body
+// force); kFastNotApplicable for nodal / quadrature fields — the exact kernels
+// take those.
 int fast_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K, double* F,
                              cudaStream_t st) {
     const int d = m->d;
-    if (pr->lambda.type != TGK_FIELD_CONSTANT || pr->mu.type != TGK_FIELD_CONSTANT) return kFastNotApplicable;
+    auto simple = [](const tgk_field& f) { return f.type == TGK_FIELD_CONSTANT || f.type == TGK_FIELD_ELEMENT; };
+    if (!simple(pr->lambda) || !simple(pr->mu)) return kFastNotApplicable;
     for (int c = 0; c < pr->n_source; ++c)
-        if (pr->source[c].type != TGK_FIELD_CONSTANT) return kFastNotApplicable;
-    if (!(pr->mu.value > 0.0)) return set_error(TGK_ERR_INPUT, "elasticity requires mu > 0");  // batch.cpp:194-195
+        if (!simple(pr->source[c])) return kFastNotApplicable;
+    const int lt = pr->lambda.type == TGK_FIELD_ELEMENT || pr->mu.type == TGK_FIELD_ELEMENT ? 1 : 0;
     const bool has_f = pr->n_source > 0;
+    int ft = has_f ? 1 : 0;
+    for (int c = 0; c < pr->n_source; ++c)
+        if (pr->source[c].type == TGK_FIELD_ELEMENT) ft = 2;
+    if (lt == 0 && !(pr->mu.value > 0.0)) return set_error(TGK_ERR_INPUT, "elasticity requires mu > 0");  // batch.cpp:194-195
     int R = m->kind == TGK_TET4 ? 32 : 64, T = 256;  // B200 sweep: C3 0.95 (R=16) -> 0.89 ms (R=32)
     if (const char* e = getenv("TGK_FAST_ER")) R = std::max(1, std::min(kFastMaxRows, atoi(e)));
     if (const char* e = getenv("TGK_FAST_ET")) T = std::max(32, std::min(kFastMaxThreads, atoi(e) / 32 * 32));
@@ -967,8 +1033,14 @@ int fast_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routi
     a.pl = *pl;
     a.lam = pr->lambda.value;
     a.mu = pr->mu.value;
-    if (d == 2 && pr->plane_stress) a.lam = 2.0 * a.lam * a.mu / (a.lam + 2.0 * a.mu);  // plane_stress_lambda
-    for (int c = 0; c < d; ++c) a.f[c] = has_f ? pr->source[c].value : 0.0;
+    a.lam_d = pr->lambda.type == TGK_FIELD_ELEMENT ? pr->lambda.data : nullptr;
+    a.mu_d = pr->mu.type == TGK_FIELD_ELEMENT ? pr->mu.data : nullptr;
+    a.plane_stress = d == 2 && pr->plane_stress;
+    if (lt == 0 && a.plane_stress) a.lam = 2.0 * a.lam * a.mu / (a.lam + 2.0 * a.mu);  // plane_stress_lambda
+    for (int c = 0; c < d; ++c) {
+        a.f[c] = has_f ? pr->source[c].value : 0.0;
+        a.fd[c] = has_f && pr->source[c].type == TGK_FIELD_ELEMENT ? pr->source[c].data : nullptr;
+    }
     a.K = K;
     a.F = F;
     a.MH = pl->MH;
@@ -980,12 +1052,19 @@ int fast_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routi
     TGK_TRY(routing_flags(r, &bad));
     a.bad = bad;
     CUDA_TRY(cudaMemsetAsync(a.bad, 0xff, sizeof(unsigned long long), st));
+    CUDA_TRY(cudaMemsetAsync(a.bad + 1, 0, sizeof(unsigned long long), st));
     if (!has_f && F) CUDA_TRY(cudaMemsetAsync(F, 0, sizeof(double) * r->N, st));
-    int rc;
-    if (m->kind == TGK_TET4) rc = has_f ? launch_fast_elast<TGK_TET4, true>(a, T, st) : launch_fast_elast<TGK_TET4, false>(a, T, st);
-    else rc = has_f ? launch_fast_elast<TGK_TRI3, true>(a, T, st) : launch_fast_elast<TGK_TRI3, false>(a, T, st);
+    const int rc = m->kind == TGK_TET4 ? dispatch_fast_elast<TGK_TET4>(lt, ft, a, T, st)
+                                       : dispatch_fast_elast<TGK_TRI3>(lt, ft, a, T, st);
     if (rc != TGK_OK) return rc;
-    return check_bad(bad, st);
+    unsigned long long h[2] = {ULLONG_MAX, 0};
+    CUDA_TRY(cudaMemcpyAsync(h, bad, sizeof h, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    // batch_geometry runs (and throws) before local_stiffness_elasticity checks mu (physics.cpp:11-52)
+    if (h[0] != ULLONG_MAX)
+        return set_error(TGK_ERR_INPUT, "element " + std::to_string(h[0]) + " has non-positive Jacobian determinant");
+    if (h[1]) return set_error(TGK_ERR_INPUT, "elasticity requires mu > 0");
+    return TGK_OK;
 }
 
 }  // namespace tgk

@@ -871,6 +871,45 @@ int tgk_assemble_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r
                              static_cast<cudaStream_t>(stream), nullptr);
 }
 
+// Batched assembly over coefficient fields (the north star's Map stage,
+// batch.cpp:183-269 rerun per field as topopt.cpp:122-127 does): member b of
+// the batch is `p` with every listed slot replaced by the per-element field
+// data + b * stride.  Any problem kind and mode; outputs stacked member-major.
+int tgk_assemble_fields_batched_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, int64_t B,
+                                  const tgk_field_batch* fb, int n_fb, double* d_K, double* d_F, double* d_M,
+                                  void* stream) {
+    if (!p || !m || !r || (n_fb > 0 && !fb)) return set_error(TGK_ERR_INPUT, "assemble_fields_batched: null argument");
+    if (B < 0 || n_fb < 0) return set_error(TGK_ERR_INPUT, "assemble_fields_batched: negative count");
+    auto slot_field = [](tgk_problem& q, int slot) -> tgk_field* {
+        switch (slot) {
+            case TGK_SLOT_DIFFUSION: return &q.diffusion;
+            case TGK_SLOT_LAMBDA: return &q.lambda;
+            case TGK_SLOT_MU: return &q.mu;
+            case TGK_SLOT_SOURCE0: case TGK_SLOT_SOURCE0 + 1: case TGK_SLOT_SOURCE0 + 2:
+                return slot - TGK_SLOT_SOURCE0 < q.n_source ? &q.source[slot - TGK_SLOT_SOURCE0] : nullptr;
+            default: return nullptr;
+        }
+    };
+    tgk_problem q = *p;
+    for (int i = 0; i < n_fb; ++i) {
+        if (!slot_field(q, fb[i].slot))
+            return set_error(TGK_ERR_INPUT, "assemble_fields_batched: field slot " + std::to_string(fb[i].slot) +
+                                                " is not a field of this problem");
+        if (!fb[i].data && B > 0) return set_error(TGK_ERR_INPUT, "assemble_fields_batched: null field data");
+    }
+    const int64_t nnz = r->nnz, N = r->N;
+    for (int64_t b = 0; b < B; ++b) {
+        for (int i = 0; i < n_fb; ++i) {
+            const int64_t stride = fb[i].stride > 0 ? fb[i].stride : m->E;
+            *slot_field(q, fb[i].slot) = tgk_field{TGK_FIELD_ELEMENT, 0.0, fb[i].data + b * stride, m->E};
+        }
+        TGK_TRY(tgk::assemble_dev(&q, m, const_cast<tgk_routing*>(r), d_K ? d_K + b * nnz : nullptr,
+                                  d_F ? d_F + b * N : nullptr, d_M && q.with_mass ? d_M + b * nnz : nullptr,
+                                  static_cast<cudaStream_t>(stream), nullptr));
+    }
+    return TGK_OK;
+}
+
 int tgk_assemble_f32_d(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, float* d_K, float* d_F,
                        float* d_M, unsigned long long* d_bad, void* stream) {
     if (!p || !m || !r) return set_error(TGK_ERR_INPUT, "tgk_assemble_f32_d: null argument");

@@ -327,15 +327,43 @@ def reduce_vector(routing: Routing, local, stream=None):
 
 
 # ---------------------------------------------------------------- batched + adjoint
-def assemble_batched(mesh, routing, rho, source=1.0, with_load=True, stream=None):
+def assemble_batched(mesh, routing, rho, source=1.0, with_load=True, stream=None, mode="exact"):
     """B per-element coefficient fields (B x E) -> K values (B x nnz) [+ one F (N)]."""
     rho = _cuda_f64(rho).reshape(-1, mesh.E)
     B = rho.shape[0]
     K = torch.empty(B, routing.nnz, dtype=torch.float64, device=_DEV)
     F = torch.empty(routing.N, dtype=torch.float64, device=_DEV) if with_load else None
     check(lib().tgk_assemble_batched_d(mesh._h, routing._h, B, _ptr(rho), float(source), _ptr(K),
-                                       _ptr(F), N.MODE_EXACT, _stream(stream)))
+                                       _ptr(F), MODES[mode], _stream(stream)))
     return K, F
+
+
+def assemble_fields_batched(mesh, routing, fields, kind="poisson", diffusion=1.0, lam=1.0, mu=1.0,
+                            plane_stress=False, sources=(), with_mass=False, with_load=True, stream=None,
+                            mode="exact"):
+    """Batched assembly over coefficient fields for any problem kind
+    (tgk_assemble_fields_batched_d): `fields` maps a slot ("diffusion", "lam",
+    "mu", "source0".."source2") to a B x E per-element tensor; member b is the
+    problem with those slots set to row b.  Returns K (B x nnz), F (B x N | None),
+    M (B x nnz | None), stacked member-major."""
+    if kind == "mass":
+        with_mass = False
+    p, keep = make_problem(kind, diffusion, lam, mu, plane_stress, sources, with_mass, mode=mode)
+    rows = {k: _cuda_f64(v).reshape(-1, mesh.E) for k, v in fields.items()}
+    Bs = {v.shape[0] for v in rows.values()}
+    if len(Bs) != 1:
+        raise ValueError("every batched field needs the same batch size")
+    B = Bs.pop()
+    fb = (N.FieldBatch * max(1, len(rows)))()
+    for i, (slot, v) in enumerate(rows.items()):
+        fb[i] = N.FieldBatch(N.SLOTS[slot], v.data_ptr(), mesh.E)
+    K = torch.empty(B, routing.nnz, dtype=torch.float64, device=_DEV)
+    F = torch.empty(B, routing.N, dtype=torch.float64, device=_DEV) if with_load else None
+    M = torch.empty(B, routing.nnz, dtype=torch.float64, device=_DEV) if with_mass else None
+    check(lib().tgk_assemble_fields_batched_d(C.byref(p), mesh._h, routing._h, B, fb, len(rows), _ptr(K),
+                                              _ptr(F), _ptr(M), _stream(stream)))
+    del keep, rows
+    return K, F, M
 
 
 def gradient_products(routing, lam, U, stream=None):

@@ -228,3 +228,142 @@ def test_fast_elasticity_c3_30(eng):
                               sources=[1.0, 1.0, 1.0])
     assert_scaled_close(np_(K), Kr, what="C3 K")
     assert_scaled_close(np_(F), Fr, what="C3 F")
+
+
+def _elast_fields(kind, E, variant):
+    rng = np.random.default_rng(11)
+    lam_e = ("element", 0.3 + rng.random(E))
+    mu_e = ("element", 0.2 + rng.random(E))
+    d = 3 if kind == "tet4" else 2
+    f_e = [("element", rng.standard_normal(E)) for _ in range(d)]
+    return {
+        "lam+mu elem, F elem": dict(lam=lam_e, mu=mu_e, sources=f_e),
+        "lam elem, mu const, F mixed": dict(lam=lam_e, mu=0.4, sources=[1.0] + f_e[1:]),
+        "lam const, mu elem, F const": dict(lam=0.6, mu=mu_e, sources=[0.5] * d),
+        "lam+mu elem, no F": dict(lam=lam_e, mu=mu_e),
+    }[variant]
+
+
+@pytest.mark.parametrize("variant", ["lam+mu elem, F elem", "lam elem, mu const, F mixed",
+                                     "lam const, mu elem, F const", "lam+mu elem, no F"])
+@pytest.mark.parametrize("kind,mesh,ps", [("tet4", "permuted", False), ("tri3", "unstructured", True),
+                                          ("tri3", "grid", False)])
+def test_fast_elasticity_element_fields(eng, kind, mesh, ps, variant):
+    """k_fast_elast with per-element Lame parameters (plane-stress transform per
+    element, batch.cpp:359-361) and per-element body force, vs the oracle
+    (batch.cpp:183-269) within the SURVEY.md 8(c) tolerance; deterministic."""
+    from paper_2602_05052_b200 import meshgen
+    if mesh == "unstructured":
+        nodes, elems = meshgen.unstructured_tri(40)
+    elif mesh == "permuted":
+        nodes, elems = permuted(*port.generate_grid("tet4", [1.0, 1.2, 0.8], [8, 7, 9]), 3)
+    else:
+        nodes, elems = port.generate_grid("tri3", [1.0, 1.1], [31, 27])
+    d = 3 if kind == "tet4" else 2
+    kw = _elast_fields(kind, elems.shape[0], variant)
+    m = eng.DeviceMesh(kind, nodes, elems)
+    rv = eng.Routing(m, d)
+    prv = port.Routing(nodes.shape[0] * d, port.dofmap(kind, elems, d))
+    K, F, _ = eng.assemble(m, rv, kind="elasticity", plane_stress=ps, mode="fast", **kw)
+    Kr, Fr, _ = port.assemble(kind, nodes, elems, prv, problem="elasticity", plane_stress=ps, **kw)
+    assert_scaled_close(np_(K), Kr, what="elasticity K")
+    assert_scaled_close(np_(F), Fr, what="elasticity F")
+    K2, F2, _ = eng.assemble(m, rv, kind="elasticity", plane_stress=ps, mode="fast", **kw)
+    assert_bitwise(np_(K2), np_(K), "rerun K")
+    assert_bitwise(np_(F2), np_(F), "rerun F")
+
+
+def test_fast_elasticity_element_errors(eng):
+    """mu <= 0 in a per-element field -> 'elasticity requires mu > 0' (batch.cpp:194-195);
+    an inverted element is reported first (batch_geometry runs before the Lame check)."""
+    from paper_2602_05052_b200._native import InputError
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [4, 4, 4])
+    E = elems.shape[0]
+    mu = np.full(E, 0.4)
+    mu[17] = 0.0
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    rv = eng.Routing(m, 3)
+    with pytest.raises(InputError, match="mu > 0"):
+        eng.assemble(m, rv, kind="elasticity", lam=0.5, mu=("element", mu), mode="fast")
+    bad = elems.copy()
+    bad[[5, 9]] = bad[[5, 9]][:, [1, 0, 2, 3]]
+    mb = eng.DeviceMesh("tet4", nodes, bad)
+    rb = eng.Routing(mb, 3)
+    with pytest.raises(InputError, match="element 5 has non-positive Jacobian determinant"):
+        eng.assemble(mb, rb, kind="elasticity", lam=0.5, mu=("element", mu), mode="fast")
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+@pytest.mark.parametrize("problem", ["poisson K+M+F", "mass", "elasticity"])
+def test_fields_batched(eng, mode, problem):
+    """tgk_assemble_fields_batched_d: batch member b equals the single-field
+    assembly with the slots set to row b (bitwise: same kernels), and the
+    oracle (exact: bitwise; fast: scaled tolerance)."""
+    from paper_2602_05052_b200 import meshgen
+    rng = np.random.default_rng(3)
+    B = 3
+    if problem == "elasticity":
+        kind = "tet4"
+        nodes, elems = permuted(*port.generate_grid("tet4", [1.0, 1.0, 1.0], [6, 7, 5]), 2)
+        d, E = 3, elems.shape[0]
+        fields = {"lam": 0.3 + rng.random((B, E)), "mu": 0.2 + rng.random((B, E)),
+                  "source1": rng.standard_normal((B, E))}
+        base = dict(kind="elasticity", lam=1.0, mu=1.0, sources=[1.0, 0.0, -1.0])
+    else:
+        kind = "tri3"
+        nodes, elems = meshgen.unstructured_tri(48)
+        d, E = 1, elems.shape[0]
+        fields = {"diffusion": 0.5 + rng.random((B, E))}
+        base = dict(kind="mass") if problem == "mass" else dict(kind="poisson", sources=[1.0], with_mass=True)
+        if problem != "mass":
+            fields["source0"] = rng.standard_normal((B, E))
+    m = eng.DeviceMesh(kind, nodes, elems)
+    rv = eng.Routing(m, d)
+    prv = port.Routing(nodes.shape[0] * d, port.dofmap(kind, elems, d))
+    K, F, M = eng.assemble_fields_batched(m, rv, {k: torch.from_numpy(v) for k, v in fields.items()},
+                                          mode=mode, **base)
+    assert K.shape == (B, rv.nnz) and F.shape == (B, rv.N)
+    assert (M is not None) == (problem == "poisson K+M+F")
+    for b in range(B):
+        kw = dict(base)
+        srcs = list(kw.pop("sources", ()))
+        kwb = {}
+        for slot, v in fields.items():
+            if slot.startswith("source"):
+                srcs[int(slot[-1])] = ("element", v[b])
+            else:
+                kwb[slot] = ("element", v[b])
+                kw.pop(slot, None)
+        Kb, Fb, Mb = eng.assemble(m, rv, sources=srcs, mode=mode, **kw, **kwb)
+        assert_bitwise(np_(K[b]), np_(Kb), f"member {b} K")
+        assert_bitwise(np_(F[b]), np_(Fb), f"member {b} F")
+        if M is not None:
+            assert_bitwise(np_(M[b]), np_(Mb), f"member {b} M")
+        pk = dict(kw)
+        pk["problem"] = pk.pop("kind")
+        Kr, Fr, Mr = port.assemble(kind, nodes, elems, prv, sources=srcs, **pk, **kwb)
+        check = assert_bitwise if mode == "exact" else (lambda a, b_, w: assert_scaled_close(a, b_, what=w))
+        check(np_(Kb), Kr, f"member {b} K vs oracle")
+        check(np_(Fb), Fr, f"member {b} F vs oracle")
+        if M is not None:
+            check(np_(Mb), Mr, f"member {b} M vs oracle")
+
+
+def test_assemble_batched_fast_mode(eng):
+    """tgk_assemble_batched_d with TGK_MODE_FAST: each field's K equals the
+    single fast-mode assembly (bitwise) and the oracle (scaled tolerance)."""
+    from paper_2602_05052_b200 import meshgen
+    nodes, elems = meshgen.unstructured_tri(48)
+    E = elems.shape[0]
+    rho = 0.5 + np.random.default_rng(4).random((4, E))
+    m = eng.DeviceMesh("tri3", nodes, elems)
+    r = eng.Routing(m, 1)
+    K, F = eng.assemble_batched(m, r, torch.from_numpy(rho), source=1.0, mode="fast")
+    pr = port.Routing(nodes.shape[0], port.dofmap("tri3", elems, 1))
+    for b in range(rho.shape[0]):
+        Kb, Fb, _ = eng.assemble(m, r, diffusion=("element", rho[b]), sources=[1.0], mode="fast")
+        assert_bitwise(np_(K[b]), np_(Kb), f"field {b}")
+        Kr, Fr, _ = port.assemble("tri3", nodes, elems, pr, diffusion=("element", rho[b]), sources=[1.0])
+        assert_scaled_close(np_(K[b]), Kr, what=f"field {b} vs oracle")
+        if b == 0:
+            assert_bitwise(np_(F), np_(Fb), "F")
