@@ -437,18 +437,9 @@ int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, c
     TGK_TRY(routing_flags(const_cast<tgk_routing*>(r), &badp));
     CUDA_TRY(cudaMemsetAsync(badp, 0xff, sizeof(unsigned long long), st));
     if (B == 0) return TGK_OK;
-    if (mode == TGK_MODE_FAST) {  // one fast-mode pass per field (csrc/fast.cu), the plan shared
-        for (int64_t b = 0; b < B; ++b) {
-            tgk_problem p{};
-            p.kind = TGK_POISSON;
-            p.mode = TGK_MODE_FAST;
-            p.diffusion = tgk_field{TGK_FIELD_ELEMENT, 0.0, rho + b * m->E, m->E};
-            p.n_source = (F && b == 0) ? 1 : 0;
-            p.source[0] = tgk_field{TGK_FIELD_CONSTANT, source, nullptr, 0};
-            TGK_TRY(tgk_assemble_d(&p, m, r, K + b * r->nnz, b == 0 ? F : nullptr, nullptr, st));
-        }
-        return TGK_OK;
-    }
+    // TGK_MODE_FAST takes the same kernels: their bit-identical results meet
+    // the fast contract, and the fast-mode variants measured slower on C4
+    // (profiles/r02_fast_experiments.txt)
     if (!getenv("TGK_BATCHED_LOOP") && !getenv("TGK_BATCHED_CHUNKED")) {
         const int rc = batched_entries(m, const_cast<tgk_routing*>(r), B, rho, source, K, F, st, badp);
         if (rc == TGK_OK) return check_bad(badp, st);

@@ -350,20 +350,16 @@ def test_fields_batched(eng, mode, problem):
 
 
 def test_assemble_batched_fast_mode(eng):
-    """tgk_assemble_batched_d with TGK_MODE_FAST: each field's K equals the
-    single fast-mode assembly (bitwise) and the oracle (scaled tolerance)."""
+    """tgk_assemble_batched_d accepts TGK_MODE_FAST and runs the batched exact
+    kernels (their bit-identical results meet the fast contract; the fast
+    batched variants measured slower, profiles/r02_fast_experiments.txt)."""
     from paper_2602_05052_b200 import meshgen
     nodes, elems = meshgen.unstructured_tri(48)
-    E = elems.shape[0]
-    rho = 0.5 + np.random.default_rng(4).random((4, E))
+    rho = 1e-3 + np.random.default_rng(4).random((13, elems.shape[0]))
     m = eng.DeviceMesh("tri3", nodes, elems)
     r = eng.Routing(m, 1)
-    K, F = eng.assemble_batched(m, r, torch.from_numpy(rho), source=1.0, mode="fast")
-    pr = port.Routing(nodes.shape[0], port.dofmap("tri3", elems, 1))
-    for b in range(rho.shape[0]):
-        Kb, Fb, _ = eng.assemble(m, r, diffusion=("element", rho[b]), sources=[1.0], mode="fast")
-        assert_bitwise(np_(K[b]), np_(Kb), f"field {b}")
-        Kr, Fr, _ = port.assemble("tri3", nodes, elems, pr, diffusion=("element", rho[b]), sources=[1.0])
-        assert_scaled_close(np_(K[b]), Kr, what=f"field {b} vs oracle")
-        if b == 0:
-            assert_bitwise(np_(F), np_(Fb), "F")
+    rt = torch.from_numpy(rho)
+    K, F = eng.assemble_batched(m, r, rt, source=1.0, mode="fast")
+    Kx, Fx = eng.assemble_batched(m, r, rt, source=1.0, mode="exact")
+    assert_bitwise(np_(K), np_(Kx), "K")
+    assert_bitwise(np_(F), np_(Fx), "F")
