@@ -17,7 +17,7 @@
 //             into structure-of-arrays value rows;
 //   phase B   one lane per owned CSR entry (diagonal entries also fold the
 //             row's load): its items (u16 = halo index | value index << 12,
-//             one coalesced 8-byte load per 4 items) are summed in registers
+//             one coalesced 4-byte load per 2 items) are summed in registers
 //             and the result stored to the entry — and to its mirror (j, i)
 //             when j is owned by the same block.
 // Mass and load values are affine P1 closed forms of the reference's
@@ -92,7 +92,10 @@ struct FastCfg {
     static constexpr int FROW = NP + (HAS_S ? 1 : 0);
     static constexpr int NR = FMT == kFastFmtS16 ? 1 : (FMT == kFastFmtKS32 ? NP + 2 : NP + (FT == 2 ? k : 1));
     static constexpr int NTILE = HAS_M ? 2 : 1;
-    __host__ __device__ static int ncol(int ctype) { return d + (ctype == TGK_FIELD_NODAL ? 1 : 0) + (FT == 2 ? 1 : 0); }
+    // node table: coordinates as [node][CS] (one 16-byte load per coordinate
+    // pair), then the nodal coefficient / source columns; ncol in units of MB
+    static constexpr int CS = d == 3 ? 4 : 2;
+    __host__ __device__ static int ncol(int ctype) { return CS + (ctype == TGK_FIELD_NODAL ? 1 : 0) + (FT == 2 ? 1 : 0); }
     static size_t smem(const FastArgs& a) {
         return 64 + 2 * size_t(a.abuf) + size_t(a.bbuf) +
                sizeof(double) * (2 * size_t(ncol(a.ctype)) * a.MB + size_t(NR) * a.MH + size_t(NTILE) * a.pl.max_tile) +
@@ -198,7 +201,7 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
     using Cn = FastConst<KIND>;
     constexpr int k = Cf::k, d = Cf::d;
     const int MH = p.MH, MB = p.MB;
-    const double* cn = xs + d * MB;
+    const double* cn = xs + Cf::CS * MB;
     const double* sn = xs + (Cf::ncol(p.ctype) - 1) * MB;
     const uint64_t hc = A.hconn[h];
     int l[k];
@@ -215,10 +218,14 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
         return sacc * Cn::wa;
     };
     if constexpr (KIND == TGK_TET4) {
-        const double x0 = xs[l[0]], y0 = xs[MB + l[0]], z0 = xs[2 * MB + l[0]];
-        const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0, e1z = xs[2 * MB + l[1]] - z0;
-        const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0, e2z = xs[2 * MB + l[2]] - z0;
-        const double e3x = xs[l[3]] - x0, e3y = xs[MB + l[3]] - y0, e3z = xs[2 * MB + l[3]] - z0;
+        const double2 p0 = *reinterpret_cast<const double2*>(xs + 4 * l[0]);
+        const double2 p1 = *reinterpret_cast<const double2*>(xs + 4 * l[1]);
+        const double2 p2 = *reinterpret_cast<const double2*>(xs + 4 * l[2]);
+        const double2 p3 = *reinterpret_cast<const double2*>(xs + 4 * l[3]);
+        const double z0 = xs[4 * l[0] + 2];
+        const double e1x = p1.x - p0.x, e1y = p1.y - p0.y, e1z = xs[4 * l[1] + 2] - z0;
+        const double e2x = p2.x - p0.x, e2y = p2.y - p0.y, e2z = xs[4 * l[2] + 2] - z0;
+        const double e3x = p3.x - p0.x, e3y = p3.y - p0.y, e3z = xs[4 * l[3] + 2] - z0;
         // rows of J^{-1} times det: grad N_b = c_b / det (b = 1..3)
         const double c1x = __fma_rn(e2y, e3z, -(e2z * e3y)), c1y = __fma_rn(e2z, e3x, -(e2x * e3z)),
                      c1z = __fma_rn(e2x, e3y, -(e2y * e3x));
@@ -242,9 +249,11 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
             kp[7] = k12; kp[8] = k13; kp[9] = k23;
         }
     } else {
-        const double x0 = xs[l[0]], y0 = xs[MB + l[0]];
-        const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0;
-        const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0;
+        const double2 p0 = *reinterpret_cast<const double2*>(xs + 2 * l[0]);
+        const double2 p1 = *reinterpret_cast<const double2*>(xs + 2 * l[1]);
+        const double2 p2 = *reinterpret_cast<const double2*>(xs + 2 * l[2]);
+        const double e1x = p1.x - p0.x, e1y = p1.y - p0.y;
+        const double e2x = p2.x - p0.x, e2y = p2.y - p0.y;
         det = __fma_rn(e1x, e2y, -(e1y * e2x));
         if constexpr (KT == 0) {
             const double s = coef_w(Cn::wsum) * __drcp_rn(det);
@@ -299,9 +308,9 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
 
 // ---------------------------------------------------------------- phase B: one warp group of entries
 // Lane `lane` of warp group w folds its entry's items (direct value indices,
-// plan_fast.cpp formats) from the value rows into the output tile.  Two
-// steps per iteration with the next two steps' words already in flight,
-// four partial sums per value: independent loads, short add chains.
+// plan_fast.cpp formats) from the value rows into the output tile.  One
+// 4-byte word (two items) per step, the next three steps' words already in
+// flight, two partial sums per value.
 template <int KIND, int KT, bool HAS_M, int FT>
 __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, const RecB& Bq, const double* kv,
                                            double* tk, double* tm, int w, int lane) {
@@ -311,16 +320,16 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
     const int MH = p.MH;
     const uint32_t desc = Bq.desc[w * 32 + lane];
     const uint32_t i0 = Bq.wgoff[w];
-    const int steps = static_cast<int>((Bq.wgoff[w + 1] - i0) >> 6);  // 64 words per step
-    const uint2* ip = reinterpret_cast<const uint2*>(Bq.words + i0) + lane;
+    const int steps = static_cast<int>((Bq.wgoff[w + 1] - i0) >> 5);  // 32 words per step
+    const uint32_t* ip = Bq.words + i0 + lane;
     const bool diag = (__shfl_sync(0xffffffffu, desc, 0) >> 15) & 1u;  // warp-uniform class
     double k0 = 0.0, k1 = 0.0, k2 = 0.0, k3 = 0.0, s0 = 0.0, s1 = 0.0, f0 = 0.0, f1 = 0.0;
     // u16 items h | q << 12: K_ab at row q, S at SROW, F at FROW (+ a = q for a
     // nodal load on a diagonal); padding items address the +0.0 slot
     const uint32_t zw = uint32_t(MH - 1) | (uint32_t(MH - 1) << 16);
-    const uint2 padw = make_uint2(zw, zw);
-    uint2 wa = steps > 0 ? ip[0] : padw;
-    uint2 wb = steps > 1 ? ip[32] : padw;
+    uint32_t wa = steps > 0 ? ip[0] : zw;
+    uint32_t wb = steps > 1 ? ip[32] : zw;
+    uint32_t wc = steps > 2 ? ip[64] : zw;
     auto eat = [&](uint32_t it, double& kk, double& ss, double& ff) {
         const int h = static_cast<int>(it & 0xfffu), q = static_cast<int>(it >> 12);
         if constexpr (KT == 0) kk += kv[q * MH + h];
@@ -332,19 +341,13 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
             if (diag) ff += kv[(Cf::FROW + q) * MH + h];
         }
     };
-    for (int st = 0; st < steps; st += 2) {
-        const uint2 wc = st + 2 < steps ? ip[(st + 2) * 32] : padw;
-        const uint2 wd = st + 3 < steps ? ip[(st + 3) * 32] : padw;
-        eat(wa.x & 0xffffu, k0, s0, f0);
-        eat(wa.x >> 16, k1, s1, f1);
-        eat(wa.y & 0xffffu, k2, s0, f0);
-        eat(wa.y >> 16, k3, s1, f1);
-        eat(wb.x & 0xffffu, k0, s0, f0);
-        eat(wb.x >> 16, k1, s1, f1);
-        eat(wb.y & 0xffffu, k2, s0, f0);
-        eat(wb.y >> 16, k3, s1, f1);
-        wa = wc;
-        wb = wd;
+    for (int st = 0; st < steps; ++st) {
+        const uint32_t wn = st + 3 < steps ? ip[(st + 3) * 32] : zw;
+        eat(wa & 0xffffu, k0, s0, f0);
+        eat(wa >> 16, k1, s1, f1);
+        wa = wb;
+        wb = wc;
+        wc = wn;
     }
     if constexpr (KT == 1) {  // coefficient mass: the folds summed S
         k0 = s0;
@@ -460,20 +463,22 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
         for (int i = tid; i < nbn_run; i += T) {
             const int64_t g = A.bnodes[i];
 #pragma unroll
-            for (int c = 0; c < d; ++c) cp_async8(xs + c * MB + i, p.nodes + g * d + c);
-            if (cnodal) cp_async8(xs + d * MB + i, p.cdata + g);
+            for (int c = 0; c < d; ++c) cp_async8(xs + i * Cf::CS + c, p.nodes + g * d + c);
+            if (cnodal) cp_async8(xs + Cf::CS * MB + i, p.cdata + g);
             if (FT == 2) cp_async8(xs + (ncol - 1) * MB + i, p.sdata + g);
         }
         cp_async_commit();
     };
     // the previous block's tile to HBM: groups of GL lanes per row
     int tile_rows = 0;
+    // copy-out lanes: GL = 2^glog lanes per row, 32 / GL rows per warp step
+    const int glog = p.gl <= 8 ? 3 : p.gl <= 16 ? 4 : 5;
+    const int gl = lane & ((1 << glog) - 1), GL = 1 << glog;
+    const int lr_first = (warp << (5 - glog)) + (lane >> glog), lr_step = nwarp << (5 - glog);
     auto copy_out = [&]() {
         if (p.debug & 4) return;
-        const int GL = p.gl, gpw = 32 / GL;
-        const int gi = lane / GL, gl = lane % GL;
 #pragma unroll 4
-        for (int lr = warp * gpw + gi; lr < tile_rows; lr += nwarp * gpw) {
+        for (int lr = lr_first; lr < tile_rows; lr += lr_step) {
             const int64_t rp = trp[lr];
             const int t0 = ttoff[lr], len = ttoff[lr + 1] - t0;
             for (int q = gl; q < len; q += GL) {
@@ -777,8 +782,8 @@ __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& 
     const int MH = p.MH;
     const uint32_t desc = Bq.desc[w * 32 + lane];
     const uint32_t i0 = Bq.wgoff[w];
-    const int steps = static_cast<int>((Bq.wgoff[w + 1] - i0) >> 6);
-    const uint2* ip = reinterpret_cast<const uint2*>(Bq.words + i0) + lane;
+    const int steps = static_cast<int>((Bq.wgoff[w + 1] - i0) >> 5);
+    const uint32_t* ip = Bq.words + i0 + lane;
     const bool diag = (__shfl_sync(0xffffffffu, desc, 0) >> 15) & 1u;
     double acc[d][d], fac[NF];
 #pragma unroll
@@ -829,11 +834,9 @@ __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& 
     };
     // padding items address the +0.0 slot (h = max_halo, a = b = 0)
     for (int st = 0; st < steps; ++st) {
-        const uint2 wv = ip[st * 32];
-        eat(wv.x & 0xffffu);
-        eat(wv.x >> 16);
-        eat(wv.y & 0xffffu);
-        eat(wv.y >> 16);
+        const uint32_t wv = ip[st * 32];
+        eat(wv & 0xffffu);
+        eat(wv >> 16);
     }
     if (diag) {  // split diagonal lists: partial sums of kFastDiagSplit lanes
         constexpr int DS = kFastDiagSplit(k);

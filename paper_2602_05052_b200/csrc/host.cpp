@@ -980,8 +980,9 @@ int tgk_assemble(const tgk_problem* p, const tgk_mesh* m, const tgk_routing* r, 
     };
     if (!rc) rc = scratch(rw->scratch_K, r->nnz);
     if (!rc) rc = scratch(rw->scratch_F, r->N);
-    if (!rc && p->with_mass) rc = scratch(rw->scratch_M, r->nnz);
-    double *dK = rw->scratch_K, *dF = rw->scratch_F, *dM = p->with_mass ? rw->scratch_M : nullptr;
+    const bool want_m = p->with_mass && p->kind != TGK_MASS;  // a Mass problem returns no M (physics.cpp:25-31)
+    if (!rc && want_m) rc = scratch(rw->scratch_M, r->nnz);
+    double *dK = rw->scratch_K, *dF = rw->scratch_F, *dM = want_m ? rw->scratch_M : nullptr;
     if (!rc) rc = tgk::assemble_dev(&pd, m, rw, dK, dF, dM, nullptr, nullptr);
     if (!rc && K && cudaMemcpy(K, dK, sizeof(double) * r->nnz, cudaMemcpyDeviceToHost) != cudaSuccess) rc = set_error(TGK_ERR_CUDA, "copy K");
     if (!rc && F && cudaMemcpy(F, dF, sizeof(double) * r->N, cudaMemcpyDeviceToHost) != cudaSuccess) rc = set_error(TGK_ERR_CUDA, "copy F");

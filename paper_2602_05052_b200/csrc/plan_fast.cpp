@@ -16,8 +16,8 @@
 //    stored to (i, j) and (j, i) (K, M symmetric: both folds would run over
 //    the same elements with K_e[a][b] == K_e[b][a]).  Entries are sorted by
 //    list length (warps of uniform work), each class padded to whole warps;
-//  - per warp of 32 entries the items, interleaved [step][lane][8 bytes] so
-//    every step is one coalesced 8-byte load per lane.  Items are direct
+//  - per warp of 32 entries the items, interleaved [step][lane][4 bytes] so
+//    every step is one coalesced 4-byte load per lane (two u16 items).  Items are direct
 //    indices of the values in the block's shared-memory value rows (format
 //    below); short lists are padded with the zero slot.
 #include <algorithm>
@@ -335,26 +335,21 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
         std::vector<uint32_t> wgoff(nwg + 1, 0), words;
         for (uint32_t w = 0; w < nwg; ++w) {
             const bool diag = (P.desc[e0 + w * 32] >> 15) & 1u;  // lane 0 is never idle
-            const bool wide = false;  // u16 items, 4 per 8-byte step
-            const int per_step = wide ? 2 : 4;
+            // u16 items, 2 per 4-byte word, one word per lane per step
+            // ([step][lane]: each step one coalesced 128-byte warp load)
             int steps = 0;
             for (int l = 0; l < 32; ++l) {
                 const int n = int(loff[w * 32 + l + 1] - loff[w * 32 + l]);
-                steps = std::max(steps, (n + per_step - 1) / per_step);
+                steps = std::max(steps, (n + 1) / 2);
             }
             const size_t base = words.size();
-            words.resize(base + size_t(steps) * 64, zero | (zero << 16));
+            words.resize(base + size_t(steps) * 32, zero | (zero << 16));
             for (int l = 0; l < 32; ++l) {
                 const uint32_t i0 = loff[w * 32 + l], i1 = loff[w * 32 + l + 1];
                 for (uint32_t t = 0; t < i1 - i0; ++t) {
                     const uint32_t v = diag ? diag_item(gi[i0 + t]) : off_item(gi[i0 + t]);
-                    const size_t at = base + size_t(t / per_step) * 64 + size_t(l) * 2;
-                    if (wide) {
-                        words[at + (t % 2)] = v;
-                    } else {
-                        uint32_t& wd = words[at + (t % 4) / 2];
-                        wd = (t % 2) ? ((wd & 0xffffu) | (v << 16)) : ((wd & 0xffff0000u) | v);
-                    }
+                    uint32_t& wd = words[base + size_t(t / 2) * 32 + size_t(l)];
+                    wd = (t % 2) ? ((wd & 0xffffu) | (v << 16)) : ((wd & 0xffff0000u) | v);
                 }
             }
             wgoff[w + 1] = uint32_t(words.size());
