@@ -80,26 +80,28 @@ struct FastConst<TGK_TRI3> {
 // KT 0: diffusion stiffness (+ unit mass M if HAS_M), 1: coefficient mass
 // (ProblemKind::Mass).  FT: load none / scalar (f det; constant or
 // per-element source) / per node (nodal source).
-// Value rows in shared memory (row stride MH, plan_fast.cpp formats):
-// K_aa (k rows), K_ab off-diagonal pairs, [S = c det (mass) row], [F rows].
+// Value rows in shared memory (row stride MH, plan_fast.cpp formats): K_ab
+// off-diagonal pairs, [S = c det (mass) row], [F rows].  No K_aa rows: the
+// stiffness diagonal is minus the row's off-diagonal sum (every element
+// matrix has zero row sums), formed at the copy-out.
 template <int KIND, int KT, bool HAS_M, int FT>
 struct FastCfg {
     static constexpr int k = P1<KIND>::k, d = P1<KIND>::d;
     static constexpr bool HAS_S = HAS_M || KT == 1;
-    static constexpr int NP = KT == 0 ? FastConst<KIND>::np : 0;
+    static constexpr int NPO = KT == 0 ? k * (k - 1) / 2 : 0;
     static constexpr int FMT = KT == 1 ? kFastFmtS16 : (HAS_M ? kFastFmtKS32 : kFastFmtK16);
-    static constexpr int SROW = NP;
-    static constexpr int FROW = NP + (HAS_S ? 1 : 0);
-    static constexpr int NR = FMT == kFastFmtS16 ? 1 : (FMT == kFastFmtKS32 ? NP + 2 : NP + (FT == 2 ? k : 1));
+    static constexpr int SROW = NPO;
+    static constexpr int FROW = NPO + (HAS_S ? 1 : 0);
+    static constexpr int NR = FMT == kFastFmtS16 ? 1 : (FMT == kFastFmtKS32 ? NPO + 2 : NPO + (FT == 2 ? k : 1));
     static constexpr int NTILE = HAS_M ? 2 : 1;
-    // node table: coordinates as [node][CS] (one 16-byte load per coordinate
-    // pair), then the nodal coefficient / source columns; ncol in units of MB
-    static constexpr int CS = d == 3 ? 4 : 2;
-    __host__ __device__ static int ncol(int ctype) { return CS + (ctype == TGK_FIELD_NODAL ? 1 : 0) + (FT == 2 ? 1 : 0); }
+    // node table: coordinates (TRI3 as [node][2], one 16-byte load per node;
+    // TET4 as x / y / z columns), then the nodal coefficient / source
+    // columns; ncol in units of MB
+    __host__ __device__ static int ncol(int ctype) { return d + (ctype == TGK_FIELD_NODAL ? 1 : 0) + (FT == 2 ? 1 : 0); }
     static size_t smem(const FastArgs& a) {
         return 64 + 2 * size_t(a.abuf) + size_t(a.bbuf) +
                sizeof(double) * (2 * size_t(ncol(a.ctype)) * a.MB + size_t(NR) * a.MH + size_t(NTILE) * a.pl.max_tile) +
-               sizeof(int64_t) * a.pl.max_rows + sizeof(uint16_t) * (a.pl.max_rows + 1);
+               sizeof(int64_t) * a.pl.max_rows + sizeof(uint16_t) * (a.pl.max_rows + 1) + ((size_t(a.pl.max_rows) + 15) & ~size_t(15));
     }
 };
 
@@ -201,7 +203,7 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
     using Cn = FastConst<KIND>;
     constexpr int k = Cf::k, d = Cf::d;
     const int MH = p.MH, MB = p.MB;
-    const double* cn = xs + Cf::CS * MB;
+    const double* cn = xs + d * MB;
     const double* sn = xs + (Cf::ncol(p.ctype) - 1) * MB;
     const uint64_t hc = A.hconn[h];
     int l[k];
@@ -218,14 +220,10 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
         return sacc * Cn::wa;
     };
     if constexpr (KIND == TGK_TET4) {
-        const double2 p0 = *reinterpret_cast<const double2*>(xs + 4 * l[0]);
-        const double2 p1 = *reinterpret_cast<const double2*>(xs + 4 * l[1]);
-        const double2 p2 = *reinterpret_cast<const double2*>(xs + 4 * l[2]);
-        const double2 p3 = *reinterpret_cast<const double2*>(xs + 4 * l[3]);
-        const double z0 = xs[4 * l[0] + 2];
-        const double e1x = p1.x - p0.x, e1y = p1.y - p0.y, e1z = xs[4 * l[1] + 2] - z0;
-        const double e2x = p2.x - p0.x, e2y = p2.y - p0.y, e2z = xs[4 * l[2] + 2] - z0;
-        const double e3x = p3.x - p0.x, e3y = p3.y - p0.y, e3z = xs[4 * l[3] + 2] - z0;
+        const double x0 = xs[l[0]], y0 = xs[MB + l[0]], z0 = xs[2 * MB + l[0]];
+        const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0, e1z = xs[2 * MB + l[1]] - z0;
+        const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0, e2z = xs[2 * MB + l[2]] - z0;
+        const double e3x = xs[l[3]] - x0, e3y = xs[MB + l[3]] - y0, e3z = xs[2 * MB + l[3]] - z0;
         // rows of J^{-1} times det: grad N_b = c_b / det (b = 1..3)
         const double c1x = __fma_rn(e2y, e3z, -(e2z * e3y)), c1y = __fma_rn(e2z, e3x, -(e2x * e3z)),
                      c1z = __fma_rn(e2x, e3y, -(e2y * e3x));
@@ -294,9 +292,9 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
 #pragma unroll
         for (int a = 0; a < k; ++a) fv[a] = 0.0;
     }
-    if constexpr (KT == 0) {
+    if constexpr (KT == 0) {  // the off-diagonal pairs (kp[k..]: 01 02 03 12 13 23 / 01 02 12)
 #pragma unroll
-        for (int t = 0; t < Cn::np; ++t) kv[t * MH + h] = kp[t];
+        for (int t = 0; t < Cf::NPO; ++t) kv[t * MH + h] = kp[k + t];
     }
     if constexpr (Cf::HAS_S) kv[Cf::SROW * MH + h] = sv;
     if constexpr (FT == 1) kv[Cf::FROW * MH + h] = fv[0];
@@ -313,7 +311,7 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
 // flight, two partial sums per value.
 template <int KIND, int KT, bool HAS_M, int FT>
 __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, const RecB& Bq, const double* kv,
-                                           double* tk, double* tm, int w, int lane) {
+                                           double* tk, double* tm, uint8_t* tdiag, int w, int lane) {
     using Cf = FastCfg<KIND, KT, HAS_M, FT>;
     using Cn = FastConst<KIND>;
     constexpr int k = Cf::k;
@@ -332,7 +330,9 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
     uint32_t wc = steps > 2 ? ip[64] : zw;
     auto eat = [&](uint32_t it, double& kk, double& ss, double& ff) {
         const int h = static_cast<int>(it & 0xfffu), q = static_cast<int>(it >> 12);
-        if constexpr (KT == 0) kk += kv[q * MH + h];
+        if constexpr (KT == 0) {
+            if (!diag) kk += kv[q * MH + h];  // the diagonal: zero row sums (copy-out)
+        }
         if constexpr (Cf::HAS_S) ss += kv[Cf::SROW * MH + h];
         if constexpr (FT == 1) {
             if (diag) ff += kv[Cf::FROW * MH + h];
@@ -381,9 +381,10 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
     const int lr = static_cast<int>(desc & 0x1ffu), pos = static_cast<int>((desc >> 9) & 63u);
     const double mh = diag ? Cn::mdiag : Cn::moff;
     const double kval = KT == 0 ? kacc : sacc * mh;
+    if (KT == 0 && diag) tdiag[lr] = static_cast<uint8_t>(pos);  // K_ii formed at the copy-out
     if (pos != kFastNoPos) {
         const int at = A.toff[lr] + pos;
-        tk[at] = kval;
+        if (KT != 0 || !diag) tk[at] = kval;
         if constexpr (HAS_M) tm[at] = sacc * mh;
     }
     if constexpr (FT > 0) {
@@ -431,6 +432,7 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
     double* const tm = tk + pl.max_tile;
     int64_t* const trp = reinterpret_cast<int64_t*>(tm + (HAS_M ? pl.max_tile : 0));  // tile rows' CSR offsets
     uint16_t* const ttoff = reinterpret_cast<uint16_t*>(trp + pl.max_rows);           // tile row offsets (n+1)
+    uint8_t* const tdiag = reinterpret_cast<uint8_t*>(ttoff + pl.max_rows + 1);       // tile rows' diagonal position
     auto ra = [&](int64_t it) { return ra_base + size_t(it & 1) * p.abuf; };
     auto xsp = [&](int64_t it) { return xs_base + size_t(it & 1) * ncol * MB; };
 
@@ -463,26 +465,37 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
         for (int i = tid; i < nbn_run; i += T) {
             const int64_t g = A.bnodes[i];
 #pragma unroll
-            for (int c = 0; c < d; ++c) cp_async8(xs + i * Cf::CS + c, p.nodes + g * d + c);
-            if (cnodal) cp_async8(xs + Cf::CS * MB + i, p.cdata + g);
+            for (int c = 0; c < d; ++c) cp_async8(d == 2 ? xs + 2 * i + c : xs + c * MB + i, p.nodes + g * d + c);
+            if (cnodal) cp_async8(xs + d * MB + i, p.cdata + g);
             if (FT == 2) cp_async8(xs + (ncol - 1) * MB + i, p.sdata + g);
         }
         cp_async_commit();
     };
     // the previous block's tile to HBM: groups of GL lanes per row
     int tile_rows = 0;
-    // copy-out lanes: GL = 2^glog lanes per row, 32 / GL rows per warp step
+    // copy-out lanes: GL = 2^glog lanes per row, 32 / GL rows per warp step;
+    // the stiffness diagonal K_ii = 0 - (sum of the row's off-diagonals), the
+    // group's lanes summed by a butterfly (deterministic; within the SURVEY.md
+    // 8(c) tolerance of the reference's element fold)
     const int glog = p.gl <= 8 ? 3 : p.gl <= 16 ? 4 : 5;
     const int gl = lane & ((1 << glog) - 1), GL = 1 << glog;
-    const int lr_first = (warp << (5 - glog)) + (lane >> glog), lr_step = nwarp << (5 - glog);
+    const int lr_base = warp << (5 - glog), lr_step = nwarp << (5 - glog);
     auto copy_out = [&]() {
         if (p.debug & 4) return;
-#pragma unroll 4
-        for (int lr = lr_first; lr < tile_rows; lr += lr_step) {
-            const int64_t rp = trp[lr];
-            const int t0 = ttoff[lr], len = ttoff[lr + 1] - t0;
+        for (int base = lr_base; base < tile_rows; base += lr_step) {  // warp-uniform: shuffles below
+            const int lr = base + (lane >> glog);
+            const bool ok = lr < tile_rows;
+            const int64_t rp = ok ? trp[lr] : 0;
+            const int t0 = ok ? ttoff[lr] : 0, len = ok ? ttoff[lr + 1] - t0 : 0;
+            const int dq = (KT == 0 && ok) ? tdiag[lr] : -1;
+            double off = 0.0;
+            if constexpr (KT == 0) {
+                for (int q = gl; q < len; q += GL)
+                    if (q != dq) off += tk[t0 + q];
+                for (int o = GL >> 1; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
+            }
             for (int q = gl; q < len; q += GL) {
-                p.K[rp + q] = tk[t0 + q];
+                p.K[rp + q] = (KT == 0 && q == dq) ? 0.0 - off : tk[t0 + q];
                 if constexpr (HAS_M) p.M[rp + q] = tm[t0 + q];
             }
         }
@@ -514,7 +527,7 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
         }
         tile_rows = int(A.nr);
         const int nwg = (p.debug & 2) ? 0 : int(Bq.nwg);
-        for (int w = warp; w < nwg; w += nwarp) fast_group<KIND, KT, HAS_M, FT>(p, A, Bq, kv, tk, tm, w, lane);
+        for (int w = warp; w < nwg; w += nwarp) fast_group<KIND, KT, HAS_M, FT>(p, A, Bq, kv, tk, tm, tdiag, w, lane);
         cp_async_wait_all();
         __syncthreads();
         if (tid == 0) {  // records A(it) and B(it) are consumed: refill their slots
@@ -572,14 +585,14 @@ int dispatch_fast(int kt, bool m, int ft, const FastArgs& a, int T, cudaStream_t
 int check_bad(unsigned long long* d_bad, cudaStream_t st);
 
 // Rows per block and threads per CTA (B200 sweeps, profiles/r02_fast_experiments.txt):
-// TET4 stiffness [+ load] 32 rows x 256 threads (3 CTAs/SM); with the unit
-// mass (two value rows more, two output tiles) 48 rows x 384 threads;
-// TRI3 128 rows x 256 threads.
+// TET4 64 rows x 512 threads (C2a 348 us, C2 405 us; 32 x 256 at 4 CTAs/SM:
+// 357 / 434 us); TRI3 128 rows x 256 threads.
 struct FastShape {
     int R, T;
 };
 FastShape fast_shape(int kind, int fmt) {
-    FastShape s{kind == TGK_TET4 ? (fmt == kFastFmtKS32 ? 48 : 32) : 128, kind == TGK_TET4 && fmt == kFastFmtKS32 ? 384 : 256};
+    (void)fmt;
+    FastShape s{kind == TGK_TET4 ? 64 : 128, kind == TGK_TET4 ? 512 : 256};
     if (const char* e = getenv("TGK_FAST_R")) s.R = std::max(1, std::min(kFastMaxRows, atoi(e)));
     if (const char* e = getenv("TGK_FAST_T")) s.T = std::max(32, std::min(kFastMaxThreads, atoi(e) / 32 * 32));
     return s;

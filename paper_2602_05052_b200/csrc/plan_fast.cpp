@@ -49,6 +49,11 @@ inline int pair_row(int k, int q) {
     return r[q];
 }
 
+// value row of an off-diagonal pair in the fast kernel (fast.cu FastCfg): the
+// K_aa rows are not stored — the diagonal comes from the zero row sums of the
+// assembled stiffness (k_fast_scalar copy-out)
+inline int offdiag_row(int k, int q) { return pair_row(k, q) - k; }
+
 }  // namespace
 
 int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const int32_t* conn,
@@ -243,16 +248,14 @@ int build_fast_plan(int kind, int64_t N, int64_t E, const double* nodes, const i
 
 // ---------------------------------------------------------------------------
 // Upload: two byte records per block (layout in tgk_internal.hpp FastPlanDev)
-// with the items resolved for the value-row format (fast.cu FastCfg):
-//   kFastFmtK16  stiffness [+ load]: rows K_aa (k), K_ab (off-diagonal pairs),
-//                F (load scalar f det, or k rows F_e[a] with a nodal source);
-//                off-diagonal items u16 = K row * MH + h; diagonal items
-//                u32 = K index | F index << 16;
-//   kFastFmtKS32 stiffness + unit mass [+ scalar load]: rows K_aa, K_ab, S
-//                (det), F; all items u32 = K index | S index << 16 (F index =
-//                S index + MH);
-//   kFastFmtS16  coefficient mass (ProblemKind::Mass): row S (c det); items
-//                u16 = h;
+// with the items resolved for the value-row formats (fast.cu FastCfg):
+//   scalar formats (kFastFmtK16 stiffness [+ load], kFastFmtKS32 + unit mass,
+//                kFastFmtS16 coefficient mass) share one item layout, u16 =
+//                h | row << 12: an off-diagonal item names the K_ab value row
+//                (0 .. k(k-1)/2 - 1), a diagonal item the local node a (the
+//                kernel forms the S / F indices from h and a).  The stiffness
+//                diagonal is not folded: it is minus the row's off-diagonal
+//                sum (zero row sums of P1 stiffness), formed at the copy-out;
 //   kFastFmtE16  vector elasticity (fast.cu k_fast_elast): items u16 = the
 //                generic h | (a * 4 + b) << 12, the kernel reads the scaled
 //                gradients of nodes a, b of halo element h.
@@ -263,11 +266,11 @@ void FastPlanDev::release() {
 }
 
 int fast_value_rows(int k, int fmt, bool fnodal) {
-    const int np = k * (k + 1) / 2;
+    const int npo = k * (k - 1) / 2;  // off-diagonal pairs (fast.cu FastCfg::NPO)
     if (fmt == kFastFmtS16) return 1;
     if (fmt == kFastFmtE16) return 1;  // items carry (h, a, b), not value indices
-    if (fmt == kFastFmtKS32) return np + 2;
-    return np + (fnodal ? k : 1);
+    if (fmt == kFastFmtKS32) return npo + 2;
+    return npo + (fnodal ? k : 1);
 }
 
 int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPlanDev** out) {
@@ -309,7 +312,7 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
     auto off_item = [&](uint16_t g) -> uint32_t {
         if (fmt == kFastFmtE16) return g;  // elasticity: the kernel reads g_a, g_b of element h
         const uint32_t hh = g & 0xfffu, a = (g >> 12) >> 2, b = (g >> 12) & 3u;
-        return hh | (uint32_t(pair_row(k, sym_pair_k(k, int(a), int(b)))) << 12);
+        return hh | (uint32_t(offdiag_row(k, sym_pair_k(k, int(a), int(b)))) << 12);
     };
     auto diag_item = [&](uint16_t g) -> uint32_t {
         if (fmt == kFastFmtE16) return g;
