@@ -87,5 +87,25 @@ def build(verbose=False) -> str:
     return LIB
 
 
+def build_module() -> str:
+    """The pybind11 module `_tgfem` (bindings/module.cpp: the reference's compiled
+    Python module over the C ABI) into lib/, linked to libtgk.so by rpath."""
+    import sysconfig
+
+    import pybind11
+    lib = build()
+    src = os.path.join(HERE, "bindings", "module.cpp")
+    out = os.path.join(OUT, "_tgfem" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if _newer([src, lib, os.path.join(ROOT, "include", "tgk.h")], out):
+        cmd = [os.environ.get("CXX", "g++"), "-O2", "-shared", "-fPIC", "-std=c++17", "-fvisibility=hidden",
+               f"-I{pybind11.get_include()}", f"-I{sysconfig.get_paths()['include']}", f"-I{os.path.join(ROOT, 'include')}",
+               src, "-o", out, f"-L{OUT}", "-ltgk", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"module build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
+    print(build_module())

@@ -33,7 +33,8 @@ namespace tgk {
 
 namespace {
 
-constexpr int kFastMaxThreads = 512;
+constexpr int kFastMaxThreads = 512;        // k_fast_elast
+constexpr int kFastScalarMaxThreads = 1024;  // k_fast_scalar (<= 64 registers)
 
 struct FastArgs {
     const double* nodes;
@@ -414,7 +415,7 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
 // block it from a second value buffer — measured slower: 474-715 vs 370 us
 // on C2a, profiles/r02_fast_experiments.txt.)
 template <int KIND, int KT, bool HAS_M, int FT>
-__global__ void __launch_bounds__(kFastMaxThreads) k_fast_scalar(FastArgs p) {
+__global__ void __launch_bounds__(kFastScalarMaxThreads) k_fast_scalar(FastArgs p) {
     using Cf = FastCfg<KIND, KT, HAS_M, FT>;
     constexpr int d = Cf::d;
     extern __shared__ __align__(128) unsigned char smb[];
@@ -594,7 +595,7 @@ FastShape fast_shape(int kind, int fmt) {
     (void)fmt;
     FastShape s{kind == TGK_TET4 ? 64 : 128, kind == TGK_TET4 ? 512 : 256};
     if (const char* e = getenv("TGK_FAST_R")) s.R = std::max(1, std::min(kFastMaxRows, atoi(e)));
-    if (const char* e = getenv("TGK_FAST_T")) s.T = std::max(32, std::min(kFastMaxThreads, atoi(e) / 32 * 32));
+    if (const char* e = getenv("TGK_FAST_T")) s.T = std::max(32, std::min(kFastScalarMaxThreads, atoi(e) / 32 * 32));
     return s;
 }
 
