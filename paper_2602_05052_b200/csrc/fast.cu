@@ -101,7 +101,7 @@ struct FastCfg {
     __host__ __device__ static int ncol(int ctype) { return d + (ctype == TGK_FIELD_NODAL ? 1 : 0) + (FT == 2 ? 1 : 0); }
     static size_t smem(const FastArgs& a) {
         return 64 + 2 * size_t(a.abuf) + size_t(a.bbuf) +
-               sizeof(double) * (2 * size_t(ncol(a.ctype)) * a.MB + size_t(NR) * a.MH + size_t(NTILE) * a.pl.max_tile) +
+               sizeof(double) * (size_t(ncol(a.ctype)) * a.MB + size_t(NR) * a.MH + size_t(NTILE) * a.pl.max_tile) +
                sizeof(int64_t) * a.pl.max_rows + sizeof(uint16_t) * (a.pl.max_rows + 1) + ((size_t(a.pl.max_rows) + 15) & ~size_t(15));
     }
 };
@@ -428,14 +428,15 @@ __global__ void __launch_bounds__(kFastScalarMaxThreads) k_fast_scalar(FastArgs 
     const bool cnodal = p.ctype == TGK_FIELD_NODAL;
     const int ncol = Cf::ncol(p.ctype);
     double* const xs_base = reinterpret_cast<double*>(rb + size_t(p.bbuf));
-    double* const kv = xs_base + 2 * size_t(ncol) * MB;  // NR x MH value rows
+    double* const kv = xs_base + size_t(ncol) * MB;  // NR x MH value rows
     double* const tk = kv + size_t(Cf::NR) * MH;          // output tile (K), then M
     double* const tm = tk + pl.max_tile;
     int64_t* const trp = reinterpret_cast<int64_t*>(tm + (HAS_M ? pl.max_tile : 0));  // tile rows' CSR offsets
     uint16_t* const ttoff = reinterpret_cast<uint16_t*>(trp + pl.max_rows);           // tile row offsets (n+1)
     uint8_t* const tdiag = reinterpret_cast<uint8_t*>(ttoff + pl.max_rows + 1);       // tile rows' diagonal position
     auto ra = [&](int64_t it) { return ra_base + size_t(it & 1) * p.abuf; };
-    auto xsp = [&](int64_t it) { return xs_base + size_t(it & 1) * ncol * MB; };
+    // one node table: block it+1's gathers start after phase A of block it (its only reader)
+    auto xsp = [&](int64_t) { return xs_base; };
 
     const int64_t nb = pl.n_blocks, G = gridDim.x, b0 = blockIdx.x;
     if (b0 >= nb) return;
@@ -698,7 +699,7 @@ struct FastElastCfg {
     static constexpr int NR = FROW + (FT == 2 ? d : 0);
     static size_t smem(const FastElastArgs& a) {
         return 64 + 2 * size_t(a.abuf) + size_t(a.bbuf) +
-               sizeof(double) * (2 * size_t(d) * a.MB + size_t(NR) * a.MH + size_t(d) * d * a.pl.max_tile) +
+               sizeof(double) * (size_t(d) * a.MB + size_t(NR) * a.MH + size_t(d) * d * a.pl.max_tile) +
                sizeof(int64_t) * a.pl.max_rows + sizeof(uint16_t) * (a.pl.max_rows + 1);
     }
 };
@@ -909,12 +910,12 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p)
     unsigned char* const ra_base = smb + 64;
     unsigned char* const rb = ra_base + 2 * size_t(p.abuf);
     double* const xs_base = reinterpret_cast<double*>(rb + size_t(p.bbuf));
-    double* const kv = xs_base + 2 * size_t(d) * MB;
+    double* const kv = xs_base + size_t(d) * MB;
     double* const tk = kv + size_t(Cf::NR) * MH;
     int64_t* const trp = reinterpret_cast<int64_t*>(tk + size_t(d) * d * pl.max_tile);
     uint16_t* const ttoff = reinterpret_cast<uint16_t*>(trp + pl.max_rows);
     auto ra = [&](int64_t it) { return ra_base + size_t(it & 1) * p.abuf; };
-    auto xsp = [&](int64_t it) { return xs_base + size_t(it & 1) * d * MB; };
+    auto xsp = [&](int64_t) { return xs_base; };  // single node table (phase A is its only reader)
     const int64_t nb = pl.n_blocks, G = gridDim.x, b0 = blockIdx.x;
     if (b0 >= nb) return;
     const int64_t n_it = (nb - b0 + G - 1) / G;
