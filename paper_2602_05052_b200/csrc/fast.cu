@@ -151,8 +151,21 @@ struct RecA {
     const uint32_t* srow;
     const uint16_t* toff;
     const uint32_t* bnodes;
-    const uint64_t* hconn;
+    const void* hconn;  // per halo element 4 x u16 (or 4 x u8 with FastPlanDev::hc8) block-local node slots
 };
+// local node a of halo element h
+template <int k>
+__device__ __forceinline__ void halo_nodes(const RecA& A, int hc8, int h, int (&l)[k]) {
+    if (hc8) {
+        const uint32_t hc = static_cast<const uint32_t*>(A.hconn)[h];
+#pragma unroll
+        for (int a = 0; a < k; ++a) l[a] = static_cast<int>((hc >> (8 * a)) & 0xff);
+    } else {
+        const uint64_t hc = static_cast<const uint64_t*>(A.hconn)[h];
+#pragma unroll
+        for (int a = 0; a < k; ++a) l[a] = static_cast<int>((hc >> (16 * a)) & 0xffff);
+    }
+}
 __device__ __forceinline__ RecA parse_a(const unsigned char* r) {
     RecA a;
     a.hbase = *reinterpret_cast<const int64_t*>(r);
@@ -170,7 +183,7 @@ __device__ __forceinline__ RecA parse_a(const unsigned char* r) {
     o += al16(2 * size_t(a.nr + 1));
     a.bnodes = reinterpret_cast<const uint32_t*>(r + o);
     o += al16(4 * size_t(a.nbn));
-    a.hconn = reinterpret_cast<const uint64_t*>(r + o);
+    a.hconn = r + o;
     return a;
 }
 struct RecB {
@@ -206,10 +219,8 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
     const int MH = p.MH, MB = p.MB;
     const double* cn = xs + d * MB;
     const double* sn = xs + (Cf::ncol(p.ctype) - 1) * MB;
-    const uint64_t hc = A.hconn[h];
     int l[k];
-#pragma unroll
-    for (int a = 0; a < k; ++a) l[a] = static_cast<int>((hc >> (16 * a)) & 0xffff);
+    halo_nodes<k>(A, p.pl.hc8, h, l);
     double det;
     double kp[Cn::np];
     auto coef_w = [&](double wsum_) -> double {
@@ -710,10 +721,8 @@ __device__ __forceinline__ void elast_element(const FastElastArgs& p, const RecA
     using Cf = FastElastCfg<KIND, LT, FT>;
     constexpr int k = Cf::k, d = Cf::d;
     const int MH = p.MH, MB = p.MB;
-    const uint64_t hc = A.hconn[h];
     int l[k];
-#pragma unroll
-    for (int a = 0; a < k; ++a) l[a] = static_cast<int>((hc >> (16 * a)) & 0xffff);
+    halo_nodes<k>(A, p.pl.hc8, h, l);
     double g[k][d], det;
     if constexpr (KIND == TGK_TET4) {
         const double x0 = xs[l[0]], y0 = xs[MB + l[0]], z0 = xs[2 * MB + l[0]];

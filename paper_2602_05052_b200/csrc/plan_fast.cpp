@@ -320,6 +320,10 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
     };
     auto al16 = [](size_t x) { return (x + 15) & ~size_t(15); };
     const int64_t nb = P.n_blocks;
+    // block-local connectivity bytes per halo element: 4 x u8 when every block's
+    // node table fits 255 entries (halves the largest part of record A)
+    const int hc8 = P.max_bnodes <= 255 ? 1 : 0;
+    const size_t hcb = hc8 ? 4 : 8;
     std::vector<int64_t> a_off(nb + 1, 0), b_off(nb + 1, 0);
     std::vector<std::vector<unsigned char>> recb(nb);
     int max_a = 0, max_b = 0, max_tile = 0, max_len = 0;
@@ -327,7 +331,7 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
     for (int64_t b = 0; b < nb; ++b) {
         const size_t nr = size_t(P.row_off[b + 1] - P.row_off[b]), nh = size_t(P.halo_off[b + 1] - P.halo_off[b]),
                      nbn = size_t(P.bnode_off[b + 1] - P.bnode_off[b]);
-        const size_t sa = 32 + al16(8 * nr) + al16(4 * nr) + al16(2 * (nr + 1)) + al16(4 * nbn) + al16(8 * nh);
+        const size_t sa = 32 + al16(8 * nr) + al16(4 * nr) + al16(2 * (nr + 1)) + al16(4 * nbn) + al16(hcb * nh);
         a_off[b + 1] = a_off[b] + int64_t(sa);
         max_a = std::max<int>(max_a, int(sa));
         // record B: header, descriptors, warp-group word offsets, words
@@ -400,7 +404,16 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
         o += al16(2 * size_t(nr + 1));
         std::memcpy(pa + o, P.bnodes.data() + n0, 4 * size_t(nbn));
         o += al16(4 * size_t(nbn));
-        std::memcpy(pa + o, P.hconn.data() + h0, 8 * size_t(nh));
+        if (hc8) {
+            for (uint32_t i = 0; i < nh; ++i) {
+                const uint64_t hc = P.hconn[h0 + i];
+                const uint32_t c8 = uint32_t(hc & 0xff) | uint32_t((hc >> 16) & 0xff) << 8 |
+                                    uint32_t((hc >> 32) & 0xff) << 16 | uint32_t((hc >> 48) & 0xff) << 24;
+                std::memcpy(pa + o + 4 * size_t(i), &c8, 4);
+            }
+        } else {
+            std::memcpy(pa + o, P.hconn.data() + h0, 8 * size_t(nh));
+        }
         std::memcpy(rb.data() + b_off[b], recb[b].data(), recb[b].size());
     }
     recb.clear();
@@ -441,6 +454,7 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
     D.max_len = max_len;
     D.max_rec_a = max_a;
     D.max_rec_b = max_b;
+    D.hc8 = hc8;
     D.n_halo = static_cast<int64_t>(P.helem.size());
     D.n_items = static_cast<int64_t>(P.items.size());
     D.n_words = n_words;

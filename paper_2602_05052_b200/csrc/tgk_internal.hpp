@@ -219,6 +219,7 @@ struct FastPlanDev {
     int64_t n_blocks = 0;
     int max_halo = 0, max_bnodes = 0, max_rows = 0, max_tile = 0, max_len = 0;
     int max_rec_a = 0, max_rec_b = 0;  // bytes
+    int hc8 = 0;                       // block-local connectivity as 4 x u8 (every node table <= 255), else 4 x u16
     int64_t n_halo = 0, n_items = 0, n_words = 0, n_entries = 0;
     int64_t row_lo = -1, row_hi = -1, elem_lo = -1, elem_hi = -1;  // the ranges it was built for
     const int64_t *rec_a_off = nullptr, *rec_b_off = nullptr;       // n_blocks+1 byte offsets
