@@ -711,7 +711,8 @@ struct FastElastCfg {
     static size_t smem(const FastElastArgs& a) {
         return 64 + 2 * size_t(a.abuf) + size_t(a.bbuf) +
                sizeof(double) * (size_t(d) * a.MB + size_t(NR) * a.MH + size_t(d) * d * a.pl.max_tile) +
-               sizeof(int64_t) * a.pl.max_rows + sizeof(uint16_t) * (a.pl.max_rows + 1);
+               sizeof(int64_t) * a.pl.max_rows + sizeof(uint16_t) * (a.pl.max_rows + 1) +
+               ((size_t(a.pl.max_rows) + 15) & ~size_t(15));
     }
 };
 
@@ -800,7 +801,7 @@ __device__ __forceinline__ void elast_element(const FastElastArgs& p, const RecA
 // diagonal entry, the row's d load values) folded over its elements.
 template <int KIND, int LT, int FT>
 __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& A, const RecB& Bq, const double* kv,
-                                            double* tk, int w, int lane) {
+                                            double* tk, uint8_t* tdiag, int w, int lane) {
     using Cf = FastElastCfg<KIND, LT, FT>;
     constexpr int k = Cf::k, d = Cf::d, NF = FT == 2 ? Cf::d : 1;
     const int MH = p.MH;
@@ -857,28 +858,37 @@ __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& 
         }
     };
     // padding items address the +0.0 slot (h = max_halo, a = b = 0)
-    for (int st = 0; st < steps; ++st) {
-        const uint32_t wv = ip[st * 32];
-        eat(wv & 0xffffu);
-        eat(wv >> 16);
-    }
-    if (diag) {  // split diagonal lists: partial sums of kFastDiagSplit lanes
-        constexpr int DS = kFastDiagSplit(k);
+    if (!diag) {
+        for (int st = 0; st < steps; ++st) {
+            const uint32_t wv = ip[st * 32];
+            eat(wv & 0xffffu);
+            eat(wv >> 16);
+        }
+    } else if constexpr (FT > 0) {  // diagonal entries fold only the load: the diagonal
+        auto eat_f = [&](uint32_t it) {  // block comes from the zero row sums (copy-out)
+            const int h = static_cast<int>(it & 0xfffu);
+            if constexpr (FT == 1) fac[0] += kv[Cf::CROW * MH + h];
+            if constexpr (FT == 2) {
+#pragma unroll
+                for (int r = 0; r < d; ++r) fac[r] += kv[(Cf::FROW + r) * MH + h];
+            }
+        };
+        for (int st = 0; st < steps; ++st) {
+            const uint32_t wv = ip[st * 32];
+            eat_f(wv & 0xffffu);
+            eat_f(wv >> 16);
+        }
+        constexpr int DS = kFastDiagSplit(k);  // split diagonal lists: partial sums of DS lanes
 #pragma unroll
         for (int o = 1; o < DS; o <<= 1) {
 #pragma unroll
-            for (int r = 0; r < d; ++r)
-#pragma unroll
-                for (int s = 0; s < d; ++s) acc[r][s] += __shfl_xor_sync(0xffffffffu, acc[r][s], o);
-            if constexpr (FT > 0) {
-#pragma unroll
-                for (int r = 0; r < NF; ++r) fac[r] += __shfl_xor_sync(0xffffffffu, fac[r], o);
-            }
+            for (int r = 0; r < NF; ++r) fac[r] += __shfl_xor_sync(0xffffffffu, fac[r], o);
         }
     }
     if (desc >= kFastPart) return;
     const int lr = static_cast<int>(desc & 0x1ffu), pos = static_cast<int>((desc >> 9) & 63u);
-    if (pos != kFastNoPos) {
+    if (diag) tdiag[lr] = static_cast<uint8_t>(pos);  // K_ii block formed at the copy-out
+    if (!diag && pos != kFastNoPos) {
         const int L = A.toff[lr + 1] - A.toff[lr];
         double* t = tk + d * d * A.toff[lr] + d * pos;
 #pragma unroll
@@ -923,6 +933,7 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p)
     double* const tk = kv + size_t(Cf::NR) * MH;
     int64_t* const trp = reinterpret_cast<int64_t*>(tk + size_t(d) * d * pl.max_tile);
     uint16_t* const ttoff = reinterpret_cast<uint16_t*>(trp + pl.max_rows);
+    uint8_t* const tdiag = reinterpret_cast<uint8_t*>(ttoff + pl.max_rows + 1);  // rows' diagonal position
     auto ra = [&](int64_t it) { return ra_base + size_t(it & 1) * p.abuf; };
     auto xsp = [&](int64_t) { return xs_base; };  // single node table (phase A is its only reader)
     const int64_t nb = pl.n_blocks, G = gridDim.x, b0 = blockIdx.x;
@@ -956,11 +967,30 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p)
         cp_async_commit();
     };
     int tile_rows = 0;
-    auto copy_out = [&]() {  // scalar row i's d rows are one contiguous d^2 L run of the vector CSR
+    // scalar row i's d rows are one contiguous d^2 L run of the vector CSR
+    // ([r][p][s]); its diagonal block K_ii[r][s] = 0 - sum over p != diagonal of
+    // block p (zero row sums: rigid translations are in every element
+    // stiffness's kernel), lane j sums (r, s) = j % d^2 over p = j / d^2, j / d^2
+    // + 32 / d^2, ..., the parts combined in a fixed order (deterministic)
+    auto copy_out = [&]() {
         if (p.debug & 4) return;
+        constexpr int DD = d * d, NP = 32 / DD;
+        const int rs = lane % DD, part = lane / DD;
         for (int lr = warp; lr < tile_rows; lr += nwarp) {
-            const int64_t rp = trp[lr] * (d * d);
-            const int t0 = ttoff[lr] * (d * d), len = (ttoff[lr + 1] - ttoff[lr]) * (d * d);
+            const int64_t rp = trp[lr] * DD;
+            const int L = ttoff[lr + 1] - ttoff[lr], t0 = ttoff[lr] * DD, len = L * DD;
+            const int pd = tdiag[lr];
+            if (pd < L) {  // warp-uniform
+                double sacc = 0.0;
+                if (part < NP)
+                    for (int q = part; q < L; q += NP)
+                        if (q != pd) sacc += tk[t0 + (rs / d) * d * L + d * q + rs % d];
+                double tot = sacc;
+#pragma unroll
+                for (int o = 1; o < NP; ++o) tot += __shfl_down_sync(0xffffffffu, sacc, o * DD);
+                if (part == 0) tk[t0 + (rs / d) * d * L + d * pd + rs % d] = 0.0 - tot;
+                __syncwarp();
+            }
             for (int q = lane; q < len; q += 32) p.K[rp + q] = tk[t0 + q];
         }
     };
@@ -991,7 +1021,7 @@ __global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p)
         }
         tile_rows = int(A.nr);
         const int nwg = (p.debug & 2) ? 0 : int(Bq.nwg);
-        for (int w = warp; w < nwg; w += nwarp) elast_group<KIND, LT, FT>(p, A, Bq, kv, tk, w, lane);
+        for (int w = warp; w < nwg; w += nwarp) elast_group<KIND, LT, FT>(p, A, Bq, kv, tk, tdiag, w, lane);
         cp_async_wait_all();
         __syncthreads();
         if (tid == 0) {
