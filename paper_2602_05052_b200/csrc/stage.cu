@@ -359,12 +359,36 @@ __global__ void k_evaluate(const int32_t* conn, int64_t E, int type, double valu
 }
 
 // reduce_matrix / reduce_vector (routing.cpp:92-99, 117-124)
-__global__ void k_segment_reduce(const uint32_t* off, const uint32_t* slots, int64_t n,
-                                 const double* local, double* out) {
+// (left fold from +0.0 in ascending slot order; the gathers of up to four
+// contributions are issued before their adds, so each thread keeps four
+// independent loads in flight instead of a dependent chain.  Staging a
+// block's whole slot range in shared memory first measured slower: 44.0 vs
+// 39.7 us on the RM workload.)
+constexpr int kSegThreads = 256;
+__global__ void k_segment_reduce(const uint32_t* __restrict__ off, const uint32_t* __restrict__ slots, int64_t n,
+                                 const double* __restrict__ local, double* __restrict__ out) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= n) return;
+    const uint32_t u1 = __ldg(off + t + 1);
+    uint32_t u = __ldg(off + t);
     double s = 0.0;
-    for (uint32_t u = off[t]; u < off[t + 1]; ++u) s += local[slots[u]];
+    for (; u + 4 <= u1; u += 4) {
+        const uint32_t a0 = __ldg(slots + u), a1 = __ldg(slots + u + 1), a2 = __ldg(slots + u + 2),
+                       a3 = __ldg(slots + u + 3);
+        const double v0 = __ldg(local + a0), v1 = __ldg(local + a1), v2 = __ldg(local + a2), v3 = __ldg(local + a3);
+        s += v0;
+        s += v1;
+        s += v2;
+        s += v3;
+    }
+    if (u + 2 <= u1) {
+        const uint32_t a0 = __ldg(slots + u), a1 = __ldg(slots + u + 1);
+        const double v0 = __ldg(local + a0), v1 = __ldg(local + a1);
+        s += v0;
+        s += v1;
+        u += 2;
+    }
+    if (u < u1) s += __ldg(local + __ldg(slots + u));
     out[t] = s;
 }
 
@@ -617,7 +641,7 @@ int tgk_reduce_matrix_d(const tgk_routing* r, const double* local, double* value
     if (!r || !r->mat_offsets)
         return set_error(TGK_ERR_INPUT, "reduce_matrix: routing built without TGK_ROUTING_SEGMENTS");
     TGK_TRY(ensure_device());
-    k_segment_reduce<<<grid_for(r->nnz, 256), 256, 0, as_stream(stream)>>>(
+    k_segment_reduce<<<grid_for(r->nnz, kSegThreads), kSegThreads, 0, as_stream(stream)>>>(
         r->mat_offsets, r->mat_slots, r->nnz, local, values);
     KERNEL_CHECK("reduce_matrix");
     return TGK_OK;
@@ -628,8 +652,8 @@ int tgk_reduce_vector_d(const tgk_routing* r, const double* local, double* F, vo
     if (!r || !r->vec_offsets)
         return set_error(TGK_ERR_INPUT, "reduce_vector: routing built without TGK_ROUTING_SEGMENTS");
     TGK_TRY(ensure_device());
-    k_segment_reduce<<<grid_for(r->N, 256), 256, 0, as_stream(stream)>>>(r->vec_offsets, r->vec_slots,
-                                                                         r->N, local, F);
+    k_segment_reduce<<<grid_for(r->N, kSegThreads), kSegThreads, 0, as_stream(stream)>>>(r->vec_offsets, r->vec_slots,
+                                                                                       r->N, local, F);
     KERNEL_CHECK("reduce_vector");
     return TGK_OK;
 }
