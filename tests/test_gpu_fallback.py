@@ -189,3 +189,19 @@ def test_scatter_add_oracle_independent_vs_reference(eng, kind, mesh):
     tm = tgfem.Mesh(kind, nodes, elems)
     d = tgfem.scatter_add_oracle(tm, lk)
     assert_bitwise(d["values"], vals, "tgfem.scatter_add_oracle")
+
+
+def test_fast_elasticity_long_rows(eng):
+    """Fast-mode elasticity on a bicone whose hub rows have 49 entries (copy-out
+    runs of 9 x 49 values, diagonal blocks from the zero row sums over 48
+    off-diagonal blocks) vs the oracle within the SURVEY.md 8(c) tolerance."""
+    nodes, elems = bicone_tet(48)
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    rv = eng.Routing(m, 3)
+    pr = port.Routing(nodes.shape[0] * 3, port.dofmap("tet4", elems, 3))
+    lam, mu = 0.5769230769230769, 0.38461538461538464
+    K, F, _ = eng.assemble(m, rv, kind="elasticity", lam=lam, mu=mu, sources=[1.0, -1.0, 0.5], mode="fast")
+    Kr, Fr, _ = port.assemble("tet4", nodes, elems, pr, problem="elasticity", lam=lam, mu=mu,
+                              sources=[1.0, -1.0, 0.5])
+    assert_scaled_close(np_(K), Kr, what="K")
+    assert_scaled_close(np_(F), Fr, what="F")
