@@ -333,6 +333,8 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
     const int steps = static_cast<int>((Bq.wgoff[w + 1] - i0) >> 5);  // 32 words per step
     const uint32_t* ip = Bq.words + i0 + lane;
     const bool diag = (__shfl_sync(0xffffffffu, desc, 0) >> 15) & 1u;  // warp-uniform class
+    // the load from the det fold S_i when the source is constant and S is folded anyway
+    const bool fs_det = FT == 1 && HAS_M && p.stype == TGK_FIELD_CONSTANT;
     double k0 = 0.0, k1 = 0.0, k2 = 0.0, k3 = 0.0, s0 = 0.0, s1 = 0.0, f0 = 0.0, f1 = 0.0;
     // u16 items h | q << 12: K_ab at row q, S at SROW, F at FROW (+ a = q for a
     // nodal load on a diagonal); padding items address the +0.0 slot
@@ -347,7 +349,7 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
         }
         if constexpr (Cf::HAS_S) ss += kv[Cf::SROW * MH + h];
         if constexpr (FT == 1) {
-            if (diag) ff += kv[Cf::FROW * MH + h];
+            if (diag && !fs_det) ff += kv[Cf::FROW * MH + h];
         }
         if constexpr (FT == 2) {
             if (diag) ff += kv[(Cf::FROW + q) * MH + h];
@@ -400,7 +402,8 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
         if constexpr (HAS_M) tm[at] = sacc * mh;
     }
     if constexpr (FT > 0) {
-        if (diag) p.F[A.srow[lr]] = FT == 1 ? facc * Cn::wa : facc;
+        // constant source with the unit mass: F_i = sum_e f wa det_e = (f wa) S_i (S = the det fold)
+        if (diag) p.F[A.srow[lr]] = FT == 1 ? (fs_det ? (p.sval * Cn::wa) * sacc : facc * Cn::wa) : facc;
     }
     if (desc >> 31) {
         const int lr2 = static_cast<int>((desc >> 16) & 0x1ffu), pos2 = static_cast<int>((desc >> 25) & 63u);
