@@ -278,7 +278,7 @@ def e2e_pipelined(ctx, N, L, engine, kind, nodes, elems, p, with_mass, h_nodes, 
             j = i & 1
             b = bufs[j]
             s_up.wait_event(ev_cmp[j])  # step i-2's assembly no longer reads mesh j
-            N.check(L.tgk_mesh_upload(meshes[j]._h, ptr(h_nodes), ptr(h_elems), C.c_void_p(s_up.cuda_stream)))
+            N.check(L.tgk_mesh_upload_async(meshes[j]._h, ptr(h_nodes), ptr(h_elems), C.c_void_p(s_up.cuda_stream)))
             ev_up[j].record(s_up)
             s_cmp.wait_event(ev_up[j])
             s_cmp.wait_event(ev_dn[j])  # step i-2's download of buffer set j is done
@@ -304,6 +304,8 @@ def e2e_pipelined(ctx, N, L, engine, kind, nodes, elems, p, with_mass, h_nodes, 
         for i in range(steps):
             step(i)
         torch.cuda.synchronize()
+        for m in meshes:  # the uploads' range checks (accumulated on the device), inside the timed region
+            N.check(L.tgk_mesh_upload_check(m._h))
         dt = (time.perf_counter() - w0) / steps
         if any(int(b["bad"].item()) != -1 for b in bufs):
             return None
@@ -629,10 +631,12 @@ def run_scalar(args, ctx, N):
             if pipe is not None:
                 e2e["sync_drop_in"] = {"value": e2e["value"], "ms_per_step": e2e["ms_per_step"], "path": path}
                 e2e.update(value=total_E / pipe, ms_per_step=pipe * 1e3,
-                           path="repeated assembly through the public async API: per step tgk_mesh_upload (pinned H2D "
-                                "of nodes + int64 connectivity) -> tgk_assemble_async_d -> D2H of K(, M), F into "
-                                "pinned host buffers; two device buffer sets on three streams so step i's D2H "
-                                "overlaps step i+1's H2D and compute (sync_drop_in: the blocking tgk_assemble)")
+                           path="repeated assembly through the public async API: per step tgk_mesh_upload_async "
+                                "(pinned H2D of nodes + int64 connectivity, narrowed and range-checked on the "
+                                "device) -> tgk_assemble_async_d -> D2H of K(, M), F into pinned host buffers; two "
+                                "device buffer sets on three streams so step i's D2H overlaps step i+1's H2D and "
+                                "compute; the range checks read back once after the steps (tgk_mesh_upload_check) "
+                                "inside the timed region (sync_drop_in: the blocking tgk_assemble)")
 
     # roofline of the fused kernel (per launch, kernel-only events)
     Nn = own_rows[1] - own_rows[0]
@@ -993,7 +997,7 @@ def main():
                     help="f32: the fp32 variant of the fused scalar kernel (tgk_assemble_f32_d)")
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"],
                     help="fp64 arithmetic mode of the scalar workloads (TGK_MODE_FAST / TGK_MODE_EXACT)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample", type=int, nargs="*", default=None)
     args = ap.parse_args()

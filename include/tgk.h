@@ -158,6 +158,16 @@ int tgk_mesh_create_d(int kind, const double* d_nodes, int64_t n_nodes, const in
  * connectivity that DIFFERS from the current one marks every routing built
  * from this mesh stale: they then fail with status 2 until rebuilt. */
 int tgk_mesh_upload(tgk_mesh* m, const double* nodes, const int64_t* elems, void* stream);
+/* Stream-ordered tgk_mesh_upload for pipelined host-to-host loops: no host
+ * synchronisation inside.  The connectivity's range check (mesh.cpp:61-64) and
+ * change detection run on the device and accumulate until
+ * tgk_mesh_upload_check(), which waits for the device, reports an out-of-range
+ * node id (status 2) and marks the mesh's routings stale if the connectivity
+ * changed.  Until then, out-of-range ids are stored as node 0 (memory-safe)
+ * and assemblies on a mesh whose connectivity changed use the routings and
+ * plans of the previous connectivity. */
+int tgk_mesh_upload_async(tgk_mesh* m, const double* nodes, const int64_t* elems, void* stream);
+int tgk_mesh_upload_check(tgk_mesh* m);
 /* Coordinates of a wrapped (tgk_mesh_create_d) mesh were changed in place. */
 int tgk_mesh_coordinates_changed(tgk_mesh* m);
 void tgk_mesh_destroy(tgk_mesh* m);

@@ -107,6 +107,8 @@ _SIGS = {
     "tgk_free_d": (_I, [_P]),
     "tgk_copy_d2h": (_I, [_P, _P, _I64]),
     "tgk_copy_h2d": (_I, [_P, _P, _I64]),
+    "tgk_mesh_upload_async": (_I, [_P, _P, _P, _P]),
+    "tgk_mesh_upload_check": (_I, [_P]),
     "tgk_routing_create_host": (_I, [_P, _I, _I64, _I64, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "tgk_routing_plan_stats": (_I, [_P, _I, _P, _P, _P, _P]),
     "tgk_routing_fast_plan_info": (_I, [_P, _P, _P, _P, _P, _P, _P]),

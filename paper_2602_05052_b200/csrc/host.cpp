@@ -150,6 +150,9 @@ static double centroid_det(int kind, const double* nodes, const int64_t* conn) {
            J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
 }
 
+int narrow_connectivity_async(tgk_mesh* m, const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst,
+                              cudaStream_t st);
+int mesh_async_flags(tgk_mesh* m, int64_t* bad, bool* changed);
 int narrow_connectivity(tgk_mesh* m, const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst, int64_t* bad,
                         cudaStream_t st);
 int fused_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* r, double* K,
@@ -447,6 +450,38 @@ int tgk_mesh_upload(tgk_mesh* m, const double* nodes, const int64_t* elems, void
     } else {
         HCUDA(cudaStreamSynchronize(st));
     }
+    return TGK_OK;
+}
+
+// Stream-ordered variant for pipelined callers: no host synchronisation; the
+// connectivity range check and change detection accumulate on the device
+// until tgk_mesh_upload_check.
+int tgk_mesh_upload_async(tgk_mesh* m, const double* nodes, const int64_t* elems, void* stream) {
+    if (!m) return set_error(TGK_ERR_INPUT, "null mesh");
+    if (!m->owned) return set_error(TGK_ERR_INPUT, "tgk_mesh_upload_async: wrapped (tgk_mesh_create_d) mesh");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (nodes) {
+        HCUDA(cudaMemcpyAsync(m->nodes, nodes, sizeof(double) * m->N * m->d, cudaMemcpyHostToDevice, st));
+        m->div_safe = -1;
+    }
+    if (elems) {
+        const int64_t n = m->E * m->k;
+        if (!m->staging) HCUDA(cudaMalloc(&m->staging, sizeof(int64_t) * std::max<int64_t>(1, n)));
+        HCUDA(cudaMemcpyAsync(m->staging, elems, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+        TGK_TRY(narrow_connectivity_async(m, m->staging, n, m->N, m->conn, st));
+    }
+    return TGK_OK;
+}
+
+int tgk_mesh_upload_check(tgk_mesh* m) {
+    if (!m) return set_error(TGK_ERR_INPUT, "null mesh");
+    int64_t bad = -1;
+    bool changed = false;
+    TGK_TRY(mesh_async_flags(m, &bad, &changed));
+    if (changed) ++m->conn_version;  // routings built before refuse to assemble (check_routing_fresh)
+    if (bad >= 0)
+        return set_error(TGK_ERR_INPUT, "element " + std::to_string(bad / m->k) + " references a node outside [0," +
+                                            std::to_string(m->N) + ")");
     return TGK_OK;
 }
 

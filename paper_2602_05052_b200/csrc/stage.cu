@@ -475,9 +475,11 @@ __global__ void k_narrow(const int64_t* src, int64_t n, int64_t n_nodes, int32_t
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = src[i];
-        if (v < 0 || v >= n_nodes) atomicMin(bad, static_cast<unsigned long long>(i));
-        diff = diff || dst[i] != static_cast<int32_t>(v);
-        dst[i] = static_cast<int32_t>(v);
+        const bool out = v < 0 || v >= n_nodes;
+        if (out) atomicMin(bad, static_cast<unsigned long long>(i));
+        const int32_t w = out ? 0 : static_cast<int32_t>(v);  // never an out-of-range node id on the device
+        diff = diff || dst[i] != w;
+        dst[i] = w;
     }
     if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) atomicOr(changed, 1ull);
 }
@@ -517,9 +519,40 @@ __global__ void k_coord_range(const double* x, int64_t n, unsigned* bad) {
 }
 
 // Persistent per-mesh flag words (device + pinned host), allocated on first use.
+// [0] coordinate certification, [1] / [2] first bad entry / changed of the
+// blocking upload, [3] / [4] the same accumulated by asynchronous uploads
+// until tgk_mesh_upload_check
 int mesh_flags(tgk_mesh* m) {
-    if (!m->d_flags) CUDA_TRY(cudaMalloc(&m->d_flags, 3 * sizeof(unsigned long long)));
-    if (!m->h_flags) CUDA_TRY(cudaMallocHost(&m->h_flags, 3 * sizeof(unsigned long long)));
+    if (!m->d_flags) {
+        CUDA_TRY(cudaMalloc(&m->d_flags, 5 * sizeof(unsigned long long)));
+        const unsigned long long init[5] = {0, ULLONG_MAX, 0, ULLONG_MAX, 0};
+        CUDA_TRY(cudaMemcpy(m->d_flags, init, sizeof init, cudaMemcpyHostToDevice));
+    }
+    if (!m->h_flags) CUDA_TRY(cudaMallocHost(&m->h_flags, 5 * sizeof(unsigned long long)));
+    return TGK_OK;
+}
+
+int narrow_connectivity_async(tgk_mesh* m, const int64_t* src, int64_t n, int64_t n_nodes, int32_t* dst,
+                              cudaStream_t st) {
+    TGK_TRY(mesh_flags(m));
+    k_narrow<<<std::min<unsigned>(grid_for(n, 256), 148 * 16), 256, 0, st>>>(src, n, n_nodes, dst, m->d_flags + 3,
+                                                                           m->d_flags + 4);
+    KERNEL_CHECK("narrow_connectivity");
+    return TGK_OK;
+}
+
+// Waits for the device, reads and resets the asynchronous upload flags.
+int mesh_async_flags(tgk_mesh* m, int64_t* bad, bool* changed) {
+    *bad = -1;
+    *changed = false;
+    if (!m->d_flags) return TGK_OK;
+    CUDA_TRY(cudaDeviceSynchronize());
+    unsigned long long h[2] = {ULLONG_MAX, 0};
+    CUDA_TRY(cudaMemcpy(h, m->d_flags + 3, sizeof h, cudaMemcpyDeviceToHost));
+    const unsigned long long init[2] = {ULLONG_MAX, 0};
+    CUDA_TRY(cudaMemcpy(m->d_flags + 3, init, sizeof init, cudaMemcpyHostToDevice));
+    *bad = h[0] == ULLONG_MAX ? -1 : static_cast<int64_t>(h[0]);
+    *changed = h[1] != 0;
     return TGK_OK;
 }
 

@@ -205,3 +205,36 @@ def test_fast_elasticity_long_rows(eng):
                               sources=[1.0, -1.0, 0.5])
     assert_scaled_close(np_(K), Kr, what="K")
     assert_scaled_close(np_(F), Fr, what="F")
+
+
+def test_async_upload_checks(eng):
+    """tgk_mesh_upload_async (the pipelined e2e path): identical connectivity
+    passes tgk_mesh_upload_check and assembles like the oracle; an out-of-range
+    node id is reported by the check (status 2) and never reaches the kernels;
+    changed connectivity marks the routings stale at the check."""
+    from paper_2602_05052_b200 import InputError
+    from paper_2602_05052_b200 import _native as N
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [3, 3, 3])
+    m = eng.DeviceMesh("tet4", nodes, elems)
+    r = eng.Routing(m, 1)
+    L = N.lib()
+    n64 = np.ascontiguousarray(nodes * 1.5)
+    e64 = np.ascontiguousarray(elems, dtype=np.int64)
+    N.check(L.tgk_mesh_upload_async(m._h, n64.ctypes.data, e64.ctypes.data, None))
+    K, F, _ = eng.assemble(m, r, sources=[1.0], mode="fast")
+    N.check(L.tgk_mesh_upload_check(m._h))
+    pr = port.Routing(nodes.shape[0], port.dofmap("tet4", elems, 1))
+    Kr, Fr, _ = port.assemble("tet4", n64, elems, pr, sources=[1.0])
+    assert_scaled_close(np_(K), Kr, what="K after async upload")
+    bad = e64.copy()
+    bad[7, 2] = nodes.shape[0] + 5
+    N.check(L.tgk_mesh_upload_async(m._h, None, bad.ctypes.data, None))
+    with pytest.raises(InputError, match="element 7 references a node outside"):
+        N.check(L.tgk_mesh_upload_check(m._h))
+    N.check(L.tgk_mesh_upload(m._h, None, e64.ctypes.data, None))  # restore (blocking path)
+    e2 = e64.copy()
+    e2[[0, 1]] = e2[[1, 0]]
+    N.check(L.tgk_mesh_upload_async(m._h, None, e2.ctypes.data, None))
+    N.check(L.tgk_mesh_upload_check(m._h))
+    with pytest.raises(InputError, match="earlier connectivity"):
+        eng.assemble(m, r, sources=[1.0])
