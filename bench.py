@@ -542,14 +542,18 @@ def run_scalar(args, ctx, N):
         raise SystemExit(f"element {bad.item()} has non-positive Jacobian determinant")
     with ClockSampler(ctx.local_rank) as clocks:
         ms = ctx.timed(step, args.steps)
-        # kernel-only duration (roofline): event pair around the fused launches alone
-        ctx.barrier()
-        ev_k0.record(ctx.stream)
-        for _ in range(args.steps):
-            kernel()
-        ev_k1.record(ctx.stream)
-        torch.cuda.synchronize()
-    ms_kernel = ev_k0.elapsed_time(ev_k1) / args.steps
+        # kernel-only duration (roofline): event pair around the fused launches
+        # alone, median of three passes of `steps` launches
+        trials = []
+        for _ in range(3):
+            ctx.barrier()
+            ev_k0.record(ctx.stream)
+            for _ in range(args.steps):
+                kernel()
+            ev_k1.record(ctx.stream)
+            torch.cuda.synchronize()
+            trials.append(ev_k0.elapsed_time(ev_k1) / args.steps)
+    ms_kernel = sorted(trials)[1]
     ms_per_step = ms / args.steps
     other = None  # the other fp64 mode's kernel time on the same inputs (both modes reported)
     if not f32:
