@@ -145,9 +145,20 @@ def test_c4_all_256_fields(eng):
 
 
 @pytest.mark.slow
-def test_c5_eight_slabs_halo_match_single_gpu(eng):
+def _close_dev(a, b, what):
+    """SURVEY.md 8(c) scaled tolerance, evaluated on the device (C5 sizes)."""
+    scale = b.abs().max()
+    bad = (a - b).abs() > 1e-12 * b.abs() + 1e-14 * scale
+    assert not bool(bad.any()), f"{what}: {int(bad.sum())} entries outside the tolerance"
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_c5_eight_slabs_halo_match_single_gpu(eng, mode):
     """C5: the 256^3 Kuhn grid (100.7M tets) as 8 z-slabs in halo mode, each rank
-    run in turn on one GPU; every owned row bit-equal to the single-GPU assembly."""
+    run in turn on one GPU; every owned row bit-equal to the single-GPU assembly
+    (exact mode), or within the SURVEY.md 8(c) tolerance of it (fast mode: the
+    slab's row blocks differ from the full mesh's), whose fast values are in
+    turn within the tolerance of the exact (reference-identical) ones."""
     from paper_2602_05052_b200 import _native as N
     from paper_2602_05052_b200 import dist as D
     n, world = 256, 8
@@ -155,7 +166,12 @@ def test_c5_eight_slabs_halo_match_single_gpu(eng):
     m = eng.DeviceMesh("tet4", nodes, elems)
     del nodes, elems
     r = eng.Routing(m, 1)
-    K1, F1, _ = eng.assemble(m, r, sources=[1.0])
+    K1, F1, _ = eng.assemble(m, r, sources=[1.0], mode=mode)
+    if mode == "fast":
+        Kx, Fx, _ = eng.assemble(m, r, sources=[1.0], mode="exact")
+        _close_dev(K1, Kx, "single-GPU fast vs exact K")
+        _close_dev(F1, Fx, "single-GPU fast vs exact F")
+        del Kx, Fx
     rp1 = torch.from_numpy(r.host_arrays(slot_of=False, segments=False)["offsets"])
     del r, m
     for rank in range(world):
@@ -164,12 +180,16 @@ def test_c5_eight_slabs_halo_match_single_gpu(eng):
         ms = eng.DeviceMesh("tet4", sn, se)
         rs = eng.Routing(ms, 1)
         N.check(N.lib().tgk_routing_set_owned_rows(rs._h, s.own_lo, s.calc_hi))
-        K, F, _ = eng.assemble(ms, rs, sources=[1.0])
+        K, F, _ = eng.assemble(ms, rs, sources=[1.0], mode=mode)
         rp = rs.host_arrays(slot_of=False, segments=False)["offsets"]
         g0, g1 = s.node_offset + s.own_lo, s.node_offset + s.own_hi
         a, b = int(rp[s.own_lo]), int(rp[s.own_hi])
         ga, gb = int(rp1[g0]), int(rp1[g1])
         assert b - a == gb - ga
-        assert torch.equal(K[a:b].view(torch.int64), K1[ga:gb].view(torch.int64)), f"rank {rank} K"
-        assert torch.equal(F[s.own_lo:s.own_hi].view(torch.int64), F1[g0:g1].view(torch.int64)), f"rank {rank} F"
+        if mode == "exact":
+            assert torch.equal(K[a:b].view(torch.int64), K1[ga:gb].view(torch.int64)), f"rank {rank} K"
+            assert torch.equal(F[s.own_lo:s.own_hi].view(torch.int64), F1[g0:g1].view(torch.int64)), f"rank {rank} F"
+        else:
+            _close_dev(K[a:b], K1[ga:gb], f"rank {rank} K")
+            _close_dev(F[s.own_lo:s.own_hi], F1[g0:g1], f"rank {rank} F")
         del K, F, rs, ms
