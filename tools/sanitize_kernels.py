@@ -2,7 +2,8 @@
 
     compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_kernels.py
 
-k_fast_scalar (K16 / KS32 / S16 formats, nodal load), k_fused_scalar (R = 64,
+k_fast_scalar (K16 / KS32 / S16 formats, nodal load), k_fast_elast (constant
+and per-element fields), k_fused_scalar (R = 64,
 128, 256), k_fused_elast2, k_batched_entries, k_adjoint_groups, the
 materialised Stage I/II drop-ins; each result is checked against the oracle
 so a silent corruption under the tool also fails."""
@@ -66,6 +67,14 @@ def main():
                               mu=0.38461538461538464, sources=[1.0, 1.0, 1.0])
     close(K, Kr, "elasticity K")
     close(F, Fr, "elasticity F")
+    print("k_fast_elast", flush=True)
+    lam_e = 0.3 + np.random.default_rng(5).random(E)
+    for kw in [dict(lam=0.5769230769230769, mu=0.38461538461538464, sources=[1.0, 1.0, 1.0]),
+               dict(lam=("element", lam_e), mu=("element", rho), sources=[("element", rho), 1.0, 0.5])]:
+        K, F, _ = engine.assemble(m, rv, kind="elasticity", mode="fast", **kw)
+        Kr, Fr, _ = port.assemble("tet4", nodes, elems, prv, problem="elasticity", **kw)
+        close(K, Kr, f"fast elasticity {'element' if isinstance(kw['lam'], tuple) else 'const'} K", exact=False)
+        close(F, Fr, "  F", exact=False)
     print("k_batched_entries / k_adjoint_groups", flush=True)
     tn, te = meshgen.unstructured_tri(24)
     tm = engine.DeviceMesh("tri3", tn, te)
