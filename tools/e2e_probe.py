@@ -44,6 +44,10 @@ def step(i, mode):
     s_up.wait_event(ev_cmp[j])
     if mode == "abi":
         N.check(L.tgk_mesh_upload(meshes[j]._h, ptr(h_nodes), ptr(h_elems), C.c_void_p(s_up.cuda_stream)))
+    elif mode == "abi_async":
+        N.check(L.tgk_mesh_upload_async(meshes[j]._h, ptr(h_nodes), ptr(h_elems), C.c_void_p(s_up.cuda_stream)))
+    elif mode == "nodes_only":  # connectivity resident: coordinates only (lower bound of the H2D side)
+        N.check(L.tgk_mesh_upload_async(meshes[j]._h, ptr(h_nodes), None, C.c_void_p(s_up.cuda_stream)))
     else:  # async copies + narrowing on the stream, no host sync
         N.check(L.tgk_copy_d2d(C.c_void_p(views[j][0]), ptr(h_nodes), h_nodes.numel() * 8, C.c_void_p(s_up.cuda_stream)))
         with torch.cuda.stream(s_up):
@@ -65,12 +69,32 @@ def step(i, mode):
     ev_dn[j].record(s_dn)
 
 
-for mode in ["abi", "async", "abi"]:
+for mode in ["abi", "async", "abi_async", "nodes_only", "abi_async"]:
     for i in range(4):
         step(i, mode)
     torch.cuda.synchronize()
     w = time.perf_counter()
-    for i in range(10):
+    for i in range(20):
         step(i, mode)
     torch.cuda.synchronize()
-    print(mode, "ms/step %.3f" % ((time.perf_counter() - w) / 10 * 1e3))
+    print(mode, "ms/step %.3f" % ((time.perf_counter() - w) / 20 * 1e3))
+
+# the narrowing kernel alone (tgk_mesh_upload_async with nodes=None, elements resident in pinned memory)
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+st = torch.cuda.current_stream()
+for _ in range(2):
+    N.check(L.tgk_mesh_upload_async(meshes[0]._h, None, ptr(h_elems), C.c_void_p(st.cuda_stream)))
+torch.cuda.synchronize()
+ev0.record(st)
+for _ in range(10):
+    N.check(L.tgk_mesh_upload_async(meshes[0]._h, None, ptr(h_elems), C.c_void_p(st.cuda_stream)))
+ev1.record(st)
+torch.cuda.synchronize()
+print("upload_async(elems) ms %.3f" % (ev0.elapsed_time(ev1) / 10))
+d_elems = torch.from_numpy(elems.reshape(-1)).to(dev)
+ev0.record(st)
+for _ in range(10):
+    h_tmp = d_elems.to(torch.int32)
+ev1.record(st)
+torch.cuda.synchronize()
+print("torch narrow only ms %.3f" % (ev0.elapsed_time(ev1) / 10))
