@@ -220,30 +220,78 @@ __global__ void k_residual(int64_t n, const int64_t* off, const int64_t* cols, c
 }
 
 // p = r + beta (p - omega v); phat = inv_diag p
-__global__ void k_bicg_p(int64_t n, const double* r, const double* v, const double* inv, double beta, double omega,
-                         double* p, double* phat) {
+// BiCGSTAB with device-resident scalars (one host synchronisation per
+// iteration): the scalars live in sc[], the iteration's exit state in *state
+// (0 running, 1 converged at s, 2 breakdown before the iteration counts,
+// 3 omega breakdown, 4 non-finite residual); every kernel after an exit is a
+// no-op, so the host learns the outcome from one read-back at the end.
+enum { S_RHO, S_ALPHA, S_OMEGA, S_BETA, S_RHONEW, S_RTV, S_SS, S_TT, S_TS, S_RR, S_RES, S_SNORM, S_COUNT };
+
+__global__ void k_it_begin(double* sc, int* state, double eps) {  // rho_new, beta (solver.cpp:150-158)
+    if (*state) return;
+    const double rn = sc[S_RHONEW];
+    if (!isfinite(rn) || fabs(rn) < eps) {
+        *state = 2;
+        return;
+    }
+    sc[S_BETA] = (rn / sc[S_RHO]) * (sc[S_ALPHA] / sc[S_OMEGA]);
+    sc[S_RHO] = rn;
+}
+__global__ void k_it_alpha(double* sc, int* state) {
+    if (*state) return;
+    const double alpha = sc[S_RHO] / sc[S_RTV];
+    if (!isfinite(alpha)) *state = 2;
+    else sc[S_ALPHA] = alpha;
+}
+__global__ void k_it_s(double* sc, int* state, double tol) {
+    if (*state) return;
+    const double sn = sqrt(sc[S_SS]);
+    sc[S_SNORM] = sn;
+    if (sn <= tol) *state = 1;
+}
+__global__ void k_it_omega(double* sc, int* state, double eps) {
+    if (*state) return;
+    const double tt = sc[S_TT], omega = sc[S_TS] / tt;
+    if (!isfinite(omega) || tt < eps) *state = 3;
+    else sc[S_OMEGA] = omega;
+}
+__global__ void k_it_end(double* sc, int* state) {
+    if (*state) return;
+    const double res = sqrt(sc[S_RR]);
+    sc[S_RES] = res;
+    if (!isfinite(res)) *state = 4;
+}
+__global__ void k_bicg_p(int64_t n, const double* r, const double* v, const double* inv, const double* sc,
+                         const int* state, double* p, double* phat) {
+    if (*state) return;
+    const double beta = sc[S_BETA], omega = sc[S_OMEGA];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double pi = r[i] + beta * (p[i] - omega * v[i]);
         p[i] = pi;
         phat[i] = inv[i] * pi;
     }
 }
-
-// s = r - alpha v
-__global__ void k_bicg_s(int64_t n, const double* r, const double* v, double alpha, double* s) {
+__global__ void k_bicg_s(int64_t n, const double* r, const double* v, const double* sc, const int* state, double* s) {
+    if (*state) return;
+    const double alpha = sc[S_ALPHA];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         s[i] = r[i] - alpha * v[i];
 }
-
-// y = inv_diag x
-__global__ void k_scale(int64_t n, const double* inv, const double* x, double* y) {
+__global__ void k_scale(int64_t n, const double* inv, const double* x, const int* state, double* y) {
+    if (state && *state) return;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = inv[i] * x[i];
 }
-
-// x += alpha phat (+ omega shat); r = s - omega t
-__global__ void k_bicg_x(int64_t n, double alpha, const double* phat, double omega, const double* shat,
-                         const double* s, const double* t, double* x, double* r, int full) {
+// x += alpha phat (+ omega shat); r = s - omega t.  stage 1 (after the s
+// check): only on state 1; stage 2 (after omega): full update on state 0,
+// x += alpha phat on state 3.
+__global__ void k_bicg_x(int64_t n, const double* sc, const int* state, int stage, const double* phat,
+                         const double* shat, const double* s, const double* t, double* x, double* r) {
+    const int st = *state;
+    const bool half = stage == 1 ? st == 1 : st == 3;
+    const bool full = stage == 2 && st == 0;
+    if (!half && !full) return;
+    const double alpha = sc[S_ALPHA], omega = sc[S_OMEGA];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (full) {
             x[i] += alpha * phat[i] + omega * shat[i];
@@ -441,12 +489,14 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
         if (converged) *converged = 1;
         return TGK_OK;
     }
-    DevBuf<double> r, p, v, phat, shat, s, t, rt, inv, best_x, part, scal;
-    DevBuf<int> flag;
+    DevBuf<double> r, p, v, phat, shat, s, t, rt, inv, best_x, part, scal, sc;
+    DevBuf<int> flag, state;
     for (DevBuf<double>* b : {&r, &p, &v, &phat, &shat, &s, &t, &rt, &inv, &best_x}) TGK_TRY(b->alloc(n));
     TGK_TRY(part.alloc(2 * kDotBlocks));
     TGK_TRY(scal.alloc(2));
+    TGK_TRY(sc.alloc(S_COUNT));
     TGK_TRY(flag.alloc(1));
+    TGK_TRY(state.alloc(1));
     const unsigned G = grid_n(n);
     auto dot = [&](const double* a, const double* b, double* out) -> int {
         k_dot_partial<<<kDotBlocks, kDotThreads, 0, st>>>(a, b, n, part.p);
@@ -455,18 +505,15 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
         CUDA_TRY(cudaStreamSynchronize(st));
         return TGK_OK;
     };
-    // (a.b, c.d) with one host synchronisation
-    auto dot2 = [&](const double* a, const double* b, const double* c, const double* d, double* o0,
-                    double* o1) -> int {
+    // device-side dot products into the scalar slots (no host synchronisation)
+    auto dot_d = [&](const double* a, const double* b, int slot) {
+        k_dot_partial<<<kDotBlocks, kDotThreads, 0, st>>>(a, b, n, part.p);
+        k_dot_final<<<1, 512, 0, st>>>(part.p, sc.p + slot);
+    };
+    auto dot2_d = [&](const double* a, const double* b, const double* c, const double* d, int slot0, int slot1) {
         k_dot2_partial<<<kDotBlocks, kDotThreads, 0, st>>>(a, b, c, d, n, part.p);
-        k_dot_final<<<1, 512, 0, st>>>(part.p, scal.p);
-        k_dot_final<<<1, 512, 0, st>>>(part.p + kDotBlocks, scal.p + 1);
-        double h[2];
-        CUDA_TRY(cudaMemcpyAsync(h, scal.p, sizeof h, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-        *o0 = h[0];
-        *o1 = h[1];
-        return TGK_OK;
+        k_dot_final<<<1, 512, 0, st>>>(part.p, sc.p + slot0);
+        k_dot_final<<<1, 512, 0, st>>>(part.p + kDotBlocks, sc.p + slot1);
     };
     auto nrm = [&](const double* a, double* out) -> int {
         TGK_TRY(dot(a, a, out));
@@ -517,47 +564,45 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
         CUDA_TRY(cudaMemcpyAsync(rt.p, r.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         CUDA_TRY(cudaMemsetAsync(p.p, 0, sizeof(double) * n, st));
         CUDA_TRY(cudaMemsetAsync(v.p, 0, sizeof(double) * n, st));
-        double rho = 1.0, alpha = 1.0, omega = 1.0;
-        double rho_next = 0.0;  // rt . r of the current r, when already known
-        bool have_rho = false;
+        {  // rho = alpha = omega = 1, rho_new = rt . r (solver.cpp:146-150)
+            const double init[3] = {1.0, 1.0, 1.0};
+            CUDA_TRY(cudaMemcpyAsync(sc.p + S_RHO, init, sizeof init, cudaMemcpyHostToDevice, st));
+            dot_d(rt.p, r.p, S_RHONEW);
+        }
+        const double eps_rho = eps_bd * norm_b * norm_b;
         while (res > tol && iters < max_iter) {
-            double rho_new = rho_next;
-            if (!have_rho) TGK_TRY(dot(rt.p, r.p, &rho_new));
-            have_rho = false;
-            if (!std::isfinite(rho_new) || std::abs(rho_new) < eps_bd * norm_b * norm_b) break;
-            const double beta = (rho_new / rho) * (alpha / omega);
-            rho = rho_new;
-            k_bicg_p<<<G, 256, 0, st>>>(n, r.p, v.p, inv.p, beta, omega, p.p, phat.p);
+            CUDA_TRY(cudaMemsetAsync(state.p, 0, sizeof(int), st));
+            k_it_begin<<<1, 1, 0, st>>>(sc.p, state.p, eps_rho);
+            k_bicg_p<<<G, 256, 0, st>>>(n, r.p, v.p, inv.p, sc.p, state.p, p.p, phat.p);
             k_spmv<<<G, 256, 0, st>>>(n, d_offsets, d_cols, d_values, phat.p, v.p);
-            double rtv = 0.0;
-            TGK_TRY(dot(rt.p, v.p, &rtv));
-            alpha = rho / rtv;
-            if (!std::isfinite(alpha)) break;
-            k_bicg_s<<<G, 256, 0, st>>>(n, r.p, v.p, alpha, s.p);
-            double s_norm = 0.0;
-            TGK_TRY(nrm(s.p, &s_norm));
-            ++iters;
-            if (s_norm <= tol) {
-                k_bicg_x<<<G, 256, 0, st>>>(n, alpha, phat.p, 0.0, nullptr, nullptr, nullptr, d_x, nullptr, 0);
-                res = s_norm;
-                break;
-            }
-            k_scale<<<G, 256, 0, st>>>(n, inv.p, s.p, shat.p);
+            dot_d(rt.p, v.p, S_RTV);
+            k_it_alpha<<<1, 1, 0, st>>>(sc.p, state.p);
+            k_bicg_s<<<G, 256, 0, st>>>(n, r.p, v.p, sc.p, state.p, s.p);
+            dot_d(s.p, s.p, S_SS);
+            k_it_s<<<1, 1, 0, st>>>(sc.p, state.p, tol);
+            k_bicg_x<<<G, 256, 0, st>>>(n, sc.p, state.p, 1, phat.p, nullptr, nullptr, nullptr, d_x, nullptr);
+            k_scale<<<G, 256, 0, st>>>(n, inv.p, s.p, state.p, shat.p);
             k_spmv<<<G, 256, 0, st>>>(n, d_offsets, d_cols, d_values, shat.p, t.p);
-            double tt = 0.0, ts = 0.0;
-            TGK_TRY(dot2(t.p, t.p, t.p, s.p, &tt, &ts));
-            omega = ts / tt;
-            if (!std::isfinite(omega) || tt < eps_bd) {
-                k_bicg_x<<<G, 256, 0, st>>>(n, alpha, phat.p, 0.0, nullptr, nullptr, nullptr, d_x, nullptr, 0);
+            dot2_d(t.p, t.p, t.p, s.p, S_TT, S_TS);
+            k_it_omega<<<1, 1, 0, st>>>(sc.p, state.p, eps_bd);
+            k_bicg_x<<<G, 256, 0, st>>>(n, sc.p, state.p, 2, phat.p, shat.p, s.p, t.p, d_x, r.p);
+            // ||r|| and the next iteration's rho = rt . r in one pass
+            dot2_d(r.p, r.p, rt.p, r.p, S_RR, S_RHONEW);
+            k_it_end<<<1, 1, 0, st>>>(sc.p, state.p);
+            double hs[S_COUNT];
+            int hstate = 0;
+            CUDA_TRY(cudaMemcpyAsync(hs, sc.p, sizeof hs, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(&hstate, state.p, sizeof hstate, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));  // the iteration's one host synchronisation
+            if (hstate == 2) break;  // rho or alpha breakdown: the iteration does not count
+            ++iters;
+            if (hstate == 1) {  // ||s|| <= tol: x += alpha phat done
+                res = hs[S_SNORM];
                 break;
             }
-            k_bicg_x<<<G, 256, 0, st>>>(n, alpha, phat.p, omega, shat.p, s.p, t.p, d_x, r.p, 1);
-            // ||r|| and the next iteration's rho = rt . r in one pass (4 host syncs per iteration)
-            double rr = 0.0;
-            TGK_TRY(dot2(r.p, r.p, rt.p, r.p, &rr, &rho_next));
-            res = std::sqrt(rr);
-            have_rho = true;
-            if (!std::isfinite(res)) break;
+            if (hstate == 3) break;  // omega breakdown: x += alpha phat done
+            res = hs[S_RES];
+            if (hstate == 4) break;
         }
         KERNEL_CHECK("bicgstab");
     }
