@@ -11,15 +11,17 @@
 //             every node the halo touches, plus nodal field values) gathered
 //             into shared memory;
 //   phase A   one thread per halo element: geometry with FMA, one
-//             reciprocal, the k(k+1)/2 unique K_e values via the gradient
-//             Gram matrix (row a = 0 from the zero row sum of P1 stiffness),
-//             and the scalars the mass / load are formed from (det, f det)
-//             into structure-of-arrays value rows;
-//   phase B   one lane per owned CSR entry (diagonal entries also fold the
-//             row's load): its items (u16 = halo index | value index << 12,
-//             one coalesced 4-byte load per 2 items) are summed in registers
-//             and the result stored to the entry — and to its mirror (j, i)
-//             when j is owned by the same block.
+//             reciprocal, the k(k-1)/2 off-diagonal K_e values via the
+//             gradient Gram matrix (row a = 0 from the zero row sum of P1
+//             stiffness), and the scalars the mass / load are formed from
+//             (det, f det) into structure-of-arrays value rows;
+//   phase B   one lane per owned CSR entry (diagonal entries fold only the
+//             row's mass / load): its items (u16 = halo index | value index
+//             << 12, one coalesced 4-byte load per 2 items) are summed in
+//             registers and the result stored to the entry — and to its
+//             mirror (j, i) when j is owned by the same block;
+//   copy-out  the tile to HBM as coalesced row segments, the stiffness
+//             diagonal formed as 0 - (sum of the row's off-diagonals).
 // Mass and load values are affine P1 closed forms of the reference's
 // quadrature (batch.cpp:250-289): M_e = c det Mhat, F_e[a] = f det |T^|/k;
 // with a nodal source F_e[a] = det sum_b Mhat[a][b] f_b.
@@ -253,7 +255,7 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
             const double k23 = s * dot3(c2x, c2y, c2z, c3x, c3y, c3z);
             const double k33 = s * dot3(c3x, c3y, c3z, c3x, c3y, c3z);
             const double k01 = -((k11 + k12) + k13), k02 = -((k12 + k22) + k23), k03 = -((k13 + k23) + k33);
-            kp[0] = -((k01 + k02) + k03);  // rows: K_aa, then 01 02 03 12 13 23
+            kp[0] = -((k01 + k02) + k03);  // kp: K_aa (unused: zero row sums), then 01 02 03 12 13 23
             kp[1] = k11; kp[2] = k22; kp[3] = k33;
             kp[4] = k01; kp[5] = k02; kp[6] = k03;
             kp[7] = k12; kp[8] = k13; kp[9] = k23;
@@ -272,7 +274,7 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
             const double k12 = -(s * __fma_rn(e2y, e1y, e2x * e1x));
             const double k22 = s * __fma_rn(e1y, e1y, e1x * e1x);
             const double k01 = -(k11 + k12), k02 = -(k12 + k22);
-            kp[0] = -(k01 + k02);  // rows: K_aa, then 01 02 12
+            kp[0] = -(k01 + k02);  // kp: K_aa (unused: zero row sums), then 01 02 12
             kp[1] = k11; kp[2] = k22;
             kp[3] = k01; kp[4] = k02; kp[5] = k12;
         }
