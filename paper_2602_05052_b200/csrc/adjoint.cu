@@ -125,7 +125,7 @@ template <int KIND, int DEG, int NPT>
 __global__ void __launch_bounds__(kGroupThreads) k_adjoint_groups(GroupArgs p) {
     constexpr int k = P1<KIND>::k, d = P1<KIND>::d, Q = Rule<KIND, DEG>::Q, T = kGroupThreads;
     using R = Rule<KIND, DEG>;
-    extern __shared__ __align__(16) double sv[];  // [2 buffers][lambda | U][max_nodes]
+    extern __shared__ __align__(16) double2 sv[];  // [2 buffers][max_nodes] of (lambda, U)
     const int MN = p.pl.max_nodes;
     const int tid = threadIdx.x;
     const int64_t g = blockIdx.x;
@@ -177,14 +177,10 @@ __global__ void __launch_bounds__(kGroupThreads) k_adjoint_groups(GroupArgs p) {
     for (int a = 0; a < k; ++a) li[a] = static_cast<int>((lc >> (16 * a)) & 0xffff);
     int buf = 0;
     for (int64_t b = b0; b < b1; ++b, buf ^= 1) {
-        double* sl = sv + size_t(buf) * 2 * MN;
-        double* su = sl + MN;
+        double2* slu = sv + size_t(buf) * MN;
 #pragma unroll
         for (int j = 0; j < NPT; ++j)
-            if (tid + j * T < nn) {
-                sl[tid + j * T] = rl[j];
-                su[tid + j * T] = ru[j];
-            }
+            if (tid + j * T < nn) slu[tid + j * T] = make_double2(rl[j], ru[j]);
         if (b + 1 < b1) {
 #pragma unroll
             for (int j = 0; j < NPT; ++j)
@@ -197,9 +193,10 @@ __global__ void __launch_bounds__(kGroupThreads) k_adjoint_groups(GroupArgs p) {
         if (ok) {
             double la[k], uc[k];
 #pragma unroll
-            for (int a = 0; a < k; ++a) {
-                la[a] = sl[li[a]];
-                uc[a] = su[li[a]];
+            for (int a = 0; a < k; ++a) {  // one 16-byte load per node
+                const double2 lu = slu[li[a]];
+                la[a] = lu.x;
+                uc[a] = lu.y;
             }
             double s = 0.0;
 #pragma unroll
