@@ -923,7 +923,10 @@ __device__ __forceinline__ void elast_group(const FastElastArgs& p, const RecA& 
 // Persistent kernel, the same pipeline as k_fast_scalar (TMA-fed records,
 // cp.async node tables, tile copy-out overlapping phase A).
 template <int KIND, int LT, int FT>
-__global__ void __launch_bounds__(kFastMaxThreads) k_fast_elast(FastElastArgs p) {
+#ifndef TGK_ELAST_MINB
+#define TGK_ELAST_MINB 2  // <= 64 registers: 2 CTAs x 512 threads (C3 0.81 vs 0.83 ms at 1 x 512 / 2 x 256)
+#endif
+__global__ void __launch_bounds__(kFastMaxThreads, TGK_ELAST_MINB) k_fast_elast(FastElastArgs p) {
     using Cf = FastElastCfg<KIND, LT, FT>;
     constexpr int d = Cf::d;
     extern __shared__ __align__(128) unsigned char smb[];
@@ -1081,7 +1084,7 @@ int fast_elasticity_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routi
     for (int c = 0; c < pr->n_source; ++c)
         if (pr->source[c].type == TGK_FIELD_ELEMENT) ft = 2;
     if (lt == 0 && !(pr->mu.value > 0.0)) return set_error(TGK_ERR_INPUT, "elasticity requires mu > 0");  // batch.cpp:194-195
-    int R = m->kind == TGK_TET4 ? 32 : 64, T = 256;  // B200 sweep: C3 0.95 (R=16) -> 0.89 ms (R=32)
+    int R = m->kind == TGK_TET4 ? 32 : 64, T = m->kind == TGK_TET4 ? 512 : 256;  // B200 sweeps (r02_fast_experiments)
     if (const char* e = getenv("TGK_FAST_ER")) R = std::max(1, std::min(kFastMaxRows, atoi(e)));
     if (const char* e = getenv("TGK_FAST_ET")) T = std::max(32, std::min(kFastMaxThreads, atoi(e) / 32 * 32));
     const FastPlanDev* pl = nullptr;
