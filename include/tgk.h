@@ -342,6 +342,17 @@ int tgk_adjoint_gather_d(const tgk_mesh* m, const tgk_routing* r, int64_t B,
                          const double* d_lambda, const double* d_U, double* d_out, int degree,
                          void* stream);
 
+/* simp_sensitivity (adjoint.cpp:101-125): for every element
+ * sens[e] = -p rho_e^(p-1) (E_max - E_min) u_e^T K0_e u_e, u_e[a] = U[map[e k + a]],
+ * in the reference's operation order (bit-identical for p = 3; pow otherwise).
+ * Any element kind / component count: d_map is the DofMap's E x k element-to-DoF
+ * array (device int64), d_unit_stiffness the E x k x k unit-coefficient local
+ * stiffness (device), d_U the n_dofs solution.  k in [1, 32]; a DoF index outside
+ * [0, n_dofs) -> status 2. */
+int tgk_simp_sensitivity_d(int64_t E, int k, const int64_t* d_map, const double* d_rho, double p, double E_min,
+                           double E_max, const double* d_unit_stiffness, const double* d_U, int64_t n_dofs,
+                           double* d_sens, void* stream);
+
 /* ------------------------------------------------------------------ consumers of the CSR */
 typedef struct tgk_condensed tgk_condensed;
 /* SparseOperator::apply (sparse.cpp:18-31): y = A x, row sums in column order from +0.0. */

@@ -288,3 +288,22 @@ def assemble(kind, nodes, elems, routing, problem="poisson", diffusion=1.0, lam=
                               int(plane_stress), len(sources), srcs, int(with_mass), _p(K), _p(F),
                               _p(M)))
     return K, F, M
+
+
+def simp_sensitivity(dofmap_arr, rho, p, E_min, E_max, K0, U):
+    """simp_sensitivity (adjoint.cpp:101-125) restated (pure Python floats, the
+    reference's operation order; small sizes only)."""
+    dm = np.asarray(dofmap_arr, dtype=np.int64)
+    E, k = dm.shape
+    K0 = np.asarray(K0, dtype=np.float64).reshape(E, k, k)
+    out = np.zeros(E)
+    for e in range(E):
+        ue = [float(U[g]) for g in dm[e]]
+        quad = 0.0
+        for a in range(k):
+            row = 0.0
+            for b in range(k):
+                row += float(K0[e, a, b]) * ue[b]
+            quad += ue[a] * row
+        out[e] = -p * float(rho[e]) ** (p - 1.0) * (E_max - E_min) * quad
+    return out

@@ -129,6 +129,7 @@ _SIGS = {
     "tgk_assemble_fields_batched_d": (_I, [_P, _P, _P, _I64, _P, _I, _P, _P, _P, _P]),
     "tgk_gradient_products_d": (_I, [_P, _I64, _P, _P, _P, _P, _P]),
     "tgk_adjoint_gather_d": (_I, [_P, _P, _I64, _P, _P, _P, _I, _P]),
+    "tgk_simp_sensitivity_d": (_I, [_I64, _I, _P, _P, _D, _D, _D, _P, _P, _I64, _P, _P]),
 }
 EXPORTS = tuple(_SIGS)
 

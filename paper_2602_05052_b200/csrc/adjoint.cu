@@ -347,6 +347,46 @@ int materialised_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_r
 
 }  // namespace tgk
 
+namespace tgk {
+namespace {
+
+// simp_sensitivity (adjoint.cpp:101-125), one thread per element in the
+// reference's operation order: u_e gathered through the DoF map, row_a =
+// left fold over b of K0_e[a][b] u_e[b], quad = left fold over a of u_e[a]
+// row_a, sens = ((-p * rho^(p-1)) * (E_max - E_min)) * quad.  rho^(p-1) as
+// rho * rho for the standard penalty p = 3 (correctly rounded like std::pow),
+// else pow.  Out-of-range DoF indices are reported, never dereferenced.
+template <int K>
+__global__ void k_simp_sensitivity(int64_t E, int kr, const int64_t* __restrict__ map, const double* __restrict__ rho,
+                                   double p, double E_min, double E_max, const double* __restrict__ K0,
+                                   const double* __restrict__ U, int64_t n_dofs, double* __restrict__ sens,
+                                   unsigned long long* bad) {
+    const int k = K > 0 ? K : kr;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        double ue[K > 0 ? K : 32];
+        bool ok = true;
+        for (int a = 0; a < k; ++a) {
+            const int64_t g = __ldg(map + e * k + a);
+            ok = ok && g >= 0 && g < n_dofs;
+            ue[a] = (g >= 0 && g < n_dofs) ? __ldg(U + g) : 0.0;
+        }
+        if (!ok) atomicMin(bad, static_cast<unsigned long long>(e));
+        const double* Ke = K0 + e * k * k;
+        double quad = 0.0;
+        for (int a = 0; a < k; ++a) {
+            double row = 0.0;
+            for (int b = 0; b < k; ++b) row += __ldg(Ke + a * k + b) * ue[b];
+            quad += ue[a] * row;
+        }
+        const double r = __ldg(rho + e);
+        const double pw = p == 3.0 ? r * r : pow(r, p - 1.0);
+        sens[e] = -p * pw * (E_max - E_min) * quad;
+    }
+}
+
+}  // namespace
+}  // namespace tgk
+
 extern "C" {
 
 int tgk_gradient_products_d(const tgk_routing* r, int64_t B, const double* lam, const double* U,
@@ -457,6 +497,41 @@ int tgk_assemble_batched_d(const tgk_mesh* m, const tgk_routing* r, int64_t B, c
                                       b == 0 ? F : nullptr, nullptr, st, badp));
         if (b + 1 == B || (b & 63) == 63) TGK_TRY(check_bad(badp, st));
     }
+    return TGK_OK;
+}
+
+int tgk_simp_sensitivity_d(int64_t E, int k, const int64_t* d_map, const double* d_rho, double p, double E_min,
+                           double E_max, const double* d_unit_stiffness, const double* d_U, int64_t n_dofs,
+                           double* d_sens, void* stream) {
+    using namespace tgk;
+    if (E < 0 || k <= 0 || k > 32 || n_dofs < 0 ||
+        (E > 0 && (!d_map || !d_rho || !d_unit_stiffness || !d_U || !d_sens)))
+        return set_error(TGK_ERR_INPUT, "simp_sensitivity: shape mismatch");  // adjoint.cpp:107-110
+    TGK_TRY(ensure_device());
+    if (E == 0) return TGK_OK;
+    cudaStream_t st = as_stream(stream);
+    DevBuf<unsigned long long> bad;
+    TGK_TRY(bad.alloc(1));
+    CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    const unsigned G = grid_for(E, 128);
+    auto go = [&](auto kern) {
+        kern<<<G, 128, 0, st>>>(E, k, d_map, d_rho, p, E_min, E_max, d_unit_stiffness, d_U, n_dofs, d_sens, bad.p);
+    };
+    switch (k) {
+        case 3: go(k_simp_sensitivity<3>); break;
+        case 4: go(k_simp_sensitivity<4>); break;
+        case 6: go(k_simp_sensitivity<6>); break;
+        case 8: go(k_simp_sensitivity<8>); break;
+        case 12: go(k_simp_sensitivity<12>); break;
+        default: go(k_simp_sensitivity<0>); break;
+    }
+    KERNEL_CHECK("simp_sensitivity");
+    unsigned long long h = ULLONG_MAX;
+    CUDA_TRY(cudaMemcpyAsync(&h, bad.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (h != ULLONG_MAX)
+        return set_error(TGK_ERR_INPUT, "simp_sensitivity: element " + std::to_string(h) + " maps a DoF outside [0," +
+                                            std::to_string(n_dofs) + ")");
     return TGK_OK;
 }
 

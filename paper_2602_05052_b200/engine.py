@@ -366,6 +366,20 @@ def assemble_fields_batched(mesh, routing, fields, kind="poisson", diffusion=1.0
     return K, F, M
 
 
+def simp_sensitivity(dof_map, rho, p, E_min, E_max, unit_stiffness, U, stream=None):
+    """simp_sensitivity (adjoint.cpp:101-125) on the GPU: dof_map E x k (the
+    DofMap's element-to-DoF array), unit_stiffness E x k x k, U (n_dofs)."""
+    dm = torch.as_tensor(np.ascontiguousarray(dof_map, dtype=np.int64)).to(_DEV)
+    E, k = dm.shape
+    rho = _cuda_f64(rho, E)
+    K0 = _cuda_f64(unit_stiffness, E * k * k)
+    U = _cuda_f64(U)
+    out = torch.empty(E, dtype=torch.float64, device=_DEV)
+    check(lib().tgk_simp_sensitivity_d(E, k, _ptr(dm), _ptr(rho), float(p), float(E_min), float(E_max), _ptr(K0),
+                                       _ptr(U), U.numel(), _ptr(out), _stream(stream)))
+    return out
+
+
 def gradient_products(routing, lam, U, stream=None):
     """gradient_products (adjoint.cpp:68-82), batched: lam, U (B x N) -> dK (B x nnz), dF (B x N)."""
     lam = _cuda_f64(lam).reshape(-1, routing.N)

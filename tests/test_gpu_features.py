@@ -295,3 +295,37 @@ def test_fp32_mode_within_tolerance(eng, kind, div, kw):
         assert_scaled_close(np_(F32).astype(np.float64), Fr, rel=1e-5, floor=1e-7, what="F fp32")
     if kw.get("with_mass"):
         assert_scaled_close(np_(M32).astype(np.float64), Mr, rel=1e-5, floor=1e-7, what="M fp32")
+
+
+@pytest.mark.parametrize("p", [3.0, 2.5])
+def test_simp_sensitivity_gpu(eng, p):
+    """tgk_simp_sensitivity_d (adjoint.cpp:101-125) on TET4 elasticity DoFs (k = 12)
+    and scalar TRI3 DoFs (k = 3) vs the restatement: bitwise for the standard
+    penalty p = 3, within 1e-15 relative (device pow) otherwise; a DoF map
+    entry out of range is an InputError."""
+    from paper_2602_05052_b200 import InputError
+    nodes, elems = port.generate_grid("tet4", [1.0, 0.8, 1.2], [5, 4, 6])
+    E = elems.shape[0]
+    rng = np.random.default_rng(12)
+    K0 = port.local("tet4", nodes, elems, 1, port.ELASTICITY, np.full(E, 0.5769230769230769),
+                    np.full(E, 0.38461538461538464))
+    U = rng.standard_normal(nodes.shape[0] * 3)
+    rho = 0.05 + 0.95 * rng.random(E)
+    dm = port.dofmap("tet4", elems, 3)
+    got = eng.simp_sensitivity(dm, rho, p, 1e-9, 1.0, K0, U).cpu().numpy()
+    want = port.simp_sensitivity(dm, rho, p, 1e-9, 1.0, K0, U)
+    if p == 3.0:
+        assert_bitwise(got, want, "simp_sensitivity k=12")
+    else:
+        np.testing.assert_allclose(got, want, rtol=1e-15, atol=0)
+    tn, te = port.generate_grid("tri3", [1.0, 1.0], [9, 7])
+    K2 = port.local("tri3", tn, te, 1, port.DIFFUSION, np.ones(te.shape[0]))
+    U2 = rng.standard_normal(tn.shape[0])
+    r2 = 0.05 + 0.95 * rng.random(te.shape[0])
+    d2 = port.dofmap("tri3", te, 1)
+    g2 = eng.simp_sensitivity(d2, r2, 3.0, 1e-9, 1.0, K2, U2).cpu().numpy()
+    assert_bitwise(g2, port.simp_sensitivity(d2, r2, 3.0, 1e-9, 1.0, K2, U2), "simp_sensitivity k=3")
+    bad = dm.copy()
+    bad[4, 7] = U.size + 3
+    with pytest.raises(InputError, match="element 4 maps a DoF outside"):
+        eng.simp_sensitivity(bad, rho, p, 1e-9, 1.0, K0, U)

@@ -149,3 +149,28 @@ def test_reference_errors():
     nodes = np.array([[0.0, 0.0], [0.0, 1.0], [1.0, 0.0]])  # clockwise: det < 0
     with pytest.raises(port.OracleError, match="element 0 has non-positive Jacobian"):
         port.local("tri3", nodes, np.array([[0, 1, 2]]), 1, port.DIFFUSION, np.ones(1))
+
+
+def _simp_case():
+    nodes, elems = port.generate_grid("tet4", [1.0, 0.8, 1.2], [3, 2, 3])
+    E = elems.shape[0]
+    rng = np.random.default_rng(12)
+    lam = np.full(E, 0.5769230769230769)
+    mu = np.full(E, 0.38461538461538464)
+    K0 = port.local("tet4", nodes, elems, 1, port.ELASTICITY, lam, mu)
+    U = rng.standard_normal(nodes.shape[0] * 3)
+    rho = 0.05 + 0.95 * rng.random(E)
+    return nodes, elems, K0, U, rho
+
+
+@pytest.mark.parametrize("p", [3.0, 2.5])
+def test_simp_sensitivity_restatement_vs_reference(p):
+    """port.simp_sensitivity against the unmodified reference library's
+    simp_sensitivity (adjoint.cpp:101-125), bitwise, on TET4 elasticity DoFs."""
+    ref = _ref()
+    nodes, elems, K0, U, rho = _simp_case()
+    dm = port.dofmap("tet4", elems, 3)
+    got = port.simp_sensitivity(dm, rho, p, 1e-9, 1.0, K0, U)
+    rm = ref.Mesh.from_arrays("tet4", nodes, elems)
+    rr = ref.Routing(rm, 3)
+    assert_bitwise(got, rr.simp_sensitivity(rho, p, 1e-9, 1.0, K0, U), f"simp_sensitivity p={p}")
