@@ -29,6 +29,8 @@ def test_adapter_library_built_and_exports_assemble():
     assert "_ZN2tg8assembleERKNS_11ProblemSpecERKNS_4MeshERKNS_6DofMapERKNS_15RoutingMatricesEb" in syms
     assert "_ZN2tg12assemble_cpuERKNS_11ProblemSpecERKNS_4MeshERKNS_6DofMapERKNS_15RoutingMatricesEb" in syms
     assert " U tgk_assemble" in syms
+    assert "_ZN2tg20simp_sensitivity_cpuERKSt6vectorIdSaIdEEdddS4_RKNS_4MeshERKNS_6DofMapES4_" in syms
+    assert " U tgk_simp_sensitivity_d" in syms
 
 
 torch = pytest.importorskip("torch")
@@ -138,3 +140,22 @@ def test_dropin_errors_match_reference(libs):
             L.assemble(m, r, diffusion=("element", np.ones(3)))
         with pytest.raises(L.RefError, match="component count"):
             L.assemble(m, r, problem="elasticity")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,comps,divs", [("tet4", 3, [4, 3, 5]), ("quad4", 2, [12, 7]), ("tri3", 1, [9, 8])])
+def test_dropin_simp_sensitivity_bitwise(libs, kind, comps, divs):
+    """tg::simp_sensitivity through adapter/adjoint_gpu.cpp (the reference's own
+    Mesh / DofMap types) vs the CPU library: bitwise for p = 3 — including the
+    QUAD4 vector-elasticity DoFs of the reference's topology optimisation."""
+    (mr, rr), (mg, rg) = _pair(libs, kind, divs=divs, comps=comps)
+    E, kd = rr.E, rr.k  # elements, local DoFs per element
+    rng = np.random.default_rng(21)
+    K0 = rng.standard_normal((E, kd, kd))
+    K0 = K0 + K0.transpose(0, 2, 1)
+    U = rng.standard_normal(rr.N)
+    rho = 0.05 + 0.95 * rng.random(E)
+    want = rr.simp_sensitivity(rho, 3.0, 1e-9, 1.0, K0, U)
+    got = rg.simp_sensitivity(rho, 3.0, 1e-9, 1.0, K0, U)
+    assert_bitwise(got, want, f"{kind} simp_sensitivity")
+
