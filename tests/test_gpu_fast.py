@@ -363,3 +363,29 @@ def test_assemble_batched_fast_mode(eng):
     Kx, Fx = eng.assemble_batched(m, r, rt, source=1.0, mode="exact")
     assert_bitwise(np_(K), np_(Kx), "K")
     assert_bitwise(np_(F), np_(Fx), "F")
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_isolated_nodes_and_tiny_meshes(eng, mode):
+    """Edge cases the reference accepts: nodes referenced by no element (empty
+    CSR rows, F_i = 0), a single element, and a mesh whose rows fit one block."""
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [3, 2, 2])
+    extra = np.array([[5.0, 5.0, 5.0], [6.0, 5.0, 5.0]])
+    nodes2 = np.vstack([nodes[:7], extra, nodes[7:]])  # two isolated nodes in the middle of the numbering
+    remap = np.where(np.arange(nodes.shape[0]) >= 7, np.arange(nodes.shape[0]) + 2, np.arange(nodes.shape[0]))
+    elems2 = remap[elems]
+    one_n = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]])
+    one_e = np.array([[0, 1, 2, 3]])
+    for nn, ee in [(nodes2, elems2), (one_n, one_e)]:
+        m = eng.DeviceMesh("tet4", nn, ee)
+        r = eng.Routing(m, 1)
+        pr = port.Routing(nn.shape[0], port.dofmap("tet4", ee, 1))
+        for kw in [dict(sources=[1.0]), dict(sources=[2.0], with_mass=True)]:
+            K, F, M = eng.assemble(m, r, mode=mode, **kw)
+            Kr, Fr, Mr = port.assemble("tet4", nn, ee, pr, **kw)
+            pairs = [(K, Kr, "K"), (F, Fr, "F")] + ([(M, Mr, "M")] if kw.get("with_mass") else [])
+            for g, w, what in pairs:
+                if mode == "exact":
+                    assert_bitwise(np_(g), w, what)
+                else:
+                    assert_scaled_close(np_(g), w, what=what)
