@@ -389,3 +389,21 @@ def test_isolated_nodes_and_tiny_meshes(eng, mode):
                     assert_bitwise(np_(g), w, what)
                 else:
                     assert_scaled_close(np_(g), w, what=what)
+
+
+def test_fast_elasticity_isolated_nodes(eng):
+    """Fast elasticity with two nodes referenced by no element: empty vector rows
+    and zero loads there, the rest within the tolerance of the oracle."""
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [3, 2, 2])
+    extra = np.array([[5.0, 5.0, 5.0], [6.0, 5.0, 5.0]])
+    nn = np.vstack([nodes[:7], extra, nodes[7:]])
+    remap = np.where(np.arange(nodes.shape[0]) >= 7, np.arange(nodes.shape[0]) + 2, np.arange(nodes.shape[0]))
+    ee = remap[elems]
+    m = eng.DeviceMesh("tet4", nn, ee)
+    rv = eng.Routing(m, 3)
+    pr = port.Routing(nn.shape[0] * 3, port.dofmap("tet4", ee, 3))
+    kw = dict(lam=0.5769230769230769, mu=0.38461538461538464, sources=[1.0, 0.5, -1.0])
+    K, F, _ = eng.assemble(m, rv, kind="elasticity", mode="fast", **kw)
+    Kr, Fr, _ = port.assemble("tet4", nn, ee, pr, problem="elasticity", **kw)
+    assert_scaled_close(np_(K), Kr, what="K")
+    assert_scaled_close(np_(F), Fr, what="F")
