@@ -10,7 +10,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <climits>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <unordered_map>
@@ -933,14 +935,34 @@ int tgk_assemble_fields_batched_d(const tgk_problem* p, const tgk_mesh* m, const
         if (!fb[i].data && B > 0) return set_error(TGK_ERR_INPUT, "assemble_fields_batched: null field data");
     }
     const int64_t nnz = r->nnz, N = r->N;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // scalar problems: one status word per member, read back once after the
+    // batch (no host synchronisation per member); elasticity checks mu per call
+    const bool async_status = p->kind != TGK_ELASTICITY && B > 0;
+    unsigned long long* d_bads = nullptr;
+    if (async_status) {
+        TGK_TRY(host_ensure_device());
+        HCUDA(cudaMalloc(&d_bads, sizeof(unsigned long long) * B));
+    }
+    std::unique_ptr<unsigned long long, cudaError_t (*)(void*)> guard(d_bads, cudaFree);
+    if (async_status) HCUDA(cudaMemsetAsync(d_bads, 0xff, sizeof(unsigned long long) * B, st));
     for (int64_t b = 0; b < B; ++b) {
         for (int i = 0; i < n_fb; ++i) {
             const int64_t stride = fb[i].stride > 0 ? fb[i].stride : m->E;
             *slot_field(q, fb[i].slot) = tgk_field{TGK_FIELD_ELEMENT, 0.0, fb[i].data + b * stride, m->E};
         }
         TGK_TRY(tgk::assemble_dev(&q, m, const_cast<tgk_routing*>(r), d_K ? d_K + b * nnz : nullptr,
-                                  d_F ? d_F + b * N : nullptr, d_M && q.with_mass ? d_M + b * nnz : nullptr,
-                                  static_cast<cudaStream_t>(stream), nullptr));
+                                  d_F ? d_F + b * N : nullptr, d_M && q.with_mass ? d_M + b * nnz : nullptr, st,
+                                  async_status ? d_bads + b : nullptr));
+    }
+    if (async_status) {
+        std::vector<unsigned long long> h(static_cast<size_t>(B));
+        HCUDA(cudaMemcpyAsync(h.data(), d_bads, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost, st));
+        HCUDA(cudaStreamSynchronize(st));
+        for (int64_t b = 0; b < B; ++b)  // the first failing member, as a per-field loop would report it
+            if (h[static_cast<size_t>(b)] != ULLONG_MAX)
+                return set_error(TGK_ERR_INPUT, "element " + std::to_string(h[static_cast<size_t>(b)]) +
+                                                    " has non-positive Jacobian determinant");
     }
     return TGK_OK;
 }

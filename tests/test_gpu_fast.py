@@ -407,3 +407,18 @@ def test_fast_elasticity_isolated_nodes(eng):
     Kr, Fr, _ = port.assemble("tet4", nn, ee, pr, problem="elasticity", **kw)
     assert_scaled_close(np_(K), Kr, what="K")
     assert_scaled_close(np_(F), Fr, what="F")
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_fields_batched_reports_inverted_element(eng, mode):
+    """tgk_assemble_fields_batched_d reads the members' status words back once:
+    an inverted element is still reported like a per-field loop would."""
+    from paper_2602_05052_b200 import InputError
+    nodes, elems = port.generate_grid("tet4", [1.0, 1.0, 1.0], [3, 3, 3])
+    bad = elems.copy()
+    bad[[5, 9]] = bad[[5, 9]][:, [1, 0, 2, 3]]
+    m = eng.DeviceMesh("tet4", nodes, bad)
+    r = eng.Routing(m, 1)
+    rho = torch.from_numpy(0.5 + np.random.default_rng(1).random((4, bad.shape[0])))
+    with pytest.raises(InputError, match="element 5 has non-positive Jacobian determinant"):
+        eng.assemble_fields_batched(m, r, {"diffusion": rho}, sources=[1.0], mode=mode)
