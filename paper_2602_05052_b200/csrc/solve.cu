@@ -480,7 +480,21 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
     if (n < 0 || (n > 0 && (!d_offsets || !d_cols || !d_values || !d_b || !d_x)))
         return set_error(TGK_ERR_INPUT, "bicgstab: bad arguments");
     TGK_TRY(ensure_device());
+    // the iteration body is replayed as one CUDA graph: capture needs a real
+    // stream, so the legacy default stream is replaced by a blocking stream
+    // (implicitly ordered after the caller's legacy-stream work)
     cudaStream_t st = as_stream(stream);
+    cudaStream_t own = nullptr;
+    if (!st) {
+        CUDA_TRY(cudaStreamCreate(&own));
+        st = own;
+    }
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() {
+            if (s) cudaStreamDestroy(s);
+        }
+    } stream_guard{own};
     int64_t iters = 0;
     if (iterations) *iterations = 0;
     if (rel_residual) *rel_residual = 0.0;
@@ -495,6 +509,21 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
     TGK_TRY(part.alloc(2 * kDotBlocks));
     TGK_TRY(scal.alloc(2));
     TGK_TRY(sc.alloc(S_COUNT));
+    struct PinnedBuf {  // read-back of the scalars + state (pinned: capturable copies)
+        double* p = nullptr;
+        ~PinnedBuf() {
+            if (p) cudaFreeHost(p);
+        }
+    } hbuf;
+    CUDA_TRY(cudaMallocHost(&hbuf.p, sizeof(double) * (S_COUNT + 1)));
+    struct GraphGuard {
+        cudaGraphExec_t e = nullptr;
+        ~GraphGuard() {
+            if (e) cudaGraphExecDestroy(e);
+        }
+    } graph_guard;
+    cudaGraphExec_t& graph_exec = graph_guard.e;
+    bool graph_tried = false;
     TGK_TRY(flag.alloc(1));
     TGK_TRY(state.alloc(1));
     const unsigned G = grid_n(n);
@@ -570,7 +599,7 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
             dot_d(rt.p, r.p, S_RHONEW);
         }
         const double eps_rho = eps_bd * norm_b * norm_b;
-        while (res > tol && iters < max_iter) {
+        auto launch_iteration = [&]() -> int {
             CUDA_TRY(cudaMemsetAsync(state.p, 0, sizeof(int), st));
             k_it_begin<<<1, 1, 0, st>>>(sc.p, state.p, eps_rho);
             k_bicg_p<<<G, 256, 0, st>>>(n, r.p, v.p, inv.p, sc.p, state.p, p.p, phat.p);
@@ -589,11 +618,31 @@ int tgk_bicgstab_d(int64_t n, const int64_t* d_offsets, const int64_t* d_cols, c
             // ||r|| and the next iteration's rho = rt . r in one pass
             dot2_d(r.p, r.p, rt.p, r.p, S_RR, S_RHONEW);
             k_it_end<<<1, 1, 0, st>>>(sc.p, state.p);
-            double hs[S_COUNT];
-            int hstate = 0;
-            CUDA_TRY(cudaMemcpyAsync(hs, sc.p, sizeof hs, cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaMemcpyAsync(&hstate, state.p, sizeof hstate, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(hbuf.p, sc.p, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(hbuf.p + S_COUNT, state.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+            return TGK_OK;
+        };
+        // one graph for the whole iteration (17 launches + 2 read-backs): captured
+        // once per solve, replayed per iteration; direct launches if capture fails
+        if (!graph_tried) {
+            graph_tried = true;
+            if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                (void)launch_iteration();
+                cudaGraph_t g = nullptr;
+                if (cudaStreamEndCapture(st, &g) == cudaSuccess && g) {
+                    if (cudaGraphInstantiate(&graph_exec, g, 0) != cudaSuccess) graph_exec = nullptr;
+                    cudaGraphDestroy(g);
+                }
+            }
+            cudaGetLastError();  // a failed capture leaves the direct path
+        }
+        while (res > tol && iters < max_iter) {
+            if (graph_exec) CUDA_TRY(cudaGraphLaunch(graph_exec, st));
+            else TGK_TRY(launch_iteration());
             CUDA_TRY(cudaStreamSynchronize(st));  // the iteration's one host synchronisation
+            const double* hs = hbuf.p;
+            int hstate = 0;
+            std::memcpy(&hstate, hbuf.p + S_COUNT, sizeof hstate);
             if (hstate == 2) break;  // rho or alpha breakdown: the iteration does not count
             ++iters;
             if (hstate == 1) {  // ||s|| <= tol: x += alpha phat done
