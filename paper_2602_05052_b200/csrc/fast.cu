@@ -344,26 +344,39 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
     uint32_t wa = steps > 0 ? ip[0] : zw;
     uint32_t wb = steps > 1 ? ip[32] : zw;
     uint32_t wc = steps > 2 ? ip[64] : zw;
-    auto eat = [&](uint32_t it, double& kk, double& ss, double& ff) {
-        const int h = static_cast<int>(it & 0xfffu), q = static_cast<int>(it >> 12);
-        if constexpr (KT == 0) {
-            if (!diag) kk += kv[q * MH + h];  // the diagonal: zero row sums (copy-out)
-        }
-        if constexpr (Cf::HAS_S) ss += kv[Cf::SROW * MH + h];
-        if constexpr (FT == 1) {
-            if (diag && !fs_det) ff += kv[Cf::FROW * MH + h];
-        }
-        if constexpr (FT == 2) {
-            if (diag) ff += kv[(Cf::FROW + q) * MH + h];
+    // the fold, specialised per warp-uniform class so the item loop carries no
+    // per-item conditionals: off-diagonal entries fold K (and S), diagonal
+    // entries only S / F (the stiffness diagonal comes from the zero row sums)
+    auto fold = [&](auto eat) {
+        for (int st = 0; st < steps; ++st) {
+            const uint32_t wn = st + 3 < steps ? ip[(st + 3) * 32] : zw;
+            eat(wa & 0xffffu, k0, s0, f0);
+            eat(wa >> 16, k1, s1, f1);
+            wa = wb;
+            wb = wc;
+            wc = wn;
         }
     };
-    for (int st = 0; st < steps; ++st) {
-        const uint32_t wn = st + 3 < steps ? ip[(st + 3) * 32] : zw;
-        eat(wa & 0xffffu, k0, s0, f0);
-        eat(wa >> 16, k1, s1, f1);
-        wa = wb;
-        wb = wc;
-        wc = wn;
+    if (!diag) {
+        fold([&](uint32_t it, double& kk, double& ss, double&) {
+            const int h = static_cast<int>(it & 0xfffu), q = static_cast<int>(it >> 12);
+            if constexpr (KT == 0) kk += kv[q * MH + h];
+            if constexpr (Cf::HAS_S) ss += kv[Cf::SROW * MH + h];
+        });
+    } else if (FT == 1 && !fs_det) {
+        fold([&](uint32_t it, double&, double& ss, double& ff) {
+            const int h = static_cast<int>(it & 0xfffu);
+            if constexpr (Cf::HAS_S) ss += kv[Cf::SROW * MH + h];
+            ff += kv[Cf::FROW * MH + h];
+        });
+    } else {
+        fold([&](uint32_t it, double&, double& ss, double& ff) {
+            const int h = static_cast<int>(it & 0xfffu), q = static_cast<int>(it >> 12);
+            if constexpr (Cf::HAS_S) ss += kv[Cf::SROW * MH + h];
+            if constexpr (FT == 2) ff += kv[(Cf::FROW + q) * MH + h];
+            (void)q;
+            (void)ff;
+        });
     }
     if constexpr (KT == 1) {  // coefficient mass: the folds summed S
         k0 = s0;
