@@ -340,16 +340,18 @@ __device__ __forceinline__ void fast_group(const FastArgs& p, const RecA& A, con
     double k0 = 0.0, k1 = 0.0, k2 = 0.0, k3 = 0.0, s0 = 0.0, s1 = 0.0, f0 = 0.0, f1 = 0.0;
     // u16 items h | q << 12: K_ab at row q, S at SROW, F at FROW (+ a = q for a
     // nodal load on a diagonal); padding items address the +0.0 slot
-    const uint32_t zw = uint32_t(MH - 1) | (uint32_t(MH - 1) << 16);
-    uint32_t wa = steps > 0 ? ip[0] : zw;
-    uint32_t wb = steps > 1 ? ip[32] : zw;
-    uint32_t wc = steps > 2 ? ip[64] : zw;
+    // prefetch indices clamped to the group's last step: unconditional loads (no
+    // branch around them); a word fetched past the last step is never folded
+    const int last = steps > 0 ? steps - 1 : 0;
+    uint32_t wa = ip[0];
+    uint32_t wb = ip[min(1, last) * 32];
+    uint32_t wc = ip[min(2, last) * 32];
     // the fold, specialised per warp-uniform class so the item loop carries no
     // per-item conditionals: off-diagonal entries fold K (and S), diagonal
     // entries only S / F (the stiffness diagonal comes from the zero row sums)
     auto fold = [&](auto eat) {
         for (int st = 0; st < steps; ++st) {
-            const uint32_t wn = st + 3 < steps ? ip[(st + 3) * 32] : zw;
+            const uint32_t wn = ip[min(st + 3, last) * 32];
             eat(wa & 0xffffu, k0, s0, f0);
             eat(wa >> 16, k1, s1, f1);
             wa = wb;
