@@ -513,6 +513,7 @@ __global__ void __launch_bounds__(kFastScalarMaxThreads) k_fast_scalar(FastArgs 
     const int glog = p.gl <= 8 ? 3 : p.gl <= 16 ? 4 : 5;
     const int gl = lane & ((1 << glog) - 1), GL = 1 << glog;
     const int lr_base = warp << (5 - glog), lr_step = nwarp << (5 - glog);
+    const bool single_pass = pl.max_len <= GL;
     auto copy_out = [&]() {
         if (p.debug & 4) return;
         for (int base = lr_base; base < tile_rows; base += lr_step) {  // warp-uniform: shuffles below
@@ -521,6 +522,18 @@ __global__ void __launch_bounds__(kFastScalarMaxThreads) k_fast_scalar(FastArgs 
             const int64_t rp = ok ? trp[lr] : 0;
             const int t0 = ok ? ttoff[lr] : 0, len = ok ? ttoff[lr + 1] - t0 : 0;
             const int dq = (KT == 0 && ok) ? tdiag[lr] : -1;
+            if (single_pass) {  // every row fits its lanes: one predicated pass, no loops
+                const bool in = gl < len;
+                const double v = in ? tk[t0 + gl] : 0.0;
+                double off = (in && gl != dq) ? v : 0.0;
+                if constexpr (KT == 0)
+                    for (int o = GL >> 1; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
+                if (in) {
+                    p.K[rp + gl] = (KT == 0 && gl == dq) ? 0.0 - off : v;
+                    if constexpr (HAS_M) p.M[rp + gl] = tm[t0 + gl];
+                }
+                continue;
+            }
             double off = 0.0;
             if constexpr (KT == 0) {
                 for (int q = gl; q < len; q += GL)
