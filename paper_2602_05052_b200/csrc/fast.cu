@@ -1016,18 +1016,24 @@ __global__ void __launch_bounds__(kFastMaxThreads, TGK_ELAST_MINB) k_fast_elast(
             const int64_t rp = trp[lr] * DD;
             const int L = ttoff[lr + 1] - ttoff[lr], t0 = ttoff[lr] * DD, len = L * DD;
             const int pd = tdiag[lr];
+            const double* src = tk + t0;
             if (pd < L) {  // warp-uniform
+                // column (r, s) of the row's blocks: src[base + d q], base = r d L + s
+                const double* col = src + (rs / d) * d * L + rs % d;
                 double sacc = 0.0;
-                if (part < NP)
-                    for (int q = part; q < L; q += NP)
-                        if (q != pd) sacc += tk[t0 + (rs / d) * d * L + d * q + rs % d];
+                if (part < NP) {
+#pragma unroll 4
+                    for (int q = part; q < L; q += NP) sacc += q != pd ? col[d * q] : 0.0;  // branch-free
+                }
                 double tot = sacc;
 #pragma unroll
                 for (int o = 1; o < NP; ++o) tot += __shfl_down_sync(0xffffffffu, sacc, o * DD);
                 if (part == 0) tk[t0 + (rs / d) * d * L + d * pd + rs % d] = 0.0 - tot;
                 __syncwarp();
             }
-            for (int q = lane; q < len; q += 32) p.K[rp + q] = tk[t0 + q];
+            double* dst = p.K + rp;
+#pragma unroll 4
+            for (int q = lane; q < len; q += 32) dst[q] = src[q];
         }
     };
     if (tid == 0) {
