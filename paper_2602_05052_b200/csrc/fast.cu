@@ -168,6 +168,10 @@ __device__ __forceinline__ void halo_nodes(const RecA& A, int hc8, int h, int (&
         for (int a = 0; a < k; ++a) l[a] = static_cast<int>((hc >> (16 * a)) & 0xffff);
     }
 }
+// STORED: read the section offsets from the header (k_fast_scalar: fewer
+// instructions); else recompute them (k_fast_elast: fewer live registers —
+// it runs capped at 64)
+template <bool STORED = true>
 __device__ __forceinline__ RecA parse_a(const unsigned char* r) {
     RecA a;
     a.hbase = *reinterpret_cast<const int64_t*>(r);
@@ -176,16 +180,23 @@ __device__ __forceinline__ RecA parse_a(const unsigned char* r) {
     a.nh = h0.y;
     a.nbn = h1.x;
     a.tile = h1.y;
-    size_t o = 32;
-    a.rp = reinterpret_cast<const int64_t*>(r + o);
-    o += al16(8 * size_t(a.nr));
-    a.srow = reinterpret_cast<const uint32_t*>(r + o);
-    o += al16(4 * size_t(a.nr));
-    a.toff = reinterpret_cast<const uint16_t*>(r + o);
-    o += al16(2 * size_t(a.nr + 1));
-    a.bnodes = reinterpret_cast<const uint32_t*>(r + o);
-    o += al16(4 * size_t(a.nbn));
-    a.hconn = r + o;
+    a.rp = reinterpret_cast<const int64_t*>(r + 32);
+    if constexpr (STORED) {
+        const uint2 of = *reinterpret_cast<const uint2*>(r + 24);  // section offsets (plan_fast.cpp)
+        a.srow = reinterpret_cast<const uint32_t*>(r + (of.x & 0xffffu));
+        a.toff = reinterpret_cast<const uint16_t*>(r + (of.x >> 16));
+        a.bnodes = reinterpret_cast<const uint32_t*>(r + (of.y & 0xffffu));
+        a.hconn = r + (of.y >> 16);
+    } else {
+        size_t o = 32 + al16(8 * size_t(a.nr));
+        a.srow = reinterpret_cast<const uint32_t*>(r + o);
+        o += al16(4 * size_t(a.nr));
+        a.toff = reinterpret_cast<const uint16_t*>(r + o);
+        o += al16(2 * size_t(a.nr + 1));
+        a.bnodes = reinterpret_cast<const uint32_t*>(r + o);
+        o += al16(4 * size_t(a.nbn));
+        a.hconn = r + o;
+    }
     return a;
 }
 struct RecB {
@@ -993,7 +1004,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, TGK_ELAST_MINB) k_fast_elast(
     auto wait_a = [&](int64_t it) { mbar_wait(&bars[it & 1], static_cast<uint32_t>((it >> 1) & 1)); };
     auto wait_b = [&](int64_t it) { mbar_wait(&bars[2], static_cast<uint32_t>(it & 1)); };
     auto gather = [&](int64_t it) {
-        const RecA A = parse_a(ra(it));
+        const RecA A = parse_a<false>(ra(it));
         double* xs = xsp(it);
         for (int i = tid; i < int(A.nbn); i += T) {
             const int64_t g = A.bnodes[i];
@@ -1046,7 +1057,7 @@ __global__ void __launch_bounds__(kFastMaxThreads, TGK_ELAST_MINB) k_fast_elast(
     cp_async_wait_all();
     __syncthreads();
     for (int64_t it = 0; it < n_it; ++it) {
-        const RecA A = parse_a(ra(it));
+        const RecA A = parse_a<false>(ra(it));
         copy_out();
         const int nh_run = (p.debug & 1) ? 0 : int(A.nh);
         for (int h = tid; h < nh_run; h += T) elast_element<KIND, LT, FT>(p, A, xsp(it), kv, h);

@@ -392,6 +392,12 @@ int ensure_fast_plan(tgk_routing* rr, int R, int fmt, bool fnodal, const FastPla
         const uint32_t hdr[4] = {nr, nh, nbn, toff[nr]};
         std::memcpy(pa, &h0, 8);
         std::memcpy(pa + 8, hdr, 16);
+        {  // byte offsets of srow / toff / bnodes / hconn (the kernels read them, no arithmetic)
+            const size_t o_srow = 32 + al16(8 * size_t(nr)), o_toff = o_srow + al16(4 * size_t(nr)),
+                         o_bn = o_toff + al16(2 * size_t(nr + 1)), o_hc = o_bn + al16(4 * size_t(nbn));
+            const uint16_t offs[4] = {uint16_t(o_srow), uint16_t(o_toff), uint16_t(o_bn), uint16_t(o_hc)};
+            std::memcpy(pa + 24, offs, 8);
+        }
         size_t o = 32;
         for (uint32_t i = 0; i < nr; ++i) {
             const int64_t rp = h.row_ptr[P.rows[r0 + i]];
