@@ -524,7 +524,10 @@ __global__ void __launch_bounds__(kFastScalarMaxThreads) k_fast_scalar(FastArgs 
     const int glog = p.gl <= 8 ? 3 : p.gl <= 16 ? 4 : 5;
     const int gl = lane & ((1 << glog) - 1), GL = 1 << glog;
     const int lr_base = warp << (5 - glog), lr_step = nwarp << (5 - glog);
-    const bool single_pass = pl.max_len <= GL;
+    // rows of up to 2 GL entries: one predicated pass with two entries per lane
+    // (8 lanes per row for C2a's <= 15-entry rows: 4 rows per warp and a
+    // 3-round butterfly instead of 2 rows and 4 rounds)
+    const bool single_pass = pl.max_len <= 2 * GL;
     auto copy_out = [&]() {
         if (p.debug & 4) return;
         for (int base = lr_base; base < tile_rows; base += lr_step) {  // warp-uniform: shuffles below
@@ -533,15 +536,20 @@ __global__ void __launch_bounds__(kFastScalarMaxThreads) k_fast_scalar(FastArgs 
             const int64_t rp = ok ? trp[lr] : 0;
             const int t0 = ok ? ttoff[lr] : 0, len = ok ? ttoff[lr + 1] - t0 : 0;
             const int dq = (KT == 0 && ok) ? tdiag[lr] : -1;
-            if (single_pass) {  // every row fits its lanes: one predicated pass, no loops
-                const bool in = gl < len;
-                const double v = in ? tk[t0 + gl] : 0.0;
-                double off = (in && gl != dq) ? v : 0.0;
+            if (single_pass) {  // every row fits two passes of its lanes: predicated, no loops
+                const int q1 = gl + GL;
+                const bool in0 = gl < len, in1 = q1 < len;
+                const double v0 = in0 ? tk[t0 + gl] : 0.0, v1 = in1 ? tk[t0 + q1] : 0.0;
+                double off = ((in0 && gl != dq) ? v0 : 0.0) + ((in1 && q1 != dq) ? v1 : 0.0);
                 if constexpr (KT == 0)
                     for (int o = GL >> 1; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
-                if (in) {
-                    p.K[rp + gl] = (KT == 0 && gl == dq) ? 0.0 - off : v;
+                if (in0) {
+                    p.K[rp + gl] = (KT == 0 && gl == dq) ? 0.0 - off : v0;
                     if constexpr (HAS_M) p.M[rp + gl] = tm[t0 + gl];
+                }
+                if (in1) {
+                    p.K[rp + q1] = (KT == 0 && q1 == dq) ? 0.0 - off : v1;
+                    if constexpr (HAS_M) p.M[rp + q1] = tm[t0 + q1];
                 }
                 continue;
             }
@@ -696,7 +704,7 @@ int fast_scalar_assemble(const tgk_problem* pr, const tgk_mesh* m, tgk_routing* 
     a.abuf = (pl->max_rec_a + 15) & ~15;
     a.bbuf = (pl->max_rec_b + 15) & ~15;
     if (const char* e = getenv("TGK_FAST_DEBUG")) a.debug = atoi(e);
-    a.gl = pl->max_len <= 8 ? 8 : pl->max_len <= 16 ? 16 : 32;
+    a.gl = pl->max_len <= 16 ? 8 : pl->max_len <= 32 ? 16 : 32;  // copy-out lanes per row (<= 2 entries each)
     const int T = shape.T;
     unsigned long long* own_bad = nullptr;
     if (!d_bad) TGK_TRY(routing_flags(r, &own_bad));
