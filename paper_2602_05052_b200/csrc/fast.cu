@@ -649,15 +649,15 @@ int dispatch_fast(int kt, bool m, int ft, const FastArgs& a, int T, cudaStream_t
 
 int check_bad(unsigned long long* d_bad, cudaStream_t st);
 
-// Rows per block and threads per CTA (B200 sweeps, profiles/r02_fast_experiments.txt):
-// TET4 64 rows x 512 threads (C2a 348 us, C2 405 us; 32 x 256 at 4 CTAs/SM:
-// 357 / 434 us); TRI3 128 rows x 256 threads.
+// Rows per block and threads per CTA (B200 sweeps, profiles/r02_fast_experiments.txt);
+// TRI3 128 rows x 256 threads.
 struct FastShape {
     int R, T;
 };
 FastShape fast_shape(int kind, int fmt) {
-    (void)fmt;
-    FastShape s{kind == TGK_TET4 ? 64 : 128, kind == TGK_TET4 ? 512 : 256};
+    // TET4 stiffness [+ load] 48 x 384 (C2a 296 us), with the unit mass 64 x 512 (C2 358 us)
+    FastShape s{kind == TGK_TET4 ? (fmt == kFastFmtKS32 ? 64 : 48) : 128,
+                kind == TGK_TET4 ? (fmt == kFastFmtKS32 ? 512 : 384) : 256};
     if (const char* e = getenv("TGK_FAST_R")) s.R = std::max(1, std::min(kFastMaxRows, atoi(e)));
     if (const char* e = getenv("TGK_FAST_T")) s.T = std::max(32, std::min(kFastScalarMaxThreads, atoi(e) / 32 * 32));
     return s;
