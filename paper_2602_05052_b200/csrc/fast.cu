@@ -108,6 +108,19 @@ struct FastCfg {
     }
 };
 
+// 1/x for the fast mode: the hardware approximation refined by two Newton
+// steps (relative error ~1 ulp, no special-case branches; x is a finite
+// non-zero determinant — non-positive ones are rejected after the call, and a
+// subnormal one, which the approximation flushes, belongs to no usable mesh)
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = __fma_rn(-x, r, 1.0);
+    r = __fma_rn(r, e, r);
+    e = __fma_rn(-x, r, 1.0);
+    return __fma_rn(r, e, r);
+}
+
 __device__ __forceinline__ double dot3(double ax, double ay, double az, double bx, double by, double bz) {
     return __fma_rn(ax, bx, __fma_rn(ay, by, az * bz));
 }
@@ -258,7 +271,7 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
                      c3z = __fma_rn(e1x, e2y, -(e1y * e2x));
         det = dot3(e1x, e1y, e1z, c1x, c1y, c1z);
         if constexpr (KT == 0) {
-            const double s = coef_w(Cn::wsum) * __drcp_rn(det);
+            const double s = coef_w(Cn::wsum) * fast_rcp(det);
             const double k11 = s * dot3(c1x, c1y, c1z, c1x, c1y, c1z);
             const double k12 = s * dot3(c1x, c1y, c1z, c2x, c2y, c2z);
             const double k13 = s * dot3(c1x, c1y, c1z, c3x, c3y, c3z);
@@ -279,7 +292,7 @@ __device__ __forceinline__ void fast_element(const FastArgs& p, const RecA& A, c
         const double e2x = p2.x - p0.x, e2y = p2.y - p0.y;
         det = __fma_rn(e1x, e2y, -(e1y * e2x));
         if constexpr (KT == 0) {
-            const double s = coef_w(Cn::wsum) * __drcp_rn(det);
+            const double s = coef_w(Cn::wsum) * fast_rcp(det);
             // grad N_1 = (e2y, -e2x) / det, grad N_2 = (-e1y, e1x) / det
             const double k11 = s * __fma_rn(e2y, e2y, e2x * e2x);
             const double k12 = -(s * __fma_rn(e2y, e1y, e2x * e1x));
@@ -789,7 +802,7 @@ __device__ __forceinline__ void elast_element(const FastElastArgs& p, const RecA
         const double c3x = __fma_rn(e1y, e2z, -(e1z * e2y)), c3y = __fma_rn(e1z, e2x, -(e1x * e2z)),
                      c3z = __fma_rn(e1x, e2y, -(e1y * e2x));
         det = dot3(e1x, e1y, e1z, c1x, c1y, c1z);
-        const double rd = __drcp_rn(det);
+        const double rd = fast_rcp(det);
         g[1][0] = c1x * rd; g[1][1] = c1y * rd; g[1][2] = c1z * rd;
         g[2][0] = c2x * rd; g[2][1] = c2y * rd; g[2][2] = c2z * rd;
         g[3][0] = c3x * rd; g[3][1] = c3y * rd; g[3][2] = c3z * rd;
@@ -800,7 +813,7 @@ __device__ __forceinline__ void elast_element(const FastElastArgs& p, const RecA
         const double e1x = xs[l[1]] - x0, e1y = xs[MB + l[1]] - y0;
         const double e2x = xs[l[2]] - x0, e2y = xs[MB + l[2]] - y0;
         det = __fma_rn(e1x, e2y, -(e1y * e2x));
-        const double rd = __drcp_rn(det);
+        const double rd = fast_rcp(det);
         g[1][0] = e2y * rd; g[1][1] = -(e2x * rd);
         g[2][0] = -(e1y * rd); g[2][1] = e1x * rd;
         g[0][0] = -(g[1][0] + g[2][0]); g[0][1] = -(g[1][1] + g[2][1]);
